@@ -1,0 +1,355 @@
+#!/usr/bin/env python
+"""Benchmark of the Spar-Sink hot path on B200 (BASELINE.json metric:
+"sparse Sinkhorn iters/s and achieved HBM GB/s vs peak; end-to-end solve time").
+
+Default workload: config 4 (n = 1e6, balanced OT, fp32 sketch values, fp64
+scalings, 300 iterations), the configuration the north-star target (>= 60% of
+HBM on 1 GPU) is quoted on. A "step" is one full 300-iteration Sinkhorn solve
+on the HBM-resident sketch (persistent loop kernel + residual readout).
+
+  python bench.py [--gpus N --steps K --warmup W] [--config c1|c2|c3|c4|c5]
+  python bench.py --impl reference ...   # the reference's CPU loop (oracle/_ref)
+
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "sparse Sinkhorn iters/s and achieved HBM GB/s vs peak; end-to-end solve time"
+
+
+def peaks() -> tuple[float, str]:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        return float(json.loads(p.read_text())["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows: list[list[str]] = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if len(r) > 2 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) > 2 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows if len(r) >= 9 for k in range(4)
+                          if r[5 + k].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_init():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch.distributed as dist
+
+        backend = "nccl" if os.environ.get("SPK_BACKEND", "nccl") == "nccl" else "gloo"
+        dist.init_process_group(backend=backend)
+    return ws, rank, local
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def max_over_ranks(x: float, ws: int) -> float:
+    if ws == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def value_bytes(values: str) -> int:
+    return 4 if values == "f32" else 8
+
+
+def cpu_same_law_sketch(w, nnz_target: float, seed: int = 77):
+    """A CPU-drawn sketch with config 4's sampling law (p uniform on the
+    support, so each row keeps ~Binomial(n, p*) uniformly placed columns with
+    values K_ij / p*). Used only by the reference arm, which must not run our
+    GPU sampler."""
+    n = w.n
+    rng = np.random.default_rng(seed)
+    ps = min(1.0, nnz_target / (float(n) * n))
+    counts = rng.binomial(n, ps, size=n)
+    rp = np.zeros(n + 1, np.int64)
+    np.cumsum(counts, out=rp[1:])
+    cols = np.empty(rp[-1], np.uint32)
+    vals = np.empty(rp[-1])
+    chunk = 20000
+    for r0 in range(0, n, chunk):
+        r1 = min(n, r0 + chunk)
+        m = rp[r1] - rp[r0]
+        c = rng.integers(0, n, size=m, dtype=np.int64)
+        rows = np.repeat(np.arange(r0, r1), counts[r0:r1])
+        # sort columns inside each row
+        order = np.lexsort((c, rows))
+        c = c[order]
+        d2 = ((w.x[rows] - w.y[c]) ** 2).sum(axis=1)
+        k = np.exp(-(d2 / w.scale) / w.eps)
+        cols[rp[r0]:rp[r1]] = c
+        vals[rp[r0]:rp[r1]] = (k / ps).astype(np.float32)
+    return rp, cols, vals
+
+
+def run_reference(args, ws, rank):
+    """--impl reference: the reference's own CPU loop (sinkhorn_ot/uot<SparseKernel>,
+    compiled from /root/reference by oracle/Makefile into oracle/_ref) on the
+    box's host; a bounded number of iterations per step."""
+    if rank != 0:
+        return
+    from oracle import Oracle, Reference
+    from paper_2306_06581_b200 import workloads as W
+
+    w = W.CONFIGS[args.config]()
+    iters = args.ref_iters
+    t0 = time.time()
+    if args.config == "c4":
+        csr = cpu_same_law_sketch(w, w.s)
+        sample = f"{iters} iterations of sinkhorn_ot<SparseKernel> per step on a CPU-drawn C4-law sketch " \
+                 f"(n=1e6, {csr[0][-1]} nnz, fp64 values)"
+    else:
+        # small configs: the reference builds its own dense K and sketch
+        R = Reference()
+        Cm, c0 = R.pairwise_cost(w.x, w.y, w.cost, w.eta)
+        Cm /= (c0 if w.scale is None else w.scale)
+        K, ratio = R.kernel_from_cost(Cm, w.eps)
+        plan = "uot" if w.uot else "ot"
+        csr = R.poisson_sparsify(plan, w.a, w.b, K, ratio, w.s, 7, w.lam, w.eps)
+        sample = f"{iters} iterations of sinkhorn_{plan}<SparseKernel> per step on the reference's own sketch"
+    prep = time.time() - t0
+    if Reference.available():
+        R = Reference()
+        kind = "reference"
+
+        def step():
+            secs, _ = R.sparse_loop_seconds(csr, w.a, w.b, w.eps, iters, w.lam, w.uot)
+            return secs
+    else:
+        O = Oracle()
+        kind = "port"
+
+        def step():
+            t, _, _ = O.time_scaling_iters(csr, w.a, w.b, iters)
+            return t * iters
+    for _ in range(args.warmup):
+        step()
+    times = [step() for _ in range(args.steps)]
+    total = sum(times)
+    value = args.steps * iters / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": w.name, "n": w.n, "iterations_per_step": iters, "nnz": int(csr[0][-1])},
+        "cpu_baseline": {"value": value, "unit": "iters/s", "cores": 1, "kind": kind, "sample": sample},
+        "e2e": {"value": value, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "extra": {"prep_s": prep, "note": "reference is single-threaded (proj/CMakeLists.txt:19; no OpenMP)"},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, ws, rank, local):
+    import torch
+
+    import paper_2306_06581_b200 as spk
+    from paper_2306_06581_b200 import workloads as W
+
+    torch.cuda.set_device(local)
+    w = W.CONFIGS[args.config]()
+    iters = args.iters or w.max_iter
+    ctx = spk.Context(local)
+    stream = torch.cuda.current_stream()
+    ctx.set_stream(stream.cuda_stream)
+    kernel = spk.Coords(w.x, w.y, w.cost, w.eta, scale=w.scale, eps=w.eps)
+    opts = spk.SparSinkOptions(values=w.values)
+    plan = "uot" if w.uot else "ot"
+
+    # ---- setup: plan + sample + CSC on the device (kept resident) ----
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    sk = ctx.sketch(kernel, w.a, w.b, plan, w.lam, w.eps, w.s, 7, opts)
+    torch.cuda.synchronize()
+    setup_s = time.perf_counter() - t0
+    cfg = spk.SolverConfig(w.eps, w.lam, w.delta, iters, w.stabilize)
+
+    # ---- warm-up + timed region: K full solves on the resident sketch ----
+    for _ in range(args.warmup):
+        sk.solve(cfg, w.uot, want_scalings=False)
+    launches0 = ctx.launches
+    loop_s, iters_done = [], 0
+    barrier(ws)
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            res = sk.solve(cfg, w.uot, want_scalings=False)
+            loop_s.append(res.report["t_loop_s"])
+            iters_done += res.report["iterations"]
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    barrier(ws)
+    elapsed = max_over_ranks(ev0.elapsed_time(ev1) * 1e-3, ws)
+    launches = ctx.launches - launches0
+    value = ws * iters_done / elapsed  # replicas: every rank runs the full problem
+
+    # ---- roofline of the dominant kernel (the persistent loop) ----
+    peak, peak_src = peaks()
+    vb = value_bytes(w.values)
+    b_iter = W.bytes_per_iteration(sk.n, sk.nnz, vb)
+    per_launch_iters = iters_done / args.steps
+    mean_loop = sum(loop_s) / len(loop_s)
+    achieved = b_iter * per_launch_iters / mean_loop / 1e9
+    traffic = None
+    prof = ROOT / "profiles" / f"ncu_{w.name.lower()}_loop.json"
+    if prof.exists():
+        traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
+
+    # ---- end to end through the C ABI with host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        e2e_times = []
+        for k in range(2):
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
+            r = ctx.spar_sink(kernel, w.a, w.b, cfg, w.s, 7, opts, uot=w.uot)
+            torch.cuda.synchronize()
+            e2e_times.append(time.perf_counter() - t1)
+        e2e_t = max_over_ranks(e2e_times[-1], ws)
+        h2d = w.x.nbytes + w.y.nbytes + w.a.nbytes + w.b.nbytes
+        d2h = r.u.nbytes + r.v.nbytes + 8 * 4
+        e2e = {"value": ws * r.report["iterations"] / e2e_t, "unit": "iters/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "solve_s": e2e_t, "objective": r.report["objective"],
+               "phases_s": {"plan": r.report["t_plan_s"], "sample": r.report["t_sample_s"],
+                            "loop": r.report["t_loop_s"], "readout": r.report["t_readout_s"]}}
+
+    # ---- CPU baseline: the reference loop on this very sketch (rank 0, N=1) ----
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        from oracle import Oracle, Reference
+
+        rp, ci, vv = sk.csr()
+        k_cpu = args.cpu_iters
+        if Reference.available():
+            secs, _ = Reference().sparse_loop_seconds((rp, ci, vv), w.a, w.b, w.eps, k_cpu, w.lam, w.uot)
+            kind = "reference"
+        else:
+            t, _, _ = Oracle().time_scaling_iters((rp, ci, vv), w.a, w.b, k_cpu)
+            secs, kind = t * k_cpu, "port"
+        cpu = {"value": k_cpu / secs, "unit": "iters/s", "cores": 1, "kind": kind,
+               "sample": f"{k_cpu} of {iters} iterations of sinkhorn_{plan}<SparseKernel> on the GPU-built "
+                         f"{w.name} sketch ({sk.nnz} nnz) copied to host, 1 core (reference is single-threaded)"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * elapsed / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": w.name, "n": sk.n, "nnz": sk.nnz, "s": w.s, "epsilon": w.eps,
+                   "lambda": w.lam if math.isfinite(w.lam) else "inf", "iterations_per_step": per_launch_iters,
+                   "sketch_values": w.values, "scalings": "f64",
+                   "parallelism": f"replicas{ws}" if ws > 1 else "single",
+                   "l2": f"inputs larger than L2: sketch {(sk.nnz * 2 * (vb + 4)) / 1e9:.2f} GB"
+                         if args.config == "c4" else "sketch L2-resident (config smaller than L2)"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "kernel": "loop_kernel (persistent, both halves)",
+                     "bytes_per_iter": b_iter, "peak_source": peak_src},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "extra": {"setup_s": setup_s, "loop_ms_per_iter": 1e3 * mean_loop / per_launch_iters,
+                  "kernel_nnz": sk.kernel_nnz, "factorized_plan": sk.factorized_plan},
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    sk.free()
+    ctx.close()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c4", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--iters", type=int, default=0, help="iterations per step (default: the config's)")
+    ap.add_argument("--cpu-iters", type=int, default=10)
+    ap.add_argument("--ref-iters", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3  # timing rule: >= 3 warm-up steps
+    ws, rank, local = dist_init()
+    if args.impl == "reference":
+        run_reference(args, ws, rank)
+    else:
+        run_ours(args, ws, rank, local)
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

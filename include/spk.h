@@ -1,0 +1,236 @@
+/*
+ * spk.h -- C ABI of the B200-native Spar-Sink hot path (libspk_b200.so).
+ *
+ * Plain pointers and sizes only; no CUDA, C++ or torch types cross this
+ * boundary. Every entry point blocks until its host outputs are written,
+ * never throws, and returns 0 or the reference's ErrorCategory value
+ * (proj/include/sparsink/errors.hpp:11): 2 = solver, 3 = degenerate sketch,
+ * 4 = input, plus 5 = CUDA/device fault. spk_last_error() then reports the
+ * exception class (SPK_E_*) and the reference-style message
+ * ("<Class>: text", errors.hpp:23-28) so a C++ shim can rethrow the SAME
+ * type (see include/sparsink_b200.hpp and INTEGRATION.md).
+ *
+ * Reference interfaces replaced (relative to /root/reference/proj):
+ *   spk_spar_sink          spar_sink_ot / spar_sink_uot   include/sparsink/solvers.hpp:159-167
+ *                          (+ coordinate overload, no n^2 host storage)
+ *   spk_sinkhorn           sinkhorn_ot / sinkhorn_uot<KernelMatrix>   solvers.hpp:137-147,209-232
+ *   spk_sketch_solve       sinkhorn_ot / sinkhorn_uot<SparseKernel>   solvers.hpp:137-147
+ *   spk_sketch_build       ot/uot/uniform_probabilities + shrink_with_uniform
+ *                          + poisson_sparsify            include/sparsink/sparsify.hpp:74-95
+ *   spk_sketch_spmv        spmv / spmv_t                  sparsify.hpp:97-98
+ *   spk_sketch_readout     ot_objective / uot_objective / marginal_residuals /
+ *                          TransportPlan::row_marginal,col_marginal  solvers.hpp:53-54,170-181
+ *   spk_plan_probs         SamplingPlan::prob on a set of (i, j)     sparsify.hpp:28-34
+ *   spk_cost_kernel        sq_euclidean_cost / euclidean_cost / wfr_cost +
+ *                          kernel_from_cost               include/sparsink/geometry.hpp:28-36
+ */
+#ifndef SPK_H_
+#define SPK_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SPK_ABI_VERSION 1
+
+/* ---- status and error classes --------------------------------------------- */
+enum spk_status {
+  SPK_OK = 0,
+  SPK_STATUS_SOLVER = 2,            /* ErrorCategory::Solver */
+  SPK_STATUS_DEGENERATE_SKETCH = 3, /* ErrorCategory::DegenerateSketch */
+  SPK_STATUS_INPUT = 4,             /* ErrorCategory::Input */
+  SPK_STATUS_DEVICE = 5             /* CUDA fault / missing device (no reference analogue) */
+};
+
+/* Exception classes of errors.hpp:30-47 (plus the plain Error base). */
+enum spk_error_kind {
+  SPK_E_NONE = 0,
+  SPK_E_ERROR = 1, /* sparsink::Error(category, msg) */
+  SPK_E_NEGATIVE_WEIGHT = 2,
+  SPK_E_LENGTH_MISMATCH = 3,
+  SPK_E_NOT_NORMALIZED = 4,
+  SPK_E_ALL_BLACK = 5,
+  SPK_E_EMPTY_OUTPUT = 6,
+  SPK_E_DIMENSION_MISMATCH = 7,
+  SPK_E_NON_POSITIVE_ETA = 8,
+  SPK_E_NON_POSITIVE_EPSILON = 9,
+  SPK_E_DEGENERATE_SUPPORT = 10,
+  SPK_E_ALL_ZERO_KERNEL = 11,
+  SPK_E_THETA_OUT_OF_RANGE = 12,
+  SPK_E_BUDGET_TOO_LARGE = 13,
+  SPK_E_EMPTY_WINDOW = 14,
+  SPK_E_INFINITE_COST_ON_SUPPORT = 15,
+  SPK_E_IO_ERROR = 16,
+  SPK_E_ZERO_DENOMINATOR = 17,
+  SPK_E_BASELINE_FAILED = 18,
+  SPK_E_DEGENERATE_SKETCH_ERROR = 19,
+  SPK_E_DEVICE = 20
+};
+
+/* ---- enums mirroring the reference ---------------------------------------- */
+enum spk_cost_kind { SPK_COST_SQEUCLID = 0, SPK_COST_EUCLID = 1, SPK_COST_WFR = 2 }; /* geometry.hpp:10 */
+enum spk_plan_kind { SPK_PLAN_OT = 0, SPK_PLAN_UOT = 1, SPK_PLAN_BARYCENTER = 2, SPK_PLAN_UNIFORM = 3 }; /* sparsify.hpp:14 */
+enum spk_empty_policy { SPK_POLICY_ERROR = 0, SPK_POLICY_MASK = 1 };  /* solvers.hpp:32 */
+enum spk_probs { SPK_PROBS_IMPORTANCE = 0, SPK_PROBS_UNIFORM = 1 };   /* solvers.hpp:149 */
+enum spk_value_type { SPK_VALUES_F64 = 0, SPK_VALUES_F32 = 1 };
+
+/* ---- plain structs ---------------------------------------------------------- */
+
+/* The Gibbs kernel and its cost, in one of two forms.
+ * Dense form (KernelMatrix + CostMatrix, geometry.hpp:13-26): K != NULL,
+ *   n*n row-major host fp64; nnz_ratio as KernelMatrix::nnz_ratio; C may be
+ *   NULL when no objective is needed.
+ * Coordinate form (new; no n^2 storage): K == NULL, x and y are n*dim
+ *   row-major host fp64 points; C_ij = cost(x_i, y_j) / cost_scale computed
+ *   exactly as pairwise_cost (geometry.cpp:16-66) and the caller's division;
+ *   cost_scale <= 0 means "divide by c0 = max finite cost" (the configs'
+ *   max-normalisation); K_ij = isinf(C) ? 0 : exp(-C_ij / kernel_epsilon)
+ *   (kernel_from_cost, geometry.cpp:83-102). */
+typedef struct {
+  int64_t n;
+  const double* K;
+  double nnz_ratio;
+  const double* C;
+  const double* x;
+  const double* y;
+  int32_t dim;
+  int32_t cost_kind;
+  double eta;
+  double cost_scale;
+  double kernel_epsilon;
+} spk_kernel_desc;
+
+/* SolverConfig (solvers.hpp:20-26) + the EmptyPolicy argument. */
+typedef struct {
+  double epsilon;
+  double lambda; /* +INFINITY = balanced */
+  double delta;
+  int64_t max_iter;
+  int32_t stabilize;    /* log-domain iterations */
+  int32_t empty_policy; /* spk_empty_policy */
+} spk_solver_cfg;
+
+/* SparSinkOptions (solvers.hpp:151-157) + storage choice. */
+typedef struct {
+  double theta;
+  int32_t probs;      /* spk_probs */
+  int32_t strict;
+  int32_t value_type; /* spk_value_type: sketch values fp64 (default) or fp32 */
+  int32_t reserved;
+} spk_sketch_opts;
+
+/* SolveReport (solvers.hpp:61-76) + TransportPlan flags (:40-43) + phase
+ * timings measured with CUDA events on the context's stream. */
+typedef struct {
+  double objective;
+  int64_t iterations;
+  double residual_row;
+  double residual_col;
+  double wall_time_s;
+  int64_t sketch_nnz; /* -1 when no sketch (dense solve) */
+  int32_t converged;
+  int32_t diverged;
+  uint64_t seed;
+  double kernel_mean;
+  int64_t masked_rows;
+  int64_t masked_cols;
+  int32_t log_domain;
+  int32_t factorized_plan;
+  int64_t kernel_nnz;
+  double t_plan_s;
+  double t_sample_s;
+  double t_loop_s;
+  double t_readout_s;
+} spk_report;
+
+typedef struct spk_ctx spk_ctx;
+typedef struct spk_sketch spk_sketch;
+
+/* ---- context ---------------------------------------------------------------- */
+int spk_ctx_create(int device, spk_ctx** out);
+void spk_ctx_destroy(spk_ctx* ctx);
+/* Use an external CUDA stream (a cudaStream_t passed as void*; NULL = the
+ * context's own stream). Lets callers time kernels on their stream. */
+int spk_ctx_set_stream(spk_ctx* ctx, void* stream);
+void* spk_ctx_stream(spk_ctx* ctx);
+/* Option keys. SPK_OPT_DETERMINISTIC=1 selects the parity kernels: one thread
+ * per output summing in the reference's index order with no FMA, and
+ * sequential residual sums, so OT scalings and iteration counts are
+ * bit-identical to the CPU reference on the same sketch. */
+enum spk_option { SPK_OPT_DETERMINISTIC = 1, SPK_OPT_LOOP_BLOCKS_PER_SM = 2 };
+int spk_ctx_set_option(spk_ctx* ctx, int key, int64_t value);
+/* Status of the last failed call on ctx: category (spk_status), class
+ * (spk_error_kind) and message. Returns the category. */
+int spk_last_error(const spk_ctx* ctx, int* category, int* kind, char* msg, size_t len);
+/* Number of kernels this context has launched so far. */
+int64_t spk_ctx_launch_count(const spk_ctx* ctx);
+
+/* ---- end-to-end solvers ---------------------------------------------------- */
+
+/* spar_sink_ot (uot = 0) / spar_sink_uot (uot = 1), solvers.hpp:159-167,
+ * bodies solvers.cpp:314-378. a, b: n host weights. u, v (and log_u, log_v
+ * when the log-domain path ran; may be NULL) receive n doubles each. */
+int spk_spar_sink(spk_ctx* ctx, const spk_kernel_desc* kd, const double* a, const double* b,
+                  const spk_solver_cfg* cfg, double s, uint64_t seed, const spk_sketch_opts* opts,
+                  int uot, double* u, double* v, double* log_u, double* log_v, spk_report* rep);
+
+/* Dense Sinkhorn: sinkhorn_ot / sinkhorn_uot on a KernelMatrix
+ * (solvers.hpp:137-147). Dense form uploads K; coordinate form recomputes
+ * K on the fly every iteration (config 5 comparator). The objective is
+ * computed when a cost is available (dense C or coordinates). */
+int spk_sinkhorn(spk_ctx* ctx, const spk_kernel_desc* kd, const double* a, const double* b,
+                 const spk_solver_cfg* cfg, int uot, double* u, double* v, double* log_u,
+                 double* log_v, spk_report* rep);
+
+/* ---- device-resident sketch ------------------------------------------------ */
+
+/* Plan (kind) -> [theta] -> poisson_sparsify on the device; builds CSR and
+ * its CSC mirror. lambda/epsilon feed uot_probabilities (sparsify.cpp:93-115).
+ * a and b are kept on the device for later solves. */
+int spk_sketch_build(spk_ctx* ctx, const spk_kernel_desc* kd, const double* a, const double* b,
+                     int plan_kind, double lambda, double epsilon, double s, uint64_t seed,
+                     const spk_sketch_opts* opts, spk_sketch** out);
+/* Upload a host CSR (SparseKernel layout, sparsify.hpp:57-71). */
+int spk_sketch_from_csr(spk_ctx* ctx, int64_t n, const int64_t* row_ptr, const uint32_t* col_idx,
+                        const double* values, int value_type, spk_sketch** out);
+void spk_sketch_free(spk_sketch* sk);
+int spk_sketch_info(const spk_sketch* sk, int64_t* n, int64_t* nnz, int64_t* kernel_nnz,
+                    int32_t* factorized_plan, double* kernel_mean);
+/* Copy CSR (row_ptr n+1, col_idx nnz, values nnz as fp64) / CSC to host. */
+int spk_sketch_copy_csr(spk_sketch* sk, int64_t* row_ptr, uint32_t* col_idx, double* values);
+int spk_sketch_copy_csc(spk_sketch* sk, int64_t* col_ptr, uint32_t* row_idx, double* values);
+/* y = K~ x (transpose = 0) or K~' x (transpose = 1); host vectors of n. */
+int spk_sketch_spmv(spk_sketch* sk, const double* x, double* y, int transpose);
+/* Sinkhorn loop on the sketch. a/b NULL = the weights given at build. u, v,
+ * log_u, log_v may be NULL (results stay on the device for readout). */
+int spk_sketch_solve(spk_ctx* ctx, spk_sketch* sk, const double* a, const double* b,
+                     const spk_solver_cfg* cfg, int uot, double* u, double* v, double* log_u,
+                     double* log_v, spk_report* rep);
+/* Plan readout of the LAST solve on this sketch: marginals (may be NULL)
+ * and the OT/UOT objective with costs from kd (dense C or coordinates). */
+int spk_sketch_readout(spk_ctx* ctx, spk_sketch* sk, const spk_kernel_desc* kd, int uot,
+                       double lambda, double epsilon, double* row_marginal, double* col_marginal,
+                       double* objective, spk_report* rep);
+
+/* ---- helpers exposed for parity tests --------------------------------------- */
+
+/* SamplingPlan::prob(i, j) (sparsify.hpp:28-34) of the plan that
+ * spk_sketch_build would use, for m query pairs. */
+int spk_plan_probs(spk_ctx* ctx, const spk_kernel_desc* kd, const double* a, const double* b,
+                   int plan_kind, double lambda, double epsilon, double theta, int64_t m,
+                   const int64_t* qi, const int64_t* qj, double* probs, int32_t* factorized);
+
+/* Cost and Gibbs kernel entries from coordinates (pairwise_cost +
+ * kernel_from_cost) for m query pairs; c0 = max finite cost over all n^2
+ * pairs when requested (NULL skips). */
+int spk_cost_kernel(spk_ctx* ctx, const spk_kernel_desc* kd, int64_t m, const int64_t* qi,
+                    const int64_t* qj, double* cost, double* kernel, double* c0);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SPK_H_ */

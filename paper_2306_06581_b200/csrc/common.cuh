@@ -1,0 +1,76 @@
+// common.cuh -- device helpers shared by the Spar-Sink kernels (sm_100a).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+#include <math_constants.h>
+
+namespace spk {
+
+constexpr uint64_t kGolden = 0x9e3779b97f4a7c15ULL;
+constexpr int kWarp = 32;
+
+// splitmix64 finalizer without the increment: the t-th draw of the
+// reference's CounterRng(seed, stream) is finalize(mix_seed(seed,stream) +
+// t*golden) (rng.hpp:29-35). Integer pipe only.
+__host__ __device__ __forceinline__ uint64_t sm_finalize(uint64_t x) {
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+  return x ^ (x >> 31);
+}
+__host__ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {  // rng.hpp:10-15
+  return sm_finalize(x + kGolden);
+}
+__host__ __device__ __forceinline__ uint64_t mix_seed(uint64_t seed, uint64_t stream) {  // rng.hpp:17-19
+  return splitmix64(seed ^ splitmix64(stream + 0x632be59bd9b4e019ULL));
+}
+// next_double (rng.hpp:38-40): top 53 bits scaled by 2^-53 (exact).
+__device__ __forceinline__ double u64_to_unit(uint64_t x) {
+  return __dmul_rn(__ull2double_rn(x >> 11), 0x1.0p-53);
+}
+
+// Exact (contraction-free) arithmetic for reference-order sums.
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+
+// pairwise_cost entry (geometry.cpp:16-59) in the reference's operation
+// order with no FMA: sequential d2, then the per-kind transform.
+template <int KIND>
+__device__ __forceinline__ double cost_entry(const double* __restrict__ p, const double* __restrict__ q,
+                                             int dim, double eta) {
+  double d2 = 0.0;
+  for (int k = 0; k < dim; ++k) {
+    const double diff = dsub(p[k], q[k]);
+    d2 = dadd(d2, dmul(diff, diff));
+  }
+  if (KIND == 0) return d2;
+  if (KIND == 1) return sqrt(d2);
+  const double d = sqrt(d2);
+  if (d >= dmul(3.14159265358979323846, eta)) return CUDART_INF;
+  const double cz = cos(d / dmul(2.0, eta));
+  double v = -log(dmul(cz, cz));
+  if (!(v >= 0.0)) v = 0.0;
+  return v;
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ long long warp_sum_ll(long long v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// std::min(1.0, x) semantics: returns 1.0 when x is NaN (sparsify.cpp:191).
+__device__ __forceinline__ double min1(double x) { return (x < 1.0) ? x : 1.0; }
+
+}  // namespace spk

@@ -1,0 +1,362 @@
+// dense.cu -- dense Sinkhorn half-step operators (north-star item 5)
+// for the persistent loop in loop_core.cuh.
+//
+// Reference: sinkhorn_ot / sinkhorn_uot on a KernelMatrix (include/sparsink/solvers.hpp:137-147)
+// with kernel_apply / kernel_apply_t (proj/src/solvers.cpp:12-34) and
+// kernel_log_apply(_t) (:52-94); default EmptyPolicy::Error.
+//
+// Three operators:
+//   DenseOp     K uploaded (n x n fp64): rows as warp dot products; columns one
+//               thread per column walking rows in order -- coalesced AND the
+//               reference's kernel_apply_t summation order.
+//   OtfExactOp  K_ij = exp(-C_ij/eps) recomputed in fp64 from coordinates
+//               every iteration (exact kernel_from_cost values, no n^2 memory).
+//   OtfFastOp   config-5 comparator: squared-Euclidean K recomputed every
+//               iteration in fp32 as exp2(A_i + B_j + <x'_i, y_j>) (one MUFU.EX2
+//               + 6 FFMA per entry), fp32 partial sums per 256-column chunk
+//               folded into fp64. SFU/FMA-bound, no n^2 memory.
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "common.cuh"
+#include "internal.h"
+#include "ksrc.cuh"
+#include "loop_core.cuh"
+
+namespace spk {
+
+namespace {
+
+using loopcore::finalize_atom;
+
+// Shared body for dense/exact operators: ROLE 0 = rows, ROLE 1 = columns.
+template <class KF>
+struct ExactOp {
+  KF k;
+  int64_t n;
+
+  template <bool LOG, bool DET>
+  __device__ double row_value(int64_t i, const double* x, int lane) const {
+    if (!LOG) {
+      if (DET) {
+        double acc = 0.0;
+        for (int64_t j = 0; j < n; ++j) acc = dadd(acc, dmul(k(i, j), __ldcg(x + j)));
+        return acc;
+      }
+      double acc = 0.0;
+      for (int64_t j = lane; j < n; j += 32) acc = fma(k(i, j), __ldcg(x + j), acc);
+      return warp_sum(acc);
+    }
+    // kernel_log_apply dense (solvers.cpp:52-71)
+    if (DET) {
+      double mx = -CUDART_INF;
+      for (int64_t j = 0; j < n; ++j) {
+        const double kij = k(i, j), xv = __ldcg(x + j);
+        if (kij == 0.0 || xv == -CUDART_INF) continue;
+        mx = fmax(mx, dadd(log(kij), xv));
+      }
+      if (mx == -CUDART_INF) return -CUDART_INF;
+      double acc = 0.0;
+      for (int64_t j = 0; j < n; ++j) {
+        const double kij = k(i, j), xv = __ldcg(x + j);
+        if (kij == 0.0 || xv == -CUDART_INF) continue;
+        acc = dadd(acc, exp(dsub(dadd(log(kij), xv), mx)));
+      }
+      return dadd(mx, log(acc));
+    }
+    double m = -CUDART_INF, s = 0.0;
+    for (int64_t j = lane; j < n; j += 32) {
+      const double kij = k(i, j), xv = __ldcg(x + j);
+      if (kij == 0.0 || xv == -CUDART_INF) continue;
+      const double t = log(kij) + xv;
+      if (t > m) {
+        s = s * exp(m - t) + 1.0;
+        m = t;
+      } else {
+        s += exp(t - m);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const double m2 = __shfl_xor_sync(0xffffffffu, m, o);
+      const double s2 = __shfl_xor_sync(0xffffffffu, s, o);
+      const double M = fmax(m, m2);
+      if (M != -CUDART_INF)
+        s = (m == -CUDART_INF ? 0.0 : s * exp(m - M)) + (m2 == -CUDART_INF ? 0.0 : s2 * exp(m2 - M));
+      m = M;
+    }
+    return m == -CUDART_INF ? -CUDART_INF : m + log(s);
+  }
+
+  // Column j: rows in ascending order, skipping u_i == 0 (solvers.cpp:28-33)
+  // or lu_i = -inf (:77-93). One thread per column.
+  template <bool LOG>
+  __device__ double col_value(int64_t j, const double* x) const {
+    if (!LOG) {
+      double acc = 0.0;
+      for (int64_t i = 0; i < n; ++i) {
+        const double xi = __ldcg(x + i);
+        if (xi == 0.0) continue;
+        acc = dadd(acc, dmul(k(i, j), xi));
+      }
+      return acc;
+    }
+    double mx = -CUDART_INF;
+    for (int64_t i = 0; i < n; ++i) {
+      const double xi = __ldcg(x + i);
+      const double kij = k(i, j);
+      if (xi == -CUDART_INF || !(kij > 0.0)) continue;
+      mx = fmax(mx, dadd(log(kij), xi));
+    }
+    if (mx == -CUDART_INF) return -CUDART_INF;
+    double acc = 0.0;
+    for (int64_t i = 0; i < n; ++i) {
+      const double xi = __ldcg(x + i);
+      const double kij = k(i, j);
+      if (xi == -CUDART_INF || !(kij > 0.0)) continue;
+      acc = dadd(acc, exp(dsub(dadd(log(kij), xi), mx)));
+    }
+    return dadd(mx, log(acc));
+  }
+
+  template <int ROLE, bool LOG, bool DET>
+  __device__ void half(const double* x, const double* wgt, const double* old, double* out, unsigned char* ne,
+                       int* dyn, double exponent, int policy, int t, unsigned long long* flag, double* absdiff,
+                       double& err, long long& masks) const {
+    const int lane = threadIdx.x & 31;
+    if (ROLE == 1 || DET) {
+      const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+      const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+      for (int64_t i = tid; i < n; i += nth) {
+        double d = 0.0;
+        const double o = __ldcg(old + i);
+        if (ne[i]) {
+          const double tmp = ROLE == 0 ? row_value<LOG, true>(i, x, lane) : col_value<LOG>(i, x);
+          d = finalize_atom<LOG>(i, tmp, o, wgt[i], exponent, policy, t, ne, dyn, out, flag, masks);
+        } else {
+          out[i] = o;
+        }
+        if (DET) absdiff[i] = d;
+        else err += d;
+      }
+    } else {
+      const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+      const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+      for (int64_t i = warp; i < n; i += nw) {
+        if (!ne[i]) {
+          if (lane == 0) out[i] = __ldcg(old + i);
+          continue;
+        }
+        const double tmp = row_value<LOG, false>(i, x, lane);
+        if (lane == 0) err += finalize_atom<LOG>(i, tmp, __ldcg(old + i), wgt[i], exponent, policy, t, ne, dyn, out, flag, masks);
+      }
+    }
+  }
+};
+
+// ---- fast fp32 on-the-fly squared-Euclidean operator (config 5) ---------------
+
+constexpr int kOtfDim = 8;     // padded point record: d <= 6 coords + bias
+constexpr int kOtfRows = 4;    // rows per lane
+constexpr int kOtfChunk = 256; // columns per fp32 partial
+
+// Point records (float4 x2): {p_0..p_{d-1}, bias, 0...}. For the output side
+// p = -2*alpha*x_i and bias = alpha*|x_i|^2; input side p = y_j, bias =
+// alpha*|y_j|^2, with alpha = -log2(e)/(scale*eps), so
+// K_ij = exp2(bias_i + bias_j + <p_i, y_j>) = exp(-|x_i - y_j|^2/(scale*eps)).
+struct OtfFastOp {
+  int64_t n;
+  int dim;
+  const float4* out_rec[2];  // [role] output-side records (2 float4 per atom)
+  const float4* in_rec[2];   // [role] input-side records
+
+  template <int ROLE, bool LOG, bool DET>
+  __device__ void half(const double* x, const double* wgt, const double* old, double* out, unsigned char* ne,
+                       int* dyn, double exponent, int policy, int t, unsigned long long* flag, double* absdiff,
+                       double& err, long long& masks) const {
+    __shared__ double red[loopcore::kBlock / 32][32 * kOtfRows];
+    const int lane = threadIdx.x & 31;
+    const int w = threadIdx.x >> 5;
+    const int nwarps = blockDim.x >> 5;
+    const float4* orec = out_rec[ROLE];
+    const float4* irec = in_rec[ROLE];
+    const int64_t tile_rows = 32 * kOtfRows;
+    const int64_t ntiles = (n + tile_rows - 1) / tile_rows;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      const int64_t r0 = tile * tile_rows;
+      float p[kOtfRows][kOtfDim];
+      double acc[kOtfRows];
+#pragma unroll
+      for (int r = 0; r < kOtfRows; ++r) {
+        const int64_t i = r0 + lane + 32 * r;
+        float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
+        if (i < n) {
+          a = orec[2 * i];
+          b = orec[2 * i + 1];
+        }
+        p[r][0] = a.x; p[r][1] = a.y; p[r][2] = a.z; p[r][3] = a.w;
+        p[r][4] = b.x; p[r][5] = b.y; p[r][6] = b.z; p[r][7] = b.w;
+        acc[r] = 0.0;
+      }
+      // warp w handles column chunks w, w + nwarps, ...
+      const int64_t nchunks = (n + kOtfChunk - 1) / kOtfChunk;
+      for (int64_t ch = w; ch < nchunks; ch += nwarps) {
+        const int64_t c0 = ch * kOtfChunk;
+        const int64_t c1 = min(c0 + kOtfChunk, n);
+        float part[kOtfRows];
+#pragma unroll
+        for (int r = 0; r < kOtfRows; ++r) part[r] = 0.f;
+        for (int64_t j = c0; j < c1; ++j) {
+          const float4 qa = __ldg(irec + 2 * j);
+          const float4 qb = __ldg(irec + 2 * j + 1);
+          const float xj = (float)__ldcg(x + j);
+#pragma unroll
+          for (int r = 0; r < kOtfRows; ++r) {
+            // bias_i (p[r][dim] slot) + bias_j (qb.w) + <p_i, y_j>
+            float e = p[r][7] + qb.w;
+            e = fmaf(p[r][0], qa.x, e);
+            e = fmaf(p[r][1], qa.y, e);
+            e = fmaf(p[r][2], qa.z, e);
+            e = fmaf(p[r][3], qa.w, e);
+            e = fmaf(p[r][4], qb.x, e);
+            e = fmaf(p[r][5], qb.y, e);
+            e = fmaf(p[r][6], qb.z, e);
+            part[r] = fmaf(exp2f(e), xj, part[r]);
+          }
+        }
+#pragma unroll
+        for (int r = 0; r < kOtfRows; ++r) acc[r] += (double)part[r];
+      }
+#pragma unroll
+      for (int r = 0; r < kOtfRows; ++r) red[w][lane + 32 * r] = acc[r];
+      __syncthreads();
+      // warp 0..: combine warps in fixed order, finalize atoms
+      for (int q = threadIdx.x; q < tile_rows; q += blockDim.x) {
+        const int64_t i = r0 + q;
+        if (i >= n) continue;
+        double tmp = 0.0;
+        for (int k = 0; k < nwarps; ++k) tmp += red[k][q];
+        const double o = __ldcg(old + i);
+        if (!ne[i]) {
+          out[i] = o;
+          continue;
+        }
+        err += finalize_atom<false>(i, tmp, o, wgt[i], exponent, policy, t, ne, dyn, out, flag, masks);
+      }
+      __syncthreads();
+    }
+  }
+};
+
+// Coverage of a dense / on-the-fly kernel: row i covered iff some K_ij > 0
+// (solvers.cpp:138-152).
+template <class KF>
+__global__ void dense_coverage_kernel(KF k, int64_t n, unsigned char* row_ne, unsigned char* col_ne,
+                                      unsigned long long* empty) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = warp; i < 2 * n; i += nw) {
+    const bool rowside = i < n;
+    const int64_t a = rowside ? i : i - n;
+    bool any = false;
+    for (int64_t j = lane; j < n && !any; j += 32) any = (rowside ? k(a, j) : k(j, a)) > 0.0;
+    any = __any_sync(0xffffffffu, any);
+    if (lane == 0) {
+      (rowside ? row_ne : col_ne)[a] = any ? 1 : 0;
+      if (!any) atomicAdd(&empty[rowside ? 0 : 1], 1ull);
+    }
+  }
+}
+
+template <bool LOG, class KF>
+void run_exact(spk_ctx* ctx, KF kf, int64_t n, const spk_solver_cfg& cfg, double exponent, int policy,
+               LoopState& st, LoopOut& out) {
+  DBuf row_ne(n), col_ne(n), empty(16);
+  SPK_CUDA(cudaMemsetAsync(empty.p, 0, 16, ctx->stream));
+  dense_coverage_kernel<KF><<<(int)std::max<int64_t>(1, std::min<int64_t>((2 * n + 7) / 8, ctx->num_sms * 16)), 256, 0,
+                              ctx->stream>>>(kf, n, row_ne.as<unsigned char>(), col_ne.as<unsigned char>(),
+                                             empty.as<unsigned long long>());
+  ++ctx->launches;
+  unsigned long long emp[2];
+  download(ctx, emp, empty, sizeof emp);
+  ExactOp<KF> op;
+  op.k = kf;
+  op.n = n;
+  const int64_t useful = (n + 15) / 16;
+  loopcore::run_core<LOG>(ctx, op, n, row_ne, col_ne, (long long)emp[0], (long long)emp[1], cfg, exponent, policy, st,
+                          useful, out);
+}
+
+__global__ void otf_records_kernel(const double* pts, int64_t n, int dim, double alpha, float4* out_rec,
+                                   float4* in_rec) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    float o[kOtfDim] = {0, 0, 0, 0, 0, 0, 0, 0};
+    float q[kOtfDim] = {0, 0, 0, 0, 0, 0, 0, 0};
+    double nrm = 0.0;
+    for (int k = 0; k < dim; ++k) {
+      const double c = pts[i * dim + k];
+      nrm += c * c;
+      o[k] = (float)(-2.0 * alpha * c);
+      q[k] = (float)c;
+    }
+    o[7] = (float)(alpha * nrm);
+    q[7] = (float)(alpha * nrm);
+    out_rec[2 * i] = make_float4(o[0], o[1], o[2], o[3]);
+    out_rec[2 * i + 1] = make_float4(o[4], o[5], o[6], o[7]);
+    in_rec[2 * i] = make_float4(q[0], q[1], q[2], q[3]);
+    in_rec[2 * i + 1] = make_float4(q[4], q[5], q[6], q[7]);
+  }
+}
+
+}  // namespace
+
+void run_dense_loop(spk_ctx* ctx, DevKernel& dk, const spk_solver_cfg& cfg, double exponent, int policy,
+                    LoopState& st, LoopOut& out) {
+  const int64_t n = dk.n;
+  const bool log_domain = cfg.stabilize != 0;
+  if (dk.dense) {
+    KDense kf{dk.K.as<double>(), n};
+    if (log_domain) run_exact<true>(ctx, kf, n, cfg, exponent, policy, st, out);
+    else run_exact<false>(ctx, kf, n, cfg, exponent, policy, st, out);
+    return;
+  }
+  const bool fast = !ctx->deterministic && !log_domain && ctx->otf_fp32 && dk.kind == SPK_COST_SQEUCLID && dk.dim <= 6;
+  if (!fast) {
+    KCoords kf = kcoords_of(dk);
+    if (log_domain) run_exact<true>(ctx, kf, n, cfg, exponent, policy, st, out);
+    else run_exact<false>(ctx, kf, n, cfg, exponent, policy, st, out);
+    return;
+  }
+  // fp32 records for both roles
+  DBuf xo(sizeof(float4) * 2 * n), xi(sizeof(float4) * 2 * n), yo(sizeof(float4) * 2 * n), yi(sizeof(float4) * 2 * n);
+  const double alpha = -1.4426950408889634 / (dk.scale * dk.eps);
+  const int g = loopcore::simple_grid(ctx, n);
+  otf_records_kernel<<<g, 256, 0, ctx->stream>>>(dk.x.as<double>(), n, dk.dim, alpha, xo.as<float4>(), xi.as<float4>());
+  otf_records_kernel<<<g, 256, 0, ctx->stream>>>(dk.y.as<double>(), n, dk.dim, alpha, yo.as<float4>(), yi.as<float4>());
+  ctx->launches += 2;
+  OtfFastOp op;
+  op.n = n;
+  op.dim = dk.dim;
+  op.out_rec[0] = xo.as<float4>();  // rows: x_i against y_j
+  op.in_rec[0] = yi.as<float4>();
+  op.out_rec[1] = yo.as<float4>();  // columns: y_j against x_i
+  op.in_rec[1] = xi.as<float4>();
+  // coverage: exp2 of finite exponents never reaches 0 for max-normalised
+  // costs with 1/eps < 700; otherwise use the exact coverage pass.
+  DBuf row_ne(n), col_ne(n), empty(16);
+  SPK_CUDA(cudaMemsetAsync(empty.p, 0, 16, ctx->stream));
+  KCoords kf = kcoords_of(dk);
+  dense_coverage_kernel<KCoords><<<(int)std::max<int64_t>(1, std::min<int64_t>((2 * n + 7) / 8, ctx->num_sms * 16)),
+                                   256, 0, ctx->stream>>>(kf, n, row_ne.as<unsigned char>(),
+                                                          col_ne.as<unsigned char>(), empty.as<unsigned long long>());
+  ++ctx->launches;
+  unsigned long long emp[2];
+  download(ctx, emp, empty, sizeof emp);
+  const int64_t useful = (n + 32 * kOtfRows - 1) / (32 * kOtfRows);
+  loopcore::run_core<false>(ctx, op, n, row_ne, col_ne, (long long)emp[0], (long long)emp[1], cfg, exponent, policy, st,
+                            useful, out);
+}
+
+}  // namespace spk

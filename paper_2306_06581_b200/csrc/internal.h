@@ -1,0 +1,204 @@
+// internal.h -- host-side structures shared by the CUDA translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/spk.h"
+
+namespace spk {
+
+// An error carrying the reference's exception class and category; thrown
+// inside the library and converted to a status at the C ABI boundary.
+struct Failure : std::runtime_error {
+  int category;
+  int kind;
+  Failure(int cat, int k, const std::string& msg) : std::runtime_error(msg), category(cat), kind(k) {}
+};
+
+[[noreturn]] void fail(int kind, const std::string& text);  // maps kind -> category, prefixes class
+[[noreturn]] void fail_device(const char* what, cudaError_t e);
+
+#define SPK_CUDA(x)                                  \
+  do {                                               \
+    cudaError_t e_ = (x);                            \
+    if (e_ != cudaSuccess) ::spk::fail_device(#x, e_); \
+  } while (0)
+
+// Device buffer with RAII.
+struct DBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DBuf() = default;
+  explicit DBuf(size_t b) { alloc(b); }
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr; o.bytes = 0; }
+  DBuf& operator=(DBuf&& o) noexcept {
+    if (this != &o) { release(); p = o.p; bytes = o.bytes; o.p = nullptr; o.bytes = 0; }
+    return *this;
+  }
+  ~DBuf() { release(); }
+  void alloc(size_t b) {
+    release();
+    bytes = b;
+    if (b) SPK_CUDA(cudaMalloc(&p, b));
+  }
+  void ensure(size_t b) { if (b > bytes) alloc(b); }
+  void release() { if (p) cudaFree(p); p = nullptr; bytes = 0; }
+  template <class T> T* as() const { return static_cast<T*>(p); }
+};
+
+}  // namespace spk
+
+// Device-resident sketch: CSR plus its CSC mirror (rows ascending inside
+// every column, so column sums run in the reference's spmv_t order).
+struct spk_sketch {
+  spk_ctx* ctx = nullptr;  // must outlive every call but spk_sketch_free
+  int device = 0;
+  int64_t n = 0;
+  int64_t nnz = 0;
+  int value_type = SPK_VALUES_F64;  // storage of values / values_t
+  spk::DBuf row_ptr, col_idx, values;   // int64[n+1], u32[nnz], f64|f32[nnz]
+  spk::DBuf col_ptr, row_idx, values_t; // CSC
+  spk::DBuf log_values, log_values_t;   // lazily built log K~ (same dtype)
+  spk::DBuf a, b;                       // f64[n] weights given at build
+  bool have_ab = false;
+  double a_total = 0.0, b_total = 0.0;
+  uint64_t seed = 0;
+  int64_t kernel_nnz = 0;
+  int factorized_plan = 0;
+  double kernel_mean = 0.0;
+  // state of the last solve (device)
+  spk::DBuf u, v, lu, lv;  // f64[n]
+  int last_log_domain = 0;
+  int last_valid = 0;
+  int64_t masked_rows = 0, masked_cols = 0;
+};
+
+struct spk_ctx {
+  int device = 0;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;
+  int num_sms = 0;
+  int deterministic = 0;
+  int loop_blocks_per_sm = 0;  // 0 = occupancy-derived
+  int otf_fp32 = 1;            // dense on-the-fly comparator computes K in fp32
+  int64_t launches = 0;
+  // last error
+  int err_category = 0;
+  int err_kind = 0;
+  std::string err_msg;
+  // scratch
+  spk::DBuf scratch;
+};
+
+namespace spk {
+
+void upload(spk_ctx* ctx, DBuf& dst, const void* src, size_t bytes);
+void download(spk_ctx* ctx, void* dst, const DBuf& src, size_t bytes);
+
+struct Timer {
+  cudaEvent_t a = nullptr, b = nullptr;
+  cudaStream_t s;
+  explicit Timer(cudaStream_t st) : s(st) {
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a, s);
+  }
+  double stop() {
+    cudaEventRecord(b, s);
+    cudaEventSynchronize(b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, a, b);
+    return ms * 1e-3;
+  }
+  ~Timer() {
+    if (a) cudaEventDestroy(a);
+    if (b) cudaEventDestroy(b);
+  }
+};
+
+// Sequential host sum exactly as new_measure (measures.cpp:18-23).
+double seq_total(const double* w, int64_t n);
+
+// Kernel source on the device: dense K (+C) or coordinates.
+struct DevKernel {
+  int64_t n = 0;
+  bool dense = false;
+  DBuf K, C;       // dense form (n*n f64); C optional
+  DBuf x, y;       // coordinate form (n*dim f64)
+  int dim = 0, kind = 0;
+  double eta = 0.0, scale = 1.0, eps = 1.0;
+  double nnz_ratio = 1.0;  // dense form: given; coordinate form: computed
+  bool have_cost = false;
+  bool max_normalised = false;  // scale == c0 (every finite C_ij <= 1)
+};
+
+void make_dev_kernel(spk_ctx* ctx, const spk_kernel_desc* kd, double default_eps, DevKernel& dk,
+                     bool need_cost);
+
+// ---- sampler.cu ----
+struct PlanInfo {
+  int kind = SPK_PLAN_OT;
+  bool factorized = true;
+  double theta = 0.0;      // lazy theta (factorized) or folded (grid)
+  int64_t kernel_nnz = 0;  // support size used by theta
+  double inv = 1.0;        // grid normaliser 1/total
+  double g_k = 0.0;        // UOT kernel exponent
+  std::vector<double> row_w, col_w;  // ra/cb, pa/pb, or 1/n
+};
+
+void build_plan(spk_ctx* ctx, DevKernel& dk, const double* a, const double* b, int plan_kind,
+                double lambda, double eps, double theta, PlanInfo& plan);
+void sample_sketch(spk_ctx* ctx, DevKernel& dk, const PlanInfo& plan, double s, uint64_t seed,
+                   int value_type, spk_sketch* sk);
+void build_csc(spk_ctx* ctx, spk_sketch* sk);
+void cost_kernel_query(spk_ctx* ctx, DevKernel& dk, int64_t m, const int64_t* qi, const int64_t* qj,
+                       double* cost, double* kern);
+void plan_probs_query(spk_ctx* ctx, DevKernel& dk, const PlanInfo& plan, int64_t m,
+                      const int64_t* qi, const int64_t* qj, double* out);
+
+// ---- loop.cu ----
+struct LoopOut {
+  int64_t iterations = 0;
+  int converged = 0, diverged = 0;
+  int64_t masked_rows = 0, masked_cols = 0;
+  double loop_s = 0.0;
+};
+// Runs the scaling loop on a sketch (sparse) or dense kernel; results in
+// sk->u/v (linear) or sk->lu/lv (log) style buffers passed in.
+struct LoopState {
+  int64_t n = 0;
+  const double* a = nullptr;  // device
+  const double* b = nullptr;
+  DBuf *u = nullptr, *v = nullptr, *lu = nullptr, *lv = nullptr;
+};
+void run_sparse_loop(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, double exponent,
+                     int policy, LoopState& st, LoopOut& out);
+void run_dense_loop(spk_ctx* ctx, DevKernel& dk, const spk_solver_cfg& cfg, double exponent,
+                    int policy, LoopState& st, LoopOut& out);
+
+// ---- readout.cu ----
+struct ReadoutOut {
+  double residual_row = 0.0, residual_col = 0.0;
+  double objective = 0.0;
+  bool have_objective = false;
+};
+// Plan marginals, residuals and objective over the sketch support
+// (for_each_entry semantics, T > 0 only).
+void sparse_readout(spk_ctx* ctx, spk_sketch* sk, DevKernel* dk, int log_domain, const double* a,
+                    const double* b, bool want_objective, int uot, double lambda, double eps,
+                    double* row_m_host, double* col_m_host, ReadoutOut& out);
+void dense_readout(spk_ctx* ctx, DevKernel& dk, int log_domain, const DBuf& u, const DBuf& v,
+                   const DBuf& lu, const DBuf& lv, const double* a, const double* b,
+                   bool want_objective, int uot, double lambda, double eps, ReadoutOut& out);
+double sketch_kernel_mean(spk_ctx* ctx, spk_sketch* sk);
+// spmv / spmv_t on the device sketch in the reference's summation order.
+void sketch_product(spk_ctx* ctx, spk_sketch* sk, const double* x_host, double* y_host, int transpose);
+
+}  // namespace spk

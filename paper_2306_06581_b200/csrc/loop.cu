@@ -1,0 +1,231 @@
+// loop.cu -- sparse half-step operator for the persistent Sinkhorn loop
+// (north-star item 3).
+//
+// u-half: rows of the CSR sketch against v  (spmv,   proj/src/sparsify.cpp:203-213)
+// v-half: columns of the CSC mirror against u (spmv_t, sparsify.cpp:215-226);
+//         the CSC keeps rows ascending inside each column, i.e. the order
+//         spmv_t accumulates them.
+// log domain: kernel_log_apply(_t) (proj/src/solvers.cpp:96-136).
+//
+// Fast mode: one warp per row/column, coalesced index/value streams, the
+// gathered scaling vector read through L2 (__ldcg: it is rewritten inside
+// the same launch, so the non-coherent path is not allowed), FMA and a
+// shuffle tree. Deterministic (parity) mode: one thread per output summing
+// in index order with contraction-free dadd/dmul, bit-identical to the CPU.
+#include <algorithm>
+#include <cmath>
+
+#include "common.cuh"
+#include "internal.h"
+#include "loop_core.cuh"
+
+namespace spk {
+
+namespace {
+
+using loopcore::finalize_atom;
+
+// Row value of one half: sum_p val[p] * x[idx[p]] over [b, e) (linear), or
+// the log-sum-exp of log(val[p]) + x[idx[p]] skipping x = -inf (log).
+template <bool LOG, bool DET, class VT>
+__device__ __forceinline__ double row_apply(const VT* __restrict__ val, const uint32_t* __restrict__ idx, long long b,
+                                            long long e, const double* x, int lane) {
+  if (!LOG) {
+    if (DET) {  // acc += v * x, j ascending, no FMA (sparsify.cpp:208-209)
+      double acc = 0.0;
+      for (long long p = b; p < e; ++p) acc = dadd(acc, dmul((double)val[p], __ldcg(x + idx[p])));
+      return acc;
+    }
+    double a0 = 0.0, a1 = 0.0;
+    long long p = b + lane;
+    for (; p + 32 < e; p += 64) {
+      const uint32_t c0 = __ldg(idx + p), c1 = __ldg(idx + p + 32);
+      const double w0 = (double)__ldg(val + p), w1 = (double)__ldg(val + p + 32);
+      a0 = fma(w0, __ldcg(x + c0), a0);
+      a1 = fma(w1, __ldcg(x + c1), a1);
+    }
+    if (p < e) a0 = fma((double)__ldg(val + p), __ldcg(x + __ldg(idx + p)), a0);
+    return warp_sum(a0 + a1);
+  } else {
+    if (DET) {  // two passes: max, then the shifted sum (solvers.cpp:99-111)
+      double mx = -CUDART_INF;
+      for (long long p = b; p < e; ++p) {
+        const double xv = __ldcg(x + idx[p]);
+        if (xv == -CUDART_INF) continue;
+        mx = fmax(mx, dadd(log((double)val[p]), xv));
+      }
+      if (mx == -CUDART_INF) return -CUDART_INF;
+      double acc = 0.0;
+      for (long long p = b; p < e; ++p) {
+        const double xv = __ldcg(x + idx[p]);
+        if (xv == -CUDART_INF) continue;
+        acc = dadd(acc, exp(dsub(dadd(log((double)val[p]), xv), mx)));
+      }
+      return dadd(mx, log(acc));
+    }
+    // online (max, scaled sum) per lane, merged across the warp
+    double m = -CUDART_INF, s = 0.0;
+    for (long long p = b + lane; p < e; p += 32) {
+      const double xv = __ldcg(x + __ldg(idx + p));
+      if (xv == -CUDART_INF) continue;
+      const double t = log((double)__ldg(val + p)) + xv;
+      if (t > m) {
+        s = s * exp(m - t) + 1.0;
+        m = t;
+      } else {
+        s += exp(t - m);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const double m2 = __shfl_xor_sync(0xffffffffu, m, o);
+      const double s2 = __shfl_xor_sync(0xffffffffu, s, o);
+      const double M = fmax(m, m2);
+      if (M != -CUDART_INF)
+        s = (m == -CUDART_INF ? 0.0 : s * exp(m - M)) + (m2 == -CUDART_INF ? 0.0 : s2 * exp(m2 - M));
+      m = M;
+    }
+    return m == -CUDART_INF ? -CUDART_INF : m + log(s);
+  }
+}
+
+template <class VT>
+struct SparseOp {
+  int64_t n;
+  const long long* row_ptr;
+  const uint32_t* col_idx;
+  const VT* val;
+  const long long* col_ptr;
+  const uint32_t* row_idx;
+  const VT* val_t;
+
+  template <int ROLE, bool LOG, bool DET>
+  __device__ void half(const double* x, const double* wgt, const double* old, double* out, unsigned char* ne,
+                       int* dyn, double exponent, int policy, int t, unsigned long long* flag, double* absdiff,
+                       double& err, long long& masks) const {
+    const long long* ptr = ROLE == 0 ? row_ptr : col_ptr;
+    const uint32_t* idx = ROLE == 0 ? col_idx : row_idx;
+    const VT* vv = ROLE == 0 ? val : val_t;
+    const int lane = threadIdx.x & 31;
+    if (DET) {
+      const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+      const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+      for (int64_t i = tid; i < n; i += nth) {
+        double d = 0.0;
+        const double o = __ldcg(old + i);
+        if (ne[i]) {
+          const double tmp = row_apply<LOG, true, VT>(vv, idx, ptr[i], ptr[i + 1], x, lane);
+          d = finalize_atom<LOG>(i, tmp, o, wgt[i], exponent, policy, t, ne, dyn, out, flag, masks);
+        } else {
+          out[i] = o;
+        }
+        absdiff[i] = d;
+      }
+    } else {
+      const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+      const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+      for (int64_t i = warp; i < n; i += nw) {
+        if (!ne[i]) {
+          if (lane == 0) out[i] = __ldcg(old + i);
+          continue;
+        }
+        const double tmp = row_apply<LOG, false, VT>(vv, idx, __ldg(ptr + i), __ldg(ptr + i + 1), x, lane);
+        if (lane == 0)
+          err += finalize_atom<LOG>(i, tmp, __ldcg(old + i), __ldg(wgt + i), exponent, policy, t, ne, dyn, out, flag,
+                                    masks);
+      }
+    }
+  }
+};
+
+// kernel_coverage (solvers.cpp:154-163): rows from row_ptr, columns from col_ptr.
+__global__ void coverage_kernel(const long long* row_ptr, const long long* col_ptr, int64_t n, unsigned char* row_ne,
+                                unsigned char* col_ne, unsigned long long* empty) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned char r = row_ptr[i + 1] > row_ptr[i];
+    const unsigned char c = col_ptr[i + 1] > col_ptr[i];
+    row_ne[i] = r;
+    col_ne[i] = c;
+    if (!r) atomicAdd(&empty[0], 1ull);
+    if (!c) atomicAdd(&empty[1], 1ull);
+  }
+}
+
+template <bool LOG, class VT>
+void run_t(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, double exponent, int policy, LoopState& st,
+           LoopOut& out) {
+  const int64_t n = sk->n;
+  DBuf row_ne(n), col_ne(n), empty(16);
+  SPK_CUDA(cudaMemsetAsync(empty.p, 0, 16, ctx->stream));
+  coverage_kernel<<<loopcore::simple_grid(ctx, n), 256, 0, ctx->stream>>>(
+      sk->row_ptr.as<long long>(), sk->col_ptr.as<long long>(), n, row_ne.as<unsigned char>(),
+      col_ne.as<unsigned char>(), empty.as<unsigned long long>());
+  ++ctx->launches;
+  unsigned long long emp[2];
+  download(ctx, emp, empty, sizeof emp);
+  SparseOp<VT> op;
+  op.n = n;
+  op.row_ptr = sk->row_ptr.as<long long>();
+  op.col_idx = sk->col_idx.as<uint32_t>();
+  op.val = sk->values.as<VT>();
+  op.col_ptr = sk->col_ptr.as<long long>();
+  op.row_idx = sk->row_idx.as<uint32_t>();
+  op.val_t = sk->values_t.as<VT>();
+  const int64_t per_block = ctx->deterministic ? loopcore::kBlock : loopcore::kBlock / 32;
+  const int64_t useful = (n + per_block - 1) / per_block;
+  loopcore::run_core<LOG>(ctx, op, n, row_ne, col_ne, (long long)emp[0], (long long)emp[1], cfg, exponent, policy,
+                          st, useful, out);
+}
+
+}  // namespace
+
+namespace {
+
+// spmv (sparsify.cpp:203-213) / spmv_t (:215-226, skipping x_i == 0) with
+// one thread per output summing in index order.
+template <class VT>
+__global__ void product_kernel(int64_t n, const long long* ptr, const uint32_t* idx, const VT* val, const double* x,
+                               double* y, int skip_zero) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (long long p = ptr[i]; p < ptr[i + 1]; ++p) {
+      const double xv = x[idx[p]];
+      if (skip_zero && xv == 0.0) continue;
+      acc = dadd(acc, dmul((double)val[p], xv));
+    }
+    y[i] = acc;
+  }
+}
+
+}  // namespace
+
+void sketch_product(spk_ctx* ctx, spk_sketch* sk, const double* x_host, double* y_host, int transpose) {
+  const int64_t n = sk->n;
+  DBuf x, y(sizeof(double) * n);
+  upload(ctx, x, x_host, sizeof(double) * n);
+  const long long* ptr = transpose ? sk->col_ptr.as<long long>() : sk->row_ptr.as<long long>();
+  const uint32_t* idx = transpose ? sk->row_idx.as<uint32_t>() : sk->col_idx.as<uint32_t>();
+  const int g = loopcore::simple_grid(ctx, n);
+  if (sk->value_type == SPK_VALUES_F32)
+    product_kernel<float><<<g, 256, 0, ctx->stream>>>(n, ptr, idx, (transpose ? sk->values_t : sk->values).as<float>(),
+                                                      x.as<double>(), y.as<double>(), transpose);
+  else
+    product_kernel<double><<<g, 256, 0, ctx->stream>>>(n, ptr, idx, (transpose ? sk->values_t : sk->values).as<double>(),
+                                                       x.as<double>(), y.as<double>(), transpose);
+  ++ctx->launches;
+  download(ctx, y_host, y, sizeof(double) * n);
+}
+
+void run_sparse_loop(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, double exponent, int policy,
+                     LoopState& st, LoopOut& out) {
+  const bool log_domain = cfg.stabilize != 0;
+  if (sk->value_type == SPK_VALUES_F32) {
+    if (log_domain) run_t<true, float>(ctx, sk, cfg, exponent, policy, st, out);
+    else run_t<false, float>(ctx, sk, cfg, exponent, policy, st, out);
+  } else {
+    if (log_domain) run_t<true, double>(ctx, sk, cfg, exponent, policy, st, out);
+    else run_t<false, double>(ctx, sk, cfg, exponent, policy, st, out);
+  }
+}
+
+}  // namespace spk
