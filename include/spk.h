@@ -160,7 +160,14 @@ void* spk_ctx_stream(spk_ctx* ctx);
  * per output summing in the reference's index order with no FMA, and
  * sequential residual sums, so OT scalings and iteration counts are
  * bit-identical to the CPU reference on the same sketch. */
-enum spk_option { SPK_OPT_DETERMINISTIC = 1, SPK_OPT_LOOP_BLOCKS_PER_SM = 2 };
+enum spk_option {
+  SPK_OPT_DETERMINISTIC = 1,
+  SPK_OPT_LOOP_BLOCKS_PER_SM = 2,
+  SPK_OPT_OTF_FP32 = 3,      /* dense on-the-fly comparator: K in fp32 (1) or fp64 (0) */
+  SPK_OPT_BLOCKED_LOOP = 4,  /* fast sparse loop: slab x block layout (1) or CSR/CSC (0) */
+  SPK_OPT_BLOCKED_MAX_W = 5, /* cap on the staged tile width (testing) */
+  SPK_OPT_TWO_PASS_SAMPLER = 6 /* sampler: always the exact two-pass kernels (testing) */
+};
 int spk_ctx_set_option(spk_ctx* ctx, int key, int64_t value);
 /* Status of the last failed call on ctx: category (spk_status), class
  * (spk_error_kind) and message. Returns the category. */
@@ -199,6 +206,11 @@ int spk_sketch_from_csr(spk_ctx* ctx, int64_t n, const int64_t* row_ptr, const u
 void spk_sketch_free(spk_sketch* sk);
 int spk_sketch_info(const spk_sketch* sk, int64_t* n, int64_t* nnz, int64_t* kernel_nnz,
                     int32_t* factorized_plan, double* kernel_mean);
+/* The sampling plan the sketch was drawn from: kind, factorized storage,
+ * grid normaliser 1/total (masked_grid_plan, sparsify.cpp:65-67), UOT kernel
+ * exponent eps/(2 lambda + eps) and theta. */
+int spk_sketch_plan(const spk_sketch* sk, int32_t* plan_kind, int32_t* factorized, double* inv, double* g_k,
+                    double* theta);
 /* Copy CSR (row_ptr n+1, col_idx nnz, values nnz as fp64) / CSC to host. */
 int spk_sketch_copy_csr(spk_sketch* sk, int64_t* row_ptr, uint32_t* col_idx, double* values);
 int spk_sketch_copy_csc(spk_sketch* sk, int64_t* col_ptr, uint32_t* row_idx, double* values);

@@ -21,7 +21,8 @@ PLAN_OT, PLAN_UOT, PLAN_BARYCENTER, PLAN_UNIFORM = 0, 1, 2, 3
 POLICY_ERROR, POLICY_MASK = 0, 1
 PROBS_IMPORTANCE, PROBS_UNIFORM = 0, 1
 VALUES_F64, VALUES_F32 = 0, 1
-OPT_DETERMINISTIC, OPT_LOOP_BLOCKS_PER_SM, OPT_OTF_FP32 = 1, 2, 3
+OPT_DETERMINISTIC, OPT_LOOP_BLOCKS_PER_SM, OPT_OTF_FP32, OPT_BLOCKED_LOOP, OPT_BLOCKED_MAX_W = 1, 2, 3, 4, 5
+OPT_TWO_PASS_SAMPLER = 6
 
 ERROR_CLASSES = {
     1: "Error", 2: "NegativeWeight", 3: "LengthMismatch", 4: "NotNormalized", 5: "AllBlack",
@@ -83,6 +84,7 @@ SIGNATURES = {
     "spk_sketch_from_csr": (C.c_int, [C.c_void_p, C.c_int64, I64P, U32P, DP, C.c_int, C.POINTER(C.c_void_p)]),
     "spk_sketch_free": (None, [C.c_void_p]),
     "spk_sketch_info": (C.c_int, [C.c_void_p, I64P, I64P, I64P, C.POINTER(C.c_int32), DP]),
+    "spk_sketch_plan": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_int32), DP, DP, DP]),
     "spk_sketch_copy_csr": (C.c_int, [C.c_void_p, I64P, U32P, DP]),
     "spk_sketch_copy_csc": (C.c_int, [C.c_void_p, I64P, U32P, DP]),
     "spk_sketch_spmv": (C.c_int, [C.c_void_p, DP, DP, C.c_int]),

@@ -281,6 +281,15 @@ class Sketch:
         except Exception:
             pass
 
+    def plan(self) -> dict:
+        """The sampling plan the sketch was drawn from (kind, factorized, 1/total, g_k, theta)."""
+        kind, fac = C.c_int32(), C.c_int32()
+        inv, gk, th = C.c_double(), C.c_double(), C.c_double()
+        _raise(self.ctx.ptr, self.lib.spk_sketch_plan(self.ptr, C.byref(kind), C.byref(fac), C.byref(inv),
+                                                      C.byref(gk), C.byref(th)))
+        return {"kind": kind.value, "factorized": bool(fac.value), "inv": inv.value, "g_k": gk.value,
+                "theta": th.value}
+
     def csr(self):
         rp = np.empty(self.n + 1, np.int64)
         ci = np.empty(max(self.nnz, 1), np.uint32)

@@ -37,6 +37,30 @@ __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a,
 // pairwise_cost entry (geometry.cpp:16-59) in the reference's operation
 // order with no FMA: sequential d2, then the per-kind transform.
 template <int KIND>
+__device__ __forceinline__ double cost_from_d2(double d2, double eta) {
+  if (KIND == 0) return d2;
+  if (KIND == 1) return sqrt(d2);
+  const double d = sqrt(d2);
+  if (d >= dmul(3.14159265358979323846, eta)) return CUDART_INF;
+  const double cz = cos(d / dmul(2.0, eta));
+  double v = -log(dmul(cz, cz));
+  if (!(v >= 0.0)) v = 0.0;
+  return v;
+}
+
+__device__ __forceinline__ double cost_from_d2_rt(int kind, double d2, double eta) {
+  if (kind == 0) return cost_from_d2<0>(d2, eta);
+  if (kind == 1) return cost_from_d2<1>(d2, eta);
+  return cost_from_d2<2>(d2, eta);
+}
+
+// K = isinf(C) ? 0 : exp(-C/eps) with C = cost(d2)/scale (geometry.cpp:83-102)
+__device__ __forceinline__ double kernel_from_d2(int kind, double d2, double eta, double scale, double eps) {
+  const double c = cost_from_d2_rt(kind, d2, eta) / scale;
+  return isinf(c) ? 0.0 : exp(-c / eps);
+}
+
+template <int KIND>
 __device__ __forceinline__ double cost_entry(const double* __restrict__ p, const double* __restrict__ q,
                                              int dim, double eta) {
   double d2 = 0.0;

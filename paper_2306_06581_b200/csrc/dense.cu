@@ -273,10 +273,13 @@ __global__ void dense_coverage_kernel(KF k, int64_t n, unsigned char* row_ne, un
 template <bool LOG, class KF>
 void run_exact(spk_ctx* ctx, KF kf, int64_t n, const spk_solver_cfg& cfg, double exponent, int policy,
                LoopState& st, LoopOut& out) {
-  DBuf row_ne(n), col_ne(n), empty(16);
+  LoopWs W;
+  W.row_ne.alloc(n);
+  W.col_ne.alloc(n);
+  DBuf empty(16);
   SPK_CUDA(cudaMemsetAsync(empty.p, 0, 16, ctx->stream));
   dense_coverage_kernel<KF><<<(int)std::max<int64_t>(1, std::min<int64_t>((2 * n + 7) / 8, ctx->num_sms * 16)), 256, 0,
-                              ctx->stream>>>(kf, n, row_ne.as<unsigned char>(), col_ne.as<unsigned char>(),
+                              ctx->stream>>>(kf, n, W.row_ne.as<unsigned char>(), W.col_ne.as<unsigned char>(),
                                              empty.as<unsigned long long>());
   ++ctx->launches;
   unsigned long long emp[2];
@@ -285,8 +288,8 @@ void run_exact(spk_ctx* ctx, KF kf, int64_t n, const spk_solver_cfg& cfg, double
   op.k = kf;
   op.n = n;
   const int64_t useful = (n + 15) / 16;
-  loopcore::run_core<LOG>(ctx, op, n, row_ne, col_ne, (long long)emp[0], (long long)emp[1], cfg, exponent, policy, st,
-                          useful, out);
+  loopcore::run_core<LOG>(ctx, op, n, W, (long long)emp[0], (long long)emp[1], cfg, exponent, policy, st, useful,
+                          out);
 }
 
 __global__ void otf_records_kernel(const double* pts, int64_t n, int dim, double alpha, float4* out_rec,
@@ -345,18 +348,21 @@ void run_dense_loop(spk_ctx* ctx, DevKernel& dk, const spk_solver_cfg& cfg, doub
   op.in_rec[1] = xi.as<float4>();
   // coverage: exp2 of finite exponents never reaches 0 for max-normalised
   // costs with 1/eps < 700; otherwise use the exact coverage pass.
-  DBuf row_ne(n), col_ne(n), empty(16);
+  LoopWs W;
+  W.row_ne.alloc(n);
+  W.col_ne.alloc(n);
+  DBuf empty(16);
   SPK_CUDA(cudaMemsetAsync(empty.p, 0, 16, ctx->stream));
   KCoords kf = kcoords_of(dk);
   dense_coverage_kernel<KCoords><<<(int)std::max<int64_t>(1, std::min<int64_t>((2 * n + 7) / 8, ctx->num_sms * 16)),
-                                   256, 0, ctx->stream>>>(kf, n, row_ne.as<unsigned char>(),
-                                                          col_ne.as<unsigned char>(), empty.as<unsigned long long>());
+                                   256, 0, ctx->stream>>>(kf, n, W.row_ne.as<unsigned char>(),
+                                                          W.col_ne.as<unsigned char>(), empty.as<unsigned long long>());
   ++ctx->launches;
   unsigned long long emp[2];
   download(ctx, emp, empty, sizeof emp);
   const int64_t useful = (n + 32 * kOtfRows - 1) / (32 * kOtfRows);
-  loopcore::run_core<false>(ctx, op, n, row_ne, col_ne, (long long)emp[0], (long long)emp[1], cfg, exponent, policy, st,
-                            useful, out);
+  loopcore::run_core<false>(ctx, op, n, W, (long long)emp[0], (long long)emp[1], cfg, exponent, policy, st, useful,
+                            out);
 }
 
 }  // namespace spk

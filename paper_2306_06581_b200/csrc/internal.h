@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -53,6 +54,31 @@ struct DBuf {
   template <class T> T* as() const { return static_cast<T*>(p); }
 };
 
+// Reusable device scratch of one Sinkhorn loop / readout (kept per sketch so
+// repeated solves allocate nothing).
+struct LoopWs {
+  DBuf row_ne, col_ne, dyn_row, dyn_col, u2, v2, la, lb, absdiff, part, flag, status, scalar;
+};
+struct ReadWs {
+  DBuf row_m, col_m, row_c, row_h, terms, flag, tmp, sums, bad;
+};
+
+// Slab x block layout of one half of a sketch (blocked.cu).
+struct BlockedHalf {
+  int P, B, W;
+  int64_t n_out, n_in;
+  const int* slab_row0;    // [P+1] global row starts
+  const int* warp_row0;    // [P*(NW+1)] local row starts per warp
+  const long long* off;    // [P*B*NW + 1] entry offsets of (slab, block, warp)
+  const uint32_t* packed;  // row_local << 16 | col_local
+  const void* val;         // f32 or f64
+};
+struct BlockedHost {
+  BlockedHalf h{};
+  DBuf slab_row0, warp_row0, off, packed, val;
+  int max_rows = 0;
+};
+
 }  // namespace spk
 
 // Device-resident sketch: CSR plus its CSC mirror (rows ascending inside
@@ -73,11 +99,21 @@ struct spk_sketch {
   int64_t kernel_nnz = 0;
   int factorized_plan = 0;
   double kernel_mean = 0.0;
+  int plan_kind = SPK_PLAN_OT;
+  double plan_inv = 1.0, plan_g_k = 0.0, plan_theta = 0.0;  // the sampling plan used
   // state of the last solve (device)
   spk::DBuf u, v, lu, lv;  // f64[n]
   int last_log_domain = 0;
   int last_valid = 0;
   int64_t masked_rows = 0, masked_cols = 0;
+  // structural coverage (kernel_coverage) computed once per sketch
+  spk::DBuf cov_row, cov_col;
+  long long cov_empty_rows = -1, cov_empty_cols = -1;
+  spk::LoopWs ws;
+  spk::ReadWs rws;
+  // fast-path layouts (built lazily by the first fast-mode solve)
+  bool blocked_tried = false;
+  std::unique_ptr<spk::BlockedHost> blk_rows, blk_cols;
 };
 
 struct spk_ctx {
@@ -88,6 +124,9 @@ struct spk_ctx {
   int deterministic = 0;
   int loop_blocks_per_sm = 0;  // 0 = occupancy-derived
   int otf_fp32 = 1;            // dense on-the-fly comparator computes K in fp32
+  int use_blocked = 0;         // fast sparse loop uses the slab x block layout
+  int blocked_max_w = 16384;   // cap on the shared tile width (tests force many blocks)
+  int force_two_pass = 0;      // sampler: skip the single-pass tiled path (testing)
   int64_t launches = 0;
   // last error
   int err_category = 0;
@@ -151,6 +190,10 @@ struct PlanInfo {
   double inv = 1.0;        // grid normaliser 1/total
   double g_k = 0.0;        // UOT kernel exponent
   std::vector<double> row_w, col_w;  // ra/cb, pa/pb, or 1/n
+  // plan-pass outputs kept on the device (grid plans): per-row support size
+  // and unnormalised row mass, used to size the sampler's row slots
+  DBuf d_row_nnz, d_row_sum;
+  bool have_rows = false;
 };
 
 void build_plan(spk_ctx* ctx, DevKernel& dk, const double* a, const double* b, int plan_kind,
@@ -180,6 +223,9 @@ struct LoopState {
 };
 void run_sparse_loop(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, double exponent,
                      int policy, LoopState& st, LoopOut& out);
+void ensure_coverage(spk_ctx* ctx, spk_sketch* sk);
+bool run_blocked(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, double exponent, int policy,
+                 LoopState& st, LoopOut& out);
 void run_dense_loop(spk_ctx* ctx, DevKernel& dk, const spk_solver_cfg& cfg, double exponent,
                     int policy, LoopState& st, LoopOut& out);
 

@@ -155,14 +155,11 @@ template <bool LOG, class VT>
 void run_t(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, double exponent, int policy, LoopState& st,
            LoopOut& out) {
   const int64_t n = sk->n;
-  DBuf row_ne(n), col_ne(n), empty(16);
-  SPK_CUDA(cudaMemsetAsync(empty.p, 0, 16, ctx->stream));
-  coverage_kernel<<<loopcore::simple_grid(ctx, n), 256, 0, ctx->stream>>>(
-      sk->row_ptr.as<long long>(), sk->col_ptr.as<long long>(), n, row_ne.as<unsigned char>(),
-      col_ne.as<unsigned char>(), empty.as<unsigned long long>());
-  ++ctx->launches;
-  unsigned long long emp[2];
-  download(ctx, emp, empty, sizeof emp);
+  LoopWs& W = sk->ws;
+  W.row_ne.ensure(n);
+  W.col_ne.ensure(n);
+  SPK_CUDA(cudaMemcpyAsync(W.row_ne.p, sk->cov_row.p, n, cudaMemcpyDeviceToDevice, ctx->stream));
+  SPK_CUDA(cudaMemcpyAsync(W.col_ne.p, sk->cov_col.p, n, cudaMemcpyDeviceToDevice, ctx->stream));
   SparseOp<VT> op;
   op.n = n;
   op.row_ptr = sk->row_ptr.as<long long>();
@@ -173,8 +170,8 @@ void run_t(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, double expon
   op.val_t = sk->values_t.as<VT>();
   const int64_t per_block = ctx->deterministic ? loopcore::kBlock : loopcore::kBlock / 32;
   const int64_t useful = (n + per_block - 1) / per_block;
-  loopcore::run_core<LOG>(ctx, op, n, row_ne, col_ne, (long long)emp[0], (long long)emp[1], cfg, exponent, policy,
-                          st, useful, out);
+  loopcore::run_core<LOG>(ctx, op, n, W, sk->cov_empty_rows, sk->cov_empty_cols, cfg, exponent, policy, st, useful,
+                          out);
 }
 
 }  // namespace
@@ -216,9 +213,31 @@ void sketch_product(spk_ctx* ctx, spk_sketch* sk, const double* x_host, double* 
   download(ctx, y_host, y, sizeof(double) * n);
 }
 
+// kernel_coverage (solvers.cpp:154-163) of the sketch's structure: once per sketch.
+void ensure_coverage(spk_ctx* ctx, spk_sketch* sk) {
+  if (sk->cov_empty_rows >= 0) return;
+  const int64_t n = sk->n;
+  sk->cov_row.alloc(n);
+  sk->cov_col.alloc(n);
+  DBuf empty(16);
+  SPK_CUDA(cudaMemsetAsync(empty.p, 0, 16, ctx->stream));
+  coverage_kernel<<<loopcore::simple_grid(ctx, n), 256, 0, ctx->stream>>>(
+      sk->row_ptr.as<long long>(), sk->col_ptr.as<long long>(), n, sk->cov_row.as<unsigned char>(),
+      sk->cov_col.as<unsigned char>(), empty.as<unsigned long long>());
+  ++ctx->launches;
+  unsigned long long emp[2];
+  download(ctx, emp, empty, sizeof emp);
+  sk->cov_empty_rows = (long long)emp[0];
+  sk->cov_empty_cols = (long long)emp[1];
+}
+
 void run_sparse_loop(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, double exponent, int policy,
                      LoopState& st, LoopOut& out) {
   const bool log_domain = cfg.stabilize != 0;
+  ensure_coverage(ctx, sk);
+  // fast linear-domain path: slab x block layout with TMA-staged scalings
+  if (!ctx->deterministic && !log_domain && ctx->use_blocked && run_blocked(ctx, sk, cfg, exponent, policy, st, out))
+    return;
   if (sk->value_type == SPK_VALUES_F32) {
     if (log_domain) run_t<true, float>(ctx, sk, cfg, exponent, policy, st, out);
     else run_t<false, float>(ctx, sk, cfg, exponent, policy, st, out);

@@ -337,11 +337,16 @@ inline int simple_grid(spk_ctx* ctx, int64_t n) {
 // Host driver shared by every operator. row_ne / col_ne hold the structural
 // coverage (kernel_coverage, solvers.cpp:138-163); masked_rows/cols their
 // zero counts. Fills st.u/st.v (and st.lu/st.lv in the log domain).
+// exact_grid > 0 demands exactly that many co-resident CTAs (one slab each);
+// dyn_smem is the operator's dynamic shared memory per CTA.
 template <bool LOG, class Op>
-void run_core(spk_ctx* ctx, const Op& op, int64_t n, DBuf& row_ne, DBuf& col_ne, long long masked_rows,
-              long long masked_cols, const spk_solver_cfg& cfg, double exponent, int policy, LoopState& st,
-              int64_t useful_blocks, LoopOut& out) {
+void run_core(spk_ctx* ctx, const Op& op, int64_t n, LoopWs& W, long long masked_rows, long long masked_cols,
+              const spk_solver_cfg& cfg, double exponent, int policy, LoopState& st, int64_t useful_blocks,
+              LoopOut& out, int exact_grid = 0, size_t dyn_smem = 0) {
   cudaStream_t s = ctx->stream;
+  const int64_t npad = (n + 15) & ~int64_t(15);  // 128-byte aligned ping-pong halves (TMA sources)
+  DBuf& row_ne = W.row_ne;
+  DBuf& col_ne = W.col_ne;
   // solvers.hpp:269-274 / :411-414
   if ((masked_rows || masked_cols) && policy == SPK_POLICY_ERROR) {
     if (LOG) fail(SPK_E_ZERO_DENOMINATOR, "kernel has empty rows or columns");
@@ -350,21 +355,28 @@ void run_core(spk_ctx* ctx, const Op& op, int64_t n, DBuf& row_ne, DBuf& col_ne,
   }
   if (masked_rows == n || masked_cols == n) fail(SPK_E_DEGENERATE_SKETCH_ERROR, "kernel has no entries at all");
 
-  DBuf dyn_row(sizeof(int) * n), dyn_col(sizeof(int) * n);
-  DBuf u2(sizeof(double) * 2 * n), v2(sizeof(double) * 2 * n), la, lb, absdiff(sizeof(double) * 2 * n);
-  zero_int_kernel<<<simple_grid(ctx, n), 256, 0, s>>>(dyn_row.as<int>(), n);
-  zero_int_kernel<<<simple_grid(ctx, n), 256, 0, s>>>(dyn_col.as<int>(), n);
-  ctx->launches += 2;
+  W.dyn_row.ensure(sizeof(int) * n);
+  W.dyn_col.ensure(sizeof(int) * n);
+  W.u2.ensure(sizeof(double) * (2 * npad + 16));
+  W.v2.ensure(sizeof(double) * (2 * npad + 16));
+  W.absdiff.ensure(sizeof(double) * 2 * n);
+  DBuf& dyn_row = W.dyn_row;
+  DBuf& dyn_col = W.dyn_col;
+  DBuf& u2 = W.u2;
+  DBuf& v2 = W.v2;
+  DBuf& absdiff = W.absdiff;
+  SPK_CUDA(cudaMemsetAsync(dyn_row.p, 0, sizeof(int) * n, s));
+  SPK_CUDA(cudaMemsetAsync(dyn_col.p, 0, sizeof(int) * n, s));
   const double* wa = st.a;
   const double* wb = st.b;
   if (LOG) {
-    la.alloc(sizeof(double) * n);
-    lb.alloc(sizeof(double) * n);
-    log_weights_kernel<<<simple_grid(ctx, n), 256, 0, s>>>(n, st.a, la.as<double>());
-    log_weights_kernel<<<simple_grid(ctx, n), 256, 0, s>>>(n, st.b, lb.as<double>());
+    W.la.ensure(sizeof(double) * n);
+    W.lb.ensure(sizeof(double) * n);
+    log_weights_kernel<<<simple_grid(ctx, n), 256, 0, s>>>(n, st.a, W.la.as<double>());
+    log_weights_kernel<<<simple_grid(ctx, n), 256, 0, s>>>(n, st.b, W.lb.as<double>());
     ctx->launches += 2;
-    wa = la.as<double>();
-    wb = lb.as<double>();
+    wa = W.la.as<double>();
+    wb = W.lb.as<double>();
   }
   init_scalings_kernel<LOG><<<simple_grid(ctx, n), 256, 0, s>>>(n, row_ne.as<unsigned char>(),
                                                                col_ne.as<unsigned char>(), u2.as<double>(),
@@ -374,13 +386,25 @@ void run_core(spk_ctx* ctx, const Op& op, int64_t n, DBuf& row_ne, DBuf& col_ne,
   // grid: co-resident CTAs (cooperative), no more than useful
   const bool det = ctx->deterministic != 0;
   auto kern = det ? loop_kernel<LOG, true, Op> : loop_kernel<LOG, false, Op>;
+  if (dyn_smem > 0)
+    SPK_CUDA(cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_smem));
   int per_sm = 0;
-  SPK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBlock, 0));
+  SPK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBlock, dyn_smem));
   if (per_sm < 1) fail_device("loop_kernel occupancy", cudaErrorLaunchOutOfResources);
   if (ctx->loop_blocks_per_sm > 0) per_sm = std::min(per_sm, ctx->loop_blocks_per_sm);
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->num_sms * per_sm, useful_blocks));
+  int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->num_sms * per_sm, useful_blocks));
+  if (exact_grid > 0) {
+    if ((int64_t)ctx->num_sms * per_sm < exact_grid)
+      fail_device("loop_kernel: slabs exceed co-resident CTAs", cudaErrorCooperativeLaunchTooLarge);
+    grid = exact_grid;
+  }
 
-  DBuf part(sizeof(Part) * 4 * grid), flag(sizeof(unsigned long long) * 4), status(sizeof(Status));
+  W.part.ensure(sizeof(Part) * 4 * grid);
+  W.flag.ensure(sizeof(unsigned long long) * 4);
+  W.status.ensure(sizeof(Status));
+  DBuf& part = W.part;
+  DBuf& flag = W.flag;
+  DBuf& status = W.status;
   fill_u64_kernel<<<1, 32, 0, s>>>(flag.as<unsigned long long>(), 4, kNone);
   ++ctx->launches;
   SPK_CUDA(cudaMemsetAsync(status.p, 0, sizeof(Status), s));
@@ -390,9 +414,9 @@ void run_core(spk_ctx* ctx, const Op& op, int64_t n, DBuf& row_ne, DBuf& col_ne,
   P.wa = wa;
   P.wb = wb;
   P.u0 = u2.as<double>();
-  P.u1 = u2.as<double>() + n;
+  P.u1 = u2.as<double>() + npad;
   P.v0 = v2.as<double>();
-  P.v1 = v2.as<double>() + n;
+  P.v1 = v2.as<double>() + npad;
   P.row_ne = row_ne.as<unsigned char>();
   P.col_ne = col_ne.as<unsigned char>();
   P.dyn_row = dyn_row.as<int>();
@@ -411,7 +435,7 @@ void run_core(spk_ctx* ctx, const Op& op, int64_t n, DBuf& row_ne, DBuf& col_ne,
   Op op_copy = op;
   void* args[] = {&P, &op_copy};
   Timer tm(s);
-  SPK_CUDA(cudaLaunchCooperativeKernel((void*)kern, dim3(grid), dim3(kBlock), args, 0, s));
+  SPK_CUDA(cudaLaunchCooperativeKernel((void*)kern, dim3(grid), dim3(kBlock), args, dyn_smem, s));
   ++ctx->launches;
   out.loop_s = tm.stop();
   SPK_CUDA(cudaGetLastError());
@@ -452,8 +476,8 @@ void run_core(spk_ctx* ctx, const Op& op, int64_t n, DBuf& row_ne, DBuf& col_ne,
     out.masked_rows = S.masked_rows;
     out.masked_cols = S.masked_cols;
   }
-  const double* uf = u2.as<double>() + (size_t)S.cur * n;
-  const double* vf = v2.as<double>() + (size_t)S.cur * n;
+  const double* uf = u2.as<double>() + (size_t)S.cur * npad;
+  const double* vf = v2.as<double>() + (size_t)S.cur * npad;
   st.u->ensure(sizeof(double) * n);
   st.v->ensure(sizeof(double) * n);
   if (LOG) {

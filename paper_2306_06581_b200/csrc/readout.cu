@@ -188,9 +188,14 @@ double sum_array(spk_ctx* ctx, const double* v, int64_t n, DBuf& tmp) {
 }
 
 // Marginal residuals + KL + objective assembly from device marginals.
-void finish(spk_ctx* ctx, int64_t n, const double* row_m, const double* col_m, const double* a, const double* b,
-            bool want_obj, int uot, double lambda, double eps, double cost, double entropy, ReadoutOut& out) {
-  DBuf terms(sizeof(double) * n), tmp, bad(sizeof(unsigned long long));
+void finish(spk_ctx* ctx, ReadWs& R, int64_t n, const double* row_m, const double* col_m, const double* a,
+            const double* b, bool want_obj, int uot, double lambda, double eps, double cost, double entropy,
+            ReadoutOut& out) {
+  R.terms.ensure(sizeof(double) * n);
+  R.bad.ensure(sizeof(unsigned long long));
+  DBuf& terms = R.terms;
+  DBuf& tmp = R.tmp;
+  DBuf& bad = R.bad;
   const int g = elem_grid(ctx, n);
   terms_kernel<<<g, 256, 0, ctx->stream>>>(n, row_m, a, 0, terms.as<double>(), nullptr);
   ++ctx->launches;
@@ -226,14 +231,22 @@ void sparse_readout_t(spk_ctx* ctx, spk_sketch* sk, DevKernel* dk, const double*
                       double* row_m_host, double* col_m_host, ReadoutOut& out) {
   const int64_t n = sk->n;
   cudaStream_t s = ctx->stream;
-  DBuf row_m(sizeof(double) * n), col_m(sizeof(double) * n), flag(sizeof(unsigned long long)), tmp;
+  ReadWs& R = sk->rws;
+  R.row_m.ensure(sizeof(double) * n);
+  R.col_m.ensure(sizeof(double) * n);
+  R.flag.ensure(sizeof(unsigned long long));
+  R.sums.ensure(2 * sizeof(double));
+  DBuf& row_m = R.row_m;
+  DBuf& col_m = R.col_m;
+  DBuf& flag = R.flag;
+  DBuf& tmp = R.tmp;
   fill_u64<<<1, 1, 0, s>>>(flag.as<unsigned long long>(), ~0ull);
   ++ctx->launches;
   const CostSrc cs = cost_src_of(dk);
   const bool obj = want_obj && dk && dk->have_cost;
   double cost = 0.0, entropy = 0.0;
   if (ctx->deterministic) {
-    DBuf sums(2 * sizeof(double));
+    DBuf& sums = R.sums;
     if (obj)
       row_seq_kernel<LOG, true, VT><<<1, 1, 0, s>>>(n, sk->row_ptr.as<long long>(), sk->col_idx.as<uint32_t>(),
                                                      sk->values.as<VT>(), u, v, cs, row_m.as<double>(),
@@ -250,7 +263,10 @@ void sparse_readout_t(spk_ctx* ctx, spk_sketch* sk, DevKernel* dk, const double*
     cost = hs[0];
     entropy = hs[1];
   } else {
-    DBuf row_c(sizeof(double) * n), row_h(sizeof(double) * n);
+    R.row_c.ensure(sizeof(double) * n);
+    R.row_h.ensure(sizeof(double) * n);
+    DBuf& row_c = R.row_c;
+    DBuf& row_h = R.row_h;
     if (obj)
       row_pass_kernel<LOG, true, VT><<<rows_grid(ctx, n), 256, 0, s>>>(
           n, sk->row_ptr.as<long long>(), sk->col_idx.as<uint32_t>(), sk->values.as<VT>(), u, v, cs,
@@ -272,7 +288,7 @@ void sparse_readout_t(spk_ctx* ctx, spk_sketch* sk, DevKernel* dk, const double*
     download(ctx, &f, flag, sizeof f);
     if (f != ~0ull) fail(SPK_E_INFINITE_COST_ON_SUPPORT, "plan mass on a blocked entry");
   }
-  finish(ctx, n, row_m.as<double>(), col_m.as<double>(), a, b, obj, uot, lambda, eps, cost, entropy, out);
+  finish(ctx, R, n, row_m.as<double>(), col_m.as<double>(), a, b, obj, uot, lambda, eps, cost, entropy, out);
   if (row_m_host) download(ctx, row_m_host, row_m, sizeof(double) * n);
   if (col_m_host) download(ctx, col_m_host, col_m, sizeof(double) * n);
 }
@@ -428,7 +444,8 @@ void dense_readout_t(spk_ctx* ctx, KF kf, DevKernel& dk, const double* u, const 
     download(ctx, &f, flag, sizeof f);
     if (f != ~0ull) fail(SPK_E_INFINITE_COST_ON_SUPPORT, "plan mass on a blocked entry");
   }
-  finish(ctx, n, row_m.as<double>(), col_m.as<double>(), a, b, obj, uot, lambda, eps, cost, entropy, out);
+  ReadWs R;
+  finish(ctx, R, n, row_m.as<double>(), col_m.as<double>(), a, b, obj, uot, lambda, eps, cost, entropy, out);
 }
 
 }  // namespace

@@ -309,6 +309,279 @@ int grid_for(spk_ctx* ctx, int64_t items, int threads) {
   return (int)std::max<int64_t>(1, std::min(need, cap));
 }
 
+// ==== tiled coordinate sampler (v2) ================================================
+//
+// One CTA = 8 warps x 4 rows; the CTA walks all columns in tiles of 256 points
+// staged in shared memory (SoA, conflict-free), each warp handles 32 columns
+// x its 4 rows per step, so every y_j is read from L2 once per 32 rows.
+// Support test: K_ij != 0  <=>  d2_ij < D0, where D0 is found once by a
+// device bisection of the exact kernel_from_cost arithmetic (monotone in d2);
+// entries within a 1e-12 relative band of D0 take the exact path. The exact
+// K (two IEEE divisions + exp) is then only computed for kept entries (and
+// for UOT, whose plan needs K^g_k). Kept entries go straight into per-row
+// slots sized from the plan pass (upper bound of the expected count + 6
+// sigma), so sampling is a single pass; any slot overflow falls back to the
+// exact two-pass kernels above.
+
+constexpr int kTileJ = 256;
+constexpr int kRPW = 4;  // rows per warp
+constexpr int kTileRows = 8 * kRPW;
+
+struct TiledArgs {
+  const double* x;
+  const double* y;
+  int64_t n;
+  int dim, kind;
+  double eta, scale, eps;
+  double lo, hi;  // d2 < lo: supported; d2 >= hi: not; else exact
+  DPlan P;
+  double s;
+  uint64_t seed;
+  // plan mode
+  long long* row_nnz;
+  double* row_sum;
+  // sample mode
+  const long long* slot_off;
+  const int* slot_cap;
+  uint32_t* pool_col;
+  void* pool_val;
+  int* row_cnt;
+  unsigned int* overflow;
+};
+
+__device__ __forceinline__ double exact_k(const TiledArgs& A, double d2) {
+  return kernel_from_d2(A.kind, d2, A.eta, A.scale, A.eps);
+}
+
+template <int DIM, bool SAMPLE, bool NEEDK, class VT>
+__global__ void __launch_bounds__(256) tiled_kernel(TiledArgs A) {
+  __shared__ double ys[DIM][kTileJ];
+  const int lane = threadIdx.x & 31;
+  const int w = threadIdx.x >> 5;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  const int64_t groups = (A.n + kTileRows - 1) / kTileRows;
+  for (int64_t g = blockIdx.x; g < groups; g += gridDim.x) {
+    double xr[kRPW][DIM];
+    uint64_t st0[kRPW];
+    uint32_t tcnt[kRPW], cnt[kRPW];
+    double racc[kRPW];
+    int64_t row[kRPW];
+    long long base[kRPW];
+    int cap[kRPW];
+#pragma unroll
+    for (int q = 0; q < kRPW; ++q) {
+      row[q] = g * kTileRows + w * kRPW + q;
+      const bool valid = row[q] < A.n;
+#pragma unroll
+      for (int k = 0; k < DIM; ++k) xr[q][k] = valid ? A.x[row[q] * DIM + k] : 0.0;
+      st0[q] = mix_seed(A.seed, (uint64_t)row[q]);
+      tcnt[q] = 0;
+      cnt[q] = 0;
+      racc[q] = 0.0;
+      base[q] = (SAMPLE && valid) ? A.slot_off[row[q]] : 0;
+      cap[q] = (SAMPLE && valid) ? A.slot_cap[row[q]] : 0;
+    }
+    for (int64_t j0 = 0; j0 < A.n; j0 += kTileJ) {
+      __syncthreads();
+      for (int e = threadIdx.x; e < kTileJ * DIM; e += blockDim.x) {
+        const int jj = e / DIM, k = e - jj * DIM;
+        const int64_t j = j0 + jj;
+        ys[k][jj] = j < A.n ? A.y[j * DIM + k] : 0.0;
+      }
+      __syncthreads();
+      const int jend = (int)min((int64_t)kTileJ, A.n - j0);
+      for (int c = 0; c < jend; c += 32) {
+        const int jj = c + lane;
+        const bool jvalid = jj < jend;
+        const int64_t j = j0 + jj;
+        double yv[DIM];
+#pragma unroll
+        for (int k = 0; k < DIM; ++k) yv[k] = ys[k][jj & (kTileJ - 1)];
+        const double cw = jvalid ? A.P.col_w[j] : 0.0;
+#pragma unroll
+        for (int q = 0; q < kRPW; ++q) {
+          const bool valid = jvalid && row[q] < A.n;
+          double d2 = 0.0;
+#pragma unroll
+          for (int k = 0; k < DIM; ++k) {
+            const double diff = dsub(xr[q][k], yv[k]);
+            d2 = dadd(d2, dmul(diff, diff));
+          }
+          double kv = -1.0;  // not computed
+          bool nz;
+          if (NEEDK || !(d2 < A.lo || d2 >= A.hi)) {
+            kv = exact_k(A, d2);
+            nz = valid && kv != 0.0;
+          } else {
+            nz = valid && d2 < A.lo;
+          }
+          if (!SAMPLE) {
+            if (nz) {
+              ++cnt[q];
+              const double rw = A.P.row_w[row[q]];
+              racc[q] += (A.P.kind == SPK_PLAN_UOT) ? dmul(dmul(rw, cw), pow(kv, A.P.g_k))
+                         : (A.P.kind == SPK_PLAN_UNIFORM) ? 1.0 : dmul(rw, cw);
+            }
+            continue;
+          }
+          const unsigned m = __ballot_sync(0xffffffffu, nz);
+          const uint32_t t = tcnt[q] + (uint32_t)__popc(m & lt_mask) + 1u;
+          tcnt[q] += (uint32_t)__popc(m);
+          bool keep = false;
+          double ps = 0.0;
+          if (nz) {
+            const double rw = A.P.row_w[row[q]];
+            double base_p;
+            if (A.P.factorized) base_p = dmul(rw, cw);
+            else {
+              const double gr = (A.P.kind == SPK_PLAN_UOT) ? dmul(dmul(rw, cw), pow(kv, A.P.g_k))
+                                : (A.P.kind == SPK_PLAN_UNIFORM) ? 1.0 : dmul(rw, cw);
+              base_p = dmul(gr, A.P.inv);
+            }
+            if (A.P.theta_mode == 1) base_p = base_p == 0.0 ? 0.0 : dadd(dmul(A.P.omt, base_p), A.P.unif);
+            else if (A.P.theta_mode == 2) base_p = base_p > 0.0 ? dadd(dmul(A.P.omt, base_p), A.P.unif) : base_p;
+            ps = min1(dmul(A.s, base_p));
+            if (ps > 0.0) {
+              if (ps >= 1.0) keep = true;
+              else keep = u64_to_unit(sm_finalize(st0[q] + (uint64_t)t * kGolden)) < ps;
+            }
+          }
+          const unsigned km = __ballot_sync(0xffffffffu, keep);
+          if (keep) {
+            const uint32_t pos = cnt[q] + (uint32_t)__popc(km & lt_mask);
+            if (pos < (uint32_t)cap[q]) {
+              if (kv < 0.0) kv = exact_k(A, d2);
+              A.pool_col[base[q] + pos] = (uint32_t)j;
+              static_cast<VT*>(A.pool_val)[base[q] + pos] = (VT)(ps >= 1.0 ? kv : kv / ps);
+            }
+          }
+          cnt[q] += (uint32_t)__popc(km);
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < kRPW; ++q) {
+      if (row[q] >= A.n) continue;
+      if (!SAMPLE) {
+        const long long c = warp_sum_ll((long long)cnt[q]);
+        const double sacc = warp_sum(racc[q]);
+        if (lane == 0) {
+          A.row_nnz[row[q]] = c;
+          A.row_sum[row[q]] = sacc;
+        }
+      } else if (lane == 0) {
+        A.row_cnt[row[q]] = (int)cnt[q];
+        if ((int)cnt[q] > cap[q]) atomicExch(A.overflow, 1u);
+      }
+    }
+  }
+}
+
+// smallest d2 with exact_k(d2) == 0 (bisection on the IEEE bit pattern)
+__global__ void threshold_kernel(TiledArgs A, double* out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  long long lo = 0;                                          // bits of +0.0
+  long long hi = __double_as_longlong(CUDART_INF);           // K(inf) == 0
+  if (exact_k(A, 0.0) == 0.0) {
+    *out = 0.0;
+    return;
+  }
+  while (hi - lo > 1) {
+    const long long mid = lo + (hi - lo) / 2;
+    if (exact_k(A, __longlong_as_double(mid)) > 0.0) lo = mid;
+    else hi = mid;
+  }
+  *out = __longlong_as_double(hi);
+}
+
+// Upper bound of each row's expected kept count -> slot capacity
+// (count is a sum of independent Bernoullis with mean <= U: cap U + 6 sqrt(U) + 16).
+__global__ void slot_cap_kernel(int64_t n, const long long* row_nnz, const double* row_sum, const double* row_w,
+                                double col_w_total, int factorized, double inv, double s, int theta_mode, double omt,
+                                double unif, int* cap) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double supp = row_nnz ? (double)row_nnz[i] : (double)n;
+    double mass = factorized ? row_w[i] * col_w_total : row_sum[i] * inv;
+    if (theta_mode) mass = omt * mass + unif * supp;
+    const double u = fmin(supp, s * mass * (1.0 + 1e-9));
+    const double c = fmin(supp, ceil(u + 6.0 * sqrt(u) + 16.0));
+    cap[i] = (int)c;
+  }
+}
+
+__global__ void compact_kernel(int64_t n, const long long* slot_off, const long long* row_ptr, const uint32_t* pool_col,
+                               const unsigned char* pool_val, int vbytes, uint32_t* col, unsigned char* val) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = warp; i < n; i += nw) {
+    const long long src = slot_off[i], dst = row_ptr[i], m = row_ptr[i + 1] - row_ptr[i];
+    for (long long k = lane; k < m; k += 32) {
+      col[dst + k] = pool_col[src + k];
+      if (vbytes == 4)
+        reinterpret_cast<float*>(val)[dst + k] = reinterpret_cast<const float*>(pool_val)[src + k];
+      else
+        reinterpret_cast<double*>(val)[dst + k] = reinterpret_cast<const double*>(pool_val)[src + k];
+    }
+  }
+}
+
+__global__ void int_to_ll_kernel(const int* a, int64_t n, long long* b) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    b[i] = a[i];
+}
+
+template <bool SAMPLE, bool NEEDK, class VT>
+void launch_tiled(spk_ctx* ctx, const TiledArgs& A) {
+  const int64_t groups = (A.n + kTileRows - 1) / kTileRows;
+#define SPK_TILED_CASE(D)                                                                                    \
+  case D: {                                                                                                  \
+    int occ = 0;                                                                                             \
+    SPK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, tiled_kernel<D, SAMPLE, NEEDK, VT>, 256, 0)); \
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(groups, (int64_t)ctx->num_sms * std::max(occ, 1))); \
+    tiled_kernel<D, SAMPLE, NEEDK, VT><<<grid, 256, 0, ctx->stream>>>(A);                                    \
+    break;                                                                                                   \
+  }
+  switch (A.dim) {
+    SPK_TILED_CASE(1)
+    SPK_TILED_CASE(2)
+    SPK_TILED_CASE(3)
+    SPK_TILED_CASE(4)
+    SPK_TILED_CASE(5)
+    SPK_TILED_CASE(6)
+    SPK_TILED_CASE(8)
+    SPK_TILED_CASE(10)
+    default:
+      fail(SPK_E_DIMENSION_MISMATCH, "tiled sampler: unsupported dimension");
+  }
+#undef SPK_TILED_CASE
+  ++ctx->launches;
+  SPK_CUDA(cudaGetLastError());
+}
+
+bool tiled_dim_ok(int dim) { return dim == 1 || dim == 2 || dim == 3 || dim == 4 || dim == 5 || dim == 6 || dim == 8 || dim == 10; }
+
+TiledArgs tiled_args(spk_ctx* ctx, const DevKernel& dk) {
+  TiledArgs A{};
+  A.x = dk.x.as<double>();
+  A.y = dk.y.as<double>();
+  A.n = dk.n;
+  A.dim = dk.dim;
+  A.kind = dk.kind;
+  A.eta = dk.eta;
+  A.scale = dk.scale;
+  A.eps = dk.eps;
+  DBuf d0(sizeof(double));
+  threshold_kernel<<<1, 32, 0, ctx->stream>>>(A, d0.as<double>());
+  ++ctx->launches;
+  double D0 = 0.0;
+  download(ctx, &D0, d0, sizeof D0);
+  // exact-path band around the threshold (absorbs any non-monotone ULP effects)
+  A.lo = D0 * (1.0 - 1e-12);
+  A.hi = std::isinf(D0) ? D0 : D0 * (1.0 + 1e-12);
+  return A;
+}
+
 }  // namespace
 
 // ---- host orchestration ----------------------------------------------------------
@@ -421,13 +694,28 @@ void build_plan(spk_ctx* ctx, DevKernel& dk, const double* a, const double* b, i
     P.col_w = cw.as<double>();
     P.kind = plan_kind;
     P.g_k = plan.g_k;
-    DBuf rn(sizeof(long long) * n), rs(sizeof(double) * n), tot(sizeof(double)), tn(sizeof(long long));
-    KSrc S = make_src(dk);
-    plan_rows_kernel<<<grid_for_rows(ctx, n, 8), 256, 0, ctx->stream>>>(S, P, rn.as<long long>(),
-                                                                         rs.as<double>());
+    plan.d_row_nnz.alloc(sizeof(long long) * n);
+    plan.d_row_sum.alloc(sizeof(double) * n);
+    plan.have_rows = true;
+    DBuf& rn = plan.d_row_nnz;
+    DBuf& rs = plan.d_row_sum;
+    DBuf tot(sizeof(double)), tn(sizeof(long long));
+    if (!dk.dense && tiled_dim_ok(dk.dim)) {
+      TiledArgs A = tiled_args(ctx, dk);
+      A.P = P;
+      A.row_nnz = rn.as<long long>();
+      A.row_sum = rs.as<double>();
+      if (plan_kind == SPK_PLAN_UOT) launch_tiled<false, true, double>(ctx, A);
+      else launch_tiled<false, false, double>(ctx, A);
+    } else {
+      KSrc S = make_src(dk);
+      plan_rows_kernel<<<grid_for_rows(ctx, n, 8), 256, 0, ctx->stream>>>(S, P, rn.as<long long>(),
+                                                                           rs.as<double>());
+      ++ctx->launches;
+    }
     reduce_rows_kernel<double><<<1, 1024, 0, ctx->stream>>>(rs.as<double>(), n, tot.as<double>());
     reduce_rows_kernel<long long><<<1, 1024, 0, ctx->stream>>>(rn.as<long long>(), n, tn.as<long long>());
-    ctx->launches += 3;
+    ctx->launches += 2;
     SPK_CUDA(cudaMemcpyAsync(&total, tot.p, sizeof total, cudaMemcpyDeviceToHost, ctx->stream));
     SPK_CUDA(cudaMemcpyAsync(&support, tn.p, sizeof support, cudaMemcpyDeviceToHost, ctx->stream));
     SPK_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -519,7 +807,83 @@ void sample_sketch(spk_ctx* ctx, DevKernel& dk, const PlanInfo& plan, double s, 
   sk->value_type = value_type;
   sk->kernel_nnz = plan.kernel_nnz;
   sk->factorized_plan = plan.factorized ? 1 : 0;
+  sk->plan_kind = plan.kind;
+  sk->plan_inv = plan.inv;
+  sk->plan_g_k = plan.g_k;
+  sk->plan_theta = plan.theta;
   sk->row_ptr.alloc(sizeof(long long) * (n + 1));
+  const size_t vbytes = value_type == SPK_VALUES_F32 ? 4 : 8;
+
+  if (!dk.dense && tiled_dim_ok(dk.dim) && (plan.factorized || plan.have_rows) && !ctx->force_two_pass) {
+    // ---- single pass: row slots sized from the plan's row masses ----
+    DBuf cap(sizeof(int) * n), capll(sizeof(long long) * n), off(sizeof(long long) * (n + 1));
+    double col_total = 0.0;
+    for (int64_t j = 0; j < n; ++j) col_total += plan.col_w[j];
+    slot_cap_kernel<<<grid_for(ctx, n, 256), 256, 0, ctx->stream>>>(
+        n, plan.have_rows ? plan.d_row_nnz.as<long long>() : nullptr,
+        plan.have_rows ? plan.d_row_sum.as<double>() : nullptr, rw.as<double>(), col_total,
+        plan.factorized ? 1 : 0, plan.inv, s, P.theta_mode, P.omt, P.unif, cap.as<int>());
+    int_to_ll_kernel<<<grid_for(ctx, n, 256), 256, 0, ctx->stream>>>(cap.as<int>(), n, capll.as<long long>());
+    ctx->launches += 2;
+    SPK_CUDA(cudaMemsetAsync(off.p, 0, sizeof(long long), ctx->stream));
+    size_t tb = 0;
+    SPK_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb, capll.as<long long>(), off.as<long long>() + 1, (int)n,
+                                           ctx->stream));
+    ctx->scratch.ensure(tb);
+    SPK_CUDA(cub::DeviceScan::InclusiveSum(ctx->scratch.p, tb, capll.as<long long>(), off.as<long long>() + 1, (int)n,
+                                           ctx->stream));
+    long long pool = 0;
+    SPK_CUDA(cudaMemcpyAsync(&pool, off.as<long long>() + n, sizeof pool, cudaMemcpyDeviceToHost, ctx->stream));
+    SPK_CUDA(cudaStreamSynchronize(ctx->stream));
+    DBuf pcol(sizeof(uint32_t) * std::max<long long>(pool, 1)), pval(vbytes * std::max<long long>(pool, 1));
+    DBuf rcnt(sizeof(int) * n), ovf(sizeof(unsigned int));
+    SPK_CUDA(cudaMemsetAsync(ovf.p, 0, sizeof(unsigned int), ctx->stream));
+    TiledArgs A = tiled_args(ctx, dk);
+    A.P = P;
+    A.s = s;
+    A.seed = seed;
+    A.slot_off = off.as<long long>();
+    A.slot_cap = cap.as<int>();
+    A.pool_col = pcol.as<uint32_t>();
+    A.pool_val = pval.p;
+    A.row_cnt = rcnt.as<int>();
+    A.overflow = ovf.as<unsigned int>();
+    const bool uotk = plan.kind == SPK_PLAN_UOT;
+    if (value_type == SPK_VALUES_F32) {
+      if (uotk) launch_tiled<true, true, float>(ctx, A);
+      else launch_tiled<true, false, float>(ctx, A);
+    } else {
+      if (uotk) launch_tiled<true, true, double>(ctx, A);
+      else launch_tiled<true, false, double>(ctx, A);
+    }
+    unsigned int overflow = 0;
+    download(ctx, &overflow, ovf, sizeof overflow);
+    if (!overflow) {
+      int_to_ll_kernel<<<grid_for(ctx, n, 256), 256, 0, ctx->stream>>>(rcnt.as<int>(), n, capll.as<long long>());
+      ++ctx->launches;
+      SPK_CUDA(cudaMemsetAsync(sk->row_ptr.p, 0, sizeof(long long), ctx->stream));
+      SPK_CUDA(cub::DeviceScan::InclusiveSum(ctx->scratch.p, tb, capll.as<long long>(), sk->row_ptr.as<long long>() + 1,
+                                             (int)n, ctx->stream));
+      long long nnz = 0;
+      SPK_CUDA(cudaMemcpyAsync(&nnz, sk->row_ptr.as<long long>() + n, sizeof nnz, cudaMemcpyDeviceToHost,
+                               ctx->stream));
+      SPK_CUDA(cudaStreamSynchronize(ctx->stream));
+      if (nnz > 0xffffffffLL) fail(SPK_E_BUDGET_TOO_LARGE, "sketch exceeds 2^32 entries");
+      sk->nnz = nnz;
+      sk->col_idx.alloc(sizeof(uint32_t) * std::max<long long>(nnz, 1));
+      sk->values.alloc(vbytes * std::max<long long>(nnz, 1));
+      compact_kernel<<<grid_for_rows(ctx, n, 8), 256, 0, ctx->stream>>>(
+          n, off.as<long long>(), sk->row_ptr.as<long long>(), pcol.as<uint32_t>(), pval.as<unsigned char>(),
+          (int)vbytes, sk->col_idx.as<uint32_t>(), sk->values.as<unsigned char>());
+      ++ctx->launches;
+      SPK_CUDA(cudaGetLastError());
+      build_csc(ctx, sk);
+      sk->kernel_mean = sketch_kernel_mean(ctx, sk);
+      return;
+    }
+    // a row outgrew its slot: redo exactly with the two-pass kernels below
+  }
+
   DBuf cnt(sizeof(long long) * n);
   const int grid = grid_for_rows(ctx, n, 8);
   sample_rows_kernel<false, double><<<grid, 256, 0, ctx->stream>>>(S, P, s, seed, cnt.as<long long>(),
@@ -540,7 +904,6 @@ void sample_sketch(spk_ctx* ctx, DevKernel& dk, const PlanInfo& plan, double s, 
   SPK_CUDA(cudaStreamSynchronize(ctx->stream));
   if (nnz > 0xffffffffLL) fail(SPK_E_BUDGET_TOO_LARGE, "sketch exceeds 2^32 entries");
   sk->nnz = nnz;
-  const size_t vbytes = value_type == SPK_VALUES_F32 ? 4 : 8;
   sk->col_idx.alloc(sizeof(uint32_t) * std::max<long long>(nnz, 1));
   sk->values.alloc(vbytes * std::max<long long>(nnz, 1));
   if (value_type == SPK_VALUES_F32)

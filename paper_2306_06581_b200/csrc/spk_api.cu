@@ -290,6 +290,9 @@ int spk_ctx_set_option(spk_ctx* ctx, int key, int64_t value) {
     case SPK_OPT_DETERMINISTIC: ctx->deterministic = value ? 1 : 0; return SPK_OK;
     case SPK_OPT_LOOP_BLOCKS_PER_SM: ctx->loop_blocks_per_sm = (int)value; return SPK_OK;
     case 3: ctx->otf_fp32 = value ? 1 : 0; return SPK_OK;
+    case 4: ctx->use_blocked = value ? 1 : 0; return SPK_OK;
+    case 5: ctx->blocked_max_w = (int)std::max<int64_t>(16, std::min<int64_t>(value, 16384)); return SPK_OK;
+    case 6: ctx->force_two_pass = value ? 1 : 0; return SPK_OK;
     default: return SPK_STATUS_INPUT;
   }
 }
@@ -466,6 +469,17 @@ int spk_sketch_info(const spk_sketch* sk, int64_t* n, int64_t* nnz, int64_t* ker
   if (kernel_nnz) *kernel_nnz = sk->kernel_nnz;
   if (factorized_plan) *factorized_plan = sk->factorized_plan;
   if (kernel_mean) *kernel_mean = sk->kernel_mean;
+  return SPK_OK;
+}
+
+int spk_sketch_plan(const spk_sketch* sk, int32_t* plan_kind, int32_t* factorized, double* inv, double* g_k,
+                    double* theta) {
+  if (!sk) return SPK_STATUS_INPUT;
+  if (plan_kind) *plan_kind = sk->plan_kind;
+  if (factorized) *factorized = sk->factorized_plan;
+  if (inv) *inv = sk->plan_inv;
+  if (g_k) *g_k = sk->plan_g_k;
+  if (theta) *theta = sk->plan_theta;
   return SPK_OK;
 }
 
