@@ -1,33 +1,37 @@
 // blocked.cu -- the fast sparse half-step: slab x block sketch layout with the
-// scaling vector staged in shared memory by TMA bulk copies (north-star item 3:
-// "shared-memory/TMA staging of the gathered scaling vector").
+// scaling vector AND the entry stream staged in shared memory by a multi-stage
+// TMA pipeline (north-star item 3: "shared-memory/TMA staging of the gathered
+// scaling vector").
 //
 // Why: at config 4 (n = 1e6, 1.1e8 entries, columns uniformly random) every
-// gathered x[j] of the CSR kernel is a random 8-byte read, i.e. one 32-byte
-// L2 sector per entry: 3.5 GB of L2->SM sectors per half, twice the sketch
-// stream itself, and the measured bound of the plain kernel.
+// gathered x[j] of the CSR kernel is a random 8-byte read, i.e. one 32-byte L2
+// sector per entry: 3.5 GB of L2->SM sectors per half on top of the 0.9 GB
+// entry stream (profiles/r1_c4_csr_loop_ncu.json: 9.5 GB L2 reads/iteration).
 //
 // Layout (built once per sketch, for the CSR and for the CSC mirror):
-//   output atoms (rows of this half) are cut into P slabs of ~equal entry
-//   count, one per persistent CTA, and each slab into NW warp ranges;
-//   input atoms (columns) are cut into B blocks of W (<= 16384) atoms.
-//   Entries are ordered (slab, block, warp, row, col) -- inside one row the
-//   columns still ascend, so every row is summed in the reference's j order
-//   (spmv, proj/src/sparsify.cpp:203-213; spmv_t :215-226 for the CSC).
-//   An entry is 8 bytes: packed (row_local << 16 | col_local) + fp32 value
-//   (12 bytes with fp64 values) -- no more than the CSR.
-// Kernel (inside the persistent loop, loop_core.cuh): for each block the CTA
-// TMA-copies x[block] (W doubles) into a double-buffered shared tile, warps
-// stream their (slab, block, warp) entries with coalesced loads, gather x from
+//   output atoms (this half's rows) are cut into P = #SMs slabs of ~equal
+//   entry count, one per persistent CTA, each slab into 16 warp ranges;
+//   input atoms (columns) are cut into B blocks of W atoms. Entries are
+//   ordered (slab, block, warp, row, col) -- inside a row the columns still
+//   ascend, so every row is summed in the reference's j order (spmv,
+//   proj/src/sparsify.cpp:203-213; spmv_t :215-226 on the CSC) -- and each
+//   (slab, block) segment is padded to 16 bytes so it is one bulk copy. An
+//   entry is packed (row_local << 16 | col_local) + value: no more bytes than
+//   the CSR entry it replaces.
+// Pipeline (inside the persistent loop, loop_core.cuh): S stages, each = the
+// x tile of a block (W doubles) + that block's entry segment; thread 0 issues
+// cp.async.bulk (TMA) copies for block b+S as soon as all 16 warps released
+// stage b (empty mbarrier), warps wait on the full mbarrier, gather x from
 // shared memory, and fold each 32-entry chunk with a segmented warp scan into
 // their own rows' shared accumulators (no atomics, deterministic order).
-// L2->SM traffic per half: the entry stream + P copies of x instead of one
+// L2->SM traffic per half: the entry stream + P tiles of x, instead of one
 // random 32-byte sector per entry.
-#include <cub/cub.cuh>
-
 #include <algorithm>
 #include <cmath>
+#include <numeric>
 #include <vector>
+
+#include <cub/cub.cuh>
 
 #include "common.cuh"
 #include "internal.h"
@@ -38,7 +42,7 @@ namespace spk {
 namespace {
 
 constexpr int kNW = loopcore::kBlock / 32;  // warps per CTA (16)
-constexpr int kMaxW = 16384;                // block width cap (col_local < 2^16)
+constexpr uint32_t kPad = 0xffffffffu;      // padding entry (never a valid packed value)
 
 // ---- PTX helpers: mbarrier + 1-D bulk copy (TMA) ------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -51,8 +55,11 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
 }
-// Bounded wait: returns false after ~2^24 polls (a lost transaction must not
-// hang the GPU; the caller records a fault and the host raises it).
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// Bounded wait: false after ~2^24 polls (a lost transaction must not hang the
+// GPU; the caller records a fault and the host raises it).
 __device__ __forceinline__ bool mbar_wait(uint64_t* bar, uint32_t parity) {
   for (int spin = 0; spin < (1 << 24); ++spin) {
     uint32_t done;
@@ -76,95 +83,110 @@ __device__ __forceinline__ void bulk_copy_g2s(void* dst, const void* src, uint32
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async;" ::: "memory"); }
 __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
 
-}  // namespace
-
-namespace {
+__host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
 template <class VT>
 struct BlockedOp {
   BlockedHalf L[2];
   int64_t n;
-  int acc_rows;  // shared accumulator capacity (max rows of a slab)
-  int W;         // shared tile width (max over halves)
-  unsigned int* fault;  // set when a TMA transaction never completed
+  int acc_rows;  // shared accumulator capacity (max rows of a slab over both halves)
+  int W;         // tile width capacity (doubles)
+  int ecap;      // entry capacity of a stage
+  int S;         // pipeline stages
+  unsigned int* fault;
 
-  static size_t smem_bytes(int W, int acc_rows) { return (size_t)2 * W * 8 + (size_t)acc_rows * 8 + 64; }
-  size_t smem_bytes() const { return smem_bytes(W, acc_rows); }
+  __host__ __device__ size_t stage_bytes() const { return align16((size_t)W * 8) + align16((size_t)ecap * 4) + align16((size_t)ecap * sizeof(VT)); }
+  __host__ __device__ size_t head_bytes() const { return align16((size_t)acc_rows * 8) + align16((size_t)2 * S * 8); }
+  size_t smem_bytes() const { return head_bytes() + (size_t)S * stage_bytes(); }
 
   template <int ROLE, bool LOG, bool DET>
   __device__ void half(const double* x, const double* wgt, const double* old, double* out, unsigned char* ne,
                        int* dyn, double exponent, int policy, int t, unsigned long long* flag, double* absdiff,
                        double& err, long long& masks) const {
     extern __shared__ __align__(128) unsigned char dsm[];
-    double* xb0 = reinterpret_cast<double*>(dsm);
-    double* xb1 = xb0 + W;
-    double* acc = xb1 + W;
-    uint64_t* bar = reinterpret_cast<uint64_t*>(acc + acc_rows);
+    double* acc = reinterpret_cast<double*>(dsm);
+    uint64_t* full = reinterpret_cast<uint64_t*>(dsm + align16((size_t)acc_rows * 8));
+    uint64_t* empty = full + S;
+    unsigned char* stages = dsm + head_bytes();
+    const size_t sb = stage_bytes();
+    const size_t off_pk = align16((size_t)W * 8);
+    const size_t off_val = off_pk + align16((size_t)ecap * 4);
+
     const BlockedHalf& H = L[ROLE];
     const int p = blockIdx.x;
     const int lane = threadIdx.x & 31;
     const int w = threadIdx.x >> 5;
-    const VT* val = static_cast<const VT*>(H.val);
+    const VT* gval = static_cast<const VT*>(H.val);
     const int r0 = H.slab_row0[p];
     const int nrows = H.slab_row0[p + 1] - r0;
+    const long long* offp = H.off + (int64_t)p * H.B * (kNW + 1);  // per block: kNW+1 padded offsets
 
     if (threadIdx.x == 0) {
-      mbar_init(&bar[0], 1);
-      mbar_init(&bar[1], 1);
+      for (int s = 0; s < S; ++s) {
+        mbar_init(&full[s], 1);
+        mbar_init(&empty[s], kNW);
+      }
       fence_mbar_init();
     }
     for (int r = threadIdx.x; r < nrows; r += blockDim.x) acc[r] = 0.0;
     __syncthreads();
 
+    // producer: stage b%S <- x tile of block b + the (slab, block) entry segment
     auto issue = [&](int b) {
+      unsigned char* st = stages + (size_t)(b % S) * sb;
       const int64_t c0 = (int64_t)b * H.W;
       const int64_t cnt = min((int64_t)H.W, H.n_in - c0);
-      const uint32_t bytes = (uint32_t)(((cnt * 8) + 15) & ~int64_t(15));
-      uint64_t* br = &bar[b & 1];
-      mbar_arrive_expect_tx(br, bytes);
-      bulk_copy_g2s((b & 1) ? xb1 : xb0, x + c0, bytes, br);
+      const uint32_t xbytes = (uint32_t)align16((size_t)cnt * 8);
+      const long long e0 = offp[(int64_t)b * (kNW + 1)];
+      const long long e1 = offp[(int64_t)b * (kNW + 1) + kNW];  // padded segment end
+      const uint32_t ne_ = (uint32_t)(e1 - e0);
+      uint64_t* br = &full[b % S];
+      mbar_arrive_expect_tx(br, xbytes + ne_ * 4u + ne_ * (uint32_t)sizeof(VT));
+      bulk_copy_g2s(st, x + c0, xbytes, br);
+      if (ne_) {
+        bulk_copy_g2s(st + off_pk, H.packed + e0, ne_ * 4u, br);
+        bulk_copy_g2s(st + off_val, gval + e0, ne_ * (uint32_t)sizeof(VT), br);
+      }
     };
     if (threadIdx.x == 0) {
-      fence_proxy_async();  // x was written by generic stores before the grid barrier
-      issue(0);
-      if (H.B > 1) issue(1);
+      fence_proxy_async();  // x was written with generic stores before the grid barrier
+      for (int b = 0; b < min(S, H.B); ++b) issue(b);
     }
-    const int wrow0 = H.warp_row0[p * (kNW + 1) + w];
-    (void)wrow0;
     for (int b = 0; b < H.B; ++b) {
-      const double* xs = (b & 1) ? xb1 : xb0;
-      if (!mbar_wait(&bar[b & 1], (uint32_t)((b >> 1) & 1))) atomicExch(fault, 1u);
-      const long long beg = H.off[((int64_t)p * H.B + b) * kNW + w];
-      const long long end = H.off[((int64_t)p * H.B + b) * kNW + w + 1];
-      for (long long c = beg; c < end; c += 128) {
-        uint32_t pk[4];
-        double pr[4];
+      const int s = b % S;
+      const uint32_t ph = (uint32_t)((b / S) & 1);
+      if (!mbar_wait(&full[s], ph)) atomicExch(fault, 1u);
+      const unsigned char* st = stages + (size_t)s * sb;
+      const double* xs = reinterpret_cast<const double*>(st);
+      const uint32_t* pk = reinterpret_cast<const uint32_t*>(st + off_pk);
+      const VT* pv = reinterpret_cast<const VT*>(st + off_val);
+      const long long seg0 = offp[(int64_t)b * (kNW + 1)];
+      const int beg = (int)(offp[(int64_t)b * (kNW + 1) + w] - seg0);
+      const int end = (int)(offp[(int64_t)b * (kNW + 1) + w + 1] - seg0);
+      for (int c = beg; c < end; c += 32) {
+        const int e = c + lane;
+        const uint32_t u = e < end ? pk[e] : kPad;
+        const uint32_t rl = u >> 16;
+        double v = 0.0;
+        if (u != kPad) v = (double)pv[e] * xs[u & 0xffffu];
+        // segmented inclusive scan over equal rl (rows ascend inside the chunk)
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const long long e = c + lane + 32 * k;
-          pk[k] = e < end ? __ldcs(H.packed + e) : 0xffffffffu;
-          pr[k] = e < end ? (double)__ldcs(val + e) : 0.0;
+        for (int d = 1; d < 32; d <<= 1) {
+          const double vo = __shfl_up_sync(0xffffffffu, v, d);
+          const uint32_t ro = __shfl_up_sync(0xffffffffu, rl, d);
+          if (lane >= d && ro == rl) v += vo;
         }
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          if (c + 32 * k >= end) break;  // warp-uniform
-          const uint32_t rl = pk[k] >> 16;
-          double s = pk[k] == 0xffffffffu ? 0.0 : pr[k] * xs[pk[k] & 0xffffu];
-          // segmented inclusive scan over equal rl (rows ascend inside the chunk)
-#pragma unroll
-          for (int d = 1; d < 32; d <<= 1) {
-            const double so = __shfl_up_sync(0xffffffffu, s, d);
-            const uint32_t ro = __shfl_up_sync(0xffffffffu, rl, d);
-            if (lane >= d && ro == rl) s += so;
-          }
-          const uint32_t rn = __shfl_down_sync(0xffffffffu, rl, 1);
-          const bool tail = (lane == 31) || (rn != rl);
-          if (tail && pk[k] != 0xffffffffu) acc[rl] += s;
-        }
+        const uint32_t rn = __shfl_down_sync(0xffffffffu, rl, 1);
+        if (u != kPad && (lane == 31 || rn != rl)) acc[rl] += v;
       }
-      __syncthreads();  // every warp is done with this tile
-      if (threadIdx.x == 0 && b + 2 < H.B) issue(b + 2);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      if (threadIdx.x == 0 && b + S < H.B) {
+        if (!mbar_wait(&empty[s], ph)) atomicExch(fault, 1u);  // all warps released stage s
+        issue(b + S);
+      }
     }
+    __syncthreads();
     // ---- finalize this slab's atoms ----
     for (int r = threadIdx.x; r < nrows; r += blockDim.x) {
       const int64_t i = r0 + r;
@@ -189,22 +211,24 @@ __global__ void key_kernel(const long long* ptr, const uint32_t* idx, int64_t n_
   for (int64_t i = warp; i < n_out; i += nw) {
     const uint32_t base = (uint32_t)slab_of[i] * (uint32_t)B;
     const uint32_t wv = warp_of[i];
-    for (long long q = ptr[i] + lane; q < ptr[i + 1]; q += 32)
-      keys[q] = (base + idx[q] / (uint32_t)W) * kNW + wv;
+    for (long long q = ptr[i] + lane; q < ptr[i + 1]; q += 32) keys[q] = (base + idx[q] / (uint32_t)W) * kNW + wv;
   }
 }
 
+// Sorted position q (key k) -> padded destination seg_base[pb] + (q - useg[pb]).
 template <class VT>
-__global__ void pack_kernel(const uint32_t* perm, const long long* ptr, const uint32_t* idx, const VT* val,
-                            const uint32_t* rows_of_pos, const int* slab_row0_of_row, int W, int64_t m,
-                            uint32_t* packed, VT* vout) {
+__global__ void pack_kernel(const uint32_t* keys_s, const uint32_t* perm, const uint32_t* idx, const VT* val,
+                            const uint32_t* rows_of_pos, const int* slab_row0_of_row, const long long* useg,
+                            const long long* seg_base, int W, int64_t m, uint32_t* packed, VT* vout) {
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < m; q += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t pb = keys_s[q] / kNW;
+    const long long dst = seg_base[pb] + (q - useg[pb]);
     const uint32_t src = perm[q];
     const uint32_t i = rows_of_pos[src];
     const uint32_t rl = i - (uint32_t)slab_row0_of_row[i];
     const uint32_t cl = idx[src] % (uint32_t)W;
-    packed[q] = (rl << 16) | cl;
-    vout[q] = val[src];
+    packed[dst] = (rl << 16) | cl;
+    vout[dst] = val[src];
   }
 }
 
@@ -232,74 +256,56 @@ int grid_cap(spk_ctx* ctx, int64_t items) {
 
 }  // namespace
 
-// Build one half's layout from (ptr, idx, val): P slabs balanced by entries.
+// Build one half's layout from (ptr, idx, val) with tile width W.
 // Returns false when the shape does not fit (rows per slab >= 2^16).
-bool build_blocked(spk_ctx* ctx, int P, int64_t n_out, int64_t n_in, int64_t m, const DBuf& ptr_d, const DBuf& idx_d,
-                   const DBuf& val_d, int vbytes, size_t smem_budget, BlockedHost& out) {
+bool build_blocked(spk_ctx* ctx, int P, int W, int64_t n_out, int64_t n_in, int64_t m, const DBuf& ptr_d,
+                   const DBuf& idx_d, const DBuf& val_d, int vbytes, BlockedHost& out) {
   std::vector<long long> ptr(n_out + 1);
   download(ctx, ptr.data(), ptr_d, sizeof(long long) * (n_out + 1));
-  // slab cut points: first row whose prefix reaches k*m/P
   std::vector<int> slab_row0(P + 1);
   slab_row0[0] = 0;
   for (int k = 1; k < P; ++k) {
     const long long target = (long long)((double)m * k / P);
     int r = (int)(std::lower_bound(ptr.begin(), ptr.end(), target) - ptr.begin());
-    r = std::max(r, slab_row0[k - 1]);
-    // also cap by rows so that no slab is far longer than n/P in rows
-    slab_row0[k] = std::min<int64_t>(r, n_out);
+    slab_row0[k] = std::max<int>(std::min<int64_t>(r, n_out), slab_row0[k - 1]);
   }
   slab_row0[P] = (int)n_out;
   int max_rows = 0;
   for (int k = 0; k < P; ++k) max_rows = std::max(max_rows, slab_row0[k + 1] - slab_row0[k]);
-  if (max_rows >= 65536) return false;
-  // shared tile width from the budget: 2 tiles of W doubles + accumulators
-  const size_t acc_bytes = (size_t)max_rows * 8 + 64;
-  if (smem_budget <= acc_bytes + 2 * 16 * 8) return false;
-  int W = kMaxW;
-  while (W > 16 && ((size_t)2 * W * 8 + acc_bytes > smem_budget || W > ctx->blocked_max_w)) W >>= 1;
+  if (max_rows >= 65535) return false;
   if ((int64_t)W > n_in) W = (int)std::max<int64_t>(16, ((n_in + 15) / 16) * 16);
   const int B = (int)((n_in + W - 1) / W);
-  // warp cut points inside each slab (balanced by entries)
-  std::vector<int> warp_row0((size_t)P * (kNW + 1));
-  std::vector<int> slab_of(n_out);
+  std::vector<int> slab_of(n_out), slab_row0_of_row(n_out);
   std::vector<unsigned char> warp_of(n_out);
   for (int k = 0; k < P; ++k) {
     const int a = slab_row0[k], z = slab_row0[k + 1];
     const long long e0 = ptr[a], e1 = ptr[z];
     int prev = a;
-    warp_row0[(size_t)k * (kNW + 1)] = 0;
-    for (int wv = 1; wv < kNW; ++wv) {
-      const long long target = e0 + (long long)((double)(e1 - e0) * wv / kNW);
-      int r = (int)(std::lower_bound(ptr.begin() + a, ptr.begin() + z, target) - ptr.begin());
-      r = std::max(r, prev);
-      warp_row0[(size_t)k * (kNW + 1) + wv] = r - a;
-      prev = r;
-    }
-    warp_row0[(size_t)k * (kNW + 1) + kNW] = z - a;
-    for (int wv = 0; wv < kNW; ++wv)
-      for (int r = a + warp_row0[(size_t)k * (kNW + 1) + wv]; r < a + warp_row0[(size_t)k * (kNW + 1) + wv + 1]; ++r) {
+    for (int wv = 0; wv < kNW; ++wv) {
+      int r_end = z;
+      if (wv + 1 < kNW) {
+        const long long target = e0 + (long long)((double)(e1 - e0) * (wv + 1) / kNW);
+        r_end = std::max(prev, (int)(std::lower_bound(ptr.begin() + a, ptr.begin() + z, target) - ptr.begin()));
+      }
+      for (int r = prev; r < r_end; ++r) {
         slab_of[r] = k;
         warp_of[r] = (unsigned char)wv;
+        slab_row0_of_row[r] = a;
       }
+      prev = r_end;
+    }
   }
-  std::vector<int> slab_row0_of_row(n_out);
-  for (int64_t r = 0; r < n_out; ++r) slab_row0_of_row[r] = slab_row0[slab_of[r]];
-
+  const int64_t npb = (int64_t)P * B;
+  const int64_t nkeys = npb * kNW;
+  if (nkeys >= (1LL << 32)) return false;
   cudaStream_t s = ctx->stream;
+  const int64_t mm = std::max<int64_t>(m, 1);
   DBuf d_slab_of, d_warp_of, d_s0r;
   upload(ctx, d_slab_of, slab_of.data(), sizeof(int) * n_out);
   upload(ctx, d_warp_of, warp_of.data(), n_out);
   upload(ctx, d_s0r, slab_row0_of_row.data(), sizeof(int) * n_out);
-  upload(ctx, out.slab_row0, slab_row0.data(), sizeof(int) * (P + 1));
-  upload(ctx, out.warp_row0, warp_row0.data(), sizeof(int) * warp_row0.size());
-  const int64_t nkeys = (int64_t)P * B * kNW;
-  if (nkeys >= (1LL << 32)) return false;
-  const int64_t mm = std::max<int64_t>(m, 1);
   DBuf keys(sizeof(uint32_t) * mm), keys_s(sizeof(uint32_t) * mm), iota(sizeof(uint32_t) * mm),
-      perm(sizeof(uint32_t) * mm), rows(sizeof(uint32_t) * mm), hist(sizeof(unsigned long long) * (nkeys + 1));
-  out.off.alloc(sizeof(long long) * (nkeys + 1));
-  out.packed.alloc(sizeof(uint32_t) * mm);
-  out.val.alloc((size_t)vbytes * mm);
+      perm(sizeof(uint32_t) * mm), rows(sizeof(uint32_t) * mm), hist(sizeof(unsigned long long) * nkeys);
   SPK_CUDA(cudaMemsetAsync(hist.p, 0, hist.bytes, s));
   key_kernel<<<grid_cap(ctx, n_out * 32), 256, 0, s>>>(ptr_d.as<long long>(), idx_d.as<uint32_t>(), n_out,
                                                         d_slab_of.as<int>(), d_warp_of.as<unsigned char>(), W, B,
@@ -311,72 +317,114 @@ bool build_blocked(spk_ctx* ctx, int P, int64_t n_out, int64_t n_in, int64_t m, 
   int end_bit = 1;
   while ((int64_t(1) << end_bit) < nkeys) ++end_bit;
   size_t tb = 0;
-  SPK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys.as<uint32_t>(), keys_s.as<uint32_t>(), iota.as<uint32_t>(),
-                                           perm.as<uint32_t>(), (int)m, 0, end_bit, s));
+  SPK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys.as<uint32_t>(), keys_s.as<uint32_t>(),
+                                           iota.as<uint32_t>(), perm.as<uint32_t>(), (int)m, 0, end_bit, s));
   ctx->scratch.ensure(tb);
   SPK_CUDA(cub::DeviceRadixSort::SortPairs(ctx->scratch.p, tb, keys.as<uint32_t>(), keys_s.as<uint32_t>(),
                                            iota.as<uint32_t>(), perm.as<uint32_t>(), (int)m, 0, end_bit, s));
-  SPK_CUDA(cudaMemsetAsync(out.off.p, 0, sizeof(long long), s));
-  SPK_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb, hist.as<unsigned long long>(),
-                                         out.off.as<unsigned long long>() + 1, (int)nkeys, s));
-  ctx->scratch.ensure(tb);
-  SPK_CUDA(cub::DeviceScan::InclusiveSum(ctx->scratch.p, tb, hist.as<unsigned long long>(),
-                                         out.off.as<unsigned long long>() + 1, (int)nkeys, s));
+  ++ctx->launches;
+  // host: padded (slab, block) segments and per-warp offsets in padded coordinates
+  std::vector<unsigned long long> h(nkeys);
+  download(ctx, h.data(), hist, sizeof(unsigned long long) * nkeys);
+  std::vector<long long> useg(npb), seg_base(npb + 1), off((size_t)npb * (kNW + 1));
+  long long u_acc = 0, p_acc = 0;
+  int ecap = 0;
+  for (int64_t pb = 0; pb < npb; ++pb) {
+    useg[pb] = u_acc;
+    seg_base[pb] = p_acc;
+    long long in_seg = 0;
+    for (int wv = 0; wv < kNW; ++wv) {
+      off[(size_t)pb * (kNW + 1) + wv] = p_acc + in_seg;
+      in_seg += (long long)h[pb * kNW + wv];
+    }
+    const long long padded = (in_seg + 3) & ~3LL;
+    off[(size_t)pb * (kNW + 1) + kNW] = p_acc + padded;  // padded end (bulk-copy extent)
+    ecap = std::max<int>(ecap, (int)padded);
+    u_acc += in_seg;
+    p_acc += padded;
+  }
+  seg_base[npb] = p_acc;
+  const int64_t total = std::max<long long>(p_acc, 4);
+  DBuf d_useg, d_seg;
+  upload(ctx, d_useg, useg.data(), sizeof(long long) * npb);
+  upload(ctx, d_seg, seg_base.data(), sizeof(long long) * (npb + 1));
+  upload(ctx, out.off, off.data(), sizeof(long long) * off.size());
+  upload(ctx, out.slab_row0, slab_row0.data(), sizeof(int) * (P + 1));
+  out.packed.alloc(sizeof(uint32_t) * total);
+  out.val.alloc((size_t)vbytes * total);
+  SPK_CUDA(cudaMemsetAsync(out.packed.p, 0xff, out.packed.bytes, s));  // padding = kPad
+  SPK_CUDA(cudaMemsetAsync(out.val.p, 0, out.val.bytes, s));
   if (vbytes == 4)
-    pack_kernel<float><<<grid_cap(ctx, m), 256, 0, s>>>(perm.as<uint32_t>(), ptr_d.as<long long>(),
+    pack_kernel<float><<<grid_cap(ctx, m), 256, 0, s>>>(keys_s.as<uint32_t>(), perm.as<uint32_t>(),
                                                          idx_d.as<uint32_t>(), val_d.as<float>(), rows.as<uint32_t>(),
-                                                         d_s0r.as<int>(), W, m, out.packed.as<uint32_t>(),
+                                                         d_s0r.as<int>(), d_useg.as<long long>(),
+                                                         d_seg.as<long long>(), W, m, out.packed.as<uint32_t>(),
                                                          out.val.as<float>());
   else
-    pack_kernel<double><<<grid_cap(ctx, m), 256, 0, s>>>(perm.as<uint32_t>(), ptr_d.as<long long>(),
-                                                          idx_d.as<uint32_t>(), val_d.as<double>(), rows.as<uint32_t>(),
-                                                          d_s0r.as<int>(), W, m, out.packed.as<uint32_t>(),
+    pack_kernel<double><<<grid_cap(ctx, m), 256, 0, s>>>(keys_s.as<uint32_t>(), perm.as<uint32_t>(),
+                                                          idx_d.as<uint32_t>(), val_d.as<double>(),
+                                                          rows.as<uint32_t>(), d_s0r.as<int>(), d_useg.as<long long>(),
+                                                          d_seg.as<long long>(), W, m, out.packed.as<uint32_t>(),
                                                           out.val.as<double>());
-  ctx->launches += 3;
+  ++ctx->launches;
   SPK_CUDA(cudaGetLastError());
   SPK_CUDA(cudaStreamSynchronize(s));
   out.max_rows = max_rows;
+  out.ecap = ecap;
   out.h.P = P;
   out.h.B = B;
   out.h.W = W;
   out.h.n_out = n_out;
   out.h.n_in = n_in;
   out.h.slab_row0 = out.slab_row0.as<int>();
-  out.h.warp_row0 = out.warp_row0.as<int>();
+  out.h.warp_row0 = nullptr;
   out.h.off = out.off.as<long long>();
   out.h.packed = out.packed.as<uint32_t>();
   out.h.val = out.val.p;
   return true;
 }
 
-// Runs the persistent loop with the blocked operator; returns false when the
-// layout cannot be used (caller falls back to the CSR operator).
 template <class VT>
 bool run_blocked_t(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, double exponent, int policy,
                    LoopState& st, LoopOut& out) {
   const int64_t n = sk->n;
+  const int P = ctx->num_sms;
+  const size_t budget = 222 * 1024;  // dynamic shared memory per CTA (static use is ~1 KB)
   if (!sk->blocked_tried) {
     sk->blocked_tried = true;
-    int per_sm = 0;
-    // one CTA per SM; the budget leaves room for the kernel's static shared memory
-    const size_t budget = 200 * 1024;
-    (void)per_sm;
-    const int P = ctx->num_sms;
-    auto R = std::make_unique<BlockedHost>(), C = std::make_unique<BlockedHost>();
-    const int vb = sk->value_type == SPK_VALUES_F32 ? 4 : 8;
-    if (build_blocked(ctx, P, n, n, sk->nnz, sk->row_ptr, sk->col_idx, sk->values, vb, budget, *R) &&
-        build_blocked(ctx, P, n, n, sk->nnz, sk->col_ptr, sk->row_idx, sk->values_t, vb, budget, *C)) {
-      sk->blk_rows = std::move(R);
-      sk->blk_cols = std::move(C);
+    const int vb = sizeof(VT);
+    // shrink the tile until acc + S stages fit (E_cap shrinks with W)
+    for (int W = std::min(ctx->blocked_max_w, 4096); W >= 16; W >>= 1) {
+      auto R = std::make_unique<BlockedHost>(), C = std::make_unique<BlockedHost>();
+      if (!build_blocked(ctx, P, W, n, n, sk->nnz, sk->row_ptr, sk->col_idx, sk->values, vb, *R) ||
+          !build_blocked(ctx, P, W, n, n, sk->nnz, sk->col_ptr, sk->row_idx, sk->values_t, vb, *C))
+        break;
+      BlockedOp<VT> probe{};
+      probe.acc_rows = std::max(R->max_rows, C->max_rows);
+      probe.W = std::max(R->h.W, C->h.W);
+      probe.ecap = std::max(R->ecap, C->ecap);
+      int S = 4;
+      for (; S >= 2; --S) {
+        probe.S = S;
+        if (probe.smem_bytes() <= budget) break;
+      }
+      if (S >= 2) {
+        sk->blocked_stages = S;
+        sk->blk_rows = std::move(R);
+        sk->blk_cols = std::move(C);
+        break;
+      }
     }
   }
   if (!sk->blk_rows) return false;
-  BlockedOp<VT> op;
+  BlockedOp<VT> op{};
   op.L[0] = sk->blk_rows->h;
   op.L[1] = sk->blk_cols->h;
   op.n = n;
   op.acc_rows = std::max(sk->blk_rows->max_rows, sk->blk_cols->max_rows);
   op.W = std::max(op.L[0].W, op.L[1].W);
+  op.ecap = std::max(sk->blk_rows->ecap, sk->blk_cols->ecap);
+  op.S = sk->blocked_stages;
   LoopWs& W = sk->ws;
   W.scalar.ensure(sizeof(unsigned int));
   SPK_CUDA(cudaMemsetAsync(W.scalar.p, 0, sizeof(unsigned int), ctx->stream));
@@ -386,10 +434,10 @@ bool run_blocked_t(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, doub
   SPK_CUDA(cudaMemcpyAsync(W.row_ne.p, sk->cov_row.p, n, cudaMemcpyDeviceToDevice, ctx->stream));
   SPK_CUDA(cudaMemcpyAsync(W.col_ne.p, sk->cov_col.p, n, cudaMemcpyDeviceToDevice, ctx->stream));
   loopcore::run_core<false>(ctx, op, n, W, sk->cov_empty_rows, sk->cov_empty_cols, cfg, exponent, policy, st,
-                            /*useful_blocks=*/op.L[0].P, out, /*exact_grid=*/op.L[0].P, op.smem_bytes());
+                            /*useful_blocks=*/P, out, /*exact_grid=*/P, op.smem_bytes());
   unsigned int fault = 0;
   download(ctx, &fault, W.scalar, sizeof fault);
-  if (fault) fail_device("blocked loop: TMA tile never arrived", cudaErrorLaunchTimeout);
+  if (fault) fail_device("blocked loop: a TMA stage never completed", cudaErrorLaunchTimeout);
   return true;
 }
 

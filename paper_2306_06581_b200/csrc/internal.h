@@ -69,7 +69,7 @@ struct BlockedHalf {
   int64_t n_out, n_in;
   const int* slab_row0;    // [P+1] global row starts
   const int* warp_row0;    // [P*(NW+1)] local row starts per warp
-  const long long* off;    // [P*B*NW + 1] entry offsets of (slab, block, warp)
+  const long long* off;    // [P*B*(NW+1)] padded entry offsets of (slab, block, warp); [NW] = segment end
   const uint32_t* packed;  // row_local << 16 | col_local
   const void* val;         // f32 or f64
 };
@@ -77,6 +77,7 @@ struct BlockedHost {
   BlockedHalf h{};
   DBuf slab_row0, warp_row0, off, packed, val;
   int max_rows = 0;
+  int ecap = 0;  // largest padded (slab, block) entry segment
 };
 
 }  // namespace spk
@@ -113,6 +114,7 @@ struct spk_sketch {
   spk::ReadWs rws;
   // fast-path layouts (built lazily by the first fast-mode solve)
   bool blocked_tried = false;
+  int blocked_stages = 0;
   std::unique_ptr<spk::BlockedHost> blk_rows, blk_cols;
 };
 

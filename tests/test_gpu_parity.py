@@ -353,6 +353,7 @@ def test_blocked_loop_matches_csr(oracle, max_w):
         ou, ov, _, _, ores = oracle.sinkhorn(a, b, 0.02, lam, -1.0, 120, policy="mask", uot=plan == "uot", csr=so)
         for values in ("f64", "f32"):
             with spk.Context(0) as c:
+                c.set_option(L.OPT_BLOCKED_LOOP, 1)
                 c.set_option(L.OPT_BLOCKED_MAX_W, max_w)
                 res = c.sketch_from_csr(*so, values_type=values).solve(spk.SolverConfig(0.02, lam, -1.0, 120),
                                                                          uot=plan == "uot", a=a, b=b)
