@@ -217,6 +217,10 @@ def run_ours(args, ws, rank, local):
     w = W.CONFIGS[args.config]()
     iters = args.iters or w.max_iter
     ctx = spk.Context(local)
+    if os.environ.get("SPK_BLOCKED") is not None:  # loop variant override (profiling)
+        from paper_2306_06581_b200 import _lib as L
+
+        ctx.set_option(L.OPT_BLOCKED_LOOP, int(os.environ["SPK_BLOCKED"]))
     stream = torch.cuda.current_stream()
     ctx.set_stream(stream.cuda_stream)
     kernel = spk.Coords(w.x, w.y, w.cost, w.eta, scale=w.scale, eps=w.eps)

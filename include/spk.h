@@ -82,7 +82,8 @@ enum spk_value_type { SPK_VALUES_F64 = 0, SPK_VALUES_F32 = 1 };
 /* The Gibbs kernel and its cost, in one of two forms.
  * Dense form (KernelMatrix + CostMatrix, geometry.hpp:13-26): K != NULL,
  *   n*n row-major host fp64; nnz_ratio as KernelMatrix::nnz_ratio; C may be
- *   NULL when no objective is needed.
+ *   NULL when no objective is needed. Cost-only form (K == NULL, C != NULL,
+ *   x == NULL): costs for a readout over a sketch.
  * Coordinate form (new; no n^2 storage): K == NULL, x and y are n*dim
  *   row-major host fp64 points; C_ij = cost(x_i, y_j) / cost_scale computed
  *   exactly as pairwise_cost (geometry.cpp:16-66) and the caller's division;
@@ -227,6 +228,18 @@ int spk_sketch_readout(spk_ctx* ctx, spk_sketch* sk, const spk_kernel_desc* kd, 
                        double lambda, double epsilon, double* row_marginal, double* col_marginal,
                        double* objective, spk_report* rep);
 
+/* Readout of a given plan T_ij = u_i K~_ij v_j (log domain: exp(lu + log K~ + lv))
+ * over a host sketch (row_ptr != NULL: CSR of n rows) or over the kernel of kd
+ * (dense K or coordinates; kd may also supply the costs). Replaces
+ * TransportPlan::row_marginal / col_marginal (solvers.cpp:215-225),
+ * ot_objective / uot_objective (:280-293) and marginal_residuals (:295-308).
+ * a, b may be NULL when uot == 0 and no residuals are wanted. */
+int spk_plan_readout(spk_ctx* ctx, const spk_kernel_desc* kd, int64_t n, const int64_t* row_ptr,
+                     const uint32_t* col_idx, const double* values, const double* u, const double* v,
+                     const double* log_u, const double* log_v, int log_domain, const double* a,
+                     const double* b, int uot, double lambda, double epsilon, double* row_marginal,
+                     double* col_marginal, double* objective, double* residual_row, double* residual_col);
+
 /* ---- helpers exposed for parity tests --------------------------------------- */
 
 /* SamplingPlan::prob(i, j) (sparsify.hpp:28-34) of the plan that
@@ -234,6 +247,10 @@ int spk_sketch_readout(spk_ctx* ctx, spk_sketch* sk, const spk_kernel_desc* kd, 
 int spk_plan_probs(spk_ctx* ctx, const spk_kernel_desc* kd, const double* a, const double* b,
                    int plan_kind, double lambda, double epsilon, double theta, int64_t m,
                    const int64_t* qi, const int64_t* qj, double* probs, int32_t* factorized);
+
+/* kernel_from_cost (geometry.cpp:83-102) on `count` host cost entries:
+ * K = isinf(C) ? 0 : exp(-C/eps); *nnz = #(K > 0). */
+int spk_kernel_from_cost(spk_ctx* ctx, const double* C, int64_t count, double epsilon, double* K, int64_t* nnz);
 
 /* Cost and Gibbs kernel entries from coordinates (pairwise_cost +
  * kernel_from_cost) for m query pairs; c0 = max finite cost over all n^2

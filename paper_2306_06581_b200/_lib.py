@@ -92,8 +92,11 @@ SIGNATURES = {
                                    C.POINTER(Report)]),
     "spk_sketch_readout": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(KernelDesc), C.c_int, C.c_double,
                                      C.c_double, DP, DP, DP, C.POINTER(Report)]),
+    "spk_plan_readout": (C.c_int, [C.c_void_p, C.POINTER(KernelDesc), C.c_int64, I64P, U32P, DP, DP, DP, DP, DP,
+                                   C.c_int, DP, DP, C.c_int, C.c_double, C.c_double, DP, DP, DP, DP, DP]),
     "spk_plan_probs": (C.c_int, [C.c_void_p, C.POINTER(KernelDesc), DP, DP, C.c_int, C.c_double, C.c_double,
                                  C.c_double, C.c_int64, I64P, I64P, DP, C.POINTER(C.c_int32)]),
+    "spk_kernel_from_cost": (C.c_int, [C.c_void_p, DP, C.c_int64, C.c_double, DP, I64P]),
     "spk_cost_kernel": (C.c_int, [C.c_void_p, C.POINTER(KernelDesc), C.c_int64, I64P, I64P, DP, DP, DP]),
 }
 

@@ -163,21 +163,44 @@ struct BlockedOp {
       const long long seg0 = offp[(int64_t)b * (kNW + 1)];
       const int beg = (int)(offp[(int64_t)b * (kNW + 1) + w] - seg0);
       const int end = (int)(offp[(int64_t)b * (kNW + 1) + w + 1] - seg0);
-      for (int c = beg; c < end; c += 32) {
-        const int e = c + lane;
-        const uint32_t u = e < end ? pk[e] : kPad;
-        const uint32_t rl = u >> 16;
-        double v = 0.0;
-        if (u != kPad) v = (double)pv[e] * xs[u & 0xffffu];
-        // segmented inclusive scan over equal rl (rows ascend inside the chunk)
+      const unsigned upto = lane == 31 ? 0xffffffffu : ((2u << lane) - 1u);
+      // 4 independent 32-entry chunks in flight per warp (ILP over the scan chains)
+      for (int c = beg; c < end; c += 128) {
+        uint32_t u[4];
+        double v[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int e = c + 32 * k + lane;
+          u[k] = e < end ? pk[e] : kPad;
+          v[k] = u[k] != kPad ? (double)pv[e] * xs[u[k] & 0xffffu] : 0.0;
+        }
+        unsigned heads[4];
+        int sstart[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          // rows ascend inside a chunk: a segment head is a row change
+          const uint32_t up = __shfl_up_sync(0xffffffffu, u[k] >> 16, 1);
+          heads[k] = __ballot_sync(0xffffffffu, lane == 0 || up != (u[k] >> 16));
+          sstart[k] = 31 - __clz(heads[k] & upto);
+        }
+        // segmented inclusive scans; steps only while some segment is that long
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
-          const double vo = __shfl_up_sync(0xffffffffu, v, d);
-          const uint32_t ro = __shfl_up_sync(0xffffffffu, rl, d);
-          if (lane >= d && ro == rl) v += vo;
+          bool need = false;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) need |= (lane - d >= sstart[k]);
+          if (!__any_sync(0xffffffffu, need)) break;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const double vo = __shfl_up_sync(0xffffffffu, v[k], d);
+            if (lane - d >= sstart[k]) v[k] += vo;
+          }
         }
-        const uint32_t rn = __shfl_down_sync(0xffffffffu, rl, 1);
-        if (u != kPad && (lane == 31 || rn != rl)) acc[rl] += v;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const bool tail = lane == 31 || ((heads[k] >> (lane + 1)) & 1u);
+          if (tail && u[k] != kPad) acc[u[k] >> 16] += v[k];  // chunk order kept: k ascending
+        }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
@@ -394,7 +417,7 @@ bool run_blocked_t(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, doub
     sk->blocked_tried = true;
     const int vb = sizeof(VT);
     // shrink the tile until acc + S stages fit (E_cap shrinks with W)
-    for (int W = std::min(ctx->blocked_max_w, 4096); W >= 16; W >>= 1) {
+    for (int W = std::min(ctx->blocked_max_w, 2048); W >= 16; W >>= 1) {
       auto R = std::make_unique<BlockedHost>(), C = std::make_unique<BlockedHost>();
       if (!build_blocked(ctx, P, W, n, n, sk->nnz, sk->row_ptr, sk->col_idx, sk->values, vb, *R) ||
           !build_blocked(ctx, P, W, n, n, sk->nnz, sk->col_ptr, sk->row_idx, sk->values_t, vb, *C))
@@ -403,7 +426,7 @@ bool run_blocked_t(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, doub
       probe.acc_rows = std::max(R->max_rows, C->max_rows);
       probe.W = std::max(R->h.W, C->h.W);
       probe.ecap = std::max(R->ecap, C->ecap);
-      int S = 4;
+      int S = 6;
       for (; S >= 2; --S) {
         probe.S = S;
         if (probe.smem_bytes() <= budget) break;

@@ -205,6 +205,8 @@ void sample_sketch(spk_ctx* ctx, DevKernel& dk, const PlanInfo& plan, double s, 
 void build_csc(spk_ctx* ctx, spk_sketch* sk);
 void cost_kernel_query(spk_ctx* ctx, DevKernel& dk, int64_t m, const int64_t* qi, const int64_t* qj,
                        double* cost, double* kern);
+void kernel_from_cost_dev(spk_ctx* ctx, const double* C_host, int64_t count, double eps, double* K_host,
+                          int64_t* nnz);
 void plan_probs_query(spk_ctx* ctx, DevKernel& dk, const PlanInfo& plan, int64_t m,
                       const int64_t* qi, const int64_t* qj, double* out);
 
@@ -244,7 +246,8 @@ void sparse_readout(spk_ctx* ctx, spk_sketch* sk, DevKernel* dk, int log_domain,
                     double* row_m_host, double* col_m_host, ReadoutOut& out);
 void dense_readout(spk_ctx* ctx, DevKernel& dk, int log_domain, const DBuf& u, const DBuf& v,
                    const DBuf& lu, const DBuf& lv, const double* a, const double* b,
-                   bool want_objective, int uot, double lambda, double eps, ReadoutOut& out);
+                   bool want_objective, int uot, double lambda, double eps, ReadoutOut& out,
+                   double* row_m_host = nullptr, double* col_m_host = nullptr);
 double sketch_kernel_mean(spk_ctx* ctx, spk_sketch* sk);
 // spmv / spmv_t on the device sketch in the reference's summation order.
 void sketch_product(spk_ctx* ctx, spk_sketch* sk, const double* x_host, double* y_host, int transpose);

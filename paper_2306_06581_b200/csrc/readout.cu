@@ -401,7 +401,8 @@ __global__ void dense_row_seq_kernel(KF k, int64_t n, const double* u, const dou
 
 template <bool LOG, class KF>
 void dense_readout_t(spk_ctx* ctx, KF kf, DevKernel& dk, const double* u, const double* v, const double* a,
-                     const double* b, bool want_obj, int uot, double lambda, double eps, ReadoutOut& out) {
+                     const double* b, bool want_obj, int uot, double lambda, double eps, ReadoutOut& out,
+                     double* row_m_host, double* col_m_host) {
   const int64_t n = dk.n;
   cudaStream_t s = ctx->stream;
   DBuf row_m(sizeof(double) * n), col_m(sizeof(double) * n), flag(sizeof(unsigned long long)), tmp;
@@ -446,23 +447,25 @@ void dense_readout_t(spk_ctx* ctx, KF kf, DevKernel& dk, const double* u, const 
   }
   ReadWs R;
   finish(ctx, R, n, row_m.as<double>(), col_m.as<double>(), a, b, obj, uot, lambda, eps, cost, entropy, out);
+  if (row_m_host) download(ctx, row_m_host, row_m, sizeof(double) * n);
+  if (col_m_host) download(ctx, col_m_host, col_m, sizeof(double) * n);
 }
 
 }  // namespace
 
 void dense_readout(spk_ctx* ctx, DevKernel& dk, int log_domain, const DBuf& u, const DBuf& v, const DBuf& lu,
                    const DBuf& lv, const double* a, const double* b, bool want_objective, int uot, double lambda,
-                   double eps, ReadoutOut& out) {
+                   double eps, ReadoutOut& out, double* rmh, double* cmh) {
   const double* pu = log_domain ? lu.as<double>() : u.as<double>();
   const double* pv = log_domain ? lv.as<double>() : v.as<double>();
   if (dk.dense) {
     KDense kf{dk.K.as<double>(), dk.n};
-    if (log_domain) dense_readout_t<true>(ctx, kf, dk, pu, pv, a, b, want_objective, uot, lambda, eps, out);
-    else dense_readout_t<false>(ctx, kf, dk, pu, pv, a, b, want_objective, uot, lambda, eps, out);
+    if (log_domain) dense_readout_t<true>(ctx, kf, dk, pu, pv, a, b, want_objective, uot, lambda, eps, out, rmh, cmh);
+    else dense_readout_t<false>(ctx, kf, dk, pu, pv, a, b, want_objective, uot, lambda, eps, out, rmh, cmh);
   } else {
     KCoords kf = kcoords_of(dk);
-    if (log_domain) dense_readout_t<true>(ctx, kf, dk, pu, pv, a, b, want_objective, uot, lambda, eps, out);
-    else dense_readout_t<false>(ctx, kf, dk, pu, pv, a, b, want_objective, uot, lambda, eps, out);
+    if (log_domain) dense_readout_t<true>(ctx, kf, dk, pu, pv, a, b, want_objective, uot, lambda, eps, out, rmh, cmh);
+    else dense_readout_t<false>(ctx, kf, dk, pu, pv, a, b, want_objective, uot, lambda, eps, out, rmh, cmh);
   }
 }
 

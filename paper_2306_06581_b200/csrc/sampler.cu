@@ -593,10 +593,10 @@ void make_dev_kernel(spk_ctx* ctx, const spk_kernel_desc* kd, double default_eps
   if (n <= 0) fail(SPK_E_LENGTH_MISMATCH, "kernel dimension must be positive");
   dk.n = n;
   dk.eps = kd->kernel_epsilon > 0.0 ? kd->kernel_epsilon : default_eps;
-  if (kd->K) {
+  if (kd->K || (kd->C && !kd->x)) {
     dk.dense = true;
     dk.nnz_ratio = kd->nnz_ratio;
-    upload(ctx, dk.K, kd->K, sizeof(double) * n * n);
+    if (kd->K) upload(ctx, dk.K, kd->K, sizeof(double) * n * n);  // cost-only form leaves K empty
     if (kd->C && need_cost) {
       upload(ctx, dk.C, kd->C, sizeof(double) * n * n);
       dk.have_cost = true;
@@ -776,6 +776,36 @@ void plan_probs_query(spk_ctx* ctx, DevKernel& dk, const PlanInfo& plan, int64_t
                                                                      dj.as<int64_t>(), dout.as<double>());
   ++ctx->launches;
   download(ctx, out, dout, sizeof(double) * m);
+}
+
+namespace {
+__global__ void kernel_from_cost_kernel(const double* C, int64_t m, double eps, double* K, unsigned long long* nnz) {
+  unsigned long long local = 0;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < m; q += (int64_t)gridDim.x * blockDim.x) {
+    const double c = C[q];
+    const double v = isinf(c) ? 0.0 : exp(-c / eps);  // geometry.cpp:95
+    K[q] = v;
+    local += v > 0.0 ? 1 : 0;
+  }
+  local = (unsigned long long)warp_sum_ll((long long)local);
+  if ((threadIdx.x & 31) == 0 && local) atomicAdd(nnz, local);
+}
+}  // namespace
+
+void kernel_from_cost_dev(spk_ctx* ctx, const double* C_host, int64_t count, double eps, double* K_host,
+                          int64_t* nnz) {
+  if (!(eps > 0.0)) fail(SPK_E_NON_POSITIVE_EPSILON, "epsilon = " + std::to_string(eps));
+  DBuf dc, dk(sizeof(double) * std::max<int64_t>(count, 1)), dn(sizeof(unsigned long long));
+  upload(ctx, dc, C_host, sizeof(double) * count);
+  SPK_CUDA(cudaMemsetAsync(dn.p, 0, dn.bytes, ctx->stream));
+  kernel_from_cost_kernel<<<grid_for(ctx, count, 256), 256, 0, ctx->stream>>>(dc.as<double>(), count, eps,
+                                                                              dk.as<double>(),
+                                                                              dn.as<unsigned long long>());
+  ++ctx->launches;
+  download(ctx, K_host, dk, sizeof(double) * count);
+  unsigned long long c = 0;
+  download(ctx, &c, dn, sizeof c);
+  if (nnz) *nnz = (int64_t)c;
 }
 
 void cost_kernel_query(spk_ctx* ctx, DevKernel& dk, int64_t m, const int64_t* qi, const int64_t* qj,

@@ -562,6 +562,68 @@ int spk_sketch_spmv(spk_sketch* sk, const double* x, double* y, int transpose) {
   });
 }
 
+int spk_plan_readout(spk_ctx* ctx, const spk_kernel_desc* kd, int64_t n, const int64_t* row_ptr,
+                     const uint32_t* col_idx, const double* values, const double* u, const double* v,
+                     const double* log_u, const double* log_v, int log_domain, const double* a, const double* b,
+                     int uot, double lambda, double epsilon, double* row_marginal, double* col_marginal,
+                     double* objective, double* residual_row, double* residual_col) {
+  if (!ctx) return SPK_STATUS_INPUT;
+  return guard(ctx, [&] {
+    if (n <= 0) fail(SPK_E_LENGTH_MISMATCH, "plan dimension must be positive");
+    if (log_domain ? (!log_u || !log_v) : (!u || !v)) fail(SPK_E_LENGTH_MISMATCH, "plan scalings missing");
+    if (uot && (!a || !b)) fail(SPK_E_LENGTH_MISMATCH, "uot_objective needs both marginals");
+    std::unique_ptr<DevKernel> dk;
+    if (kd) {
+      dk = std::make_unique<DevKernel>();
+      make_dev_kernel(ctx, kd, epsilon, *dk, /*need_cost=*/true);
+      if (dk->n != n) fail(SPK_E_LENGTH_MISMATCH, "kernel dimension != plan dimension");
+    }
+    std::vector<double> zeros;
+    if (!a || !b) zeros.assign(n, 0.0);
+    DBuf da, db;
+    upload(ctx, da, a ? a : zeros.data(), sizeof(double) * n);
+    upload(ctx, db, b ? b : zeros.data(), sizeof(double) * n);
+    ReadoutOut ro;
+    const bool want_obj = objective != nullptr;
+    if (row_ptr) {
+      spk_sketch sk;
+      sk.ctx = ctx;
+      sk.device = ctx->device;
+      sk.n = n;
+      sk.nnz = row_ptr[n];
+      sk.value_type = SPK_VALUES_F64;
+      upload(ctx, sk.row_ptr, row_ptr, sizeof(int64_t) * (n + 1));
+      upload(ctx, sk.col_idx, col_idx, sizeof(uint32_t) * sk.nnz);
+      upload(ctx, sk.values, values, sizeof(double) * sk.nnz);
+      build_csc(ctx, &sk);
+      if (log_domain) {
+        upload(ctx, sk.lu, log_u, sizeof(double) * n);
+        upload(ctx, sk.lv, log_v, sizeof(double) * n);
+      } else {
+        upload(ctx, sk.u, u, sizeof(double) * n);
+        upload(ctx, sk.v, v, sizeof(double) * n);
+      }
+      sparse_readout(ctx, &sk, dk.get(), log_domain, da.as<double>(), db.as<double>(), want_obj, uot, lambda,
+                     epsilon, row_marginal, col_marginal, ro);
+    } else {
+      if (!dk) fail(SPK_E_LENGTH_MISMATCH, "spk_plan_readout needs a sketch or a kernel");
+      DBuf du, dv, dlu, dlv;
+      if (log_domain) {
+        upload(ctx, dlu, log_u, sizeof(double) * n);
+        upload(ctx, dlv, log_v, sizeof(double) * n);
+      } else {
+        upload(ctx, du, u, sizeof(double) * n);
+        upload(ctx, dv, v, sizeof(double) * n);
+      }
+      dense_readout(ctx, *dk, log_domain, du, dv, dlu, dlv, da.as<double>(), db.as<double>(), want_obj, uot, lambda,
+                    epsilon, ro, row_marginal, col_marginal);
+    }
+    if (objective) *objective = ro.have_objective ? ro.objective : std::numeric_limits<double>::quiet_NaN();
+    if (residual_row) *residual_row = ro.residual_row;
+    if (residual_col) *residual_col = ro.residual_col;
+  });
+}
+
 int spk_plan_probs(spk_ctx* ctx, const spk_kernel_desc* kd, const double* a, const double* b, int plan_kind,
                    double lambda, double epsilon, double theta, int64_t m, const int64_t* qi, const int64_t* qj,
                    double* probs, int32_t* factorized) {
@@ -574,6 +636,11 @@ int spk_plan_probs(spk_ctx* ctx, const spk_kernel_desc* kd, const double* a, con
     if (factorized) *factorized = plan.factorized ? 1 : 0;
     if (m > 0) plan_probs_query(ctx, dk, plan, m, qi, qj, probs);
   });
+}
+
+int spk_kernel_from_cost(spk_ctx* ctx, const double* C, int64_t count, double epsilon, double* K, int64_t* nnz) {
+  if (!ctx) return SPK_STATUS_INPUT;
+  return guard(ctx, [&] { kernel_from_cost_dev(ctx, C, count, epsilon, K, nnz); });
 }
 
 int spk_cost_kernel(spk_ctx* ctx, const spk_kernel_desc* kd, int64_t m, const int64_t* qi, const int64_t* qj,
