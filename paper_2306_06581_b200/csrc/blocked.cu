@@ -1,7 +1,6 @@
 // blocked.cu -- the fast sparse half-step: slab x block sketch layout with the
-// scaling vector AND the entry stream staged in shared memory by a multi-stage
-// TMA pipeline (north-star item 3: "shared-memory/TMA staging of the gathered
-// scaling vector").
+// scaling vector staged in shared memory by TMA (north-star item 3:
+// "shared-memory/TMA staging of the gathered scaling vector").
 //
 // Why: at config 4 (n = 1e6, 1.1e8 entries, columns uniformly random) every
 // gathered x[j] of the CSR kernel is a random 8-byte read, i.e. one 32-byte L2
@@ -11,19 +10,23 @@
 // Layout (built once per sketch, for the CSR and for the CSC mirror):
 //   output atoms (this half's rows) are cut into P = #SMs slabs of ~equal
 //   entry count, one per persistent CTA, each slab into 16 warp ranges;
-//   input atoms (columns) are cut into B blocks of W atoms. Entries are
-//   ordered (slab, block, warp, row, col) -- inside a row the columns still
-//   ascend, so every row is summed in the reference's j order (spmv,
-//   proj/src/sparsify.cpp:203-213; spmv_t :215-226 on the CSC) -- and each
-//   (slab, block) segment is padded to 16 bytes so it is one bulk copy. An
-//   entry is packed (row_local << 16 | col_local) + value: no more bytes than
-//   the CSR entry it replaces.
-// Pipeline (inside the persistent loop, loop_core.cuh): S stages, each = the
-// x tile of a block (W doubles) + that block's entry segment; thread 0 issues
-// cp.async.bulk (TMA) copies for block b+S as soon as all 16 warps released
-// stage b (empty mbarrier), warps wait on the full mbarrier, gather x from
-// shared memory, and fold each 32-entry chunk with a segmented warp scan into
-// their own rows' shared accumulators (no atomics, deterministic order).
+//   input atoms are cut into B blocks of W = 8192 atoms (one 64 KB x tile).
+//   Entries are ordered (slab, warp, block, row, col): each warp's whole half
+//   is ONE contiguous stream, and inside a row the columns still ascend, so
+//   every row is summed in the reference's j order (spmv,
+//   proj/src/sparsify.cpp:203-213; spmv_t :215-226 on the CSC). Each
+//   (slab, warp, block) segment is padded to 32 entries. An entry is packed
+//   (row_local << 16 | col_local) + value: no more bytes than a CSR entry.
+// Half-step (inside the persistent loop, loop_core.cuh), 17 warps per CTA:
+//   * producer warp: cp.async.bulk (TMA) of x tile b into stage b%2 as soon as
+//     every consumer released stage b-2 (empty mbarrier) -- 64 KB copies, the
+//     size at which 1-D bulk copies stream at full rate on B200
+//     (profiles/microbench/r1_tma_stream_b200.txt: 8 KB 2.3 TB/s, 64 KB 7.1 TB/s);
+//   * 16 consumer warps stream their entries with coalesced loads, 256
+//     entries double-buffered in registers ahead of use (independent of the
+//     tile pipeline), gather x from the shared tile, and fold each 32-entry
+//     chunk with a head-mask segmented scan (usually one shuffle step) into
+//     their own rows' shared accumulators (no atomics, deterministic).
 // L2->SM traffic per half: the entry stream + P tiles of x, instead of one
 // random 32-byte sector per entry.
 #include <algorithm>
@@ -41,8 +44,11 @@ namespace spk {
 
 namespace {
 
-constexpr int kNW = loopcore::kBlock / 32;  // warps per CTA (16)
-constexpr uint32_t kPad = 0xffffffffu;      // padding entry (never a valid packed value)
+constexpr int kNW = 16;                 // consumer warps per CTA
+constexpr int kThreadsBlocked = 32 * (kNW + 1);
+constexpr int kTileW = 8192;            // x tile: 64 KB of fp64
+constexpr int kGroup = 8;               // chunks of 32 entries per prefetch group
+constexpr uint32_t kPad = 0xffffffffu;  // padding entry (never a valid packed value)
 
 // ---- PTX helpers: mbarrier + 1-D bulk copy (TMA) ------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -87,17 +93,33 @@ __host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) & ~size
 
 template <class VT>
 struct BlockedOp {
+  static constexpr int kThreads = kThreadsBlocked;
+  static constexpr int kMinBlocks = 1;  // one CTA per SM: full register file, ~200 KB shared
   BlockedHalf L[2];
   int64_t n;
   int acc_rows;  // shared accumulator capacity (max rows of a slab over both halves)
-  int W;         // tile width capacity (doubles)
-  int ecap;      // entry capacity of a stage
-  int S;         // pipeline stages
   unsigned int* fault;
 
-  __host__ __device__ size_t stage_bytes() const { return align16((size_t)W * 8) + align16((size_t)ecap * 4) + align16((size_t)ecap * sizeof(VT)); }
-  __host__ __device__ size_t head_bytes() const { return align16((size_t)acc_rows * 8) + align16((size_t)2 * S * 8); }
-  size_t smem_bytes() const { return head_bytes() + (size_t)S * stage_bytes(); }
+  __host__ __device__ size_t head_bytes() const { return align16((size_t)acc_rows * 8) + 64; }
+  size_t smem_bytes() const { return head_bytes() + (size_t)2 * kTileW * 8; }
+
+  // One 32-entry chunk: gather, segmented scan by row, tail add.
+  __device__ __forceinline__ void fold(uint32_t u, double v, const double* xs, double* acc, int lane,
+                                       unsigned upto) const {
+    if (u != kPad) v *= xs[u & 0xffffu];
+    else v = 0.0;
+    const uint32_t rl = u >> 16;
+    const uint32_t up = __shfl_up_sync(0xffffffffu, rl, 1);
+    const unsigned heads = __ballot_sync(0xffffffffu, lane == 0 || up != rl);
+    const int sstart = 31 - __clz(heads & upto);
+    for (int d = 1; d < 32; d <<= 1) {
+      if (!__any_sync(0xffffffffu, lane - d >= sstart)) break;
+      const double vo = __shfl_up_sync(0xffffffffu, v, d);
+      if (lane - d >= sstart) v += vo;
+    }
+    const bool tail = lane == 31 || ((heads >> (lane + 1)) & 1u);
+    if (tail && u != kPad) acc[rl] += v;
+  }
 
   template <int ROLE, bool LOG, bool DET>
   __device__ void half(const double* x, const double* wgt, const double* old, double* out, unsigned char* ne,
@@ -106,11 +128,8 @@ struct BlockedOp {
     extern __shared__ __align__(128) unsigned char dsm[];
     double* acc = reinterpret_cast<double*>(dsm);
     uint64_t* full = reinterpret_cast<uint64_t*>(dsm + align16((size_t)acc_rows * 8));
-    uint64_t* empty = full + S;
-    unsigned char* stages = dsm + head_bytes();
-    const size_t sb = stage_bytes();
-    const size_t off_pk = align16((size_t)W * 8);
-    const size_t off_val = off_pk + align16((size_t)ecap * 4);
+    uint64_t* empty = full + 2;
+    double* tiles = reinterpret_cast<double*>(dsm + head_bytes());
 
     const BlockedHalf& H = L[ROLE];
     const int p = blockIdx.x;
@@ -119,94 +138,85 @@ struct BlockedOp {
     const VT* gval = static_cast<const VT*>(H.val);
     const int r0 = H.slab_row0[p];
     const int nrows = H.slab_row0[p + 1] - r0;
-    const long long* offp = H.off + (int64_t)p * H.B * (kNW + 1);  // per block: kNW+1 padded offsets
+    const int B = H.B;
 
     if (threadIdx.x == 0) {
-      for (int s = 0; s < S; ++s) {
-        mbar_init(&full[s], 1);
-        mbar_init(&empty[s], kNW);
-      }
+      mbar_init(&full[0], 1);
+      mbar_init(&full[1], 1);
+      mbar_init(&empty[0], kNW);
+      mbar_init(&empty[1], kNW);
       fence_mbar_init();
     }
     for (int r = threadIdx.x; r < nrows; r += blockDim.x) acc[r] = 0.0;
     __syncthreads();
 
-    // producer: stage b%S <- x tile of block b + the (slab, block) entry segment
-    auto issue = [&](int b) {
-      unsigned char* st = stages + (size_t)(b % S) * sb;
-      const int64_t c0 = (int64_t)b * H.W;
-      const int64_t cnt = min((int64_t)H.W, H.n_in - c0);
-      const uint32_t xbytes = (uint32_t)align16((size_t)cnt * 8);
-      const long long e0 = offp[(int64_t)b * (kNW + 1)];
-      const long long e1 = offp[(int64_t)b * (kNW + 1) + kNW];  // padded segment end
-      const uint32_t ne_ = (uint32_t)(e1 - e0);
-      uint64_t* br = &full[b % S];
-      mbar_arrive_expect_tx(br, xbytes + ne_ * 4u + ne_ * (uint32_t)sizeof(VT));
-      bulk_copy_g2s(st, x + c0, xbytes, br);
-      if (ne_) {
-        bulk_copy_g2s(st + off_pk, H.packed + e0, ne_ * 4u, br);
-        bulk_copy_g2s(st + off_val, gval + e0, ne_ * (uint32_t)sizeof(VT), br);
+    if (w == kNW) {
+      // ---- producer warp: x tiles, two stages ----
+      if (lane == 0) {
+        fence_proxy_async();  // x was written with generic stores before the grid barrier
+        for (int b = 0; b < B; ++b) {
+          const int s = b & 1;
+          if (b >= 2 && !mbar_wait(&empty[s], (uint32_t)(((b - 2) >> 1) & 1))) atomicExch(fault, 1u);
+          const int64_t c0 = (int64_t)b * H.W;
+          const int64_t cnt = min((int64_t)H.W, H.n_in - c0);
+          const uint32_t bytes = (uint32_t)align16((size_t)cnt * 8);
+          mbar_arrive_expect_tx(&full[s], bytes);
+          bulk_copy_g2s(tiles + (size_t)s * kTileW, x + c0, bytes, &full[s]);
+        }
       }
-    };
-    if (threadIdx.x == 0) {
-      fence_proxy_async();  // x was written with generic stores before the grid barrier
-      for (int b = 0; b < min(S, H.B); ++b) issue(b);
-    }
-    for (int b = 0; b < H.B; ++b) {
-      const int s = b % S;
-      const uint32_t ph = (uint32_t)((b / S) & 1);
-      if (!mbar_wait(&full[s], ph)) atomicExch(fault, 1u);
-      const unsigned char* st = stages + (size_t)s * sb;
-      const double* xs = reinterpret_cast<const double*>(st);
-      const uint32_t* pk = reinterpret_cast<const uint32_t*>(st + off_pk);
-      const VT* pv = reinterpret_cast<const VT*>(st + off_val);
-      const long long seg0 = offp[(int64_t)b * (kNW + 1)];
-      const int beg = (int)(offp[(int64_t)b * (kNW + 1) + w] - seg0);
-      const int end = (int)(offp[(int64_t)b * (kNW + 1) + w + 1] - seg0);
+    } else {
+      // ---- consumer warps: one contiguous entry stream per warp ----
+      const long long* ofs = H.off + ((int64_t)p * kNW + w) * (B + 1);  // block starts, padded, [B] = end
+      const long long sbeg = ofs[0], send = ofs[B];
       const unsigned upto = lane == 31 ? 0xffffffffu : ((2u << lane) - 1u);
-      // 4 independent 32-entry chunks in flight per warp (ILP over the scan chains)
-      for (int c = beg; c < end; c += 128) {
-        uint32_t u[4];
-        double v[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const int e = c + 32 * k + lane;
-          u[k] = e < end ? pk[e] : kPad;
-          v[k] = u[k] != kPad ? (double)pv[e] * xs[u[k] & 0xffffu] : 0.0;
-        }
-        unsigned heads[4];
-        int sstart[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          // rows ascend inside a chunk: a segment head is a row change
-          const uint32_t up = __shfl_up_sync(0xffffffffu, u[k] >> 16, 1);
-          heads[k] = __ballot_sync(0xffffffffu, lane == 0 || up != (u[k] >> 16));
-          sstart[k] = 31 - __clz(heads[k] & upto);
-        }
-        // segmented inclusive scans; steps only while some segment is that long
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-          bool need = false;
-#pragma unroll
-          for (int k = 0; k < 4; ++k) need |= (lane - d >= sstart[k]);
-          if (!__any_sync(0xffffffffu, need)) break;
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const double vo = __shfl_up_sync(0xffffffffu, v[k], d);
-            if (lane - d >= sstart[k]) v[k] += vo;
-          }
-        }
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const bool tail = lane == 31 || ((heads[k] >> (lane + 1)) & 1u);
-          if (tail && u[k] != kPad) acc[u[k] >> 16] += v[k];  // chunk order kept: k ascending
-        }
+      int cb = 0;  // current block
+      long long cb_end = ofs[1];
+      if (!mbar_wait(&full[0], 0u)) atomicExch(fault, 1u);
+      uint32_t ua[kGroup], ub[kGroup];
+      VT va[kGroup], vb[kGroup];
+      // two register groups of 8 chunks: load group g+1 while folding group g
+#define SPK_LOAD(G0, UU, VV)                                     \
+  _Pragma("unroll") for (int k = 0; k < kGroup; ++k) {           \
+    const long long e = (G0) + 32 * k + lane;                    \
+    UU[k] = e < send ? __ldcs(H.packed + e) : kPad;              \
+    VV[k] = e < send ? __ldcs(gval + e) : (VT)0;                 \
+  }
+#define SPK_CONSUME(G0, UU, VV)                                                          \
+  _Pragma("unroll") for (int k = 0; k < kGroup; ++k) {                                   \
+    const long long c = (G0) + 32 * k;                                                   \
+    if (c < send) { /* warp-uniform; no break so the group stays in registers */        \
+      while (c >= cb_end) { /* leave block cb (release its tile), enter the next */      \
+        __syncwarp();                                                                    \
+        if (lane == 0) mbar_arrive(&empty[cb & 1]);                                      \
+        ++cb;                                                                            \
+        cb_end = ofs[cb + 1];                                                            \
+        if (!mbar_wait(&full[cb & 1], (uint32_t)((cb >> 1) & 1))) atomicExch(fault, 1u); \
+      }                                                                                  \
+      fold(UU[k], (double)VV[k], tiles + (size_t)(cb & 1) * kTileW, acc, lane, upto);    \
+    }                                                                                    \
+  }
+      const long long step = 32LL * kGroup;
+      long long g = sbeg;
+      if (g < send) { SPK_LOAD(g, ua, va) }
+      while (g < send) {
+        const long long g1 = g + step;
+        if (g1 < send) { SPK_LOAD(g1, ub, vb) }
+        SPK_CONSUME(g, ua, va)
+        g = g1;
+        if (g >= send) break;
+        const long long g2 = g + step;
+        if (g2 < send) { SPK_LOAD(g2, ua, va) }
+        SPK_CONSUME(g, ub, vb)
+        g = g2;
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
-      if (threadIdx.x == 0 && b + S < H.B) {
-        if (!mbar_wait(&empty[s], ph)) atomicExch(fault, 1u);  // all warps released stage s
-        issue(b + S);
+#undef SPK_LOAD
+#undef SPK_CONSUME
+      // release the remaining blocks in order (tile present before release)
+      for (;;) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[cb & 1]);
+        if (++cb >= B) break;
+        if (!mbar_wait(&full[cb & 1], (uint32_t)((cb >> 1) & 1))) atomicExch(fault, 1u);
       }
     }
     __syncthreads();
@@ -226,26 +236,26 @@ struct BlockedOp {
 
 // ---- layout builder --------------------------------------------------------------
 
+// key = ((slab * NW + warp) * B + block): the warp's whole stream is contiguous
 __global__ void key_kernel(const long long* ptr, const uint32_t* idx, int64_t n_out, const int* slab_of,
                            const unsigned char* warp_of, int W, int B, uint32_t* keys) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t i = warp; i < n_out; i += nw) {
-    const uint32_t base = (uint32_t)slab_of[i] * (uint32_t)B;
-    const uint32_t wv = warp_of[i];
-    for (long long q = ptr[i] + lane; q < ptr[i + 1]; q += 32) keys[q] = (base + idx[q] / (uint32_t)W) * kNW + wv;
+    const uint32_t base = ((uint32_t)slab_of[i] * kNW + warp_of[i]) * (uint32_t)B;
+    for (long long q = ptr[i] + lane; q < ptr[i + 1]; q += 32) keys[q] = base + idx[q] / (uint32_t)W;
   }
 }
 
-// Sorted position q (key k) -> padded destination seg_base[pb] + (q - useg[pb]).
+// Sorted position q (key k) -> padded destination seg_base[k] + (q - useg[k]).
 template <class VT>
 __global__ void pack_kernel(const uint32_t* keys_s, const uint32_t* perm, const uint32_t* idx, const VT* val,
                             const uint32_t* rows_of_pos, const int* slab_row0_of_row, const long long* useg,
                             const long long* seg_base, int W, int64_t m, uint32_t* packed, VT* vout) {
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < m; q += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t pb = keys_s[q] / kNW;
-    const long long dst = seg_base[pb] + (q - useg[pb]);
+    const uint32_t k = keys_s[q];
+    const long long dst = seg_base[k] + (q - useg[k]);
     const uint32_t src = perm[q];
     const uint32_t i = rows_of_pos[src];
     const uint32_t rl = i - (uint32_t)slab_row0_of_row[i];
@@ -279,8 +289,8 @@ int grid_cap(spk_ctx* ctx, int64_t items) {
 
 }  // namespace
 
-// Build one half's layout from (ptr, idx, val) with tile width W.
-// Returns false when the shape does not fit (rows per slab >= 2^16).
+// Build one half's layout from (ptr, idx, val). Returns false when the shape
+// does not fit (rows per slab >= 2^16).
 bool build_blocked(spk_ctx* ctx, int P, int W, int64_t n_out, int64_t n_in, int64_t m, const DBuf& ptr_d,
                    const DBuf& idx_d, const DBuf& val_d, int vbytes, BlockedHost& out) {
   std::vector<long long> ptr(n_out + 1);
@@ -296,7 +306,6 @@ bool build_blocked(spk_ctx* ctx, int P, int W, int64_t n_out, int64_t n_in, int6
   int max_rows = 0;
   for (int k = 0; k < P; ++k) max_rows = std::max(max_rows, slab_row0[k + 1] - slab_row0[k]);
   if (max_rows >= 65535) return false;
-  if ((int64_t)W > n_in) W = (int)std::max<int64_t>(16, ((n_in + 15) / 16) * 16);
   const int B = (int)((n_in + W - 1) / W);
   std::vector<int> slab_of(n_out), slab_row0_of_row(n_out);
   std::vector<unsigned char> warp_of(n_out);
@@ -318,8 +327,7 @@ bool build_blocked(spk_ctx* ctx, int P, int W, int64_t n_out, int64_t n_in, int6
       prev = r_end;
     }
   }
-  const int64_t npb = (int64_t)P * B;
-  const int64_t nkeys = npb * kNW;
+  const int64_t nkeys = (int64_t)P * kNW * B;
   if (nkeys >= (1LL << 32)) return false;
   cudaStream_t s = ctx->stream;
   const int64_t mm = std::max<int64_t>(m, 1);
@@ -346,31 +354,26 @@ bool build_blocked(spk_ctx* ctx, int P, int W, int64_t n_out, int64_t n_in, int6
   SPK_CUDA(cub::DeviceRadixSort::SortPairs(ctx->scratch.p, tb, keys.as<uint32_t>(), keys_s.as<uint32_t>(),
                                            iota.as<uint32_t>(), perm.as<uint32_t>(), (int)m, 0, end_bit, s));
   ++ctx->launches;
-  // host: padded (slab, block) segments and per-warp offsets in padded coordinates
+  // host: each (slab, warp, block) segment padded to 32 entries; per-warp block starts
   std::vector<unsigned long long> h(nkeys);
   download(ctx, h.data(), hist, sizeof(unsigned long long) * nkeys);
-  std::vector<long long> useg(npb), seg_base(npb + 1), off((size_t)npb * (kNW + 1));
+  std::vector<long long> useg(nkeys), seg_base(nkeys), off((size_t)P * kNW * (B + 1));
   long long u_acc = 0, p_acc = 0;
-  int ecap = 0;
-  for (int64_t pb = 0; pb < npb; ++pb) {
-    useg[pb] = u_acc;
-    seg_base[pb] = p_acc;
-    long long in_seg = 0;
-    for (int wv = 0; wv < kNW; ++wv) {
-      off[(size_t)pb * (kNW + 1) + wv] = p_acc + in_seg;
-      in_seg += (long long)h[pb * kNW + wv];
+  for (int64_t sw = 0; sw < (int64_t)P * kNW; ++sw) {
+    for (int b = 0; b < B; ++b) {
+      const int64_t k = sw * B + b;
+      useg[k] = u_acc;
+      seg_base[k] = p_acc;
+      off[(size_t)sw * (B + 1) + b] = p_acc;
+      u_acc += (long long)h[k];
+      p_acc += ((long long)h[k] + 31) & ~31LL;
     }
-    const long long padded = (in_seg + 3) & ~3LL;
-    off[(size_t)pb * (kNW + 1) + kNW] = p_acc + padded;  // padded end (bulk-copy extent)
-    ecap = std::max<int>(ecap, (int)padded);
-    u_acc += in_seg;
-    p_acc += padded;
+    off[(size_t)sw * (B + 1) + B] = p_acc;
   }
-  seg_base[npb] = p_acc;
-  const int64_t total = std::max<long long>(p_acc, 4);
+  const int64_t total = std::max<long long>(p_acc, 32);
   DBuf d_useg, d_seg;
-  upload(ctx, d_useg, useg.data(), sizeof(long long) * npb);
-  upload(ctx, d_seg, seg_base.data(), sizeof(long long) * (npb + 1));
+  upload(ctx, d_useg, useg.data(), sizeof(long long) * nkeys);
+  upload(ctx, d_seg, seg_base.data(), sizeof(long long) * nkeys);
   upload(ctx, out.off, off.data(), sizeof(long long) * off.size());
   upload(ctx, out.slab_row0, slab_row0.data(), sizeof(int) * (P + 1));
   out.packed.alloc(sizeof(uint32_t) * total);
@@ -393,7 +396,7 @@ bool build_blocked(spk_ctx* ctx, int P, int W, int64_t n_out, int64_t n_in, int6
   SPK_CUDA(cudaGetLastError());
   SPK_CUDA(cudaStreamSynchronize(s));
   out.max_rows = max_rows;
-  out.ecap = ecap;
+  out.ecap = 0;
   out.h.P = P;
   out.h.B = B;
   out.h.W = W;
@@ -416,26 +419,15 @@ bool run_blocked_t(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, doub
   if (!sk->blocked_tried) {
     sk->blocked_tried = true;
     const int vb = sizeof(VT);
-    // shrink the tile until acc + S stages fit (E_cap shrinks with W)
-    for (int W = std::min(ctx->blocked_max_w, 2048); W >= 16; W >>= 1) {
-      auto R = std::make_unique<BlockedHost>(), C = std::make_unique<BlockedHost>();
-      if (!build_blocked(ctx, P, W, n, n, sk->nnz, sk->row_ptr, sk->col_idx, sk->values, vb, *R) ||
-          !build_blocked(ctx, P, W, n, n, sk->nnz, sk->col_ptr, sk->row_idx, sk->values_t, vb, *C))
-        break;
+    const int W = std::min(kTileW, std::max(16, ctx->blocked_max_w));
+    auto R = std::make_unique<BlockedHost>(), C = std::make_unique<BlockedHost>();
+    if (build_blocked(ctx, P, W, n, n, sk->nnz, sk->row_ptr, sk->col_idx, sk->values, vb, *R) &&
+        build_blocked(ctx, P, W, n, n, sk->nnz, sk->col_ptr, sk->row_idx, sk->values_t, vb, *C)) {
       BlockedOp<VT> probe{};
       probe.acc_rows = std::max(R->max_rows, C->max_rows);
-      probe.W = std::max(R->h.W, C->h.W);
-      probe.ecap = std::max(R->ecap, C->ecap);
-      int S = 6;
-      for (; S >= 2; --S) {
-        probe.S = S;
-        if (probe.smem_bytes() <= budget) break;
-      }
-      if (S >= 2) {
-        sk->blocked_stages = S;
+      if (probe.smem_bytes() <= budget) {
         sk->blk_rows = std::move(R);
         sk->blk_cols = std::move(C);
-        break;
       }
     }
   }
@@ -445,9 +437,6 @@ bool run_blocked_t(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, doub
   op.L[1] = sk->blk_cols->h;
   op.n = n;
   op.acc_rows = std::max(sk->blk_rows->max_rows, sk->blk_cols->max_rows);
-  op.W = std::max(op.L[0].W, op.L[1].W);
-  op.ecap = std::max(sk->blk_rows->ecap, sk->blk_cols->ecap);
-  op.S = sk->blocked_stages;
   LoopWs& W = sk->ws;
   W.scalar.ensure(sizeof(unsigned int));
   SPK_CUDA(cudaMemsetAsync(W.scalar.p, 0, sizeof(unsigned int), ctx->stream));
@@ -460,7 +449,7 @@ bool run_blocked_t(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, doub
                             /*useful_blocks=*/P, out, /*exact_grid=*/P, op.smem_bytes());
   unsigned int fault = 0;
   download(ctx, &fault, W.scalar, sizeof fault);
-  if (fault) fail_device("blocked loop: a TMA stage never completed", cudaErrorLaunchTimeout);
+  if (fault) fail_device("blocked loop: a TMA tile never completed", cudaErrorLaunchTimeout);
   return true;
 }
 

@@ -33,6 +33,8 @@ using loopcore::finalize_atom;
 // Shared body for dense/exact operators: ROLE 0 = rows, ROLE 1 = columns.
 template <class KF>
 struct ExactOp {
+  static constexpr int kThreads = loopcore::kBlock;
+  static constexpr int kMinBlocks = 2;
   KF k;
   int64_t n;
 
@@ -166,6 +168,8 @@ constexpr int kOtfChunk = 256; // columns per fp32 partial
 // alpha*|y_j|^2, with alpha = -log2(e)/(scale*eps), so
 // K_ij = exp2(bias_i + bias_j + <p_i, y_j>) = exp(-|x_i - y_j|^2/(scale*eps)).
 struct OtfFastOp {
+  static constexpr int kThreads = loopcore::kBlock;
+  static constexpr int kMinBlocks = 2;
   int64_t n;
   int dim;
   const float4* out_rec[2];  // [role] output-side records (2 float4 per atom)

@@ -87,7 +87,9 @@ struct BlockedHost {
 struct spk_sketch {
   spk_ctx* ctx = nullptr;  // must outlive every call but spk_sketch_free
   int device = 0;
-  int64_t n = 0;
+  int64_t n = 0;         // rows (all atoms, or this shard's row slab)
+  int64_t n_cols = 0;    // columns when != n (row slab of a sharded sketch), else 0
+  int64_t row_base = 0;  // global index of local row 0
   int64_t nnz = 0;
   int value_type = SPK_VALUES_F64;  // storage of values / values_t
   spk::DBuf row_ptr, col_idx, values;   // int64[n+1], u32[nnz], f64|f32[nnz]
@@ -200,8 +202,10 @@ struct PlanInfo {
 
 void build_plan(spk_ctx* ctx, DevKernel& dk, const double* a, const double* b, int plan_kind,
                 double lambda, double eps, double theta, PlanInfo& plan);
+// Samples rows [row0, row1) (default: all) of the plan into sk (a row slab
+// with global column indices when sharded).
 void sample_sketch(spk_ctx* ctx, DevKernel& dk, const PlanInfo& plan, double s, uint64_t seed,
-                   int value_type, spk_sketch* sk);
+                   int value_type, spk_sketch* sk, int64_t row0 = 0, int64_t row1 = -1);
 void build_csc(spk_ctx* ctx, spk_sketch* sk);
 void cost_kernel_query(spk_ctx* ctx, DevKernel& dk, int64_t m, const int64_t* qi, const int64_t* qj,
                        double* cost, double* kern);

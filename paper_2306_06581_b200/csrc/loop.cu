@@ -91,6 +91,8 @@ __device__ __forceinline__ double row_apply(const VT* __restrict__ val, const ui
 
 template <class VT>
 struct SparseOp {
+  static constexpr int kThreads = loopcore::kBlock;
+  static constexpr int kMinBlocks = 2;
   int64_t n;
   const long long* row_ptr;
   const uint32_t* col_idx;

@@ -171,7 +171,7 @@ __device__ inline void reduce_parts(const Part* p, int nb, double& err, long lon
 //       unsigned long long* flag, double* absdiff, double& err, long long& masks) const;
 // ROLE 0 = rows of K (u-half, x = v), ROLE 1 = columns (v-half, x = u).
 template <bool LOG, bool DET, class Op>
-__global__ void __launch_bounds__(kBlock) loop_kernel(Common P, Op op) {
+__global__ void __launch_bounds__(Op::kThreads, Op::kMinBlocks) loop_kernel(Common P, Op op) {
   cg::grid_group grid = cg::this_grid();
   const int nb = gridDim.x;
   double* U[2] = {P.u0, P.u1};
@@ -389,7 +389,7 @@ void run_core(spk_ctx* ctx, const Op& op, int64_t n, LoopWs& W, long long masked
   if (dyn_smem > 0)
     SPK_CUDA(cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_smem));
   int per_sm = 0;
-  SPK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBlock, dyn_smem));
+  SPK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, Op::kThreads, dyn_smem));
   if (per_sm < 1) fail_device("loop_kernel occupancy", cudaErrorLaunchOutOfResources);
   if (ctx->loop_blocks_per_sm > 0) per_sm = std::min(per_sm, ctx->loop_blocks_per_sm);
   int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->num_sms * per_sm, useful_blocks));
@@ -435,7 +435,7 @@ void run_core(spk_ctx* ctx, const Op& op, int64_t n, LoopWs& W, long long masked
   Op op_copy = op;
   void* args[] = {&P, &op_copy};
   Timer tm(s);
-  SPK_CUDA(cudaLaunchCooperativeKernel((void*)kern, dim3(grid), dim3(kBlock), args, dyn_smem, s));
+  SPK_CUDA(cudaLaunchCooperativeKernel((void*)kern, dim3(grid), dim3(Op::kThreads), args, dyn_smem, s));
   ++ctx->launches;
   out.loop_s = tm.stop();
   SPK_CUDA(cudaGetLastError());

@@ -156,17 +156,18 @@ __global__ void reduce_rows_kernel(const T* v, int64_t n, T* out) {
 // ---- passes 2/3: Poisson sampling (poisson_sparsify :169-201) --------------------
 
 template <bool EMIT, class VT>
-__global__ void sample_rows_kernel(KSrc S, DPlan P, double s, uint64_t seed, long long* row_cnt,
-                                   const long long* row_ptr, uint32_t* col_out, VT* val_out) {
+__global__ void sample_rows_kernel(KSrc S, DPlan P, double s, uint64_t seed, int64_t row_base, int64_t n_rows,
+                                   long long* row_cnt, const long long* row_ptr, uint32_t* col_out, VT* val_out) {
   const int lane = threadIdx.x & 31;
   const unsigned lt_mask = (1u << lane) - 1u;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t i = warp; i < S.n; i += nwarps) {
+  for (int64_t li = warp; li < n_rows; li += nwarps) {
+    const int64_t i = row_base + li;  // global row: RNG stream, coordinates, plan weights
     const uint64_t state0 = mix_seed(seed, (uint64_t)i);
     uint64_t base_t = 0;
     long long cnt = 0;
-    const long long out0 = EMIT ? row_ptr[i] : 0;
+    const long long out0 = EMIT ? row_ptr[li] : 0;
     for (int64_t j0 = 0; j0 < S.n; j0 += 32) {
       const int64_t j = j0 + lane;
       const double k = (j < S.n) ? kernel_entry(S, i, j) : 0.0;
@@ -195,7 +196,7 @@ __global__ void sample_rows_kernel(KSrc S, DPlan P, double s, uint64_t seed, lon
       }
       cnt += __popc(km);
     }
-    if (!EMIT && lane == 0) row_cnt[i] = cnt;
+    if (!EMIT && lane == 0) row_cnt[li] = cnt;
   }
 }
 
@@ -330,7 +331,9 @@ constexpr int kTileRows = 8 * kRPW;
 struct TiledArgs {
   const double* x;
   const double* y;
-  int64_t n;
+  int64_t n;        // columns (target points)
+  int64_t n_rows;   // rows handled (a slab of sources for sharded builds)
+  int64_t row_base; // global index of local row 0
   int dim, kind;
   double eta, scale, eps;
   double lo, hi;  // d2 < lo: supported; d2 >= hi: not; else exact
@@ -359,7 +362,7 @@ __global__ void __launch_bounds__(256) tiled_kernel(TiledArgs A) {
   const int lane = threadIdx.x & 31;
   const int w = threadIdx.x >> 5;
   const unsigned lt_mask = (1u << lane) - 1u;
-  const int64_t groups = (A.n + kTileRows - 1) / kTileRows;
+  const int64_t groups = (A.n_rows + kTileRows - 1) / kTileRows;
   for (int64_t g = blockIdx.x; g < groups; g += gridDim.x) {
     double xr[kRPW][DIM];
     uint64_t st0[kRPW];
@@ -371,10 +374,10 @@ __global__ void __launch_bounds__(256) tiled_kernel(TiledArgs A) {
 #pragma unroll
     for (int q = 0; q < kRPW; ++q) {
       row[q] = g * kTileRows + w * kRPW + q;
-      const bool valid = row[q] < A.n;
+      const bool valid = row[q] < A.n_rows;
 #pragma unroll
-      for (int k = 0; k < DIM; ++k) xr[q][k] = valid ? A.x[row[q] * DIM + k] : 0.0;
-      st0[q] = mix_seed(A.seed, (uint64_t)row[q]);
+      for (int k = 0; k < DIM; ++k) xr[q][k] = valid ? A.x[(A.row_base + row[q]) * DIM + k] : 0.0;
+      st0[q] = mix_seed(A.seed, (uint64_t)(A.row_base + row[q]));
       tcnt[q] = 0;
       cnt[q] = 0;
       racc[q] = 0.0;
@@ -400,7 +403,7 @@ __global__ void __launch_bounds__(256) tiled_kernel(TiledArgs A) {
         const double cw = jvalid ? A.P.col_w[j] : 0.0;
 #pragma unroll
         for (int q = 0; q < kRPW; ++q) {
-          const bool valid = jvalid && row[q] < A.n;
+          const bool valid = jvalid && row[q] < A.n_rows;
           double d2 = 0.0;
 #pragma unroll
           for (int k = 0; k < DIM; ++k) {
@@ -418,7 +421,7 @@ __global__ void __launch_bounds__(256) tiled_kernel(TiledArgs A) {
           if (!SAMPLE) {
             if (nz) {
               ++cnt[q];
-              const double rw = A.P.row_w[row[q]];
+              const double rw = A.P.row_w[A.row_base + row[q]];
               racc[q] += (A.P.kind == SPK_PLAN_UOT) ? dmul(dmul(rw, cw), pow(kv, A.P.g_k))
                          : (A.P.kind == SPK_PLAN_UNIFORM) ? 1.0 : dmul(rw, cw);
             }
@@ -430,7 +433,7 @@ __global__ void __launch_bounds__(256) tiled_kernel(TiledArgs A) {
           bool keep = false;
           double ps = 0.0;
           if (nz) {
-            const double rw = A.P.row_w[row[q]];
+            const double rw = A.P.row_w[A.row_base + row[q]];
             double base_p;
             if (A.P.factorized) base_p = dmul(rw, cw);
             else {
@@ -461,7 +464,7 @@ __global__ void __launch_bounds__(256) tiled_kernel(TiledArgs A) {
     }
 #pragma unroll
     for (int q = 0; q < kRPW; ++q) {
-      if (row[q] >= A.n) continue;
+      if (row[q] >= A.n_rows) continue;
       if (!SAMPLE) {
         const long long c = warp_sum_ll((long long)cnt[q]);
         const double sacc = warp_sum(racc[q]);
@@ -496,12 +499,12 @@ __global__ void threshold_kernel(TiledArgs A, double* out) {
 
 // Upper bound of each row's expected kept count -> slot capacity
 // (count is a sum of independent Bernoullis with mean <= U: cap U + 6 sqrt(U) + 16).
-__global__ void slot_cap_kernel(int64_t n, const long long* row_nnz, const double* row_sum, const double* row_w,
-                                double col_w_total, int factorized, double inv, double s, int theta_mode, double omt,
+__global__ void slot_cap_kernel(int64_t n, int64_t row_base, int64_t n_cols, const long long* row_nnz,
+                                const double* row_sum, const double* row_w, double col_w_total, int factorized, double inv, double s, int theta_mode, double omt,
                                 double unif, int* cap) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const double supp = row_nnz ? (double)row_nnz[i] : (double)n;
-    double mass = factorized ? row_w[i] * col_w_total : row_sum[i] * inv;
+    const double supp = row_nnz ? (double)row_nnz[i] : (double)n_cols;
+    double mass = factorized ? row_w[row_base + i] * col_w_total : row_sum[i] * inv;
     if (theta_mode) mass = omt * mass + unif * supp;
     const double u = fmin(supp, s * mass * (1.0 + 1e-9));
     const double c = fmin(supp, ceil(u + 6.0 * sqrt(u) + 16.0));
@@ -533,7 +536,7 @@ __global__ void int_to_ll_kernel(const int* a, int64_t n, long long* b) {
 
 template <bool SAMPLE, bool NEEDK, class VT>
 void launch_tiled(spk_ctx* ctx, const TiledArgs& A) {
-  const int64_t groups = (A.n + kTileRows - 1) / kTileRows;
+  const int64_t groups = (A.n_rows + kTileRows - 1) / kTileRows;
 #define SPK_TILED_CASE(D)                                                                                    \
   case D: {                                                                                                  \
     int occ = 0;                                                                                             \
@@ -566,6 +569,8 @@ TiledArgs tiled_args(spk_ctx* ctx, const DevKernel& dk) {
   A.x = dk.x.as<double>();
   A.y = dk.y.as<double>();
   A.n = dk.n;
+  A.n_rows = dk.n;
+  A.row_base = 0;
   A.dim = dk.dim;
   A.kind = dk.kind;
   A.eta = dk.eta;
@@ -822,17 +827,21 @@ void cost_kernel_query(spk_ctx* ctx, DevKernel& dk, int64_t m, const int64_t* qi
 }
 
 void sample_sketch(spk_ctx* ctx, DevKernel& dk, const PlanInfo& plan, double s, uint64_t seed,
-                   int value_type, spk_sketch* sk) {
-  const int64_t n = dk.n;
-  const double nn = static_cast<double>(n) * static_cast<double>(n);
+                   int value_type, spk_sketch* sk, int64_t row0, int64_t row1) {
+  const int64_t ncols = dk.n;
+  if (row1 < 0) row1 = ncols;
+  const int64_t n = row1 - row0;  // rows sampled here (all of them unless sharded)
+  const double nn = static_cast<double>(ncols) * static_cast<double>(ncols);
   if (!(s > 0.0) || s >= nn) fail(SPK_E_BUDGET_TOO_LARGE, "budget s must satisfy 0 < s < n^2");
   DBuf rw, cw;
-  upload(ctx, rw, plan.row_w.data(), sizeof(double) * n);
-  upload(ctx, cw, plan.col_w.data(), sizeof(double) * n);
+  upload(ctx, rw, plan.row_w.data(), sizeof(double) * ncols);
+  upload(ctx, cw, plan.col_w.data(), sizeof(double) * ncols);
   DPlan P = device_plan(plan, rw.as<double>(), cw.as<double>());
   KSrc S = make_src(dk);
 
   sk->n = n;
+  sk->n_cols = (n == ncols) ? 0 : ncols;
+  sk->row_base = row0;
   sk->seed = seed;
   sk->value_type = value_type;
   sk->kernel_nnz = plan.kernel_nnz;
@@ -848,9 +857,9 @@ void sample_sketch(spk_ctx* ctx, DevKernel& dk, const PlanInfo& plan, double s, 
     // ---- single pass: row slots sized from the plan's row masses ----
     DBuf cap(sizeof(int) * n), capll(sizeof(long long) * n), off(sizeof(long long) * (n + 1));
     double col_total = 0.0;
-    for (int64_t j = 0; j < n; ++j) col_total += plan.col_w[j];
+    for (int64_t j = 0; j < ncols; ++j) col_total += plan.col_w[j];
     slot_cap_kernel<<<grid_for(ctx, n, 256), 256, 0, ctx->stream>>>(
-        n, plan.have_rows ? plan.d_row_nnz.as<long long>() : nullptr,
+        n, row0, dk.n, plan.have_rows ? plan.d_row_nnz.as<long long>() : nullptr,
         plan.have_rows ? plan.d_row_sum.as<double>() : nullptr, rw.as<double>(), col_total,
         plan.factorized ? 1 : 0, plan.inv, s, P.theta_mode, P.omt, P.unif, cap.as<int>());
     int_to_ll_kernel<<<grid_for(ctx, n, 256), 256, 0, ctx->stream>>>(cap.as<int>(), n, capll.as<long long>());
@@ -869,6 +878,8 @@ void sample_sketch(spk_ctx* ctx, DevKernel& dk, const PlanInfo& plan, double s, 
     DBuf rcnt(sizeof(int) * n), ovf(sizeof(unsigned int));
     SPK_CUDA(cudaMemsetAsync(ovf.p, 0, sizeof(unsigned int), ctx->stream));
     TiledArgs A = tiled_args(ctx, dk);
+    A.n_rows = n;
+    A.row_base = row0;
     A.P = P;
     A.s = s;
     A.seed = seed;
@@ -916,7 +927,7 @@ void sample_sketch(spk_ctx* ctx, DevKernel& dk, const PlanInfo& plan, double s, 
 
   DBuf cnt(sizeof(long long) * n);
   const int grid = grid_for_rows(ctx, n, 8);
-  sample_rows_kernel<false, double><<<grid, 256, 0, ctx->stream>>>(S, P, s, seed, cnt.as<long long>(),
+  sample_rows_kernel<false, double><<<grid, 256, 0, ctx->stream>>>(S, P, s, seed, row0, n, cnt.as<long long>(),
                                                                    nullptr, nullptr, nullptr);
   ++ctx->launches;
   // row_ptr = exclusive scan of counts, row_ptr[n] = nnz
@@ -937,11 +948,14 @@ void sample_sketch(spk_ctx* ctx, DevKernel& dk, const PlanInfo& plan, double s, 
   sk->col_idx.alloc(sizeof(uint32_t) * std::max<long long>(nnz, 1));
   sk->values.alloc(vbytes * std::max<long long>(nnz, 1));
   if (value_type == SPK_VALUES_F32)
-    sample_rows_kernel<true, float><<<grid, 256, 0, ctx->stream>>>(
-        S, P, s, seed, nullptr, sk->row_ptr.as<long long>(), sk->col_idx.as<uint32_t>(), sk->values.as<float>());
+    sample_rows_kernel<true, float><<<grid, 256, 0, ctx->stream>>>(S, P, s, seed, row0, n, nullptr,
+                                                                   sk->row_ptr.as<long long>(),
+                                                                   sk->col_idx.as<uint32_t>(), sk->values.as<float>());
   else
-    sample_rows_kernel<true, double><<<grid, 256, 0, ctx->stream>>>(
-        S, P, s, seed, nullptr, sk->row_ptr.as<long long>(), sk->col_idx.as<uint32_t>(), sk->values.as<double>());
+    sample_rows_kernel<true, double><<<grid, 256, 0, ctx->stream>>>(S, P, s, seed, row0, n, nullptr,
+                                                                    sk->row_ptr.as<long long>(),
+                                                                    sk->col_idx.as<uint32_t>(),
+                                                                    sk->values.as<double>());
   ++ctx->launches;
   SPK_CUDA(cudaGetLastError());
   build_csc(ctx, sk);
@@ -950,11 +964,12 @@ void sample_sketch(spk_ctx* ctx, DevKernel& dk, const PlanInfo& plan, double s, 
 
 void build_csc(spk_ctx* ctx, spk_sketch* sk) {
   const int64_t n = sk->n, m = sk->nnz;
+  const int64_t nc = sk->n_cols ? sk->n_cols : n;  // columns
   const size_t vbytes = sk->value_type == SPK_VALUES_F32 ? 4 : 8;
-  sk->col_ptr.alloc(sizeof(long long) * (n + 1));
+  sk->col_ptr.alloc(sizeof(long long) * (nc + 1));
   sk->row_idx.alloc(sizeof(uint32_t) * std::max<int64_t>(m, 1));
   sk->values_t.alloc(vbytes * std::max<int64_t>(m, 1));
-  DBuf cnt(sizeof(long long) * n);
+  DBuf cnt(sizeof(long long) * nc);
   SPK_CUDA(cudaMemsetAsync(cnt.p, 0, cnt.bytes, ctx->stream));
   SPK_CUDA(cudaMemsetAsync(sk->col_ptr.p, 0, sizeof(long long), ctx->stream));
   if (m > 0) {
@@ -967,7 +982,7 @@ void build_csc(spk_ctx* ctx, spk_sketch* sk) {
                                                                      cnt.as<long long>());
     ctx->launches += 3;
     int end_bit = 1;
-    while ((int64_t(1) << end_bit) < n) ++end_bit;
+    while ((int64_t(1) << end_bit) < nc) ++end_bit;
     size_t tmp_bytes = 0;
     // Stable LSD radix sort by column: equal columns keep CSR (row-major)
     // order, i.e. rows ascend inside each column as spmv_t visits them.
@@ -991,10 +1006,10 @@ void build_csc(spk_ctx* ctx, spk_sketch* sk) {
   }
   size_t tmp_bytes = 0;
   SPK_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tmp_bytes, cnt.as<long long>(), sk->col_ptr.as<long long>() + 1,
-                                         (int)n, ctx->stream));
+                                         (int)nc, ctx->stream));
   ctx->scratch.ensure(tmp_bytes);
   SPK_CUDA(cub::DeviceScan::InclusiveSum(ctx->scratch.p, tmp_bytes, cnt.as<long long>(),
-                                         sk->col_ptr.as<long long>() + 1, (int)n, ctx->stream));
+                                         sk->col_ptr.as<long long>() + 1, (int)nc, ctx->stream));
   ++ctx->launches;
   SPK_CUDA(cudaGetLastError());
 }
@@ -1024,7 +1039,8 @@ double sketch_kernel_mean(spk_ctx* ctx, spk_sketch* sk) {
       download(ctx, &acc, out, sizeof acc);
     }
   }
-  const double nd = static_cast<double>(sk->n);
+  // A row shard holds a partial sum of the full n x n estimate; shards add up.
+  const double nd = static_cast<double>(sk->n_cols ? sk->n_cols : sk->n);
   return acc / (nd * nd);
 }
 
