@@ -165,7 +165,7 @@ enum spk_option {
   SPK_OPT_DETERMINISTIC = 1,
   SPK_OPT_LOOP_BLOCKS_PER_SM = 2,
   SPK_OPT_OTF_FP32 = 3,      /* dense on-the-fly comparator: K in fp32 (1) or fp64 (0) */
-  SPK_OPT_BLOCKED_LOOP = 4,  /* fast sparse loop: slab x block layout (1) or CSR/CSC (0) */
+  SPK_OPT_BLOCKED_LOOP = 4,  /* fast sparse loop: slab x block layout (1), CSR/CSC (0), auto (2, default: n >= 2^17) */
   SPK_OPT_BLOCKED_MAX_W = 5, /* cap on the staged tile width (testing) */
   SPK_OPT_TWO_PASS_SAMPLER = 6 /* sampler: always the exact two-pass kernels (testing) */
 };
@@ -239,6 +239,89 @@ int spk_plan_readout(spk_ctx* ctx, const spk_kernel_desc* kd, int64_t n, const i
                      const double* log_u, const double* log_v, int log_domain, const double* a,
                      const double* b, int uot, double lambda, double epsilon, double* row_marginal,
                      double* col_marginal, double* objective, double* residual_row, double* residual_col);
+
+/* ---- row/column-sharded Spar-Sink (one process per GPU) ----------------------
+ *
+ * rank r of a world of W owns atoms [r*m, min(n, (r+1)*m)),
+ * m = ceil(n / W) -- those ROWS of K~ (sampled locally with the reference's
+ * per-row RNG streams, so the union over ranks is bit-identical to the
+ * single-GPU sketch) and those COLUMNS (a CSC assembled once by an
+ * all-to-all of the row slabs' entries). Each half-step is then local: the
+ * rank updates its slab of u (or v) from the full gathered v (or u), and
+ * one all-gather (the caller's collective, NCCL over NVLink) completes the
+ * vector. A gathered vector holds W blocks of `stride` = m + SPK_SHARD_TAIL
+ * doubles: the rank's slab followed by its tail (residual partial, mask
+ * count, first failing index), so the stop decisions ride on the same
+ * collective and every rank takes them identically on the device without a
+ * host round trip. Replaces the loop of detail::scaling_loop /
+ * log_scaling_loop (solvers.hpp:256-513) for a row/column-partitioned
+ * SparseKernel; the caller-side driver is paper_2306_06581_b200/sharded.py.
+ * Buffers named *_dev are device pointers on the context's device. */
+#define SPK_SHARD_TAIL 8
+typedef struct spk_shard spk_shard;
+
+/* Plan stage 1: the support / grid-normaliser pass (masked_grid_plan,
+ * sparsify.cpp:49-67) over this rank's rows. *needs_pass = 0 when the plan
+ * is factorized (no pass; outputs untouched). row_sum_dev / row_nnz_dev:
+ * slab-length device arrays. */
+int spk_shard_plan_rows(spk_ctx* ctx, const spk_kernel_desc* kd, const double* a, const double* b,
+                        int plan_kind, double lambda, double epsilon, int32_t world, int32_t rank,
+                        double* row_sum_dev, int64_t* row_nnz_dev, int32_t* needs_pass);
+/* Plan stage 2 + poisson_sparsify of this rank's rows. row_sum_all_dev /
+ * row_nnz_all_dev: the n per-row values of stage 1 gathered in rank order
+ * (NULL when no pass is needed); the normaliser is their fixed-order total,
+ * bit-identical to the single-GPU plan. kd must be the coordinate form. */
+int spk_shard_create(spk_ctx* ctx, const spk_kernel_desc* kd, const double* a, const double* b,
+                     int plan_kind, double lambda, double epsilon, double s, uint64_t seed,
+                     const spk_sketch_opts* opts, int32_t world, int32_t rank,
+                     const double* row_sum_all_dev, const int64_t* row_nnz_all_dev, spk_shard** out);
+void spk_shard_free(spk_shard* sh);
+/* Geometry and sizes: n, slab width m, gathered block stride, this rank's
+ * slab [lo, hi), nnz of its row slab and (after import) of its column slab,
+ * value bytes (4 or 8), its share of kernel_mean, kernel support, plan flag. */
+int spk_shard_info(const spk_shard* sh, int64_t* n, int64_t* m, int64_t* stride, int64_t* lo, int64_t* hi,
+                   int64_t* row_nnz, int64_t* col_nnz, int32_t* value_bytes, double* kernel_mean_part,
+                   int64_t* kernel_nnz, int32_t* factorized_plan);
+/* Column exchange, send side: the row slab's entries grouped by column
+ * (rows ascending inside a column). counts_dev: W*m int64 per-column counts
+ * (block d = columns owned by rank d, zero-padded to m); rows_dev: row_nnz
+ * uint32 GLOBAL row indices; vals_dev: row_nnz values (value_bytes each);
+ * send_sizes: W host int64 entry totals per destination. */
+int spk_shard_export(spk_shard* sh, int64_t* counts_dev, uint32_t* rows_dev, void* vals_dev, int64_t* send_sizes);
+/* Receive side: recv_counts_dev = W*m int64 (source-major), entries from
+ * sources 0..W-1 concatenated in order (`total` of them). Builds the column
+ * slab's CSC with rows ascending inside each column (spmv_t order). */
+int spk_shard_import(spk_shard* sh, const int64_t* recv_counts_dev, const uint32_t* recv_rows_dev,
+                     const void* recv_vals_dev, int64_t total);
+/* Structural coverage of this rank's rows and columns (kernel_coverage,
+ * solvers.cpp:138-163): empty counts of its slab. */
+int spk_shard_coverage(spk_shard* sh, int64_t* empty_rows, int64_t* empty_cols);
+/* Start a loop (sinkhorn_ot/uot checks, solvers.hpp:209-232, on the
+ * weights given at create): totals of the coverage counts over all ranks
+ * and the policy. Writes this rank's block (and tail) of u0_dev / v0_dev
+ * (gathered-layout buffers); the caller all-gathers v0 before iteration 1. */
+int spk_shard_begin(spk_shard* sh, const spk_solver_cfg* cfg, int uot, int policy, int64_t empty_rows_total,
+                    int64_t empty_cols_total, double* u0_dev, double* v0_dev);
+/* One half-step of iteration t >= 1. half 0: u-slab from x_dev = gathered
+ * v of t-1 into out_dev (own block of gathered u of t), old_dev = gathered
+ * u of t-1. half 1: v-slab from x_dev = gathered u of t, old_dev = gathered
+ * v of t-1, out_dev = gathered v of t. First applies the decision of the
+ * previous half (its tails in x_dev); no-op once the loop has stopped. */
+int spk_shard_half(spk_shard* sh, int half, int64_t t, const double* x_dev, const double* old_dev, double* out_dev);
+/* Decision on the v-half of iteration t_last (its gathered vector) after
+ * the caller's last iteration. */
+int spk_shard_finish(spk_shard* sh, int64_t t_last, const double* v_last_dev);
+/* Loop state (synchronises): iterations, converged, diverged, masked
+ * counts into rep; *stopped; *final_parity = which of the two ping-pong
+ * buffers holds the result. Returns the reference's error status
+ * (ZeroDenominator / DegenerateSketchError) when the loop raised. */
+int spk_shard_status(spk_shard* sh, spk_report* rep, int32_t* stopped, int32_t* final_parity);
+/* Readout partials of this rank (for_each_entry over its row slab, column
+ * marginals over its column slab): out[0..7] = residual_row, residual_col,
+ * <T,C>, H(T), KL row term, KL column term, first row with mass on an
+ * infinite cost + 1 (0 = none), first atom with KL mass off support + 1. */
+int spk_shard_readout(spk_shard* sh, const double* u_dev, const double* v_dev, int log_domain, int uot,
+                      int want_objective, double* out);
 
 /* ---- helpers exposed for parity tests --------------------------------------- */
 

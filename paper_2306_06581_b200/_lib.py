@@ -98,7 +98,26 @@ SIGNATURES = {
                                  C.c_double, C.c_int64, I64P, I64P, DP, C.POINTER(C.c_int32)]),
     "spk_kernel_from_cost": (C.c_int, [C.c_void_p, DP, C.c_int64, C.c_double, DP, I64P]),
     "spk_cost_kernel": (C.c_int, [C.c_void_p, C.POINTER(KernelDesc), C.c_int64, I64P, I64P, DP, DP, DP]),
+    # row/column-sharded solve (device pointers travel as c_void_p)
+    "spk_shard_plan_rows": (C.c_int, [C.c_void_p, C.POINTER(KernelDesc), DP, DP, C.c_int, C.c_double, C.c_double,
+                                      C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.POINTER(C.c_int32)]),
+    "spk_shard_create": (C.c_int, [C.c_void_p, C.POINTER(KernelDesc), DP, DP, C.c_int, C.c_double, C.c_double,
+                                   C.c_double, C.c_uint64, C.POINTER(SketchOpts), C.c_int32, C.c_int32, C.c_void_p,
+                                   C.c_void_p, C.POINTER(C.c_void_p)]),
+    "spk_shard_free": (None, [C.c_void_p]),
+    "spk_shard_info": (C.c_int, [C.c_void_p, I64P, I64P, I64P, I64P, I64P, I64P, I64P, C.POINTER(C.c_int32), DP, I64P,
+                                 C.POINTER(C.c_int32)]),
+    "spk_shard_export": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, I64P]),
+    "spk_shard_import": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64]),
+    "spk_shard_coverage": (C.c_int, [C.c_void_p, I64P, I64P]),
+    "spk_shard_begin": (C.c_int, [C.c_void_p, C.POINTER(SolverCfg), C.c_int, C.c_int, C.c_int64, C.c_int64, C.c_void_p,
+                                  C.c_void_p]),
+    "spk_shard_half": (C.c_int, [C.c_void_p, C.c_int, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "spk_shard_finish": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p]),
+    "spk_shard_status": (C.c_int, [C.c_void_p, C.POINTER(Report), C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
+    "spk_shard_readout": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, DP]),
 }
+SHARD_TAIL = 8  # SPK_SHARD_TAIL
 
 _lib = None
 

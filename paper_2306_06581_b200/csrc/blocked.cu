@@ -31,6 +31,8 @@
 // random 32-byte sector per entry.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <numeric>
 #include <vector>
 
@@ -44,9 +46,10 @@ namespace spk {
 
 namespace {
 
-constexpr int kNW = 16;                 // consumer warps per CTA
+constexpr int kNW = 15;                 // consumer warps per CTA (+1 producer = 16 warps: 4 per SMSP, 128 registers)
 constexpr int kThreadsBlocked = 32 * (kNW + 1);
-constexpr int kTileW = 8192;            // x tile: 64 KB of fp64
+constexpr int kTileW = 4096;            // x tile: 32 KB of fp64
+constexpr int kStages = 4;              // tile ring depth
 constexpr int kGroup = 8;               // chunks of 32 entries per prefetch group
 constexpr uint32_t kPad = 0xffffffffu;  // padding entry (never a valid packed value)
 
@@ -64,10 +67,11 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-// Bounded wait: false after ~2^24 polls (a lost transaction must not hang the
+// Bounded wait: false after ~2^20 polls (a lost transaction must not hang the
 // GPU; the caller records a fault and the host raises it).
-__device__ __forceinline__ bool mbar_wait(uint64_t* bar, uint32_t parity) {
-  for (int spin = 0; spin < (1 << 24); ++spin) {
+__device__ __forceinline__ bool mbar_wait(uint64_t* bar, uint32_t parity, const unsigned int* fault) {
+  if (__ldcg(fault)) return false;  // already failed: drain fast
+  for (int spin = 0; spin < (1 << 20); ++spin) {
     uint32_t done;
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
@@ -89,36 +93,34 @@ __device__ __forceinline__ void bulk_copy_g2s(void* dst, const void* src, uint32
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async;" ::: "memory"); }
 __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
 
+__device__ __forceinline__ void record_fault(unsigned int* fault, unsigned int code) {
+  if (atomicCAS(fault, 0u, code) == 0u) fault[1] = blockIdx.x;
+}
+
 __host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
 template <class VT>
 struct BlockedOp {
   static constexpr int kThreads = kThreadsBlocked;
-  static constexpr int kMinBlocks = 1;  // one CTA per SM: full register file, ~200 KB shared
+  static constexpr int kMinBlocks = 1;  // one CTA per SM: full register file, ~190 KB shared
   BlockedHalf L[2];
   int64_t n;
-  int acc_rows;  // shared accumulator capacity (max rows of a slab over both halves)
-  unsigned int* fault;
+  int acc_rows;         // shared accumulator capacity (max rows of a slab over both halves)
+  unsigned int* fault;  // [0] first fault code, [1] its CTA
 
-  __host__ __device__ size_t head_bytes() const { return align16((size_t)acc_rows * 8) + 64; }
-  size_t smem_bytes() const { return head_bytes() + (size_t)2 * kTileW * 8; }
+  __host__ __device__ size_t head_bytes() const { return align16((size_t)(acc_rows + 1) * 8) + 128; }
+  size_t smem_bytes() const { return head_bytes() + (size_t)kStages * kTileW * 8; }
 
-  // One 32-entry chunk: gather, segmented scan by row, tail add.
-  __device__ __forceinline__ void fold(uint32_t u, double v, const double* xs, double* acc, int lane,
-                                       unsigned upto) const {
-    if (u != kPad) v *= xs[u & 0xffffu];
-    else v = 0.0;
-    const uint32_t rl = u >> 16;
-    const uint32_t up = __shfl_up_sync(0xffffffffu, rl, 1);
-    const unsigned heads = __ballot_sync(0xffffffffu, lane == 0 || up != rl);
-    const int sstart = 31 - __clz(heads & upto);
-    for (int d = 1; d < 32; d <<= 1) {
-      if (!__any_sync(0xffffffffu, lane - d >= sstart)) break;
-      const double vo = __shfl_up_sync(0xffffffffu, v, d);
-      if (lane - d >= sstart) v += vo;
-    }
-    const bool tail = lane == 31 || ((heads >> (lane + 1)) & 1u);
-    if (tail && u != kPad) acc[rl] += v;
+  // One 32-entry chunk: the layout guarantees its rows are distinct, so every
+  // lane adds its product straight into its row's accumulator. A row's
+  // entries arrive in column order (earlier chunks, earlier blocks), so each
+  // row is summed exactly like the reference's spmv / spmv_t loop
+  // (sparsify.cpp:203-226): acc += v * x, no FMA.
+  __device__ __forceinline__ void fold(uint32_t u, double v, const double* xs, double* acc) const {
+    // padding (u = kPad, v = 0) lands in the sink row acc[acc_rows], never read
+    const uint32_t rl = min(u >> 16, (uint32_t)acc_rows);
+    acc[rl] = __dadd_rn(acc[rl], __dmul_rn(v, xs[u & (kTileW - 1)]));
+    __syncwarp();  // the next chunk may revisit a row through another lane
   }
 
   template <int ROLE, bool LOG, bool DET>
@@ -127,8 +129,9 @@ struct BlockedOp {
                        double& err, long long& masks) const {
     extern __shared__ __align__(128) unsigned char dsm[];
     double* acc = reinterpret_cast<double*>(dsm);
-    uint64_t* full = reinterpret_cast<uint64_t*>(dsm + align16((size_t)acc_rows * 8));
-    uint64_t* empty = full + 2;
+    uint64_t* full = reinterpret_cast<uint64_t*>(dsm + align16((size_t)(acc_rows + 1) * 8));
+    uint64_t* empty = full + kStages;
+    uint32_t* ph = reinterpret_cast<uint32_t*>(empty + kStages);  // phases completed per stage
     double* tiles = reinterpret_cast<double*>(dsm + head_bytes());
 
     const BlockedHalf& H = L[ROLE];
@@ -140,23 +143,33 @@ struct BlockedOp {
     const int nrows = H.slab_row0[p + 1] - r0;
     const int B = H.B;
 
-    if (threadIdx.x == 0) {
-      mbar_init(&full[0], 1);
-      mbar_init(&full[1], 1);
-      mbar_init(&empty[0], kNW);
-      mbar_init(&empty[1], kNW);
+    // Barriers are initialised once per launch (first half of iteration 1)
+    // and never re-initialised; each stage's phase count carries over from
+    // half to half in shared memory.
+    if (ROLE == 0 && t == 1 && threadIdx.x == 0) {
+      for (int s = 0; s < kStages; ++s) {
+        mbar_init(&full[s], 1);
+        mbar_init(&empty[s], kNW);
+        ph[s] = 0u;
+      }
       fence_mbar_init();
     }
     for (int r = threadIdx.x; r < nrows; r += blockDim.x) acc[r] = 0.0;
     __syncthreads();
+    uint32_t ph_s[kStages];
+#pragma unroll
+    for (int s = 0; s < kStages; ++s) ph_s[s] = ph[s];
+    // parity of the phase of stage b % kStages that block b completes
+    auto par = [&](int b) -> uint32_t { return (ph_s[b % kStages] + (uint32_t)(b / kStages)) & 1u; };
 
     if (w == kNW) {
-      // ---- producer warp: x tiles, two stages ----
+      // ---- producer warp: x tiles through a kStages-deep ring ----
       if (lane == 0) {
         fence_proxy_async();  // x was written with generic stores before the grid barrier
         for (int b = 0; b < B; ++b) {
-          const int s = b & 1;
-          if (b >= 2 && !mbar_wait(&empty[s], (uint32_t)(((b - 2) >> 1) & 1))) atomicExch(fault, 1u);
+          const int s = b % kStages;
+          if (b >= kStages && !mbar_wait(&empty[s], par(b - kStages), fault))
+            record_fault(fault, 0x10000000u | ((unsigned)ROLE << 24) | (unsigned)b);
           const int64_t c0 = (int64_t)b * H.W;
           const int64_t cnt = min((int64_t)H.W, H.n_in - c0);
           const uint32_t bytes = (uint32_t)align16((size_t)cnt * 8);
@@ -164,36 +177,40 @@ struct BlockedOp {
           bulk_copy_g2s(tiles + (size_t)s * kTileW, x + c0, bytes, &full[s]);
         }
       }
+      __syncwarp();
     } else {
       // ---- consumer warps: one contiguous entry stream per warp ----
       const long long* ofs = H.off + ((int64_t)p * kNW + w) * (B + 1);  // block starts, padded, [B] = end
       const long long sbeg = ofs[0], send = ofs[B];
-      const unsigned upto = lane == 31 ? 0xffffffffu : ((2u << lane) - 1u);
       int cb = 0;  // current block
       long long cb_end = ofs[1];
-      if (!mbar_wait(&full[0], 0u)) atomicExch(fault, 1u);
+      const double* xs = tiles;  // tile of the current block
+      if (!mbar_wait(&full[0], par(0), fault)) record_fault(fault, 0x20000000u | ((unsigned)ROLE << 24));
       uint32_t ua[kGroup], ub[kGroup];
       VT va[kGroup], vb[kGroup];
-      // two register groups of 8 chunks: load group g+1 while folding group g
-#define SPK_LOAD(G0, UU, VV)                                     \
-  _Pragma("unroll") for (int k = 0; k < kGroup; ++k) {           \
-    const long long e = (G0) + 32 * k + lane;                    \
-    UU[k] = e < send ? __ldcs(H.packed + e) : kPad;              \
-    VV[k] = e < send ? __ldcs(gval + e) : (VT)0;                 \
+      // Two register groups of kGroup chunks: group g+1 loads while group g
+      // folds. The entry arrays carry 2*kGroup chunks of padding past the last
+      // stream, so the loads need no bounds checks.
+#define SPK_LOAD(G0, UU, VV)                                   \
+  _Pragma("unroll") for (int k = 0; k < kGroup; ++k) {         \
+    UU[k] = __ldcs(H.packed + (G0) + 32 * k + lane);           \
+    VV[k] = __ldcs(gval + (G0) + 32 * k + lane);               \
   }
-#define SPK_CONSUME(G0, UU, VV)                                                          \
-  _Pragma("unroll") for (int k = 0; k < kGroup; ++k) {                                   \
-    const long long c = (G0) + 32 * k;                                                   \
-    if (c < send) { /* warp-uniform; no break so the group stays in registers */        \
-      while (c >= cb_end) { /* leave block cb (release its tile), enter the next */      \
-        __syncwarp();                                                                    \
-        if (lane == 0) mbar_arrive(&empty[cb & 1]);                                      \
-        ++cb;                                                                            \
-        cb_end = ofs[cb + 1];                                                            \
-        if (!mbar_wait(&full[cb & 1], (uint32_t)((cb >> 1) & 1))) atomicExch(fault, 1u); \
-      }                                                                                  \
-      fold(UU[k], (double)VV[k], tiles + (size_t)(cb & 1) * kTileW, acc, lane, upto);    \
-    }                                                                                    \
+#define SPK_CONSUME(G0, UU, VV)                                                              \
+  _Pragma("unroll") for (int k = 0; k < kGroup; ++k) {                                       \
+    const long long c = (G0) + 32 * k;                                                       \
+    if (c < send) { /* warp-uniform; no break so the group stays in registers */            \
+      while (c >= cb_end && cb + 1 < B) { /* release tile cb, enter the next */             \
+        __syncwarp();                                                                        \
+        if (lane == 0) mbar_arrive(&empty[cb % kStages]);                                    \
+        ++cb;                                                                                \
+        cb_end = ofs[cb + 1];                                                                \
+        xs = tiles + (size_t)(cb % kStages) * kTileW;                                        \
+        if (!mbar_wait(&full[cb % kStages], par(cb), fault))                                 \
+          record_fault(fault, 0x30000000u | ((unsigned)ROLE << 24) | (unsigned)cb);          \
+      }                                                                                      \
+      fold(UU[k], (double)VV[k], xs, acc);                                                  \
+    }                                                                                        \
   }
       const long long step = 32LL * kGroup;
       long long g = sbeg;
@@ -214,12 +231,17 @@ struct BlockedOp {
       // release the remaining blocks in order (tile present before release)
       for (;;) {
         __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[cb & 1]);
+        if (lane == 0) mbar_arrive(&empty[cb % kStages]);
         if (++cb >= B) break;
-        if (!mbar_wait(&full[cb & 1], (uint32_t)((cb >> 1) & 1))) atomicExch(fault, 1u);
+        if (!mbar_wait(&full[cb % kStages], par(cb), fault))
+          record_fault(fault, 0x40000000u | ((unsigned)ROLE << 24) | (unsigned)cb);
       }
     }
     __syncthreads();
+    if (threadIdx.x == 0) {  // block b used stage b % kStages once
+#pragma unroll
+      for (int s = 0; s < kStages; ++s) ph[s] = ph_s[s] + (uint32_t)((B - s + kStages - 1) / kStages);
+    }
     // ---- finalize this slab's atoms ----
     for (int r = threadIdx.x; r < nrows; r += blockDim.x) {
       const int64_t i = r0 + r;
@@ -237,40 +259,88 @@ struct BlockedOp {
 // ---- layout builder --------------------------------------------------------------
 
 // key = ((slab * NW + warp) * B + block): the warp's whole stream is contiguous
+// key = segment (slab, warp, block) | bank class of the row | row. Sorting by
+// it (stably) lists each segment's rows grouped by shared-memory bank class,
+// every row's entries consecutive in column order; chunk c then takes list
+// positions c, c+C, ... and so spreads its rows over all banks.
 __global__ void key_kernel(const long long* ptr, const uint32_t* idx, int64_t n_out, const int* slab_of,
-                           const unsigned char* warp_of, int W, int B, uint32_t* keys) {
+                           const unsigned char* warp_of, const int* slab_row0_of_row, int W, int B, uint32_t* seg,
+                           unsigned long long* key) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t i = warp; i < n_out; i += nw) {
     const uint32_t base = ((uint32_t)slab_of[i] * kNW + warp_of[i]) * (uint32_t)B;
-    for (long long q = ptr[i] + lane; q < ptr[i + 1]; q += 32) keys[q] = base + idx[q] / (uint32_t)W;
+    const uint32_t rl = (uint32_t)(i - slab_row0_of_row[i]);
+    for (long long q = ptr[i] + lane; q < ptr[i + 1]; q += 32) {
+      const uint32_t sg = base + idx[q] / (uint32_t)W;
+      seg[q] = sg;
+      key[q] = ((unsigned long long)sg << 20) | ((unsigned long long)(rl & 15u) << 16) | rl;
+    }
   }
 }
 
-// Sorted position q (key k) -> padded destination seg_base[k] + (q - useg[k]).
-template <class VT>
-__global__ void pack_kernel(const uint32_t* keys_s, const uint32_t* perm, const uint32_t* idx, const VT* val,
-                            const uint32_t* rows_of_pos, const int* slab_row0_of_row, const long long* useg,
-                            const long long* seg_base, int W, int64_t m, uint32_t* packed, VT* vout) {
+__global__ void split_kernel(const unsigned long long* key_s, int64_t m, uint32_t* seg_s, uint32_t* rl) {
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < m; q += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t k = keys_s[q];
-    const long long dst = seg_base[k] + (q - useg[k]);
-    const uint32_t src = perm[q];
-    const uint32_t i = rows_of_pos[src];
-    const uint32_t rl = i - (uint32_t)slab_row0_of_row[i];
-    const uint32_t cl = idx[src] % (uint32_t)W;
-    packed[dst] = (rl << 16) | cl;
-    vout[dst] = val[src];
+    const unsigned long long k = key_s[q];
+    seg_s[q] = (uint32_t)(k >> 20);
+    rl[q] = (uint32_t)(k & 0xffffu);
   }
 }
 
-__global__ void rows_of_pos_kernel(const long long* ptr, int64_t n, uint32_t* rows) {
-  const int lane = threadIdx.x & 31;
-  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t i = warp; i < n; i += nw)
-    for (long long p = ptr[i] + lane; p < ptr[i + 1]; p += 32) rows[p] = (uint32_t)i;
+// Start of the run of equal (segment, row) containing q (max-scanned next).
+__global__ void run_head_kernel(const uint32_t* keys_s, const uint32_t* rl, int64_t m, uint32_t* start) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < m; q += (int64_t)gridDim.x * blockDim.x) {
+    const bool head = q == 0 || keys_s[q] != keys_s[q - 1] || rl[q] != rl[q - 1];
+    start[q] = head ? (uint32_t)q : 0u;
+  }
+}
+
+// Run length (the row's entry count in its segment) at each run head, and
+// the segment's longest run.
+__global__ void runlen_kernel(const uint32_t* keys_s, const uint32_t* rl, const uint32_t* start, int64_t m,
+                              uint32_t* runlen, unsigned int* maxrun) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < m; q += (int64_t)gridDim.x * blockDim.x) {
+    if (start[q] != (uint32_t)q) continue;
+    int64_t e = q + 1;
+    while (e < m && keys_s[e] == keys_s[q] && rl[e] == rl[q]) ++e;
+    runlen[q] = (uint32_t)(e - q);
+    atomicMax(&maxrun[keys_s[q]], (unsigned int)(e - q));
+  }
+}
+
+// Chunk placement. A segment of E entries (rows grouped by bank class, each
+// row's entries consecutive in column order) gets C = max(ceil(E/32), longest run)
+// chunks of 32 slots; list position p maps to chunk p mod C, slot p div C.
+// A row's m <= C consecutive positions hit m distinct chunks, so no chunk
+// holds a row twice; its entries then take those chunks in ascending order,
+// so the row is still summed in column order when the chunks run in order.
+template <class VT>
+__global__ void place_kernel(const uint32_t* keys_s, const uint32_t* perm, const uint32_t* rl, const uint32_t* start,
+                             const uint32_t* runlen, const long long* useg, const long long* seg_base,
+                             const long long* nchunk, const uint32_t* idx, const VT* val, int W, int64_t m,
+                             uint32_t* packed, VT* vout) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < m; q += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t key = keys_s[q];
+    const long long C = nchunk[key];
+    const long long ps = (long long)start[q] - useg[key];  // the row's first list position
+    const long long kk = (long long)q - (long long)start[q];
+    const long long mr = runlen[start[q]];
+    const long long a = ps % C, wrap = a + mr - C;
+    long long c, pp;
+    if (wrap > 0 && kk < wrap) {
+      c = kk;
+      pp = ps + (C - a) + c;
+    } else {
+      c = wrap > 0 ? a + (kk - wrap) : a + kk;
+      pp = ps + (c - a);
+    }
+    const long long slot = pp / C;  // even slots -> lanes 0-15, odd -> 16-31: each half-warp spans the classes
+    const long long d = seg_base[key] + c * 32 + ((slot & 1) << 4) + (slot >> 1);
+    const uint32_t src = perm[q];
+    packed[d] = (rl[q] << 16) | (idx[src] % (uint32_t)W);
+    vout[d] = val[src];
+  }
 }
 
 __global__ void iota_u32(uint32_t* v, int64_t m) {
@@ -336,66 +406,95 @@ bool build_blocked(spk_ctx* ctx, int P, int W, int64_t n_out, int64_t n_in, int6
   upload(ctx, d_warp_of, warp_of.data(), n_out);
   upload(ctx, d_s0r, slab_row0_of_row.data(), sizeof(int) * n_out);
   DBuf keys(sizeof(uint32_t) * mm), keys_s(sizeof(uint32_t) * mm), iota(sizeof(uint32_t) * mm),
-      perm(sizeof(uint32_t) * mm), rows(sizeof(uint32_t) * mm), hist(sizeof(unsigned long long) * nkeys);
+      perm(sizeof(uint32_t) * mm), hist(sizeof(unsigned long long) * nkeys),
+      key64(sizeof(unsigned long long) * mm), key64_s(sizeof(unsigned long long) * mm);
   SPK_CUDA(cudaMemsetAsync(hist.p, 0, hist.bytes, s));
   key_kernel<<<grid_cap(ctx, n_out * 32), 256, 0, s>>>(ptr_d.as<long long>(), idx_d.as<uint32_t>(), n_out,
-                                                        d_slab_of.as<int>(), d_warp_of.as<unsigned char>(), W, B,
-                                                        keys.as<uint32_t>());
-  rows_of_pos_kernel<<<grid_cap(ctx, n_out * 32), 256, 0, s>>>(ptr_d.as<long long>(), n_out, rows.as<uint32_t>());
+                                                        d_slab_of.as<int>(), d_warp_of.as<unsigned char>(),
+                                                        d_s0r.as<int>(), W, B, keys.as<uint32_t>(),
+                                                        key64.as<unsigned long long>());
   iota_u32<<<grid_cap(ctx, m), 256, 0, s>>>(iota.as<uint32_t>(), m);
   key_hist_kernel<<<grid_cap(ctx, m), 256, 0, s>>>(keys.as<uint32_t>(), m, hist.as<unsigned long long>());
-  ctx->launches += 4;
+  ctx->launches += 3;
   int end_bit = 1;
   while ((int64_t(1) << end_bit) < nkeys) ++end_bit;
   size_t tb = 0;
-  SPK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys.as<uint32_t>(), keys_s.as<uint32_t>(),
-                                           iota.as<uint32_t>(), perm.as<uint32_t>(), (int)m, 0, end_bit, s));
+  SPK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, key64.as<unsigned long long>(),
+                                           key64_s.as<unsigned long long>(), iota.as<uint32_t>(), perm.as<uint32_t>(),
+                                           (int)m, 0, 20 + end_bit, s));
   ctx->scratch.ensure(tb);
-  SPK_CUDA(cub::DeviceRadixSort::SortPairs(ctx->scratch.p, tb, keys.as<uint32_t>(), keys_s.as<uint32_t>(),
-                                           iota.as<uint32_t>(), perm.as<uint32_t>(), (int)m, 0, end_bit, s));
+  SPK_CUDA(cub::DeviceRadixSort::SortPairs(ctx->scratch.p, tb, key64.as<unsigned long long>(),
+                                           key64_s.as<unsigned long long>(), iota.as<uint32_t>(), perm.as<uint32_t>(),
+                                           (int)m, 0, 20 + end_bit, s));
   ++ctx->launches;
-  // host: each (slab, warp, block) segment padded to 32 entries; per-warp block starts
+  // run starts / lengths -> chunk counts -> conflict-free placement
+  DBuf rl(sizeof(uint32_t) * mm), start(sizeof(uint32_t) * mm), runlen(sizeof(uint32_t) * mm),
+      maxrun(sizeof(unsigned int) * nkeys);
+  SPK_CUDA(cudaMemsetAsync(maxrun.p, 0, maxrun.bytes, s));
+  split_kernel<<<grid_cap(ctx, m), 256, 0, s>>>(key64_s.as<unsigned long long>(), m, keys_s.as<uint32_t>(),
+                                                rl.as<uint32_t>());
+  run_head_kernel<<<grid_cap(ctx, m), 256, 0, s>>>(keys_s.as<uint32_t>(), rl.as<uint32_t>(), m,
+                                                   start.as<uint32_t>());
+  ctx->launches += 2;
+  tb = 0;
+  SPK_CUDA(cub::DeviceScan::InclusiveScan(nullptr, tb, start.as<uint32_t>(), start.as<uint32_t>(), cub::Max(), (int)m,
+                                          s));
+  ctx->scratch.ensure(tb);
+  SPK_CUDA(cub::DeviceScan::InclusiveScan(ctx->scratch.p, tb, start.as<uint32_t>(), start.as<uint32_t>(), cub::Max(),
+                                          (int)m, s));
+  runlen_kernel<<<grid_cap(ctx, m), 256, 0, s>>>(keys_s.as<uint32_t>(), rl.as<uint32_t>(), start.as<uint32_t>(), m,
+                                                 runlen.as<uint32_t>(), maxrun.as<unsigned int>());
+  ctx->launches += 2;
   std::vector<unsigned long long> h(nkeys);
+  std::vector<unsigned int> mx(nkeys);
   download(ctx, h.data(), hist, sizeof(unsigned long long) * nkeys);
-  std::vector<long long> useg(nkeys), seg_base(nkeys), off((size_t)P * kNW * (B + 1));
+  download(ctx, mx.data(), maxrun, sizeof(unsigned int) * nkeys);
+  std::vector<long long> useg(nkeys), seg_base(nkeys), nch(nkeys), off((size_t)P * kNW * (B + 1));
   long long u_acc = 0, p_acc = 0;
   for (int64_t sw = 0; sw < (int64_t)P * kNW; ++sw) {
     for (int b = 0; b < B; ++b) {
       const int64_t k = sw * B + b;
       useg[k] = u_acc;
+      u_acc += (long long)h[k];
+      nch[k] = std::max<long long>(((long long)h[k] + 31) / 32, (long long)mx[k]);
       seg_base[k] = p_acc;
       off[(size_t)sw * (B + 1) + b] = p_acc;
-      u_acc += (long long)h[k];
-      p_acc += ((long long)h[k] + 31) & ~31LL;
+      p_acc += 32 * nch[k];
     }
     off[(size_t)sw * (B + 1) + B] = p_acc;
   }
-  const int64_t total = std::max<long long>(p_acc, 32);
-  DBuf d_useg, d_seg;
+  const int64_t total = p_acc + 2 * 32 * kGroup;  // unguarded prefetch runs up to 2 groups past a stream
+  if (std::getenv("SPK_DEBUG_BLOCKED"))
+    std::fprintf(stderr, "[blocked] n_out %lld B %d W %d entries %lld padded %lld (x%.3f) max_rows %d\n",
+                 (long long)n_out, B, W, (long long)m, (long long)p_acc, (double)p_acc / std::max<int64_t>(m, 1),
+                 max_rows);
+  DBuf d_useg, d_seg, d_nch;
   upload(ctx, d_useg, useg.data(), sizeof(long long) * nkeys);
   upload(ctx, d_seg, seg_base.data(), sizeof(long long) * nkeys);
+  upload(ctx, d_nch, nch.data(), sizeof(long long) * nkeys);
   upload(ctx, out.off, off.data(), sizeof(long long) * off.size());
   upload(ctx, out.slab_row0, slab_row0.data(), sizeof(int) * (P + 1));
   out.packed.alloc(sizeof(uint32_t) * total);
   out.val.alloc((size_t)vbytes * total);
   SPK_CUDA(cudaMemsetAsync(out.packed.p, 0xff, out.packed.bytes, s));  // padding = kPad
   SPK_CUDA(cudaMemsetAsync(out.val.p, 0, out.val.bytes, s));
-  if (vbytes == 4)
-    pack_kernel<float><<<grid_cap(ctx, m), 256, 0, s>>>(keys_s.as<uint32_t>(), perm.as<uint32_t>(),
-                                                         idx_d.as<uint32_t>(), val_d.as<float>(), rows.as<uint32_t>(),
-                                                         d_s0r.as<int>(), d_useg.as<long long>(),
-                                                         d_seg.as<long long>(), W, m, out.packed.as<uint32_t>(),
-                                                         out.val.as<float>());
-  else
-    pack_kernel<double><<<grid_cap(ctx, m), 256, 0, s>>>(keys_s.as<uint32_t>(), perm.as<uint32_t>(),
-                                                          idx_d.as<uint32_t>(), val_d.as<double>(),
-                                                          rows.as<uint32_t>(), d_s0r.as<int>(), d_useg.as<long long>(),
-                                                          d_seg.as<long long>(), W, m, out.packed.as<uint32_t>(),
-                                                          out.val.as<double>());
-  ++ctx->launches;
+  if (m > 0) {
+    if (vbytes == 4)
+      place_kernel<float><<<grid_cap(ctx, m), 256, 0, s>>>(
+          keys_s.as<uint32_t>(), perm.as<uint32_t>(), rl.as<uint32_t>(), start.as<uint32_t>(), runlen.as<uint32_t>(),
+          d_useg.as<long long>(), d_seg.as<long long>(), d_nch.as<long long>(), idx_d.as<uint32_t>(),
+          val_d.as<float>(), W, m, out.packed.as<uint32_t>(), out.val.as<float>());
+    else
+      place_kernel<double><<<grid_cap(ctx, m), 256, 0, s>>>(
+          keys_s.as<uint32_t>(), perm.as<uint32_t>(), rl.as<uint32_t>(), start.as<uint32_t>(), runlen.as<uint32_t>(),
+          d_useg.as<long long>(), d_seg.as<long long>(), d_nch.as<long long>(), idx_d.as<uint32_t>(),
+          val_d.as<double>(), W, m, out.packed.as<uint32_t>(), out.val.as<double>());
+    ++ctx->launches;
+  }
   SPK_CUDA(cudaGetLastError());
   SPK_CUDA(cudaStreamSynchronize(s));
   out.max_rows = max_rows;
+  out.padded = p_acc;
   out.ecap = 0;
   out.h.P = P;
   out.h.B = B;
@@ -425,7 +524,10 @@ bool run_blocked_t(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, doub
         build_blocked(ctx, P, W, n, n, sk->nnz, sk->col_ptr, sk->row_idx, sk->values_t, vb, *C)) {
       BlockedOp<VT> probe{};
       probe.acc_rows = std::max(R->max_rows, C->max_rows);
-      if (probe.smem_bytes() <= budget) {
+      // auto mode keeps the CSR loop when rows are too few per warp to fill
+      // conflict-free chunks (padding would outweigh the staged gathers)
+      const bool dense_pad = ctx->use_blocked == 2 && (double)(R->padded + C->padded) > 1.35 * 2.0 * (double)sk->nnz;
+      if (probe.smem_bytes() <= budget && !dense_pad) {
         sk->blk_rows = std::move(R);
         sk->blk_cols = std::move(C);
       }
@@ -438,8 +540,8 @@ bool run_blocked_t(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, doub
   op.n = n;
   op.acc_rows = std::max(sk->blk_rows->max_rows, sk->blk_cols->max_rows);
   LoopWs& W = sk->ws;
-  W.scalar.ensure(sizeof(unsigned int));
-  SPK_CUDA(cudaMemsetAsync(W.scalar.p, 0, sizeof(unsigned int), ctx->stream));
+  W.scalar.ensure(sizeof(unsigned int) * 2);
+  SPK_CUDA(cudaMemsetAsync(W.scalar.p, 0, sizeof(unsigned int) * 2, ctx->stream));
   op.fault = W.scalar.as<unsigned int>();
   W.row_ne.ensure(n);
   W.col_ne.ensure(n);
@@ -447,9 +549,15 @@ bool run_blocked_t(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, doub
   SPK_CUDA(cudaMemcpyAsync(W.col_ne.p, sk->cov_col.p, n, cudaMemcpyDeviceToDevice, ctx->stream));
   loopcore::run_core<false>(ctx, op, n, W, sk->cov_empty_rows, sk->cov_empty_cols, cfg, exponent, policy, st,
                             /*useful_blocks=*/P, out, /*exact_grid=*/P, op.smem_bytes());
-  unsigned int fault = 0;
-  download(ctx, &fault, W.scalar, sizeof fault);
-  if (fault) fail_device("blocked loop: a TMA tile never completed", cudaErrorLaunchTimeout);
+  unsigned int fw[2] = {0u, 0u};
+  download(ctx, fw, W.scalar, sizeof fw);
+  if (fw[0]) {
+    // code: 1 producer / 2-4 consumer barrier wait timed out; then half and block
+    const std::string msg = "blocked loop: a tile barrier timed out (site " + std::to_string(fw[0] >> 28) +
+                            ", half " + std::to_string((fw[0] >> 24) & 15) + ", block " +
+                            std::to_string(fw[0] & 0xffffff) + ", CTA " + std::to_string(fw[1]) + ")";
+    fail_device(msg.c_str(), cudaErrorLaunchTimeout);
+  }
   return true;
 }
 

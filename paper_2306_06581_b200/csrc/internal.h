@@ -78,6 +78,7 @@ struct BlockedHost {
   DBuf slab_row0, warp_row0, off, packed, val;
   int max_rows = 0;
   int ecap = 0;  // largest padded (slab, block) entry segment
+  int64_t padded = 0;  // entries after chunk padding
 };
 
 }  // namespace spk
@@ -128,7 +129,7 @@ struct spk_ctx {
   int deterministic = 0;
   int loop_blocks_per_sm = 0;  // 0 = occupancy-derived
   int otf_fp32 = 1;            // dense on-the-fly comparator computes K in fp32
-  int use_blocked = 0;         // fast sparse loop uses the slab x block layout
+  int use_blocked = 2;         // fast sparse loop layout: 0 CSR/CSC, 1 slab x block, 2 auto (large n)
   int blocked_max_w = 16384;   // cap on the shared tile width (tests force many blocks)
   int force_two_pass = 0;      // sampler: skip the single-pass tiled path (testing)
   int64_t launches = 0;
@@ -168,6 +169,47 @@ struct Timer {
 
 // Sequential host sum exactly as new_measure (measures.cpp:18-23).
 double seq_total(const double* w, int64_t n);
+// sinkhorn_ot / sinkhorn_uot argument checks; returns the exponent f.
+double solver_exponent(const spk_solver_cfg& cfg, int uot, double a_total, double b_total);
+
+// Runs f, converting library failures into the C ABI status and the
+// context's last-error record.
+template <class F>
+int guard(spk_ctx* ctx, F&& f) {
+  try {
+    if (ctx) SPK_CUDA(cudaSetDevice(ctx->device));
+    (void)cudaGetLastError();  // drop stale non-sticky errors from other callers
+    f();
+    if (ctx) {
+      ctx->err_category = 0;
+      ctx->err_kind = 0;
+      ctx->err_msg.clear();
+    }
+    return SPK_OK;
+  } catch (const Failure& e) {
+    if (ctx) {
+      ctx->err_category = e.category;
+      ctx->err_kind = e.kind;
+      ctx->err_msg = e.what();
+    }
+    return e.category;
+  } catch (const std::bad_alloc&) {
+    if (ctx) {
+      ctx->err_category = SPK_STATUS_DEVICE;
+      ctx->err_kind = SPK_E_DEVICE;
+      ctx->err_msg = "host allocation failed";
+    }
+    return SPK_STATUS_DEVICE;
+  } catch (const std::exception& e) {
+    if (ctx) {
+      ctx->err_category = SPK_STATUS_DEVICE;
+      ctx->err_kind = SPK_E_DEVICE;
+      ctx->err_msg = e.what();
+    }
+    return SPK_STATUS_DEVICE;
+  }
+}
+
 
 // Kernel source on the device: dense K (+C) or coordinates.
 struct DevKernel {
@@ -196,12 +238,22 @@ struct PlanInfo {
   std::vector<double> row_w, col_w;  // ra/cb, pa/pb, or 1/n
   // plan-pass outputs kept on the device (grid plans): per-row support size
   // and unnormalised row mass, used to size the sampler's row slots
-  DBuf d_row_nnz, d_row_sum;
+  DBuf d_row_nnz, d_row_sum;  // indexed by GLOBAL row
   bool have_rows = false;
+  bool zero_mass = false;
 };
 
 void build_plan(spk_ctx* ctx, DevKernel& dk, const double* a, const double* b, int plan_kind,
                 double lambda, double eps, double theta, PlanInfo& plan);
+// The three stages of build_plan, separable so row slabs of the n^2 pass can
+// run on different GPUs: host O(n) weights (returns whether the support /
+// normaliser pass is needed), the pass over rows [row0, row1) into local
+// arrays, and the fixed-order totals over plan.d_row_* (all n rows).
+bool plan_weights(spk_ctx* ctx, DevKernel& dk, const double* a, const double* b, int plan_kind, double lambda,
+                  double eps, PlanInfo& plan);
+void plan_pass_rows(spk_ctx* ctx, DevKernel& dk, const PlanInfo& plan, int64_t row0, int64_t row1,
+                    long long* row_nnz, double* row_sum);
+void plan_finish(spk_ctx* ctx, DevKernel& dk, bool need_pass, double theta, PlanInfo& plan);
 // Samples rows [row0, row1) (default: all) of the plan into sk (a row slab
 // with global column indices when sharded).
 void sample_sketch(spk_ctx* ctx, DevKernel& dk, const PlanInfo& plan, double s, uint64_t seed,

@@ -503,8 +503,8 @@ __global__ void slot_cap_kernel(int64_t n, int64_t row_base, int64_t n_cols, con
                                 const double* row_sum, const double* row_w, double col_w_total, int factorized, double inv, double s, int theta_mode, double omt,
                                 double unif, int* cap) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const double supp = row_nnz ? (double)row_nnz[i] : (double)n_cols;
-    double mass = factorized ? row_w[row_base + i] * col_w_total : row_sum[i] * inv;
+    const double supp = row_nnz ? (double)row_nnz[row_base + i] : (double)n_cols;
+    double mass = factorized ? row_w[row_base + i] * col_w_total : row_sum[row_base + i] * inv;
     if (theta_mode) mass = omt * mass + unif * supp;
     const double u = fmin(supp, s * mass * (1.0 + 1e-9));
     const double c = fmin(supp, ceil(u + 6.0 * sqrt(u) + 16.0));
@@ -640,8 +640,9 @@ void make_dev_kernel(spk_ctx* ctx, const spk_kernel_desc* kd, double default_eps
   }
 }
 
-void build_plan(spk_ctx* ctx, DevKernel& dk, const double* a, const double* b, int plan_kind,
-                double lambda, double eps, double theta, PlanInfo& plan) {
+bool plan_weights(spk_ctx* ctx, DevKernel& dk, const double* a, const double* b, int plan_kind, double lambda,
+                  double eps, PlanInfo& plan) {
+  (void)ctx;
   const int64_t n = dk.n;
   plan.kind = plan_kind;
   plan.theta = 0.0;
@@ -676,7 +677,8 @@ void build_plan(spk_ctx* ctx, DevKernel& dk, const double* a, const double* b, i
     for (int64_t i = 0; i < n; ++i) plan.row_w[i] = plan.col_w[i] = 1.0 / static_cast<double>(n);
   }
 
-  // ---- support size and grid normaliser (device pass over n^2 entries) ----
+  plan.zero_mass = zero_mass;
+  // ---- does the plan need the support / grid-normaliser pass over n^2 entries? ----
   const double nn = static_cast<double>(n) * static_cast<double>(n);
   bool need_pass = true;
   if (dk.dense) {
@@ -688,43 +690,60 @@ void build_plan(spk_ctx* ctx, DevKernel& dk, const double* a, const double* b, i
     // every C_ij = cost/c0 <= 1, so every K_ij >= exp(-1/eps) > 0: full support
     need_pass = false;
   }
+  return need_pass;
+}
+
+void plan_pass_rows(spk_ctx* ctx, DevKernel& dk, const PlanInfo& plan, int64_t row0, int64_t row1,
+                    long long* row_nnz, double* row_sum) {
+  const int64_t n = dk.n;
+  const int64_t rows = row1 - row0;
+  if (rows <= 0) return;
+  DBuf rw, cw;
+  upload(ctx, rw, plan.row_w.data(), sizeof(double) * n);
+  upload(ctx, cw, plan.col_w.data(), sizeof(double) * n);
+  DPlan P{};
+  P.row_w = rw.as<double>();
+  P.col_w = cw.as<double>();
+  P.kind = plan.kind;
+  P.g_k = plan.g_k;
+  if (!dk.dense && tiled_dim_ok(dk.dim)) {
+    TiledArgs A = tiled_args(ctx, dk);
+    A.n_rows = rows;
+    A.row_base = row0;
+    A.P = P;
+    A.row_nnz = row_nnz;
+    A.row_sum = row_sum;
+    if (plan.kind == SPK_PLAN_UOT) launch_tiled<false, true, double>(ctx, A);
+    else launch_tiled<false, false, double>(ctx, A);
+  } else {
+    if (row0 != 0 || row1 != n) fail(SPK_E_DIMENSION_MISMATCH, "row-range plan pass needs the coordinate form");
+    KSrc S = make_src(dk);
+    plan_rows_kernel<<<grid_for_rows(ctx, n, 8), 256, 0, ctx->stream>>>(S, P, row_nnz, row_sum);
+    ++ctx->launches;
+  }
+  // keep rw/cw alive until the pass has run (DBuf frees synchronously)
+  SPK_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+void plan_finish(spk_ctx* ctx, DevKernel& dk, bool need_pass, double theta, PlanInfo& plan) {
+  const int64_t n = dk.n;
+  const int plan_kind = plan.kind;
+  const double nn = static_cast<double>(n) * static_cast<double>(n);
   long long support = static_cast<long long>(n) * n;
   double total = 0.0;
   if (need_pass) {
-    DBuf rw, cw;
-    upload(ctx, rw, plan.row_w.data(), sizeof(double) * n);
-    upload(ctx, cw, plan.col_w.data(), sizeof(double) * n);
-    DPlan P{};
-    P.row_w = rw.as<double>();
-    P.col_w = cw.as<double>();
-    P.kind = plan_kind;
-    P.g_k = plan.g_k;
-    plan.d_row_nnz.alloc(sizeof(long long) * n);
-    plan.d_row_sum.alloc(sizeof(double) * n);
-    plan.have_rows = true;
-    DBuf& rn = plan.d_row_nnz;
-    DBuf& rs = plan.d_row_sum;
+    // Fixed-order tree over the per-row sums: the same bits whichever GPU (or
+    // set of GPUs) produced the rows.
     DBuf tot(sizeof(double)), tn(sizeof(long long));
-    if (!dk.dense && tiled_dim_ok(dk.dim)) {
-      TiledArgs A = tiled_args(ctx, dk);
-      A.P = P;
-      A.row_nnz = rn.as<long long>();
-      A.row_sum = rs.as<double>();
-      if (plan_kind == SPK_PLAN_UOT) launch_tiled<false, true, double>(ctx, A);
-      else launch_tiled<false, false, double>(ctx, A);
-    } else {
-      KSrc S = make_src(dk);
-      plan_rows_kernel<<<grid_for_rows(ctx, n, 8), 256, 0, ctx->stream>>>(S, P, rn.as<long long>(),
-                                                                           rs.as<double>());
-      ++ctx->launches;
-    }
-    reduce_rows_kernel<double><<<1, 1024, 0, ctx->stream>>>(rs.as<double>(), n, tot.as<double>());
-    reduce_rows_kernel<long long><<<1, 1024, 0, ctx->stream>>>(rn.as<long long>(), n, tn.as<long long>());
+    reduce_rows_kernel<double><<<1, 1024, 0, ctx->stream>>>(plan.d_row_sum.as<double>(), n, tot.as<double>());
+    reduce_rows_kernel<long long><<<1, 1024, 0, ctx->stream>>>(plan.d_row_nnz.as<long long>(), n,
+                                                               tn.as<long long>());
     ctx->launches += 2;
     SPK_CUDA(cudaMemcpyAsync(&total, tot.p, sizeof total, cudaMemcpyDeviceToHost, ctx->stream));
     SPK_CUDA(cudaMemcpyAsync(&support, tn.p, sizeof support, cudaMemcpyDeviceToHost, ctx->stream));
     SPK_CUDA(cudaStreamSynchronize(ctx->stream));
   }
+  const bool zero_mass = plan.zero_mass;
   if (!dk.dense) {
     dk.nnz_ratio = static_cast<double>(support) / nn;  // kernel_from_cost :100
     if (support == 0) fail(SPK_E_ALL_ZERO_KERNEL, "kernel has no support");
@@ -745,6 +764,19 @@ void build_plan(spk_ctx* ctx, DevKernel& dk, const double* a, const double* b, i
     if (!(theta >= 0.0 && theta < 1.0)) fail(SPK_E_THETA_OUT_OF_RANGE, "theta = " + std::to_string(theta));
     plan.theta = theta;
   }
+}
+
+void build_plan(spk_ctx* ctx, DevKernel& dk, const double* a, const double* b, int plan_kind, double lambda,
+                double eps, double theta, PlanInfo& plan) {
+  const bool need_pass = plan_weights(ctx, dk, a, b, plan_kind, lambda, eps, plan);
+  if (need_pass) {
+    const int64_t n = dk.n;
+    plan.d_row_nnz.alloc(sizeof(long long) * n);
+    plan.d_row_sum.alloc(sizeof(double) * n);
+    plan.have_rows = true;
+    plan_pass_rows(ctx, dk, plan, 0, n, plan.d_row_nnz.as<long long>(), plan.d_row_sum.as<double>());
+  }
+  plan_finish(ctx, dk, need_pass, theta, plan);
 }
 
 namespace {

@@ -56,42 +56,6 @@ int category_of(int kind) {
   }
 }
 
-template <class F>
-int guard(spk_ctx* ctx, F&& f) {
-  try {
-    if (ctx) SPK_CUDA(cudaSetDevice(ctx->device));
-    (void)cudaGetLastError();  // drop stale non-sticky errors from other callers
-    f();
-    if (ctx) {
-      ctx->err_category = 0;
-      ctx->err_kind = 0;
-      ctx->err_msg.clear();
-    }
-    return SPK_OK;
-  } catch (const Failure& e) {
-    if (ctx) {
-      ctx->err_category = e.category;
-      ctx->err_kind = e.kind;
-      ctx->err_msg = e.what();
-    }
-    return e.category;
-  } catch (const std::bad_alloc&) {
-    if (ctx) {
-      ctx->err_category = SPK_STATUS_DEVICE;
-      ctx->err_kind = SPK_E_DEVICE;
-      ctx->err_msg = "host allocation failed";
-    }
-    return SPK_STATUS_DEVICE;
-  } catch (const std::exception& e) {
-    if (ctx) {
-      ctx->err_category = SPK_STATUS_DEVICE;
-      ctx->err_kind = SPK_E_DEVICE;
-      ctx->err_msg = e.what();
-    }
-    return SPK_STATUS_DEVICE;
-  }
-}
-
 double now_s() {
   return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
@@ -101,18 +65,6 @@ void init_report(spk_report* rep) {
   std::memset(rep, 0, sizeof *rep);
   rep->objective = std::numeric_limits<double>::quiet_NaN();
   rep->sketch_nnz = -1;
-}
-
-// sinkhorn_ot / sinkhorn_uot argument checks (solvers.hpp:213-216, :226-228);
-// returns the exponent f.
-double solver_exponent(const spk_solver_cfg& cfg, int uot, double a_total, double b_total) {
-  if (!uot) {
-    if (std::abs(a_total - 1.0) > 1e-8 || std::abs(b_total - 1.0) > 1e-8)
-      fail(SPK_E_NOT_NORMALIZED, "sinkhorn_ot requires simplex inputs");
-    return 1.0;
-  }
-  if (!(cfg.lambda > 0) || !std::isfinite(cfg.lambda)) fail(SPK_E_ERROR, "sinkhorn_uot needs finite lambda > 0");
-  return cfg.lambda / (cfg.lambda + cfg.epsilon);
 }
 
 void check_cfg(const spk_solver_cfg* cfg) {
@@ -210,6 +162,18 @@ void strict_coverage(spk_ctx* ctx, spk_sketch* sk) {
 
 }  // namespace
 
+// sinkhorn_ot / sinkhorn_uot argument checks (solvers.hpp:213-216, :226-228);
+// returns the exponent f.
+double solver_exponent(const spk_solver_cfg& cfg, int uot, double a_total, double b_total) {
+  if (!uot) {
+    if (std::abs(a_total - 1.0) > 1e-8 || std::abs(b_total - 1.0) > 1e-8)
+      fail(SPK_E_NOT_NORMALIZED, "sinkhorn_ot requires simplex inputs");
+    return 1.0;
+  }
+  if (!(cfg.lambda > 0) || !std::isfinite(cfg.lambda)) fail(SPK_E_ERROR, "sinkhorn_uot needs finite lambda > 0");
+  return cfg.lambda / (cfg.lambda + cfg.epsilon);
+}
+
 [[noreturn]] void fail(int kind, const std::string& text) {
   const char* cls = class_name(kind);
   throw Failure(category_of(kind), kind, cls ? std::string(cls) + ": " + text : text);
@@ -290,7 +254,7 @@ int spk_ctx_set_option(spk_ctx* ctx, int key, int64_t value) {
     case SPK_OPT_DETERMINISTIC: ctx->deterministic = value ? 1 : 0; return SPK_OK;
     case SPK_OPT_LOOP_BLOCKS_PER_SM: ctx->loop_blocks_per_sm = (int)value; return SPK_OK;
     case 3: ctx->otf_fp32 = value ? 1 : 0; return SPK_OK;
-    case 4: ctx->use_blocked = value ? 1 : 0; return SPK_OK;
+    case 4: ctx->use_blocked = (int)std::max<int64_t>(0, std::min<int64_t>(value, 2)); return SPK_OK;
     case 5: ctx->blocked_max_w = (int)std::max<int64_t>(16, std::min<int64_t>(value, 16384)); return SPK_OK;
     case 6: ctx->force_two_pass = value ? 1 : 0; return SPK_OK;
     default: return SPK_STATUS_INPUT;
