@@ -91,9 +91,11 @@ def dist_init():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if ws > 1:
+    if ws > 1 or (os.environ.get("SPK_SHARDED") == "1" and "MASTER_ADDR" in os.environ):
+        import torch
         import torch.distributed as dist
 
+        torch.cuda.set_device(local)
         backend = "nccl" if os.environ.get("SPK_BACKEND", "nccl") == "nccl" else "gloo"
         dist.init_process_group(backend=backend)
     return ws, rank, local
@@ -306,7 +308,8 @@ def run_ours(args, ws, rank, local):
     line = {
         "metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * elapsed / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "strong" if args.config in ("c2", "c4") else "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
         "config": {"workload": w.name, "n": sk.n, "nnz": sk.nnz, "s": w.s, "epsilon": w.eps,
                    "lambda": w.lam if math.isfinite(w.lam) else "inf", "iterations_per_step": per_launch_iters,
                    "sketch_values": w.values, "scalings": "f64",
@@ -329,6 +332,99 @@ def run_ours(args, ws, rank, local):
     ctx.close()
 
 
+def run_sharded(args, ws, rank, local):
+    """N > 1: config 4's rows and columns sharded across the N GPUs (SURVEY
+    §8(e)); one NCCL all-gather per half-iteration. Strong scaling: the same
+    n = 1e6 problem at every N."""
+    import torch
+
+    import paper_2306_06581_b200 as spk
+    from paper_2306_06581_b200 import sharded as S
+    from paper_2306_06581_b200 import workloads as W
+
+    torch.cuda.set_device(local)
+    w = W.CONFIGS[args.config]()
+    iters = args.iters or w.max_iter
+    comm = S.TorchComm()
+    shard = S.CudaShard(local)
+    kernel = spk.Coords(w.x, w.y, w.cost, w.eta, scale=w.scale, eps=w.eps)
+    opts = spk.SparSinkOptions(values=w.values)
+    plan = "uot" if w.uot else "ot"
+    stream = torch.cuda.current_stream()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    sk = S.ShardedSketch(comm, shard, kernel, w.a, w.b, plan, w.lam, w.eps, w.s, 7, opts)
+    torch.cuda.synchronize()
+    setup_s = max_over_ranks(time.perf_counter() - t0, ws)
+    cfg = spk.SolverConfig(w.eps, w.lam, w.delta, iters, w.stabilize)
+    for _ in range(args.warmup):
+        sk.solve(cfg, w.uot, want_scalings=False)
+    launches0 = shard.launches
+    loop_ev = []
+
+    def on_loop(ev):
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(stream)
+        loop_ev.append(e)
+
+    iters_done = 0
+    barrier(ws)
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            res = sk.solve(cfg, w.uot, on_loop=on_loop, want_scalings=False)
+            iters_done += res.report["iterations"]
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    barrier(ws)
+    elapsed = max_over_ranks(ev0.elapsed_time(ev1) * 1e-3, ws)
+    loop_s = max_over_ranks(sum(loop_ev[2 * k].elapsed_time(loop_ev[2 * k + 1]) for k in range(args.steps)) * 1e-3,
+                            ws)
+    launches = shard.launches - launches0
+    value = iters_done / elapsed  # one problem shared by all ranks
+    peak, peak_src = peaks()
+    vb = value_bytes(w.values)
+    b_iter = W.bytes_per_iteration(sk.n, sk.nnz, vb)
+    achieved = b_iter * iters_done / loop_s / 1e9  # whole-job algorithmic bytes over the loop time
+
+    e2e = None
+    if not args.no_e2e:
+        torch.cuda.synchronize()
+        barrier(ws)
+        t1 = time.perf_counter()
+        r = S.spar_sink_sharded(comm, shard, kernel, w.a, w.b, cfg, w.s, 7, opts, uot=w.uot)
+        torch.cuda.synchronize()
+        e2e_t = max_over_ranks(time.perf_counter() - t1, ws)
+        h2d = w.x.nbytes + w.y.nbytes + w.a.nbytes + w.b.nbytes
+        d2h = r.u.nbytes + r.v.nbytes + 8 * 4
+        e2e = {"value": r.report["iterations"] / e2e_t, "unit": "iters/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "solve_s": e2e_t, "objective": r.report["objective"]}
+    line = {
+        "metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * elapsed / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": w.name, "n": sk.n, "nnz": sk.nnz, "s": w.s, "epsilon": w.eps,
+                   "lambda": w.lam if math.isfinite(w.lam) else "inf", "iterations_per_step": iters_done / args.steps,
+                   "sketch_values": w.values, "scalings": "f64", "parallelism": f"rowcol-shard{ws}",
+                   "l2": f"inputs larger than L2: sketch {(sk.nnz * 2 * (vb + 4)) / 1e9:.2f} GB"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak * ws, "unit": "GB/s",
+                     "frac": achieved / (peak * ws), "traffic": None,
+                     "kernel": "shard half_kernel (+ NCCL all-gather), whole job", "bytes_per_iter": b_iter,
+                     "peak_source": f"{ws} x {peak_src}"},
+        "cpu_baseline": None,
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "extra": {"setup_s": setup_s, "loop_ms_per_iter": 1e3 * loop_s / iters_done, "kernel_nnz":
+                  sk.info["kernel_nnz"], "factorized_plan": sk.info["factorized"]},
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    shard.close()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -347,11 +443,13 @@ def main():
     ws, rank, local = dist_init()
     if args.impl == "reference":
         run_reference(args, ws, rank)
+    elif (ws > 1 and args.config in ("c2", "c4")) or os.environ.get("SPK_SHARDED") == "1":
+        run_sharded(args, ws, rank, local)  # rows/columns of one problem across the GPUs
     else:
-        run_ours(args, ws, rank, local)
-    if ws > 1:
-        import torch.distributed as dist
+        run_ours(args, ws, rank, local)  # N = 1, or replicas for the small configs
+    import torch.distributed as dist
 
+    if dist.is_available() and dist.is_initialized():
         dist.destroy_process_group()
 
 

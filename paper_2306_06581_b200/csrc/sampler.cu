@@ -310,36 +310,59 @@ int grid_for(spk_ctx* ctx, int64_t items, int threads) {
   return (int)std::max<int64_t>(1, std::min(need, cap));
 }
 
-// ==== tiled coordinate sampler (v2) ================================================
+// ==== tiled coordinate sampler (v3) ================================================
 //
 // One CTA = 8 warps x 4 rows; the CTA walks all columns in tiles of 256 points
 // staged in shared memory (SoA, conflict-free), each warp handles 32 columns
 // x its 4 rows per step, so every y_j is read from L2 once per 32 rows.
-// Support test: K_ij != 0  <=>  d2_ij < D0, where D0 is found once by a
-// device bisection of the exact kernel_from_cost arithmetic (monotone in d2);
-// entries within a 1e-12 relative band of D0 take the exact path. The exact
-// K (two IEEE divisions + exp) is then only computed for kept entries (and
-// for UOT, whose plan needs K^g_k). Kept entries go straight into per-row
-// slots sized from the plan pass (upper bound of the expected count + 6
-// sigma), so sampling is a single pass; any slot overflow falls back to the
-// exact two-pass kernels above.
+//
+// Support (K_ij != 0  <=>  d2_ij < D0; D0 found once by a device bisection of
+// the exact kernel_from_cost arithmetic, entries within 1e-12 of D0 take the
+// exact path): screened first in fp32 -- d2 from fp32 copies of the points
+// with an error bound 2^-18 (|x|^2 + |y|^2), far above the worst-case fp32
+// error -- so the reference-order fp64 d2 is only computed for pairs the
+// screen cannot decide.
+//
+// Draw: every supported entry consumes draw t of its row (t = 1 + #supported
+// entries to its left: ballot + popc). keep needs u_t < p* <= P_i, a per-row
+// bound of p*, so the screen evaluates only the top 32 bits of the splitmix64
+// output (out_hi = z_hi ^ (z_hi >> 31), z_hi = mulhi of the last multiply)
+// and rejects out_hi > floor(P_i 2^32) + 1; survivors (a ~P_i fraction)
+// take the exact path: full draw, exact K (two IEEE divisions + exp), exact
+// p* (SamplingPlan::prob), keep iff u < p*. Index sets are therefore the
+// reference's bit for bit. Kept entries go straight into per-row slots sized
+// from the plan pass (expected count + 6 sigma); a slot overflow falls back
+// to the exact two-pass kernels above.
+//
+// Plan pass (masked_grid_plan): supported count per row and the row's grid
+// mass -- for OT-like plans rw_i * (sum of all cb_j - sum of cb_j off the
+// support), so supported pairs cost only the screen; UOT needs K^g_k on
+// every supported pair and takes the exact path there.
 
-constexpr int kTileJ = 256;
+constexpr int kTileJ = 1024;
 constexpr int kRPW = 4;  // rows per warp
 constexpr int kTileRows = 8 * kRPW;
 
 struct TiledArgs {
-  const double* x;
+  const double* x;   // fp64 points (exact path)
   const double* y;
-  int64_t n;        // columns (target points)
-  int64_t n_rows;   // rows handled (a slab of sources for sharded builds)
-  int64_t row_base; // global index of local row 0
+  const float* xf;   // fp32 copies and squared norms (screen)
+  const float* yf;
+  const float* xn;
+  const float* yn;
+  int64_t n;         // columns (target points)
+  int64_t n_rows;    // rows handled (a slab of sources for sharded builds)
+  int64_t row_base;  // global index of local row 0
   int dim, kind;
   double eta, scale, eps;
-  double lo, hi;  // d2 < lo: supported; d2 >= hi: not; else exact
+  double lo, hi;     // d2 < lo: supported; d2 >= hi: not; else exact
+  float lof, hif;    // the same bounds in fp32 (rounded outwards)
+  float mg;          // screen margin factor; +inf disables the screen
   DPlan P;
   double s;
   uint64_t seed;
+  double colw_total;  // plan pass: sum of all column weights
+  double col_bound;   // sample pass: max column factor of the plan
   // plan mode
   long long* row_nnz;
   double* row_sum;
@@ -356,16 +379,74 @@ __device__ __forceinline__ double exact_k(const TiledArgs& A, double d2) {
   return kernel_from_d2(A.kind, d2, A.eta, A.scale, A.eps);
 }
 
+// pairwise_cost's sequential d2 (geometry.cpp:16-59), no FMA.
+template <int DIM>
+__device__ __forceinline__ double exact_d2(const double* __restrict__ xp, const double* __restrict__ yp) {
+  double d2 = 0.0;
+#pragma unroll
+  for (int k = 0; k < DIM; ++k) {
+    const double diff = dsub(xp[k], yp[k]);
+    d2 = dadd(d2, dmul(diff, diff));
+  }
+  return d2;
+}
+
+// Top 32 bits of sm_finalize(x) (the splitmix64 output): the last xor-shift
+// only touches bit 0 of the high word, and the high word of the last product
+// needs one mulhi and two low multiplies.
+__device__ __forceinline__ uint32_t sm_finalize_hi(uint64_t x) {
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  x = x ^ (x >> 27);
+  const uint32_t lo = (uint32_t)x, hi = (uint32_t)(x >> 32);
+  const uint32_t zh = __umulhi(lo, 0x133111ebu) + lo * 0x94d049bbu + hi * 0x133111ebu;
+  return zh ^ (zh >> 31);
+}
+
+// The grid entry / prob of a supported entry, given its row and column
+// weights (same operations as grid_raw / plan_prob).
+__device__ __forceinline__ double plan_prob_w(const DPlan& P, double rw, double cw, double k) {
+  double base;
+  if (P.factorized) {
+    base = dmul(rw, cw);
+  } else {
+    const double g = (P.kind == SPK_PLAN_UOT) ? dmul(dmul(rw, cw), pow(k, P.g_k))
+                     : (P.kind == SPK_PLAN_UNIFORM) ? 1.0 : dmul(rw, cw);
+    base = dmul(g, P.inv);
+  }
+  if (P.theta_mode == 1) return base == 0.0 ? 0.0 : dadd(dmul(P.omt, base), P.unif);
+  if (P.theta_mode == 2) return base > 0.0 ? dadd(dmul(P.omt, base), P.unif) : base;
+  return base;
+}
+
+// Per-row screen threshold on out_hi: p* <= P_i for every supported j.
+__device__ __forceinline__ uint32_t row_threshold(const TiledArgs& A, double rw) {
+  const DPlan& P = A.P;
+  double b;
+  if (P.factorized) b = rw * A.col_bound;
+  else b = ((P.kind == SPK_PLAN_UNIFORM) ? 1.0 : rw * A.col_bound) * P.inv;  // UOT: K^g_k <= 1
+  if (P.theta_mode) b = P.omt * b + P.unif;
+  const double Pi = A.s * b * (1.0 + 0x1p-30);
+  if (!(Pi < 1.0)) return 0xffffffffu;
+  const double t = floor(Pi * 4294967296.0) + 1.0;
+  return t >= 4294967295.0 ? 0xffffffffu : (uint32_t)t;
+}
+
 template <int DIM, bool SAMPLE, bool NEEDK, class VT>
 __global__ void __launch_bounds__(256) tiled_kernel(TiledArgs A) {
-  __shared__ double ys[DIM][kTileJ];
+  __shared__ float yfs[DIM][kTileJ];  // the screen's fp32 columns (exact paths read y from L2)
+  __shared__ float yns[kTileJ];
   const int lane = threadIdx.x & 31;
   const int w = threadIdx.x >> 5;
   const unsigned lt_mask = (1u << lane) - 1u;
   const int64_t groups = (A.n_rows + kTileRows - 1) / kTileRows;
   for (int64_t g = blockIdx.x; g < groups; g += gridDim.x) {
-    double xr[kRPW][DIM];
+    float xr[kRPW][DIM];
+    float xmg[kRPW];  // screen margin share of the row
+    float d2s[kRPW];
+    bool rvalid[kRPW];
+    double rw[kRPW];
     uint64_t st0[kRPW];
+    uint32_t th[kRPW];
     uint32_t tcnt[kRPW], cnt[kRPW];
     double racc[kRPW];
     int64_t row[kRPW];
@@ -375,9 +456,14 @@ __global__ void __launch_bounds__(256) tiled_kernel(TiledArgs A) {
     for (int q = 0; q < kRPW; ++q) {
       row[q] = g * kTileRows + w * kRPW + q;
       const bool valid = row[q] < A.n_rows;
+      const int64_t gi = A.row_base + (valid ? row[q] : 0);
 #pragma unroll
-      for (int k = 0; k < DIM; ++k) xr[q][k] = valid ? A.x[(A.row_base + row[q]) * DIM + k] : 0.0;
-      st0[q] = mix_seed(A.seed, (uint64_t)(A.row_base + row[q]));
+      for (int k = 0; k < DIM; ++k) xr[q][k] = valid ? A.xf[gi * DIM + k] : 0.f;
+      xmg[q] = A.mg * (valid ? A.xn[gi] : 0.f);
+      rvalid[q] = valid;
+      rw[q] = valid ? A.P.row_w[gi] : 0.0;
+      st0[q] = mix_seed(A.seed, (uint64_t)gi);
+      th[q] = SAMPLE ? row_threshold(A, rw[q]) : 0u;
       tcnt[q] = 0;
       cnt[q] = 0;
       racc[q] = 0.0;
@@ -389,41 +475,80 @@ __global__ void __launch_bounds__(256) tiled_kernel(TiledArgs A) {
       for (int e = threadIdx.x; e < kTileJ * DIM; e += blockDim.x) {
         const int jj = e / DIM, k = e - jj * DIM;
         const int64_t j = j0 + jj;
-        ys[k][jj] = j < A.n ? A.y[j * DIM + k] : 0.0;
+        yfs[k][jj] = j < A.n ? A.yf[j * DIM + k] : 0.f;
       }
+      for (int jj = threadIdx.x; jj < kTileJ; jj += blockDim.x) yns[jj] = j0 + jj < A.n ? A.yn[j0 + jj] : 0.f;
       __syncthreads();
       const int jend = (int)min((int64_t)kTileJ, A.n - j0);
       for (int c = 0; c < jend; c += 32) {
         const int jj = c + lane;
         const bool jvalid = jj < jend;
         const int64_t j = j0 + jj;
-        double yv[DIM];
+        const int js = jj & (kTileJ - 1);
+        float yv[DIM];
 #pragma unroll
-        for (int k = 0; k < DIM; ++k) yv[k] = ys[k][jj & (kTileJ - 1)];
+        for (int k = 0; k < DIM; ++k) yv[k] = yfs[k][js];
+        const float ymg = A.mg * yns[js];
+        // fp32 screen of the 4 x 32 pairs
+        bool in[kRPW];
+        bool all = true;
+#pragma unroll
+        for (int q = 0; q < kRPW; ++q) {
+          float d2f = 0.f;
+#pragma unroll
+          for (int k = 0; k < DIM; ++k) {
+            const float df = xr[q][k] - yv[k];
+            d2f = fmaf(df, df, d2f);
+          }
+          in[q] = jvalid && rvalid[q] && d2f + (xmg[q] + ymg) < A.lof;
+          all = all && in[q];
+          d2s[q] = d2f;
+        }
+        all = __all_sync(0xffffffffu, all);
+        if (!SAMPLE && !NEEDK && all) continue;  // all on the support: nothing off it to count
+        if (SAMPLE && all) {
+          // every pair supported: draw t of row q at lane l is tcnt + l + 1
+          bool cand = false;
+#pragma unroll
+          for (int q = 0; q < kRPW; ++q)
+            cand = cand || sm_finalize_hi(st0[q] + (uint64_t)(tcnt[q] + lane + 1u) * kGolden) <= th[q];
+          if (!__any_sync(0xffffffffu, cand)) {
+#pragma unroll
+            for (int q = 0; q < kRPW; ++q) tcnt[q] += 32u;
+            continue;  // no draw can be below its p*: nothing kept in these 128 pairs
+          }
+        }
+        // general path: exact classification where the screen could not tell
         const double cw = jvalid ? A.P.col_w[j] : 0.0;
 #pragma unroll
         for (int q = 0; q < kRPW; ++q) {
-          const bool valid = jvalid && row[q] < A.n_rows;
-          double d2 = 0.0;
-#pragma unroll
-          for (int k = 0; k < DIM; ++k) {
-            const double diff = dsub(xr[q][k], yv[k]);
-            d2 = dadd(d2, dmul(diff, diff));
-          }
+          const bool valid = jvalid && rvalid[q];
+          const double* xp = A.x + (A.row_base + row[q]) * DIM;
           double kv = -1.0;  // not computed
           bool nz;
-          if (NEEDK || !(d2 < A.lo || d2 >= A.hi)) {
-            kv = exact_k(A, d2);
-            nz = valid && kv != 0.0;
-          } else {
-            nz = valid && d2 < A.lo;
+          if (in[q]) {
+            nz = true;
+          } else if (!valid || d2s[q] - (xmg[q] + ymg) >= A.hif) {
+            nz = false;
+          } else {  // the screen cannot tell: reference arithmetic
+            const double d2 = exact_d2<DIM>(xp, A.y + j * DIM);
+            if (NEEDK || !(d2 < A.lo || d2 >= A.hi)) {
+              kv = exact_k(A, d2);
+              nz = kv != 0.0;
+            } else {
+              nz = d2 < A.lo;
+            }
           }
           if (!SAMPLE) {
-            if (nz) {
+            if (NEEDK) {  // UOT grid (pa_i pb_j) K^g_k on every supported entry
+              if (nz) {
+                if (kv < 0.0) kv = exact_k(A, exact_d2<DIM>(xp, A.y + j * DIM));
+                ++cnt[q];
+                racc[q] += dmul(dmul(rw[q], cw), pow(kv, A.P.g_k));
+              }
+            } else if (valid && !nz) {  // off the support: count and weight
               ++cnt[q];
-              const double rw = A.P.row_w[A.row_base + row[q]];
-              racc[q] += (A.P.kind == SPK_PLAN_UOT) ? dmul(dmul(rw, cw), pow(kv, A.P.g_k))
-                         : (A.P.kind == SPK_PLAN_UNIFORM) ? 1.0 : dmul(rw, cw);
+              racc[q] += cw;
             }
             continue;
           }
@@ -433,27 +558,17 @@ __global__ void __launch_bounds__(256) tiled_kernel(TiledArgs A) {
           bool keep = false;
           double ps = 0.0;
           if (nz) {
-            const double rw = A.P.row_w[A.row_base + row[q]];
-            double base_p;
-            if (A.P.factorized) base_p = dmul(rw, cw);
-            else {
-              const double gr = (A.P.kind == SPK_PLAN_UOT) ? dmul(dmul(rw, cw), pow(kv, A.P.g_k))
-                                : (A.P.kind == SPK_PLAN_UNIFORM) ? 1.0 : dmul(rw, cw);
-              base_p = dmul(gr, A.P.inv);
-            }
-            if (A.P.theta_mode == 1) base_p = base_p == 0.0 ? 0.0 : dadd(dmul(A.P.omt, base_p), A.P.unif);
-            else if (A.P.theta_mode == 2) base_p = base_p > 0.0 ? dadd(dmul(A.P.omt, base_p), A.P.unif) : base_p;
-            ps = min1(dmul(A.s, base_p));
-            if (ps > 0.0) {
-              if (ps >= 1.0) keep = true;
-              else keep = u64_to_unit(sm_finalize(st0[q] + (uint64_t)t * kGolden)) < ps;
+            const uint64_t x0 = st0[q] + (uint64_t)t * kGolden;
+            if (sm_finalize_hi(x0) <= th[q]) {  // may be kept: exact draw, K and p*
+              if (kv < 0.0) kv = exact_k(A, exact_d2<DIM>(xp, A.y + j * DIM));
+              ps = min1(dmul(A.s, plan_prob_w(A.P, rw[q], cw, kv)));
+              if (ps > 0.0) keep = ps >= 1.0 || u64_to_unit(sm_finalize(x0)) < ps;
             }
           }
           const unsigned km = __ballot_sync(0xffffffffu, keep);
           if (keep) {
             const uint32_t pos = cnt[q] + (uint32_t)__popc(km & lt_mask);
             if (pos < (uint32_t)cap[q]) {
-              if (kv < 0.0) kv = exact_k(A, d2);
               A.pool_col[base[q] + pos] = (uint32_t)j;
               static_cast<VT*>(A.pool_val)[base[q] + pos] = (VT)(ps >= 1.0 ? kv : kv / ps);
             }
@@ -469,8 +584,15 @@ __global__ void __launch_bounds__(256) tiled_kernel(TiledArgs A) {
         const long long c = warp_sum_ll((long long)cnt[q]);
         const double sacc = warp_sum(racc[q]);
         if (lane == 0) {
-          A.row_nnz[row[q]] = c;
-          A.row_sum[row[q]] = sacc;
+          if (NEEDK) {
+            A.row_nnz[row[q]] = c;
+            A.row_sum[row[q]] = sacc;
+          } else {  // c, sacc: count and column weight OFF the support
+            const long long supp = A.n - c;
+            A.row_nnz[row[q]] = supp;
+            A.row_sum[row[q]] = (A.P.kind == SPK_PLAN_UNIFORM) ? (double)supp
+                                                                : dmul(rw[q], dsub(A.colw_total, sacc));
+          }
         }
       } else if (lane == 0) {
         A.row_cnt[row[q]] = (int)cnt[q];
@@ -497,11 +619,24 @@ __global__ void threshold_kernel(TiledArgs A, double* out) {
   *out = __longlong_as_double(hi);
 }
 
+// fp32 copies of the points and their squared norms (screen inputs).
+__global__ void to_f32_kernel(const double* x, int64_t n, int dim, float* xf, float* xn) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    float s = 0.f;
+    for (int k = 0; k < dim; ++k) {
+      const float v = (float)x[i * dim + k];
+      xf[i * dim + k] = v;
+      s += v * v;
+    }
+    xn[i] = s;
+  }
+}
+
 // Upper bound of each row's expected kept count -> slot capacity
 // (count is a sum of independent Bernoullis with mean <= U: cap U + 6 sqrt(U) + 16).
 __global__ void slot_cap_kernel(int64_t n, int64_t row_base, int64_t n_cols, const long long* row_nnz,
-                                const double* row_sum, const double* row_w, double col_w_total, int factorized, double inv, double s, int theta_mode, double omt,
-                                double unif, int* cap) {
+                                const double* row_sum, const double* row_w, double col_w_total, int factorized,
+                                double inv, double s, int theta_mode, double omt, double unif, int* cap) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const double supp = row_nnz ? (double)row_nnz[row_base + i] : (double)n_cols;
     double mass = factorized ? row_w[row_base + i] * col_w_total : row_sum[row_base + i] * inv;
@@ -564,12 +699,41 @@ void launch_tiled(spk_ctx* ctx, const TiledArgs& A) {
 
 bool tiled_dim_ok(int dim) { return dim == 1 || dim == 2 || dim == 3 || dim == 4 || dim == 5 || dim == 6 || dim == 8 || dim == 10; }
 
-TiledArgs tiled_args(spk_ctx* ctx, const DevKernel& dk) {
+float f32_down(double v) {
+  if (std::isinf(v)) return v > 0 ? INFINITY : -INFINITY;
+  float f = (float)v;
+  if ((double)f > v) f = std::nextafter(f, -INFINITY);
+  return f;
+}
+float f32_up(double v) {
+  if (std::isinf(v)) return v > 0 ? INFINITY : -INFINITY;
+  float f = (float)v;
+  if ((double)f < v) f = std::nextafter(f, INFINITY);
+  return f;
+}
+
+TiledArgs tiled_args(spk_ctx* ctx, DevKernel& dk) {
   TiledArgs A{};
+  const int64_t n = dk.n;
+  if (!dk.xf.p) {
+    dk.xf.alloc(sizeof(float) * n * dk.dim);
+    dk.yf.alloc(sizeof(float) * n * dk.dim);
+    dk.xn.alloc(sizeof(float) * n);
+    dk.yn.alloc(sizeof(float) * n);
+    to_f32_kernel<<<grid_for(ctx, n, 256), 256, 0, ctx->stream>>>(dk.x.as<double>(), n, dk.dim, dk.xf.as<float>(),
+                                                                   dk.xn.as<float>());
+    to_f32_kernel<<<grid_for(ctx, n, 256), 256, 0, ctx->stream>>>(dk.y.as<double>(), n, dk.dim, dk.yf.as<float>(),
+                                                                   dk.yn.as<float>());
+    ctx->launches += 2;
+  }
   A.x = dk.x.as<double>();
   A.y = dk.y.as<double>();
-  A.n = dk.n;
-  A.n_rows = dk.n;
+  A.xf = dk.xf.as<float>();
+  A.yf = dk.yf.as<float>();
+  A.xn = dk.xn.as<float>();
+  A.yn = dk.yn.as<float>();
+  A.n = n;
+  A.n_rows = n;
   A.row_base = 0;
   A.dim = dk.dim;
   A.kind = dk.kind;
@@ -584,6 +748,11 @@ TiledArgs tiled_args(spk_ctx* ctx, const DevKernel& dk) {
   // exact-path band around the threshold (absorbs any non-monotone ULP effects)
   A.lo = D0 * (1.0 - 1e-12);
   A.hi = std::isinf(D0) ? D0 : D0 * (1.0 + 1e-12);
+  A.lof = f32_down(A.lo);
+  A.hif = f32_up(A.hi);
+  // fp32 screen: |d2_f32 - d2| <= ~2^-20 (|x|^2 + |y|^2) for |coords| < 1e15;
+  // 2^-18 leaves a 4x margin. Larger or non-finite coordinates: exact path only.
+  A.mg = dk.max_abs < 1e15 ? 0x1p-18f : INFINITY;
   return A;
 }
 
@@ -619,6 +788,13 @@ void make_dev_kernel(spk_ctx* ctx, const spk_kernel_desc* kd, double default_eps
   dk.eta = kd->eta;
   upload(ctx, dk.x, kd->x, sizeof(double) * n * kd->dim);
   upload(ctx, dk.y, kd->y, sizeof(double) * n * kd->dim);
+  double mx = 0.0;  // any non-finite coordinate disables the fp32 screen
+  for (int64_t k = 0; k < n * kd->dim; ++k) {
+    const double ax = std::fabs(kd->x[k]), ay = std::fabs(kd->y[k]);
+    mx = std::max(mx, std::isfinite(ax) ? ax : INFINITY);
+    mx = std::max(mx, std::isfinite(ay) ? ay : INFINITY);
+  }
+  dk.max_abs = mx;
   dk.have_cost = true;
   if (kd->cost_scale > 0.0) {
     dk.scale = kd->cost_scale;
@@ -713,6 +889,9 @@ void plan_pass_rows(spk_ctx* ctx, DevKernel& dk, const PlanInfo& plan, int64_t r
     A.P = P;
     A.row_nnz = row_nnz;
     A.row_sum = row_sum;
+    double ct = 0.0;
+    for (int64_t j = 0; j < n; ++j) ct += plan.col_w[j];
+    A.colw_total = ct;
     if (plan.kind == SPK_PLAN_UOT) launch_tiled<false, true, double>(ctx, A);
     else launch_tiled<false, false, double>(ctx, A);
   } else {
@@ -915,6 +1094,9 @@ void sample_sketch(spk_ctx* ctx, DevKernel& dk, const PlanInfo& plan, double s, 
     A.P = P;
     A.s = s;
     A.seed = seed;
+    double cb = 0.0;  // largest column factor of the plan (UOT: pb_j; K^g_k <= 1)
+    for (int64_t j = 0; j < ncols; ++j) cb = std::max(cb, plan.col_w[j]);
+    A.col_bound = cb;
     A.slot_off = off.as<long long>();
     A.slot_cap = cap.as<int>();
     A.pool_col = pcol.as<uint32_t>();

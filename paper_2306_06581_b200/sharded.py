@@ -287,117 +287,137 @@ def gathered_to_full(buf: torch.Tensor, n: int, m: int, world: int) -> np.ndarra
     return blocks.reshape(-1)[:n].cpu().numpy().astype(np.float64, copy=True)
 
 
+class ShardedSketch:
+    """This rank's share of a sharded sketch: build_sketch (solvers.cpp:314-335)
+    over W ranks -- the plan's row-sum gather, local sampling, the column
+    exchange and the coverage totals. Solve it (repeatedly) with solve()."""
+
+    def __init__(self, comm: Comm, shard, kernel: Coords, a, b, plan: str, lambda_: float, epsilon: float, s: float,
+                 seed: int, opts: SparSinkOptions | None = None):
+        self.comm, self.shard = comm, shard
+        self.opts = opts = opts or SparSinkOptions()
+        self.a = a = np.ascontiguousarray(a, dtype=np.float64)
+        self.b = b = np.ascontiguousarray(b, dtype=np.float64)
+        self.seed = seed
+        kd, keep = kernel.desc()
+        self.n, W, r = int(kd.n), comm.world, comm.rank
+        self.m, self.lo, self.hi = m, _, _ = slab(self.n, W, r)
+        plan_kind = L.PLAN_UNIFORM if opts.probs == "uniform" else (L.PLAN_UOT if plan == "uot" else L.PLAN_OT)
+        shard.bind_stream()
+        # 1. plan: support / normaliser pass over this rank's rows, gathered in rank order
+        need, rs, rn = shard.plan_rows(kd, a, b, plan_kind, lambda_, epsilon, W, r, m)
+        rs_all = rn_all = None
+        if need:
+            rs_all, rn_all = shard.zeros(W * m), shard.zeros(W * m, torch.int64)
+            rs_all[r * m:(r + 1) * m].copy_(rs[:m])
+            rn_all[r * m:(r + 1) * m].copy_(rn[:m])
+            comm.all_gather(rs_all, m)
+            comm.all_gather(rn_all, m)
+        # 2. sample this rank's rows
+        shard.create(kd, a, b, plan_kind, lambda_, epsilon, s, seed, opts, W, r, rs_all, rn_all)
+        del rs_all, rn_all
+        self.info = info = shard.info()
+        self.stride = info["stride"]
+        # 3. column exchange: every rank's entries of my columns, sources in rank order
+        counts, rows, vals, send_sizes = shard.export(W, m, info["row_nnz"], info["value_bytes"])
+        self.dev = counts.device
+        send_t = torch.tensor(send_sizes, dtype=torch.int64, device=self.dev)
+        recv_t = torch.zeros_like(send_t)
+        comm.all_to_all(recv_t, send_t, [1] * W, [1] * W)
+        recv_sizes = [int(x) for x in recv_t.cpu().tolist()]
+        recv_counts = torch.zeros_like(counts)
+        comm.all_to_all(recv_counts, counts, [m] * W, [m] * W)
+        total = sum(recv_sizes)
+        recv_rows = shard.zeros(max(total, 1), torch.int32)
+        recv_vals = shard.zeros(max(total, 1), vals.dtype)
+        comm.all_to_all(recv_rows[:total], rows, recv_sizes, send_sizes)
+        comm.all_to_all(recv_vals[:total], vals, recv_sizes, send_sizes)
+        del counts, rows, vals
+        shard.import_(recv_counts, recv_rows, recv_vals, total)
+        del recv_counts, recv_rows, recv_vals
+        # 4. coverage totals and sketch-wide scalars
+        er, ec = shard.coverage()
+        tot = torch.tensor([er, ec, info["row_nnz"]], dtype=torch.int64, device=self.dev)
+        comm.all_reduce_sum(tot)
+        self.empty_rows, self.empty_cols, self.nnz = (int(x) for x in tot.cpu().tolist())
+        km = torch.zeros(W, dtype=torch.float64, device=self.dev)
+        km[r] = info["kernel_mean_part"]
+        comm.all_gather(km, 1)
+        self.kernel_mean = float(sum(km.cpu().tolist()))  # rank order
+        if opts.strict and (self.empty_rows or self.empty_cols):  # strict check (solvers.cpp:325-333)
+            from .api import ERRORS
+            raise ERRORS["DegenerateSketchError"](
+                f"DegenerateSketchError: sketch orphaned {self.empty_rows} rows and {self.empty_cols} columns; "
+                "raise s or theta, or use a different seed")
+        S = self.stride * W
+        self.U = [shard.zeros(S), shard.zeros(S)]
+        self.V = [shard.zeros(S), shard.zeros(S)]
+
+    def solve(self, cfg: SolverConfig, uot: bool = False, check_every: int = 0, on_loop=None,
+              want_scalings: bool = True) -> ShardedResult:
+        """sinkhorn_ot / sinkhorn_uot<SparseKernel> (solvers.hpp:209-232) on the
+        sharded sketch, then the objective. check_every > 0 reads the loop state
+        every that many iterations (a stream sync) to stop early once converged;
+        0 runs max_iter iterations and decides at the end. on_loop("start"/"end")
+        brackets the iteration loop (bench timing)."""
+        comm, shard = self.comm, self.shard
+        W, r, m, n, stride = comm.world, comm.rank, self.m, self.n, self.stride
+        U, V = self.U, self.V
+        policy = L.POLICY_ERROR if self.opts.strict else L.POLICY_MASK
+        shard.bind_stream()
+        shard.begin(cfg, uot, policy, self.empty_rows, self.empty_cols, U[0], V[0])
+        comm.all_gather(V[0], stride)
+        # the loop: two half-steps, two all-gathers per iteration
+        if on_loop:
+            on_loop("start")
+        t = 0
+        for t in range(1, int(cfg.max_iter) + 1):
+            shard.half(0, t, V[(t - 1) & 1], U[(t - 1) & 1], U[t & 1])
+            comm.all_gather(U[t & 1], stride)
+            shard.half(1, t, U[t & 1], V[(t - 1) & 1], V[t & 1])
+            comm.all_gather(V[t & 1], stride)
+            if check_every and t % check_every == 0 and shard.status()[1]:
+                break
+        shard.finish(t, V[t & 1])
+        if on_loop:
+            on_loop("end")
+        rep, _, par = shard.status()  # raises ZeroDenominator / DegenerateSketchError like the reference
+        # readout partials, summed in rank order on every rank
+        log_domain = bool(cfg.stabilize)
+        part = torch.zeros(W * 8, dtype=torch.float64, device=self.dev)
+        part[r * 8:(r + 1) * 8] = torch.from_numpy(shard.readout(U[par], V[par], log_domain, uot, True))
+        comm.all_gather(part, 8)
+        P = part.view(W, 8).cpu().numpy()
+        res_row, res_col, cost, ent, kl_a, kl_b = (float(sum(P[q, k] for q in range(W))) for k in range(6))
+        inf_rows = [int(x) - 1 for x in P[:, 6] if x > 0]
+        kl_bad = [int(x) - 1 for x in P[:, 7] if x > 0]
+        if inf_rows:
+            from .api import ERRORS
+            raise ERRORS["InfiniteCostOnSupport"](
+                f"InfiniteCostOnSupport: plan mass on a blocked entry (row {min(inf_rows)})")
+        if uot and kl_bad:
+            from .api import SparsinkError
+            raise SparsinkError("Error: KL undefined: mass off support")
+        lam, eps = cfg.lambda_, cfg.epsilon
+        objective = (cost + lam * kl_a + lam * kl_b - eps * ent) if uot else (cost - eps * ent)
+        uf = vf = lu = lv = None
+        if want_scalings:
+            uf, vf = gathered_to_full(U[par], n, m, W), gathered_to_full(V[par], n, m, W)
+            if log_domain:
+                lu, lv = uf, vf
+                uf, vf = np.exp(lu), np.exp(lv)
+        rep.update(objective=objective, residual_row=res_row, residual_col=res_col, seed=self.seed,
+                   kernel_mean=self.kernel_mean, world=W, sketch_nnz=self.nnz)
+        return ShardedResult(uf, vf, lu, lv, rep)
+
+
 def spar_sink_sharded(comm: Comm, shard, kernel: Coords, a, b, cfg: SolverConfig, s: float, seed: int,
                       opts: SparSinkOptions | None = None, uot: bool = False, check_every: int = 0,
                       on_loop=None) -> ShardedResult:
-    """spar_sink_ot / spar_sink_uot (solvers.cpp:339-378) over W ranks.
-
-    Every rank passes the same inputs; every rank returns the full u, v and
-    the same report. check_every > 0 reads the loop state every that many
-    iterations (a stream sync) to stop early once converged; 0 runs max_iter
-    iterations (the fixed-iteration configs) and decides at the end.
-    `on_loop(event)` is called with "start"/"end" around the iteration loop
-    (bench timing)."""
-    opts = opts or SparSinkOptions()
-    a = np.ascontiguousarray(a, dtype=np.float64)
-    b = np.ascontiguousarray(b, dtype=np.float64)
-    kd, keep = kernel.desc()
-    n, W, r = int(kd.n), comm.world, comm.rank
-    m, lo, hi = slab(n, W, r)
-    plan_kind = L.PLAN_UNIFORM if opts.probs == "uniform" else (L.PLAN_UOT if uot else L.PLAN_OT)
-    policy = L.POLICY_ERROR if opts.strict else L.POLICY_MASK
-    shard.bind_stream()
-
-    # 1. plan: support / normaliser pass over this rank's rows, gathered in rank order
-    need, rs, rn = shard.plan_rows(kd, a, b, plan_kind, cfg.lambda_, cfg.epsilon, W, r, m)
-    rs_all = rn_all = None
-    if need:
-        rs_all, rn_all = shard.zeros(W * m), shard.zeros(W * m, torch.int64)
-        rs_all[r * m:(r + 1) * m].copy_(rs[:m])
-        rn_all[r * m:(r + 1) * m].copy_(rn[:m])
-        comm.all_gather(rs_all, m)
-        comm.all_gather(rn_all, m)
-    # 2. sample this rank's rows
-    shard.create(kd, a, b, plan_kind, cfg.lambda_, cfg.epsilon, s, seed, opts, W, r, rs_all, rn_all)
-    del rs_all, rn_all
-    info = shard.info()
-    stride = info["stride"]
-    # 3. column exchange: every rank's entries of my columns, sources in rank order
-    counts, rows, vals, send_sizes = shard.export(W, m, info["row_nnz"], info["value_bytes"])
-    send_t = torch.tensor(send_sizes, dtype=torch.int64, device=counts.device)
-    recv_t = torch.zeros_like(send_t)
-    comm.all_to_all(recv_t, send_t, [1] * W, [1] * W)
-    recv_sizes = [int(x) for x in recv_t.cpu().tolist()]
-    recv_counts = torch.zeros_like(counts)
-    comm.all_to_all(recv_counts, counts, [m] * W, [m] * W)
-    total = sum(recv_sizes)
-    recv_rows = shard.zeros(max(total, 1), torch.int32)
-    recv_vals = shard.zeros(max(total, 1), vals.dtype)
-    comm.all_to_all(recv_rows[:total], rows, recv_sizes, send_sizes)
-    comm.all_to_all(recv_vals[:total], vals, recv_sizes, send_sizes)
-    del counts, rows, vals
-    shard.import_(recv_counts, recv_rows, recv_vals, total)
-    del recv_counts, recv_rows, recv_vals
-    # 4. coverage totals, start
-    er, ec = shard.coverage()
-    cov = torch.tensor([er, ec], dtype=torch.int64, device=send_t.device)
-    comm.all_reduce_sum(cov)
-    er_tot, ec_tot = (int(x) for x in cov.cpu().tolist())
-    if opts.strict and (er_tot or ec_tot):  # build_sketch's strict check (solvers.cpp:325-333)
-        from .api import ERRORS
-        raise ERRORS["DegenerateSketchError"](
-            f"DegenerateSketchError: sketch orphaned {er_tot} rows and {ec_tot} columns; raise s or theta, "
-            "or use a different seed")
-    U = [shard.zeros(W * stride), shard.zeros(W * stride)]
-    V = [shard.zeros(W * stride), shard.zeros(W * stride)]
-    shard.begin(cfg, uot, policy, er_tot, ec_tot, U[0], V[0])
-    comm.all_gather(V[0], stride)
-    # 5. the loop: two half-steps, two all-gathers per iteration
-    if on_loop:
-        on_loop("start")
-    t = 0
-    for t in range(1, int(cfg.max_iter) + 1):
-        shard.half(0, t, V[(t - 1) & 1], U[(t - 1) & 1], U[t & 1])
-        comm.all_gather(U[t & 1], stride)
-        shard.half(1, t, U[t & 1], V[(t - 1) & 1], V[t & 1])
-        comm.all_gather(V[t & 1], stride)
-        if check_every and t % check_every == 0 and shard.status()[1]:
-            break
-    shard.finish(t, V[t & 1])
-    if on_loop:
-        on_loop("end")
-    rep, _, par = shard.status()  # raises ZeroDenominator / DegenerateSketchError like the reference
-    # 6. readout partials, summed in rank order on every rank
-    log_domain = bool(cfg.stabilize)
-    part = torch.zeros(W * 8, dtype=torch.float64, device=send_t.device)
-    part[r * 8:(r + 1) * 8] = torch.from_numpy(shard.readout(U[par], V[par], log_domain, uot, True))
-    comm.all_gather(part, 8)
-    P = part.view(W, 8).cpu().numpy()
-    res_row, res_col, cost, ent, kl_a, kl_b = (float(sum(P[q, k] for q in range(W))) for k in range(6))
-    inf_rows = [int(x) - 1 for x in P[:, 6] if x > 0]
-    kl_bad = [int(x) - 1 for x in P[:, 7] if x > 0]
-    if inf_rows:
-        from .api import ERRORS
-        raise ERRORS["InfiniteCostOnSupport"](f"InfiniteCostOnSupport: plan mass on a blocked entry (row {min(inf_rows)})")
-    if uot and kl_bad:
-        from .api import SparsinkError
-        raise SparsinkError("Error: KL undefined: mass off support")
-    lam, eps = cfg.lambda_, cfg.epsilon
-    objective = (cost + lam * kl_a + lam * kl_b - eps * ent) if uot else (cost - eps * ent)
-    uf, vf = gathered_to_full(U[par], n, m, W), gathered_to_full(V[par], n, m, W)
-    lu = lv = None
-    if log_domain:
-        lu, lv = uf, vf
-        uf, vf = np.exp(lu), np.exp(lv)
-    km = torch.zeros(W, dtype=torch.float64, device=send_t.device)
-    km[r] = info["kernel_mean_part"]
-    comm.all_gather(km, 1)
-    rep.update(objective=objective, residual_row=res_row, residual_col=res_col, seed=seed,
-               kernel_mean=float(sum(km.cpu().tolist())), world=W)
-    snnz = torch.tensor([info["row_nnz"]], dtype=torch.int64, device=send_t.device)
-    comm.all_reduce_sum(snnz)
-    rep["sketch_nnz"] = int(snnz.item())
-    return ShardedResult(uf, vf, lu, lv, rep)
+    """spar_sink_ot / spar_sink_uot (solvers.cpp:339-378) over W ranks: every
+    rank passes the same inputs and returns the full u, v and the same report."""
+    sk = ShardedSketch(comm, shard, kernel, a, b, "uot" if uot else "ot", cfg.lambda_, cfg.epsilon, s, seed, opts)
+    return sk.solve(cfg, uot, check_every, on_loop)
 
 
 def run_emulated(world: int, fn, device: int = 0):
