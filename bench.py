@@ -265,10 +265,12 @@ def run_ours(args, ws, rank, local):
     per_launch_iters = iters_done / args.steps
     mean_loop = sum(loop_s) / len(loop_s)
     achieved = b_iter * per_launch_iters / mean_loop / 1e9
-    traffic = None
+    traffic = None  # DRAM bytes per launch from the committed ncu --set full capture of this kernel
     prof = ROOT / "profiles" / f"ncu_{w.name.lower()}_loop.json"
     if prof.exists():
-        traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
+        k0 = json.loads(prof.read_text())["kernels"][0]
+        if "dram_bytes_per_iteration" in k0:
+            traffic = k0["dram_bytes_per_iteration"] * per_launch_iters
 
     # ---- end to end through the C ABI with host buffers ----
     e2e = None

@@ -1,7 +1,7 @@
 """Summarise ncu outputs into small committed files under profiles/.
 
   python profiles/summarize.py launches <launches.csv> <out.json>
-  python profiles/summarize.py full <report.ncu-rep> <out.json> [algorithmic_bytes_per_launch]
+  python profiles/summarize.py full <report.ncu-rep> <out.json> [algorithmic_bytes_per_launch] [iterations_per_launch]
 """
 import csv
 import io
@@ -49,7 +49,7 @@ WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
 
 
-def full(rep, out, alg=None):
+def full(rep, out, alg=None, iters=None):
     txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(txt)))
     hdr, units = rows[0], rows[1]
@@ -74,6 +74,9 @@ def full(rep, out, alg=None):
             d["dram_bytes_per_launch"] = d["dram__bytes_read.sum"] + d.get("dram__bytes_write.sum", 0.0)
         if alg:
             d["algorithmic_bytes_per_launch"] = float(alg)
+        if iters and "dram_bytes_per_launch" in d:
+            d["iterations_per_launch"] = int(iters)
+            d["dram_bytes_per_iteration"] = d["dram_bytes_per_launch"] / int(iters)
         kernels.append(d)
     json.dump({"source": rep, "kernels": kernels}, open(out, "w"), indent=1)
     print(json.dumps(kernels, indent=1)[:3000])
@@ -83,4 +86,5 @@ if __name__ == "__main__":
     if sys.argv[1] == "launches":
         launches(sys.argv[2], sys.argv[3])
     else:
-        full(sys.argv[2], sys.argv[3], sys.argv[4] if len(sys.argv) > 4 else None)
+        full(sys.argv[2], sys.argv[3], sys.argv[4] if len(sys.argv) > 4 else None,
+             sys.argv[5] if len(sys.argv) > 5 else None)
