@@ -371,3 +371,42 @@ def sinkhorn_ot(kernel, a, b, cfg: SolverConfig, policy: str = "error", ctx: Con
 
 def sinkhorn_uot(kernel, a, b, cfg: SolverConfig, policy: str = "error", ctx: Context | None = None) -> Result:
     return (ctx or default_context()).sinkhorn(kernel, a, b, cfg, uot=True, policy=policy)
+
+
+# ---- batched frame pairs (config 3) ----------------------------------------------
+_M64 = 0xFFFFFFFFFFFFFFFF
+
+
+def _splitmix64(x: int) -> int:
+    x = (x + 0x9E3779B97F4A7C15) & _M64
+    x = ((x ^ (x >> 30)) * 0xBF58476D1CE4E5B9) & _M64
+    x = ((x ^ (x >> 27)) * 0x94D049BB133111EB) & _M64
+    return x ^ (x >> 31)
+
+
+def mix_seed(seed: int, stream: int) -> int:
+    """rng.hpp:17-19: the per-stream seed (also the per-pair seed of pairwise_wfr)."""
+    return _splitmix64((seed & _M64) ^ _splitmix64((stream + 0x632BE59BD9B4E019) & _M64))
+
+
+def frame_pairs(frames: int) -> list[tuple[int, int]]:
+    """All unordered pairs i < j in the reference's pairwise_wfr order (harness.cpp:387-393)."""
+    return [(i, j) for i in range(frames) for j in range(i + 1, frames)]
+
+
+def spar_sink_pairs(ctx: Context, coords, masses, cfg: SolverConfig, s: float, seed: int, eta: float,
+                    opts: SparSinkOptions | None = None, pairs=None, rank: int = 0, world: int = 1,
+                    scale: float = 1.0) -> list[tuple[int, tuple[int, int], dict]]:
+    """Config 3's batch: spar_sink_uot with the WFR cost between frame pairs
+    (pairwise_wfr, proj/src/harness.cpp:349-406). Pair k (in frame_pairs
+    order) uses seed mix_seed(seed, k) as the reference does (:393). Pairs are
+    independent: rank r of `world` takes pairs k = r, r + world, ... (no
+    communication). Returns (k, pair, report) for this rank's pairs."""
+    pairs = pairs if pairs is not None else frame_pairs(masses.shape[0])
+    kern = Coords(coords, coords, "wfr", eta, scale=scale, eps=cfg.epsilon)
+    out = []
+    for k in range(rank, len(pairs), world):
+        i, j = pairs[k]
+        r = ctx.spar_sink(kern, masses[i], masses[j], cfg, s, mix_seed(seed, k), opts, uot=True)
+        out.append((k, (i, j), r.report))
+    return out

@@ -51,6 +51,7 @@ __device__ __forceinline__ double row_apply(const VT* __restrict__ val, const ui
       const double xv = __ldcg(x + __ldg(idx + p));
       if (xv == -CUDART_INF) continue;
       const double t = log((double)__ldg(val + p)) + xv;
+      if (t == -CUDART_INF) continue;  // a zero K~ (e.g. fp32 underflow) adds nothing
       if (t > m) {
         s = s * exp(m - t) + 1.0;
         m = t;

@@ -502,3 +502,86 @@ def test_tiled_sampler_matches_two_pass(ctx, oracle):
                 assert np.array_equal(rp, so[0]) and np.array_equal(ci, so[1]), (kind, plan, theta)
                 np.testing.assert_allclose(vv, so[2], rtol=value_rtol(kind), atol=SUBNORMAL_ATOL)
             assert np.array_equal(outs[0][2], outs[1][2])
+
+
+def test_config3_frame_pair(ctx, oracle):
+    """Config 3 (one WFR frame pair at full size, n = 12544): UOT grid plan on
+    a 22%-support kernel, fp32 sketch values, log-domain loop. Index sets bit
+    for bit against the oracle's dense path; values to one fp32 ulp; the
+    log-domain solve against the oracle on the same sketch within the fp32
+    bar (fp32 log K~ values)."""
+    from paper_2306_06581_b200 import workloads as W
+
+    w = W.c3()
+    Cm, _ = oracle.pairwise_cost(w.x, w.y, "wfr", w.eta)
+    K, r = oracle.kernel_from_cost(Cm, w.eps)
+    del Cm
+    plan = oracle.plan("uot", w.a, w.b, K, r, w.lam, w.eps)
+    so = oracle.poisson_sparsify(K, plan, w.s, 7)
+    oracle.free_plan(plan)
+    del K
+    kern = spk.Coords(w.x, w.y, "wfr", w.eta, scale=1.0, eps=w.eps)
+    sk = ctx.sketch(kern, w.a, w.b, "uot", w.lam, w.eps, w.s, 7, spk.SparSinkOptions(values="f32"))
+    rp, ci, vv = sk.csr()
+    assert np.array_equal(rp, so[0]) and np.array_equal(ci, so[1]), "index sets differ from the oracle"
+    np.testing.assert_allclose(vv, so[2].astype(np.float32).astype(np.float64), rtol=1.2e-7)
+    cfg = spk.SolverConfig(w.eps, w.lam, -1.0, 150, stabilize=True)
+    g = sk.solve(cfg, uot=True, a=w.a, b=w.b)
+    _, _, olu, olv, ores = oracle.sinkhorn(w.a, w.b, w.eps, w.lam, -1.0, 150, stabilize=True, policy="mask",
+                                           uot=True, csr=(rp, ci, vv))
+    assert g.report["iterations"] == ores["iterations"] == 150
+    fin = np.isfinite(olu)
+    assert np.array_equal(fin, np.isfinite(g.log_u))
+    # fp32 log K~ (|log K~| up to ~700): absolute error ~1e-4 in the log scalings
+    np.testing.assert_allclose(g.log_u[fin], olu[fin], rtol=1e-5, atol=2e-3)
+    fin = np.isfinite(olv)
+    np.testing.assert_allclose(g.log_v[fin], olv[fin], rtol=1e-5, atol=2e-3)
+    _, _, gobj, _ = sk.readout(kern, uot=True, lambda_=w.lam, epsilon=w.eps)
+    _, _, oobj = oracle.readout((rp, ci, vv), np.exp(olu), np.exp(olv), w.a, w.b, w.eps, w.lam, True, lu=olu, lv=olv,
+                                coords=(w.x, w.y, "wfr", w.eta, 1.0))
+    assert gobj == pytest.approx(oobj, rel=1e-4)
+
+
+def test_config5_dense_vs_sparse(ctx):
+    """Config 5 at full size (n = 5e4): the dense on-the-fly comparator against
+    Spar-Sink at s = 4, 8, 16 n ln n. The sketch estimate of the objective
+    approaches the dense one as s grows (the paper's RMAE trend)."""
+    from paper_2306_06581_b200 import workloads as W
+
+    w = W.c5()
+    kern = spk.Coords(w.x, w.y, "sqeuclid", scale=None, eps=w.eps)
+    cfg = spk.SolverConfig(w.eps, w.lam, w.delta, w.max_iter)
+    dense = ctx.sinkhorn(kern, w.a, w.b, cfg)
+    assert dense.report["iterations"] == 200 and np.isfinite(dense.report["objective"])
+    errs = []
+    for mult in (4, 8, 16):
+        sp = ctx.spar_sink(kern, w.a, w.b, cfg, mult * w.n * math.log(w.n), 7)
+        errs.append(abs(sp.report["objective"] - dense.report["objective"]) / abs(dense.report["objective"]))
+    # the entropic objective of a sketch plan converges slowly in s (measured
+    # here: ~0.34 / 0.31 / 0.27 at 4 / 8 / 16 n ln n, eps = 0.05); the trend
+    # must be monotone
+    assert all(np.isfinite(errs)) and errs[0] < 0.5, errs
+    assert errs[0] > errs[1] > errs[2], errs
+
+
+def test_config3_pairs_batch_split_across_ranks(ctx):
+    """Config 3's batch driver: pairs split round-robin over ranks give the
+    same per-pair results as solving each pair alone with mix_seed(seed, k)."""
+    from paper_2306_06581_b200 import api
+    from paper_2306_06581_b200 import workloads as W
+
+    coords, masses = W.c3_frames(3, frames=6, side=40)
+    n = coords.shape[0]
+    cfg = spk.SolverConfig(0.01, 1.0, 1e-6, 300, stabilize=True)
+    s = 10 * n * math.log(n)
+    pairs = api.frame_pairs(6)[:5]
+    got = {}
+    for r in range(2):
+        for k, pr, rep in api.spar_sink_pairs(ctx, coords, masses, cfg, s, 3, 0.1, pairs=pairs, rank=r, world=2):
+            got[k] = rep
+    assert sorted(got) == list(range(5))
+    kern = spk.Coords(coords, coords, "wfr", 0.1, scale=1.0, eps=0.01)
+    for k, (i, j) in enumerate(pairs):
+        one = ctx.spar_sink(kern, masses[i], masses[j], cfg, s, api.mix_seed(3, k), uot=True)
+        assert one.report["objective"] == got[k]["objective"]
+        assert one.report["sketch_nnz"] == got[k]["sketch_nnz"]

@@ -47,3 +47,20 @@ def test_bytes_per_iteration_formula():
     # C4 ~1.848 GB with fp32 values
     assert abs(W.bytes_per_iteration(10**6, 110_524_084, 4) / 1e9 - 1.848) < 0.01
     assert abs(W.bytes_per_iteration(1000, 55_262, 8) / 1e6 - 1.41) < 0.02
+
+
+def test_pair_seeds_follow_the_reference_rng(oracle):
+    """mix_seed(seed, k) (rng.hpp:17-19) is the per-pair seed of the batched
+    frame pairs (harness.cpp:393): its first draw must equal the oracle's
+    first draw of stream k."""
+    from paper_2306_06581_b200 import api
+
+    for seed, k in ((7, 0), (7, 5), (3, 495), (2**63 + 11, 17)):
+        m = api.mix_seed(seed, k)
+        x = (m + 0x9E3779B97F4A7C15) & api._M64
+        x = ((x ^ (x >> 30)) * 0xBF58476D1CE4E5B9) & api._M64
+        x = ((x ^ (x >> 27)) * 0x94D049BB133111EB) & api._M64
+        x ^= x >> 31
+        assert (x >> 11) * 2.0**-53 == oracle.rng_doubles(seed, k, 1)[0]
+    pairs = api.frame_pairs(32)
+    assert len(pairs) == 496 and pairs[0] == (0, 1) and pairs[-1] == (30, 31)
