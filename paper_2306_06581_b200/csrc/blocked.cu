@@ -68,21 +68,29 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 // Bounded wait: false after ~2^20 polls (a lost transaction must not hang the
-// GPU; the caller records a fault and the host raises it).
-__device__ __forceinline__ bool mbar_wait(uint64_t* bar, uint32_t parity, const unsigned int* fault) {
-  if (__ldcg(fault)) return false;  // already failed: drain fast
+// GPU; the caller records a fault and the host raises it). The fault word is
+// only read once a poll has failed (every 256th poll), so a wait on an
+// already-complete phase costs no global load; after a fault, waits drain fast.
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
+  uint32_t done;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n}"
+      : "=r"(done)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return done != 0;
+}
+__device__ __noinline__ bool mbar_wait_slow(uint64_t* bar, uint32_t parity, const unsigned int* fault) {
   for (int spin = 0; spin < (1 << 20); ++spin) {
-    uint32_t done;
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n}"
-        : "=r"(done)
-        : "r"(smem_u32(bar)), "r"(parity)
-        : "memory");
-    if (done) return true;
+    if ((spin & 255) == 0 && __ldcg(fault)) return false;
+    if (mbar_try(bar, parity)) return true;
   }
   return false;
+}
+__device__ __forceinline__ bool mbar_wait(uint64_t* bar, uint32_t parity, const unsigned int* fault) {
+  return mbar_try(bar, parity) || mbar_wait_slow(bar, parity, fault);
 }
 __device__ __forceinline__ void bulk_copy_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(
@@ -156,11 +164,13 @@ struct BlockedOp {
     }
     for (int r = threadIdx.x; r < nrows; r += blockDim.x) acc[r] = 0.0;
     __syncthreads();
-    uint32_t ph_s[kStages];
+    static_assert(kStages == 4, "parity mask below packs 4 stages");
+    uint32_t phm = 0;  // bit s: parity of the phases stage s completed so far
 #pragma unroll
-    for (int s = 0; s < kStages; ++s) ph_s[s] = ph[s];
+    for (int s = 0; s < kStages; ++s) phm |= (ph[s] & 1u) << s;
+    const uint32_t ph_base0 = ph[0], ph_base1 = ph[1], ph_base2 = ph[2], ph_base3 = ph[3];
     // parity of the phase of stage b % kStages that block b completes
-    auto par = [&](int b) -> uint32_t { return (ph_s[b % kStages] + (uint32_t)(b / kStages)) & 1u; };
+    auto par = [&](int b) -> uint32_t { return ((phm >> (b & 3)) ^ (uint32_t)(b >> 2)) & 1u; };
 
     if (w == kNW) {
       // ---- producer warp: x tiles through a kStages-deep ring ----
@@ -184,6 +194,7 @@ struct BlockedOp {
       const long long sbeg = ofs[0], send = ofs[B];
       int cb = 0;  // current block
       long long cb_end = ofs[1];
+      long long cb_next = B > 1 ? ofs[2] : send;  // next boundary, loaded one transition early
       const double* xs = tiles;  // tile of the current block
       if (!mbar_wait(&full[0], par(0), fault)) record_fault(fault, 0x20000000u | ((unsigned)ROLE << 24));
       uint32_t ua[kGroup], ub[kGroup];
@@ -202,11 +213,12 @@ struct BlockedOp {
     if (c < send) { /* warp-uniform; no break so the group stays in registers */            \
       while (c >= cb_end && cb + 1 < B) { /* release tile cb, enter the next */             \
         __syncwarp();                                                                        \
-        if (lane == 0) mbar_arrive(&empty[cb % kStages]);                                    \
+        if (lane == 0) mbar_arrive(&empty[cb & (kStages - 1)]);                                    \
         ++cb;                                                                                \
-        cb_end = ofs[cb + 1];                                                                \
-        xs = tiles + (size_t)(cb % kStages) * kTileW;                                        \
-        if (!mbar_wait(&full[cb % kStages], par(cb), fault))                                 \
+        cb_end = cb_next;                                                                    \
+        cb_next = cb + 2 <= B ? ofs[cb + 2] : send;                                          \
+        xs = tiles + (size_t)(cb & (kStages - 1)) * kTileW;                                        \
+        if (!mbar_wait(&full[cb & (kStages - 1)], par(cb), fault))                                 \
           record_fault(fault, 0x30000000u | ((unsigned)ROLE << 24) | (unsigned)cb);          \
       }                                                                                      \
       fold(UU[k], (double)VV[k], xs, acc);                                                  \
@@ -231,16 +243,18 @@ struct BlockedOp {
       // release the remaining blocks in order (tile present before release)
       for (;;) {
         __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[cb % kStages]);
+        if (lane == 0) mbar_arrive(&empty[cb & (kStages - 1)]);
         if (++cb >= B) break;
-        if (!mbar_wait(&full[cb % kStages], par(cb), fault))
+        if (!mbar_wait(&full[cb & (kStages - 1)], par(cb), fault))
           record_fault(fault, 0x40000000u | ((unsigned)ROLE << 24) | (unsigned)cb);
       }
     }
     __syncthreads();
     if (threadIdx.x == 0) {  // block b used stage b % kStages once
 #pragma unroll
-      for (int s = 0; s < kStages; ++s) ph[s] = ph_s[s] + (uint32_t)((B - s + kStages - 1) / kStages);
+      for (int s = 0; s < kStages; ++s)
+        ph[s] = (s == 0 ? ph_base0 : s == 1 ? ph_base1 : s == 2 ? ph_base2 : ph_base3) +
+                (uint32_t)((B - s + kStages - 1) / kStages);
     }
     // ---- finalize this slab's atoms ----
     for (int r = threadIdx.x; r < nrows; r += blockDim.x) {
