@@ -49,7 +49,9 @@ namespace {
 constexpr int kNW = 15;                 // consumer warps per CTA (+1 producer = 16 warps: 4 per SMSP, 128 registers)
 constexpr int kThreadsBlocked = 32 * (kNW + 1);
 constexpr int kTileW = 4096;            // x tile: 32 KB of fp64
-constexpr int kStages = 4;              // tile ring depth
+constexpr int kStages = 3;              // tile ring depth
+constexpr int kGE = 128;                // entries per cp.async group (4 chunks)
+constexpr int kMaxSlots = 5;            // entry-ring depth cap (groups)
 constexpr int kGroup = 8;               // chunks of 32 entries per prefetch group
 constexpr uint32_t kPad = 0xffffffffu;  // padding entry (never a valid packed value)
 
@@ -98,6 +100,21 @@ __device__ __forceinline__ void bulk_copy_g2s(void* dst, const void* src, uint32
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+// 16-byte global -> shared copy (Ampere-style cp.async, L2 only), grouped per thread.
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+// wait until at most n of this thread's groups are pending (n: 0..4)
+__device__ __forceinline__ void cp_async_wait_pending(int n) {
+  switch (n) {
+    case 0: asm volatile("cp.async.wait_group 0;" ::: "memory"); break;
+    case 1: asm volatile("cp.async.wait_group 1;" ::: "memory"); break;
+    case 2: asm volatile("cp.async.wait_group 2;" ::: "memory"); break;
+    case 3: asm volatile("cp.async.wait_group 3;" ::: "memory"); break;
+    default: asm volatile("cp.async.wait_group 4;" ::: "memory"); break;
+  }
+}
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async;" ::: "memory"); }
 __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
 
@@ -116,8 +133,12 @@ struct BlockedOp {
   int acc_rows;         // shared accumulator capacity (max rows of a slab over both halves)
   unsigned int* fault;  // [0] first fault code, [1] its CTA
 
+  int slots;            // entry-ring depth per consumer warp (groups of kGE entries)
+
   __host__ __device__ size_t head_bytes() const { return align16((size_t)(acc_rows + 1) * 8) + 128; }
-  size_t smem_bytes() const { return head_bytes() + (size_t)kStages * kTileW * 8; }
+  __host__ __device__ size_t ring_offset() const { return head_bytes() + (size_t)kStages * kTileW * 8; }
+  __host__ __device__ size_t ring_packed_bytes() const { return (size_t)kNW * slots * kGE * sizeof(uint32_t); }
+  size_t smem_bytes() const { return ring_offset() + ring_packed_bytes() + (size_t)kNW * slots * kGE * sizeof(VT); }
 
   // One 32-entry chunk: the layout guarantees its rows are distinct, so every
   // lane adds its product straight into its row's accumulator. A row's
@@ -164,97 +185,109 @@ struct BlockedOp {
     }
     for (int r = threadIdx.x; r < nrows; r += blockDim.x) acc[r] = 0.0;
     __syncthreads();
-    static_assert(kStages == 4, "parity mask below packs 4 stages");
-    uint32_t phm = 0;  // bit s: parity of the phases stage s completed so far
+    // bit s: parity of the next phase of stage s; flipped after every wait on it
+    uint32_t pmask = 0;
 #pragma unroll
-    for (int s = 0; s < kStages; ++s) phm |= (ph[s] & 1u) << s;
-    const uint32_t ph_base0 = ph[0], ph_base1 = ph[1], ph_base2 = ph[2], ph_base3 = ph[3];
-    // parity of the phase of stage b % kStages that block b completes
-    auto par = [&](int b) -> uint32_t { return ((phm >> (b & 3)) ^ (uint32_t)(b >> 2)) & 1u; };
+    for (int s = 0; s < kStages; ++s) pmask |= (ph[s] & 1u) << s;
+    uint32_t ph0[kStages];
+#pragma unroll
+    for (int s = 0; s < kStages; ++s) ph0[s] = ph[s];
 
     if (w == kNW) {
       // ---- producer warp: x tiles through a kStages-deep ring ----
       if (lane == 0) {
         fence_proxy_async();  // x was written with generic stores before the grid barrier
+        int s = 0;
         for (int b = 0; b < B; ++b) {
-          const int s = b % kStages;
-          if (b >= kStages && !mbar_wait(&empty[s], par(b - kStages), fault))
-            record_fault(fault, 0x10000000u | ((unsigned)ROLE << 24) | (unsigned)b);
+          if (b >= kStages) {  // stage s last held block b - kStages: wait for its release
+            if (!mbar_wait(&empty[s], (pmask >> s) & 1u, fault))
+              record_fault(fault, 0x10000000u | ((unsigned)ROLE << 24) | (unsigned)b);
+            pmask ^= 1u << s;
+          }
           const int64_t c0 = (int64_t)b * H.W;
           const int64_t cnt = min((int64_t)H.W, H.n_in - c0);
           const uint32_t bytes = (uint32_t)align16((size_t)cnt * 8);
           mbar_arrive_expect_tx(&full[s], bytes);
           bulk_copy_g2s(tiles + (size_t)s * kTileW, x + c0, bytes, &full[s]);
+          s = s + 1 == kStages ? 0 : s + 1;
         }
       }
       __syncwarp();
     } else {
-      // ---- consumer warps: one contiguous entry stream per warp ----
+      // ---- consumer warps: one contiguous entry stream per warp, streamed by
+      // cp.async into a per-warp shared ring of `slots` groups (128 entries
+      // each), slots - 1 groups in flight ahead of the one being folded ----
       const long long* ofs = H.off + ((int64_t)p * kNW + w) * (B + 1);  // block starts, padded, [B] = end
       const long long sbeg = ofs[0], send = ofs[B];
-      int cb = 0;  // current block
+      uint32_t* rp = reinterpret_cast<uint32_t*>(dsm + ring_offset()) + (size_t)w * slots * kGE;
+      VT* rv = reinterpret_cast<VT*>(dsm + ring_offset() + ring_packed_bytes()) + (size_t)w * slots * kGE;
+      const int ngroups = (int)((send - sbeg + kGE - 1) / kGE);
+      int issue_slot = 0;
+      auto issue = [&](int gi) {
+        if (gi < ngroups) {
+          const long long e0 = sbeg + (long long)gi * kGE;
+          cp_async16(rp + issue_slot * kGE + lane * 4, H.packed + e0 + lane * 4);
+          if (sizeof(VT) == 4) {
+            cp_async16(rv + issue_slot * kGE + lane * 4, gval + e0 + lane * 4);
+          } else {
+            cp_async16(rv + issue_slot * kGE + lane * 2, gval + e0 + lane * 2);
+            cp_async16(rv + issue_slot * kGE + 64 + lane * 2, gval + e0 + 64 + lane * 2);
+          }
+        }
+        cp_async_commit();  // (empty past the end: keeps the group count uniform)
+        issue_slot = issue_slot + 1 == slots ? 0 : issue_slot + 1;
+      };
+      for (int gi = 0; gi < slots - 1; ++gi) issue(gi);
+      int cb = 0, cs = 0;  // current block and its stage
       long long cb_end = ofs[1];
       long long cb_next = B > 1 ? ofs[2] : send;  // next boundary, loaded one transition early
-      const double* xs = tiles;  // tile of the current block
-      if (!mbar_wait(&full[0], par(0), fault)) record_fault(fault, 0x20000000u | ((unsigned)ROLE << 24));
-      uint32_t ua[kGroup], ub[kGroup];
-      VT va[kGroup], vb[kGroup];
-      // Two register groups of kGroup chunks: group g+1 loads while group g
-      // folds. The entry arrays carry 2*kGroup chunks of padding past the last
-      // stream, so the loads need no bounds checks.
-#define SPK_LOAD(G0, UU, VV)                                   \
-  _Pragma("unroll") for (int k = 0; k < kGroup; ++k) {         \
-    UU[k] = __ldcs(H.packed + (G0) + 32 * k + lane);           \
-    VV[k] = __ldcs(gval + (G0) + 32 * k + lane);               \
-  }
-#define SPK_CONSUME(G0, UU, VV)                                                              \
-  _Pragma("unroll") for (int k = 0; k < kGroup; ++k) {                                       \
-    const long long c = (G0) + 32 * k;                                                       \
-    if (c < send) { /* warp-uniform; no break so the group stays in registers */            \
-      while (c >= cb_end && cb + 1 < B) { /* release tile cb, enter the next */             \
-        __syncwarp();                                                                        \
-        if (lane == 0) mbar_arrive(&empty[cb & (kStages - 1)]);                                    \
-        ++cb;                                                                                \
-        cb_end = cb_next;                                                                    \
-        cb_next = cb + 2 <= B ? ofs[cb + 2] : send;                                          \
-        xs = tiles + (size_t)(cb & (kStages - 1)) * kTileW;                                        \
-        if (!mbar_wait(&full[cb & (kStages - 1)], par(cb), fault))                                 \
-          record_fault(fault, 0x30000000u | ((unsigned)ROLE << 24) | (unsigned)cb);          \
-      }                                                                                      \
-      fold(UU[k], (double)VV[k], xs, acc);                                                  \
-    }                                                                                        \
-  }
-      const long long step = 32LL * kGroup;
-      long long g = sbeg;
-      if (g < send) { SPK_LOAD(g, ua, va) }
-      while (g < send) {
-        const long long g1 = g + step;
-        if (g1 < send) { SPK_LOAD(g1, ub, vb) }
-        SPK_CONSUME(g, ua, va)
-        g = g1;
-        if (g >= send) break;
-        const long long g2 = g + step;
-        if (g2 < send) { SPK_LOAD(g2, ua, va) }
-        SPK_CONSUME(g, ub, vb)
-        g = g2;
+      const double* xs = tiles;                   // tile of the current block
+      if (!mbar_wait(&full[0], pmask & 1u, fault)) record_fault(fault, 0x20000000u | ((unsigned)ROLE << 24));
+      pmask ^= 1u;
+      int slot = 0;
+      for (int g = 0; g < ngroups; ++g) {
+        issue(g + slots - 1);
+        cp_async_wait_pending(slots - 1);  // group g has landed
+        __syncwarp();
+        const long long gbase = sbeg + (long long)g * kGE;
+#pragma unroll
+        for (int k = 0; k < kGE / 32; ++k) {
+          const long long c = gbase + 32 * k;
+          if (c < send) {  // warp-uniform
+            while (c >= cb_end && cb + 1 < B) {  // release tile cb, enter the next
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&empty[cs]);
+              ++cb;
+              cs = cs + 1 == kStages ? 0 : cs + 1;
+              cb_end = cb_next;
+              cb_next = cb + 2 <= B ? ofs[cb + 2] : send;
+              xs = tiles + (size_t)cs * kTileW;
+              if (!mbar_wait(&full[cs], (pmask >> cs) & 1u, fault))
+                record_fault(fault, 0x30000000u | ((unsigned)ROLE << 24) | (unsigned)cb);
+              pmask ^= 1u << cs;
+            }
+            fold(rp[slot * kGE + 32 * k + lane], (double)rv[slot * kGE + 32 * k + lane], xs, acc);
+          }
+        }
+        __syncwarp();  // every lane is done with this slot before it is refilled
+        slot = slot + 1 == slots ? 0 : slot + 1;
       }
-#undef SPK_LOAD
-#undef SPK_CONSUME
+      cp_async_wait_pending(0);
       // release the remaining blocks in order (tile present before release)
       for (;;) {
         __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[cb & (kStages - 1)]);
+        if (lane == 0) mbar_arrive(&empty[cs]);
         if (++cb >= B) break;
-        if (!mbar_wait(&full[cb & (kStages - 1)], par(cb), fault))
+        cs = cs + 1 == kStages ? 0 : cs + 1;
+        if (!mbar_wait(&full[cs], (pmask >> cs) & 1u, fault))
           record_fault(fault, 0x40000000u | ((unsigned)ROLE << 24) | (unsigned)cb);
+        pmask ^= 1u << cs;
       }
     }
     __syncthreads();
     if (threadIdx.x == 0) {  // block b used stage b % kStages once
 #pragma unroll
-      for (int s = 0; s < kStages; ++s)
-        ph[s] = (s == 0 ? ph_base0 : s == 1 ? ph_base1 : s == 2 ? ph_base2 : ph_base3) +
-                (uint32_t)((B - s + kStages - 1) / kStages);
+      for (int s = 0; s < kStages; ++s) ph[s] = ph0[s] + (uint32_t)((B - s + kStages - 1) / kStages);
     }
     // ---- finalize this slab's atoms ----
     for (int r = threadIdx.x; r < nrows; r += blockDim.x) {
@@ -528,7 +561,8 @@ bool run_blocked_t(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, doub
                    LoopState& st, LoopOut& out) {
   const int64_t n = sk->n;
   const int P = ctx->num_sms;
-  const size_t budget = 222 * 1024;  // dynamic shared memory per CTA (static use is ~1 KB)
+  // dynamic shared memory per CTA: 227 KB minus the loop kernel's static use
+  const size_t budget = 232448 - 1024;
   if (!sk->blocked_tried) {
     sk->blocked_tried = true;
     const int vb = sizeof(VT);
@@ -538,6 +572,7 @@ bool run_blocked_t(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, doub
         build_blocked(ctx, P, W, n, n, sk->nnz, sk->col_ptr, sk->row_idx, sk->values_t, vb, *C)) {
       BlockedOp<VT> probe{};
       probe.acc_rows = std::max(R->max_rows, C->max_rows);
+      probe.slots = 2;
       // auto mode keeps the CSR loop when rows are too few per warp to fill
       // conflict-free chunks (padding would outweigh the staged gathers)
       const bool dense_pad = ctx->use_blocked == 2 && (double)(R->padded + C->padded) > 1.35 * 2.0 * (double)sk->nnz;
@@ -553,6 +588,8 @@ bool run_blocked_t(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, doub
   op.L[1] = sk->blk_cols->h;
   op.n = n;
   op.acc_rows = std::max(sk->blk_rows->max_rows, sk->blk_cols->max_rows);
+  op.slots = kMaxSlots;  // deepest entry ring that fits
+  while (op.slots > 2 && op.smem_bytes() > budget) --op.slots;
   LoopWs& W = sk->ws;
   W.scalar.ensure(sizeof(unsigned int) * 2);
   SPK_CUDA(cudaMemsetAsync(W.scalar.p, 0, sizeof(unsigned int) * 2, ctx->stream));
