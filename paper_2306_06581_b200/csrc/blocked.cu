@@ -145,9 +145,9 @@ struct BlockedOp {
   // entries arrive in column order (earlier chunks, earlier blocks), so each
   // row is summed exactly like the reference's spmv / spmv_t loop
   // (sparsify.cpp:203-226): acc += v * x, no FMA.
-  __device__ __forceinline__ void fold(uint32_t u, double v, const double* xs, double* acc) const {
+  __device__ __forceinline__ static void fold(uint32_t u, double v, const double* xs, double* acc, uint32_t arows) {
     // padding (u = kPad, v = 0) lands in the sink row acc[acc_rows], never read
-    const uint32_t rl = min(u >> 16, (uint32_t)acc_rows);
+    const uint32_t rl = min(u >> 16, arows);
     acc[rl] = __dadd_rn(acc[rl], __dmul_rn(v, xs[u & (kTileW - 1)]));
     __syncwarp();  // the next chunk may revisit a row through another lane
   }
@@ -245,28 +245,37 @@ struct BlockedOp {
       if (!mbar_wait(&full[0], pmask & 1u, fault)) record_fault(fault, 0x20000000u | ((unsigned)ROLE << 24));
       pmask ^= 1u;
       int slot = 0;
+      const uint32_t arows = (uint32_t)acc_rows;
       for (int g = 0; g < ngroups; ++g) {
         issue(g + slots - 1);
         cp_async_wait_pending(slots - 1);  // group g has landed
         __syncwarp();
         const long long gbase = sbeg + (long long)g * kGE;
+        const uint32_t* up = rp + slot * kGE + lane;
+        const VT* vp = rv + slot * kGE + lane;
+        if (gbase + kGE <= cb_end && gbase + kGE <= send) {
+          // the whole group lies inside the current block: no boundary checks
 #pragma unroll
-        for (int k = 0; k < kGE / 32; ++k) {
-          const long long c = gbase + 32 * k;
-          if (c < send) {  // warp-uniform
-            while (c >= cb_end && cb + 1 < B) {  // release tile cb, enter the next
-              __syncwarp();
-              if (lane == 0) mbar_arrive(&empty[cs]);
-              ++cb;
-              cs = cs + 1 == kStages ? 0 : cs + 1;
-              cb_end = cb_next;
-              cb_next = cb + 2 <= B ? ofs[cb + 2] : send;
-              xs = tiles + (size_t)cs * kTileW;
-              if (!mbar_wait(&full[cs], (pmask >> cs) & 1u, fault))
-                record_fault(fault, 0x30000000u | ((unsigned)ROLE << 24) | (unsigned)cb);
-              pmask ^= 1u << cs;
+          for (int k = 0; k < kGE / 32; ++k) fold(up[32 * k], (double)vp[32 * k], xs, acc, arows);
+        } else {
+#pragma unroll
+          for (int k = 0; k < kGE / 32; ++k) {
+            const long long c = gbase + 32 * k;
+            if (c < send) {  // warp-uniform
+              while (c >= cb_end && cb + 1 < B) {  // release tile cb, enter the next
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[cs]);
+                ++cb;
+                cs = cs + 1 == kStages ? 0 : cs + 1;
+                cb_end = cb_next;
+                cb_next = cb + 2 <= B ? ofs[cb + 2] : send;
+                xs = tiles + (size_t)cs * kTileW;
+                if (!mbar_wait(&full[cs], (pmask >> cs) & 1u, fault))
+                  record_fault(fault, 0x30000000u | ((unsigned)ROLE << 24) | (unsigned)cb);
+                pmask ^= 1u << cs;
+              }
+              fold(up[32 * k], (double)vp[32 * k], xs, acc, arows);
             }
-            fold(rp[slot * kGE + 32 * k + lane], (double)rv[slot * kGE + 32 * k + lane], xs, acc);
           }
         }
         __syncwarp();  // every lane is done with this slot before it is refilled
