@@ -51,7 +51,6 @@ constexpr int kThreadsBlocked = 32 * (kNW + 1);
 constexpr int kTileW = 4096;            // x tile: 32 KB of fp64
 constexpr int kStages = 3;              // tile ring depth
 constexpr int kGE = 128;                // entries per cp.async group (4 chunks)
-constexpr int kMaxSlots = 5;            // entry-ring depth cap (groups)
 constexpr int kGroup = 8;               // chunks of 32 entries per prefetch group
 constexpr uint32_t kPad = 0xffffffffu;  // padding entry (never a valid packed value)
 
@@ -105,15 +104,10 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-// wait until at most n of this thread's groups are pending (n: 0..4)
-__device__ __forceinline__ void cp_async_wait_pending(int n) {
-  switch (n) {
-    case 0: asm volatile("cp.async.wait_group 0;" ::: "memory"); break;
-    case 1: asm volatile("cp.async.wait_group 1;" ::: "memory"); break;
-    case 2: asm volatile("cp.async.wait_group 2;" ::: "memory"); break;
-    case 3: asm volatile("cp.async.wait_group 3;" ::: "memory"); break;
-    default: asm volatile("cp.async.wait_group 4;" ::: "memory"); break;
-  }
+// wait until at most N of this thread's groups are pending
+template <int N>
+__device__ __forceinline__ void cp_async_wait_group() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async;" ::: "memory"); }
 __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
@@ -133,12 +127,12 @@ struct BlockedOp {
   int acc_rows;         // shared accumulator capacity (max rows of a slab over both halves)
   unsigned int* fault;  // [0] first fault code, [1] its CTA
 
-  int slots;            // entry-ring depth per consumer warp (groups of kGE entries)
+  static constexpr int kSlots = sizeof(VT) == 4 ? 5 : 3;  // entry-ring depth per consumer warp (groups)
 
   __host__ __device__ size_t head_bytes() const { return align16((size_t)(acc_rows + 1) * 8) + 128; }
   __host__ __device__ size_t ring_offset() const { return head_bytes() + (size_t)kStages * kTileW * 8; }
-  __host__ __device__ size_t ring_packed_bytes() const { return (size_t)kNW * slots * kGE * sizeof(uint32_t); }
-  size_t smem_bytes() const { return ring_offset() + ring_packed_bytes() + (size_t)kNW * slots * kGE * sizeof(VT); }
+  __host__ __device__ size_t ring_packed_bytes() const { return (size_t)kNW * kSlots * kGE * sizeof(uint32_t); }
+  size_t smem_bytes() const { return ring_offset() + ring_packed_bytes() + (size_t)kNW * kSlots * kGE * sizeof(VT); }
 
   // One 32-entry chunk: the layout guarantees its rows are distinct, so every
   // lane adds its product straight into its row's accumulator. A row's
@@ -215,60 +209,64 @@ struct BlockedOp {
       __syncwarp();
     } else {
       // ---- consumer warps: one contiguous entry stream per warp, streamed by
-      // cp.async into a per-warp shared ring of `slots` groups (128 entries
-      // each), slots - 1 groups in flight ahead of the one being folded ----
+      // cp.async into a per-warp shared ring of kSlots groups (kGE entries
+      // each), kSlots - 1 groups in flight ahead of the one being folded.
+      // Stream positions are 32-bit offsets from the warp's stream start. ----
       const long long* ofs = H.off + ((int64_t)p * kNW + w) * (B + 1);  // block starts, padded, [B] = end
-      const long long sbeg = ofs[0], send = ofs[B];
-      uint32_t* rp = reinterpret_cast<uint32_t*>(dsm + ring_offset()) + (size_t)w * slots * kGE;
-      VT* rv = reinterpret_cast<VT*>(dsm + ring_offset() + ring_packed_bytes()) + (size_t)w * slots * kGE;
-      const int ngroups = (int)((send - sbeg + kGE - 1) / kGE);
-      int issue_slot = 0;
-      auto issue = [&](int gi) {
-        if (gi < ngroups) {
-          const long long e0 = sbeg + (long long)gi * kGE;
-          cp_async16(rp + issue_slot * kGE + lane * 4, H.packed + e0 + lane * 4);
-          if (sizeof(VT) == 4) {
-            cp_async16(rv + issue_slot * kGE + lane * 4, gval + e0 + lane * 4);
-          } else {
-            cp_async16(rv + issue_slot * kGE + lane * 2, gval + e0 + lane * 2);
-            cp_async16(rv + issue_slot * kGE + 64 + lane * 2, gval + e0 + 64 + lane * 2);
-          }
+      const long long sbeg = ofs[0];
+      const int slen = (int)(ofs[B] - sbeg);
+      uint32_t* rp = reinterpret_cast<uint32_t*>(dsm + ring_offset()) + (size_t)w * kSlots * kGE;
+      VT* rv = reinterpret_cast<VT*>(dsm + ring_offset() + ring_packed_bytes()) + (size_t)w * kSlots * kGE;
+      const int ngroups = (slen + kGE - 1) / kGE;
+      constexpr int kVL = 16 / (int)sizeof(VT);  // values per 16-byte copy
+      const uint32_t* gp = H.packed + sbeg + lane * 4;
+      const VT* gq = gval + sbeg + lane * kVL;
+      int issue_slot = 0, issued = 0;
+      auto issue = [&]() {
+        if (issued < ngroups) {
+          cp_async16(rp + issue_slot * kGE + lane * 4, gp);
+          cp_async16(rv + issue_slot * kGE + lane * kVL, gq);
+          if (sizeof(VT) == 8) cp_async16(rv + issue_slot * kGE + 64 + lane * kVL, gq + 64);
+          gp += kGE;
+          gq += kGE;
         }
+        ++issued;
         cp_async_commit();  // (empty past the end: keeps the group count uniform)
-        issue_slot = issue_slot + 1 == slots ? 0 : issue_slot + 1;
+        issue_slot = issue_slot + 1 == kSlots ? 0 : issue_slot + 1;
       };
-      for (int gi = 0; gi < slots - 1; ++gi) issue(gi);
+#pragma unroll
+      for (int gi = 0; gi < kSlots - 1; ++gi) issue();
       int cb = 0, cs = 0;  // current block and its stage
-      long long cb_end = ofs[1];
-      long long cb_next = B > 1 ? ofs[2] : send;  // next boundary, loaded one transition early
-      const double* xs = tiles;                   // tile of the current block
+      int cb_end = (int)(ofs[1] - sbeg);
+      int cb_next = (int)((B > 1 ? ofs[2] : ofs[B]) - sbeg);  // next boundary, loaded one transition early
+      const double* xs = tiles;                               // tile of the current block
       if (!mbar_wait(&full[0], pmask & 1u, fault)) record_fault(fault, 0x20000000u | ((unsigned)ROLE << 24));
       pmask ^= 1u;
       int slot = 0;
       const uint32_t arows = (uint32_t)acc_rows;
       for (int g = 0; g < ngroups; ++g) {
-        issue(g + slots - 1);
-        cp_async_wait_pending(slots - 1);  // group g has landed
+        issue();
+        cp_async_wait_group<kSlots - 1>();  // group g has landed
         __syncwarp();
-        const long long gbase = sbeg + (long long)g * kGE;
+        const int gbase = g * kGE;
         const uint32_t* up = rp + slot * kGE + lane;
         const VT* vp = rv + slot * kGE + lane;
-        if (gbase + kGE <= cb_end && gbase + kGE <= send) {
+        if (gbase + kGE <= cb_end && gbase + kGE <= slen) {
           // the whole group lies inside the current block: no boundary checks
 #pragma unroll
           for (int k = 0; k < kGE / 32; ++k) fold(up[32 * k], (double)vp[32 * k], xs, acc, arows);
         } else {
 #pragma unroll
           for (int k = 0; k < kGE / 32; ++k) {
-            const long long c = gbase + 32 * k;
-            if (c < send) {  // warp-uniform
+            const int c = gbase + 32 * k;
+            if (c < slen) {  // warp-uniform
               while (c >= cb_end && cb + 1 < B) {  // release tile cb, enter the next
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty[cs]);
                 ++cb;
                 cs = cs + 1 == kStages ? 0 : cs + 1;
                 cb_end = cb_next;
-                cb_next = cb + 2 <= B ? ofs[cb + 2] : send;
+                cb_next = (int)((cb + 2 <= B ? ofs[cb + 2] : ofs[B]) - sbeg);
                 xs = tiles + (size_t)cs * kTileW;
                 if (!mbar_wait(&full[cs], (pmask >> cs) & 1u, fault))
                   record_fault(fault, 0x30000000u | ((unsigned)ROLE << 24) | (unsigned)cb);
@@ -279,9 +277,9 @@ struct BlockedOp {
           }
         }
         __syncwarp();  // every lane is done with this slot before it is refilled
-        slot = slot + 1 == slots ? 0 : slot + 1;
+        slot = slot + 1 == kSlots ? 0 : slot + 1;
       }
-      cp_async_wait_pending(0);
+      cp_async_wait_group<0>();
       // release the remaining blocks in order (tile present before release)
       for (;;) {
         __syncwarp();
@@ -581,7 +579,6 @@ bool run_blocked_t(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, doub
         build_blocked(ctx, P, W, n, n, sk->nnz, sk->col_ptr, sk->row_idx, sk->values_t, vb, *C)) {
       BlockedOp<VT> probe{};
       probe.acc_rows = std::max(R->max_rows, C->max_rows);
-      probe.slots = 2;
       // auto mode keeps the CSR loop when rows are too few per warp to fill
       // conflict-free chunks (padding would outweigh the staged gathers)
       const bool dense_pad = ctx->use_blocked == 2 && (double)(R->padded + C->padded) > 1.35 * 2.0 * (double)sk->nnz;
@@ -597,8 +594,6 @@ bool run_blocked_t(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, doub
   op.L[1] = sk->blk_cols->h;
   op.n = n;
   op.acc_rows = std::max(sk->blk_rows->max_rows, sk->blk_cols->max_rows);
-  op.slots = kMaxSlots;  // deepest entry ring that fits
-  while (op.slots > 2 && op.smem_bytes() > budget) --op.slots;
   LoopWs& W = sk->ws;
   W.scalar.ensure(sizeof(unsigned int) * 2);
   SPK_CUDA(cudaMemsetAsync(W.scalar.p, 0, sizeof(unsigned int) * 2, ctx->stream));
