@@ -389,12 +389,51 @@ class Reference:
         L.ref_time_scaling_iters.argtypes = [C.c_int64, I64P, U32P, DP, DP, DP, C.c_int64, DP, DP]
         L.ref_sparse_loop_timed.argtypes = [C.c_int64, I64P, U32P, DP, DP, DP, C.c_double, C.c_double, C.c_int64,
                                             C.c_int, DP, C.POINTER(ref_result)]
+        L.ref_measure_from_image.argtypes = [DP, C.c_int64, C.c_int64, DP, DP]
+        L.ref_mean_pool.argtypes = [DP, C.c_int64, C.c_int64, C.c_int64, C.c_int64, DP, I64P, I64P]
+        L.ref_pairwise_wfr.argtypes = [DP, C.c_int64, C.c_int64, C.c_int64, C.c_double, C.c_double, C.c_double,
+                                       C.c_double, C.c_uint64, C.c_int64, C.c_int, DP, I64P, I64P]
+        L.ref_predict_ed.argtypes = [DP, C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_int64, I64P, DP]
 
     def _check(self, rc):
         if rc:
             cat = C.c_int()
             msg = self.lib.ref_last_error(C.byref(cat)).decode()
             raise OracleError(rc, msg)
+
+    # -- frame-pair caller (measures.cpp:36-85, harness.cpp:349-437) ---------------
+    def measure_from_image(self, px, h, w):
+        px = np.ascontiguousarray(px, dtype=np.float64)
+        coords, weights = np.empty(2 * h * w), np.empty(h * w)
+        self._check(self.lib.ref_measure_from_image(px.ctypes.data_as(DP), h, w, coords.ctypes.data_as(DP),
+                                                    weights.ctypes.data_as(DP)))
+        return coords.reshape(h * w, 2), weights
+
+    def mean_pool(self, px, h, w, filt, stride):
+        px = np.ascontiguousarray(px, dtype=np.float64)
+        out = np.empty(h * w)
+        oh, ow = np.zeros(1, np.int64), np.zeros(1, np.int64)
+        self._check(self.lib.ref_mean_pool(px.ctypes.data_as(DP), h, w, filt, stride, out.ctypes.data_as(DP),
+                                           oh.ctypes.data_as(I64P), ow.ctypes.data_as(I64P)))
+        return out[:int(oh[0]) * int(ow[0])].copy(), int(oh[0]), int(ow[0])
+
+    def pairwise_wfr(self, frames, h, w, eta, lam, eps, s_mult, seed, stride=1, exact=False):
+        fr = np.ascontiguousarray(frames, dtype=np.float64)
+        nf = fr.shape[0]
+        d = np.empty(nf * nf)
+        m, failed = np.zeros(1, np.int64), np.zeros(1, np.int64)
+        self._check(self.lib.ref_pairwise_wfr(fr.ctypes.data_as(DP), nf, h, w, eta, lam, eps, s_mult, seed, stride,
+                                              int(exact), d.ctypes.data_as(DP), m.ctypes.data_as(I64P),
+                                              failed.ctypes.data_as(I64P)))
+        mm = int(m[0])
+        return d[:mm * mm].reshape(mm, mm).copy(), int(failed[0])
+
+    def predict_ed(self, d, t_es, lo, hi, t_true):
+        d = np.ascontiguousarray(d, dtype=np.float64)
+        th, err = np.zeros(1, np.int64), np.zeros(1)
+        self._check(self.lib.ref_predict_ed(d.ctypes.data_as(DP), d.shape[0], t_es, lo, hi, t_true,
+                                            th.ctypes.data_as(I64P), err.ctypes.data_as(DP)))
+        return int(th[0]), float(err[0])
 
     def rng_doubles(self, seed, stream, count):
         out = np.empty(count)

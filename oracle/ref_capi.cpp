@@ -20,6 +20,7 @@
 
 #include "sparsink/errors.hpp"
 #include "sparsink/geometry.hpp"
+#include "sparsink/harness.hpp"
 #include "sparsink/measures.hpp"
 #include "sparsink/rng.hpp"
 #include "sparsink/solvers.hpp"
@@ -358,6 +359,61 @@ int ref_sparse_loop_timed(int64_t n, const int64_t* rp, const uint32_t* ci, cons
                         : sinkhorn_ot(sk, da, db, cfg, EmptyPolicy::Mask);
     *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     fill(res, r);
+  });
+}
+
+
+// ---- frame-pair caller: measures.cpp:36-85, harness.cpp:349-437 ----
+
+static FrameImage frame(const double* px, int64_t h, int64_t w) {
+  FrameImage f;
+  f.height = (std::size_t)h;
+  f.width = (std::size_t)w;
+  f.pixels.assign(px, px + h * w);
+  return f;
+}
+
+int ref_measure_from_image(const double* px, int64_t h, int64_t w, double* coords, double* weights) {
+  return guard([&] {
+    DiscreteMeasure m = measure_from_image(frame(px, h, w));
+    std::memcpy(coords, m.support.coords.data(), sizeof(double) * m.support.coords.size());
+    std::memcpy(weights, m.weights.data(), sizeof(double) * m.weights.size());
+  });
+}
+
+int ref_mean_pool(const double* px, int64_t h, int64_t w, int64_t filter, int64_t stride, double* out, int64_t* oh,
+                  int64_t* ow) {
+  return guard([&] {
+    FrameImage o = mean_pool(frame(px, h, w), (std::size_t)filter, (std::size_t)stride);
+    *oh = (int64_t)o.height;
+    *ow = (int64_t)o.width;
+    std::memcpy(out, o.pixels.data(), sizeof(double) * o.pixels.size());
+  });
+}
+
+int ref_pairwise_wfr(const double* frames, int64_t nframes, int64_t h, int64_t w, double eta, double lambda,
+                     double eps, double s_mult, uint64_t seed, int64_t stride, int exact, double* dist, int64_t* m,
+                     int64_t* failed) {
+  return guard([&] {
+    std::vector<FrameImage> fs;
+    for (int64_t k = 0; k < nframes; ++k) fs.push_back(frame(frames + k * h * w, h, w));
+    PairwiseWfrResult r = pairwise_wfr(fs, eta, lambda, eps, s_mult, seed, (std::size_t)stride, exact != 0);
+    *m = (int64_t)r.distances.rows();
+    *failed = (int64_t)r.failed_pairs;
+    for (int64_t i = 0; i < *m; ++i)
+      for (int64_t j = 0; j < *m; ++j) dist[i * *m + j] = r.distances(i, j);
+  });
+}
+
+int ref_predict_ed(const double* d, int64_t m, int64_t t_es, int64_t lo, int64_t hi, int64_t t_true, int64_t* t_hat,
+                   double* err) {
+  return guard([&] {
+    Matrix dm((std::size_t)m, (std::size_t)m, 0.0);
+    for (int64_t i = 0; i < m; ++i)
+      for (int64_t j = 0; j < m; ++j) dm(i, j) = d[i * m + j];
+    EdPrediction p = predict_ed(dm, (std::size_t)t_es, (std::size_t)lo, (std::size_t)hi, (std::size_t)t_true);
+    *t_hat = (int64_t)p.t_ed_hat;
+    *err = p.error;
   });
 }
 
