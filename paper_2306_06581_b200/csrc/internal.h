@@ -224,6 +224,7 @@ struct DevKernel {
   bool max_normalised = false;  // scale == c0 (every finite C_ij <= 1)
   double max_abs = 0.0;         // largest |coordinate| (enables the fp32 support screen)
   DBuf xf, yf, xn, yn;          // fp32 coordinates + squared norms (built on first use)
+  DBuf ytr;                     // per sampler column tile: max |y_j|
 };
 
 void make_dev_kernel(spk_ctx* ctx, const spk_kernel_desc* kd, double default_eps, DevKernel& dk,

@@ -358,6 +358,7 @@ struct TiledArgs {
   double lo, hi;     // d2 < lo: supported; d2 >= hi: not; else exact
   float lof, hif;    // the same bounds in fp32 (rounded outwards)
   float mg;          // screen margin factor; +inf disables the screen
+  const double* ytile_r;  // per column tile: max |y_j| (rounded up)
   DPlan P;
   double s;
   uint64_t seed;
@@ -441,6 +442,7 @@ __global__ void __launch_bounds__(256) tiled_kernel(TiledArgs A) {
   const int64_t groups = (A.n_rows + kTileRows - 1) / kTileRows;
   for (int64_t g = blockIdx.x; g < groups; g += gridDim.x) {
     float xr[kRPW][DIM];
+    double xnorm[kRPW];  // |x_i| rounded up (inf for padding rows): whole-tile support test
     float xmg[kRPW];  // screen margin share of the row
     float d2s[kRPW];
     bool rvalid[kRPW];
@@ -460,6 +462,12 @@ __global__ void __launch_bounds__(256) tiled_kernel(TiledArgs A) {
 #pragma unroll
       for (int k = 0; k < DIM; ++k) xr[q][k] = valid ? A.xf[gi * DIM + k] : 0.f;
       xmg[q] = A.mg * (valid ? A.xn[gi] : 0.f);
+      {
+        double sq = 0.0;
+#pragma unroll
+        for (int k = 0; k < DIM; ++k) sq += A.x[gi * DIM + k] * A.x[gi * DIM + k];
+        xnorm[q] = valid ? sqrt(sq) * (1.0 + 1e-15) : CUDART_INF;
+      }
       rvalid[q] = valid;
       rw[q] = valid ? A.P.row_w[gi] : 0.0;
       st0[q] = mix_seed(A.seed, (uint64_t)gi);
@@ -480,6 +488,18 @@ __global__ void __launch_bounds__(256) tiled_kernel(TiledArgs A) {
       for (int jj = threadIdx.x; jj < kTileJ; jj += blockDim.x) yns[jj] = j0 + jj < A.n ? A.yn[j0 + jj] : 0.f;
       __syncthreads();
       const int jend = (int)min((int64_t)kTileJ, A.n - j0);
+      // |x_i - y_j| <= |x_i| + max_tile |y_j|: when that bound is inside the
+      // support for all 4 rows, every pair of the tile is supported
+      bool tile_all = true;
+      {
+        const double R = A.ytile_r[j0 / kTileJ];
+#pragma unroll
+        for (int q = 0; q < kRPW; ++q) {
+          const double b = xnorm[q] + R;
+          tile_all = tile_all && b * b * (1.0 + 1e-12) < A.lo;
+        }
+      }
+      if (!SAMPLE && !NEEDK && tile_all) continue;  // nothing off the support in this tile
       for (int c = 0; c < jend; c += 32) {
         const int jj = c + lane;
         const bool jvalid = jj < jend;
@@ -489,20 +509,29 @@ __global__ void __launch_bounds__(256) tiled_kernel(TiledArgs A) {
 #pragma unroll
         for (int k = 0; k < DIM; ++k) yv[k] = yfs[k][js];
         const float ymg = A.mg * yns[js];
-        // fp32 screen of the 4 x 32 pairs
+        // fp32 screen of the 4 x 32 pairs (skipped when the tile is known supported)
         bool in[kRPW];
         bool all = true;
+        if (tile_all) {
 #pragma unroll
-        for (int q = 0; q < kRPW; ++q) {
-          float d2f = 0.f;
-#pragma unroll
-          for (int k = 0; k < DIM; ++k) {
-            const float df = xr[q][k] - yv[k];
-            d2f = fmaf(df, df, d2f);
+          for (int q = 0; q < kRPW; ++q) {
+            in[q] = jvalid;
+            d2s[q] = 0.f;
           }
-          in[q] = jvalid && rvalid[q] && d2f + (xmg[q] + ymg) < A.lof;
-          all = all && in[q];
-          d2s[q] = d2f;
+          all = jvalid;
+        } else {
+#pragma unroll
+          for (int q = 0; q < kRPW; ++q) {
+            float d2f = 0.f;
+#pragma unroll
+            for (int k = 0; k < DIM; ++k) {
+              const float df = xr[q][k] - yv[k];
+              d2f = fmaf(df, df, d2f);
+            }
+            in[q] = jvalid && rvalid[q] && d2f + (xmg[q] + ymg) < A.lof;
+            all = all && in[q];
+            d2s[q] = d2f;
+          }
         }
         all = __all_sync(0xffffffffu, all);
         if (!SAMPLE && !NEEDK && all) continue;  // all on the support: nothing off it to count
@@ -619,6 +648,25 @@ __global__ void threshold_kernel(TiledArgs A, double* out) {
   *out = __longlong_as_double(hi);
 }
 
+// Largest |y_j| over each column tile, rounded up (whole-tile support test).
+__global__ void tile_radius_kernel(const double* y, int64_t n, int dim, double* r) {
+  const int64_t j0 = (int64_t)blockIdx.x * kTileJ;
+  double m = 0.0;
+  for (int64_t j = j0 + threadIdx.x; j < min(n, j0 + kTileJ); j += blockDim.x) {
+    double s = 0.0;
+    for (int k = 0; k < dim; ++k) s += y[j * dim + k] * y[j * dim + k];
+    m = fmax(m, s);
+  }
+  m = warp_max(m);
+  __shared__ double sm[32];
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = fmax(m, sm[w]);
+    r[blockIdx.x] = isfinite(m) ? sqrt(m) * (1.0 + 1e-15) : CUDART_INF;
+  }
+}
+
 // fp32 copies of the points and their squared norms (screen inputs).
 __global__ void to_f32_kernel(const double* x, int64_t n, int dim, float* xf, float* xn) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -724,7 +772,10 @@ TiledArgs tiled_args(spk_ctx* ctx, DevKernel& dk) {
                                                                    dk.xn.as<float>());
     to_f32_kernel<<<grid_for(ctx, n, 256), 256, 0, ctx->stream>>>(dk.y.as<double>(), n, dk.dim, dk.yf.as<float>(),
                                                                    dk.yn.as<float>());
-    ctx->launches += 2;
+    const int64_t tiles = (n + kTileJ - 1) / kTileJ;
+    dk.ytr.alloc(sizeof(double) * tiles);
+    tile_radius_kernel<<<(int)tiles, 256, 0, ctx->stream>>>(dk.y.as<double>(), n, dk.dim, dk.ytr.as<double>());
+    ctx->launches += 3;
   }
   A.x = dk.x.as<double>();
   A.y = dk.y.as<double>();
@@ -732,6 +783,7 @@ TiledArgs tiled_args(spk_ctx* ctx, DevKernel& dk) {
   A.yf = dk.yf.as<float>();
   A.xn = dk.xn.as<float>();
   A.yn = dk.yn.as<float>();
+  A.ytile_r = dk.ytr.as<double>();
   A.n = n;
   A.n_rows = n;
   A.row_base = 0;
