@@ -323,6 +323,28 @@ int spk_shard_status(spk_shard* sh, spk_report* rep, int32_t* stopped, int32_t* 
 int spk_shard_readout(spk_shard* sh, const double* u_dev, const double* v_dev, int log_domain, int uot,
                       int want_objective, double* out);
 
+/* ---- barycenters --------------------------------------------
+ * BarycenterResult (barycenter.hpp:20-26) without the weights (written to q). */
+typedef struct {
+  int64_t iterations;
+  int32_t converged;
+  int32_t diverged;
+  int64_t masked_atoms;
+  double wall_time_s;
+} spk_ibp_report;
+
+/* ibp<SparseKernel> (barycenter.hpp:48-206) on m device sketches of one
+ * dimension n: b = m x n host weights (row-major), w = m barycenter weights,
+ * policy = spk_empty_policy. q receives the n barycenter weights. */
+int spk_ibp(spk_ctx* ctx, spk_sketch* const* sketches, int32_t m, const double* b, const double* w, double delta,
+            int64_t max_iter, int32_t policy, double* q, spk_ibp_report* rep);
+/* spar_ibp (barycenter.cpp:8-40): sketch each kernel kds[k] with the
+ * column-constant plan and seed mix_seed(seed, k), then ibp (Mask policy;
+ * strict: orphan check + Error policy). */
+int spk_spar_ibp(spk_ctx* ctx, const spk_kernel_desc* kds, int32_t m, const double* b, const double* w, double delta,
+                 int64_t max_iter, double s, uint64_t seed, int32_t strict, int32_t value_type, double* q,
+                 spk_ibp_report* rep);
+
 /* ---- helpers exposed for parity tests --------------------------------------- */
 
 /* SamplingPlan::prob(i, j) (sparsify.hpp:28-34) of the plan that

@@ -350,6 +350,11 @@ def _seq(w) -> float:
     return t
 
 
+class ref_ibp_result(C.Structure):
+    _fields_ = [("iterations", C.c_int64), ("converged", C.c_int32), ("diverged", C.c_int32),
+                ("masked_atoms", C.c_int64)]
+
+
 class Reference:
     """ctypes view of the compiled, unmodified reference (oracle/_ref)."""
 
@@ -394,6 +399,10 @@ class Reference:
         L.ref_pairwise_wfr.argtypes = [DP, C.c_int64, C.c_int64, C.c_int64, C.c_double, C.c_double, C.c_double,
                                        C.c_double, C.c_uint64, C.c_int64, C.c_int, DP, I64P, I64P]
         L.ref_predict_ed.argtypes = [DP, C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_int64, I64P, DP]
+        L.ref_ibp.argtypes = [C.c_int32, C.c_int64, DP, DP, I64P, U32P, DP, I64P, DP, DP, C.c_double, C.c_int64,
+                              C.c_int, DP, C.POINTER(ref_ibp_result)]
+        L.ref_spar_ibp.argtypes = [C.c_int32, C.c_int64, DP, DP, DP, DP, C.c_double, C.c_int64, C.c_double,
+                                   C.c_uint64, C.c_int, DP, C.POINTER(ref_ibp_result)]
 
     def _check(self, rc):
         if rc:
@@ -427,6 +436,44 @@ class Reference:
                                               failed.ctypes.data_as(I64P)))
         mm = int(m[0])
         return d[:mm * mm].reshape(mm, mm).copy(), int(failed[0])
+
+    def ibp(self, b, w, delta=1e-6, max_iter=1000, policy="error", Ks=None, ratios=None, sketches=None):
+        """ibp on m dense kernels (Ks, ratios) or m CSR sketches [(rp, ci, val), ...]."""
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        w = np.ascontiguousarray(w, dtype=np.float64)
+        m, n = b.shape
+        q = np.empty(n)
+        res = ref_ibp_result()
+        pol = 1 if policy == "mask" else 0
+        if sketches is not None:
+            rp = np.ascontiguousarray(np.concatenate([s[0] for s in sketches]), dtype=np.int64)
+            ci = np.ascontiguousarray(np.concatenate([s[1] for s in sketches]), dtype=np.uint32)
+            val = np.ascontiguousarray(np.concatenate([s[2] for s in sketches]), dtype=np.float64)
+            nnz = np.array([len(s[1]) for s in sketches], dtype=np.int64)
+            self._check(self.lib.ref_ibp(m, n, None, None, rp.ctypes.data_as(I64P), ci.ctypes.data_as(U32P),
+                                         val.ctypes.data_as(DP), nnz.ctypes.data_as(I64P), b.ctypes.data_as(DP),
+                                         w.ctypes.data_as(DP), delta, max_iter, pol, q.ctypes.data_as(DP),
+                                         C.byref(res)))
+        else:
+            K = np.ascontiguousarray(np.stack(Ks), dtype=np.float64)
+            r = np.ascontiguousarray(ratios, dtype=np.float64)
+            self._check(self.lib.ref_ibp(m, n, K.ctypes.data_as(DP), r.ctypes.data_as(DP), None, None, None, None,
+                                         b.ctypes.data_as(DP), w.ctypes.data_as(DP), delta, max_iter, pol,
+                                         q.ctypes.data_as(DP), C.byref(res)))
+        return q, {k: getattr(res, k) for k, _ in res._fields_}
+
+    def spar_ibp(self, Ks, ratios, b, w, s, seed, delta=1e-6, max_iter=1000, strict=False):
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        w = np.ascontiguousarray(w, dtype=np.float64)
+        m, n = b.shape
+        K = np.ascontiguousarray(np.stack(Ks), dtype=np.float64)
+        r = np.ascontiguousarray(ratios, dtype=np.float64)
+        q = np.empty(n)
+        res = ref_ibp_result()
+        self._check(self.lib.ref_spar_ibp(m, n, K.ctypes.data_as(DP), r.ctypes.data_as(DP), b.ctypes.data_as(DP),
+                                          w.ctypes.data_as(DP), delta, max_iter, s, seed, int(strict),
+                                          q.ctypes.data_as(DP), C.byref(res)))
+        return q, {k: getattr(res, k) for k, _ in res._fields_}
 
     def predict_ed(self, d, t_es, lo, hi, t_true):
         d = np.ascontiguousarray(d, dtype=np.float64)

@@ -21,6 +21,7 @@
 #include "sparsink/errors.hpp"
 #include "sparsink/geometry.hpp"
 #include "sparsink/harness.hpp"
+#include "sparsink/barycenter.hpp"
 #include "sparsink/measures.hpp"
 #include "sparsink/rng.hpp"
 #include "sparsink/solvers.hpp"
@@ -414,6 +415,75 @@ int ref_predict_ed(const double* d, int64_t m, int64_t t_es, int64_t lo, int64_t
     EdPrediction p = predict_ed(dm, (std::size_t)t_es, (std::size_t)lo, (std::size_t)hi, (std::size_t)t_true);
     *t_hat = (int64_t)p.t_ed_hat;
     *err = p.error;
+  });
+}
+
+
+// ---- barycenters (barycenter.hpp:48-206, barycenter.cpp:8-40) ----------------------
+
+struct ref_ibp_result {
+  int64_t iterations;
+  int32_t converged, diverged;
+  int64_t masked_atoms;
+};
+
+static void fill_ibp(ref_ibp_result* r, const BarycenterResult& b, double* q) {
+  r->iterations = (int64_t)b.iterations;
+  r->converged = b.converged;
+  r->diverged = b.diverged;
+  r->masked_atoms = (int64_t)b.masked_atoms;
+  std::memcpy(q, b.weights.data(), sizeof(double) * b.weights.size());
+}
+
+// ibp<KernelMatrix> (dense) or ibp<SparseKernel> (rp != NULL: m CSR sketches back to back)
+int ref_ibp(int32_t m, int64_t n, const double* K, const double* nnz_ratio, const int64_t* rp, const uint32_t* ci,
+            const double* val, const int64_t* nnz, const double* b, const double* w, double delta, int64_t max_iter,
+            int policy, double* q, ref_ibp_result* res) {
+  return guard([&] {
+    std::vector<DiscreteMeasure> ms;
+    for (int k = 0; k < m; ++k) ms.push_back(measure(b + k * n, n));
+    std::vector<const DiscreteMeasure*> mp;
+    for (auto& x : ms) mp.push_back(&x);
+    BarycenterConfig cfg;
+    cfg.delta = delta;
+    cfg.max_iter = (std::size_t)max_iter;
+    const EmptyPolicy pol = policy ? EmptyPolicy::Mask : EmptyPolicy::Error;
+    std::vector<double> wv(w, w + m);
+    if (rp) {
+      std::vector<SparseKernel> sks;
+      int64_t off = 0;
+      for (int k = 0; k < m; ++k) {
+        sks.push_back(sketch(n, rp + k * (n + 1), ci + off, val + off));
+        off += nnz[k];
+      }
+      std::vector<const SparseKernel*> kp;
+      for (auto& x : sks) kp.push_back(&x);
+      fill_ibp(res, ibp(kp, mp, wv, cfg, pol), q);
+    } else {
+      std::vector<KernelMatrix> ks;
+      for (int k = 0; k < m; ++k) ks.push_back(kernel(K + k * n * n, n, 1.0, nnz_ratio[k]));
+      std::vector<const KernelMatrix*> kp;
+      for (auto& x : ks) kp.push_back(&x);
+      fill_ibp(res, ibp(kp, mp, wv, cfg, pol), q);
+    }
+  });
+}
+
+int ref_spar_ibp(int32_t m, int64_t n, const double* K, const double* nnz_ratio, const double* b, const double* w,
+                 double delta, int64_t max_iter, double s, uint64_t seed, int strict, double* q, ref_ibp_result* res) {
+  return guard([&] {
+    std::vector<DiscreteMeasure> ms;
+    for (int k = 0; k < m; ++k) ms.push_back(measure(b + k * n, n));
+    std::vector<const DiscreteMeasure*> mp;
+    for (auto& x : ms) mp.push_back(&x);
+    std::vector<KernelMatrix> ks;
+    for (int k = 0; k < m; ++k) ks.push_back(kernel(K + k * n * n, n, 1.0, nnz_ratio[k]));
+    std::vector<const KernelMatrix*> kp;
+    for (auto& x : ks) kp.push_back(&x);
+    BarycenterConfig cfg;
+    cfg.delta = delta;
+    cfg.max_iter = (std::size_t)max_iter;
+    fill_ibp(res, spar_ibp(kp, mp, std::vector<double>(w, w + m), cfg, s, seed, strict != 0), q);
   });
 }
 

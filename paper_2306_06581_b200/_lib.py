@@ -119,6 +119,20 @@ SIGNATURES = {
 }
 SHARD_TAIL = 8  # SPK_SHARD_TAIL
 
+
+class IbpReport(C.Structure):
+    _fields_ = [("iterations", C.c_int64), ("converged", C.c_int32), ("diverged", C.c_int32),
+                ("masked_atoms", C.c_int64), ("wall_time_s", C.c_double)]
+
+    def as_dict(self) -> dict:
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+SIGNATURES["spk_ibp"] = (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.c_int32, DP, DP, C.c_double, C.c_int64,
+                                   C.c_int32, DP, C.POINTER(IbpReport)])
+SIGNATURES["spk_spar_ibp"] = (C.c_int, [C.c_void_p, C.POINTER(KernelDesc), C.c_int32, DP, DP, C.c_double, C.c_int64,
+                                        C.c_double, C.c_uint64, C.c_int32, C.c_int32, DP, C.POINTER(IbpReport)])
+
 _lib = None
 
 

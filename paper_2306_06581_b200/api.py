@@ -410,3 +410,43 @@ def spar_sink_pairs(ctx: Context, coords, masses, cfg: SolverConfig, s: float, s
         r = ctx.spar_sink(kern, masses[i], masses[j], cfg, s, mix_seed(seed, k), opts, uot=True)
         out.append((k, (i, j), r.report))
     return out
+
+
+# ---- barycenters (ibp / spar_ibp, include/sparsink/barycenter.hpp) ------------------
+def ibp(ctx: Context, sketches, b, w, delta: float = 1e-6, max_iter: int = 1000, policy: str = "error"):
+    """ibp<SparseKernel> (barycenter.hpp:48-206) on device sketches (Sketch
+    objects of one dimension n); b: (m, n) measure weights, w: m weights.
+    Returns (q, report)."""
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    w = np.ascontiguousarray(w, dtype=np.float64)
+    m = len(sketches)
+    ptrs = (C.c_void_p * m)(*[sk.ptr for sk in sketches])
+    q = np.empty(b.shape[1])
+    rep = L.IbpReport()
+    _raise(ctx.ptr, ctx.lib.spk_ibp(ctx.ptr, ptrs, m, L.dptr(b), L.dptr(w), float(delta), int(max_iter),
+                                    L.POLICY_MASK if policy == "mask" else L.POLICY_ERROR, L.dptr(q),
+                                    C.byref(rep)))
+    return q, rep.as_dict()
+
+
+def spar_ibp(ctx: Context, kernels, b, w, s: float, seed: int, delta: float = 1e-6, max_iter: int = 1000,
+             strict: bool = False, values: str = "f64"):
+    """spar_ibp (barycenter.cpp:8-40): one sketch per kernel (column-constant
+    plan, seed mix_seed(seed, k)), then ibp. kernels: Dense or Coords (with
+    eps) of one dimension n. Returns (q, report)."""
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    w = np.ascontiguousarray(w, dtype=np.float64)
+    m = len(kernels)
+    descs = (L.KernelDesc * m)()
+    keep = []
+    for k, kern in enumerate(kernels):
+        d, kk = kern.desc()
+        descs[k] = d
+        keep.append(kk)
+    q = np.empty(b.shape[1])
+    rep = L.IbpReport()
+    _raise(ctx.ptr, ctx.lib.spk_spar_ibp(ctx.ptr, descs, m, L.dptr(b), L.dptr(w), float(delta), int(max_iter),
+                                         float(s), C.c_uint64(seed & _M64), int(strict),
+                                         L.VALUES_F32 if values == "f32" else L.VALUES_F64, L.dptr(q),
+                                         C.byref(rep)))
+    return q, rep.as_dict()
