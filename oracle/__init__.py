@@ -401,6 +401,14 @@ class Reference:
         L.ref_predict_ed.argtypes = [DP, C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_int64, I64P, DP]
         L.ref_ibp.argtypes = [C.c_int32, C.c_int64, DP, DP, I64P, U32P, DP, I64P, DP, DP, C.c_double, C.c_int64,
                               C.c_int, DP, C.POINTER(ref_ibp_result)]
+        L.ref_save_triplet_csv.argtypes = [C.c_int64, I64P, U32P, DP, C.c_char_p]
+        L.ref_save_metadata_json.argtypes = [C.c_int64, I64P, C.c_uint64, C.c_double, C.c_double, C.c_int,
+                                             C.c_char_p]
+        L.ref_report_json.argtypes = [C.c_double, C.c_int64, C.c_double, C.c_double, C.c_double, C.c_int64, C.c_int,
+                                      C.c_int, C.c_uint64, C.c_char_p, C.c_int64]
+        L.ref_write_measure_csv.argtypes = [DP, DP, C.c_int64, C.c_int, C.c_char_p]
+        L.ref_read_measure_csv.argtypes = [C.c_char_p, C.c_int, DP, DP, C.c_int64, I64P, C.POINTER(C.c_int)]
+        L.ref_matrix_save.argtypes = [DP, C.c_int64, C.c_int64, C.c_char_p, C.c_char_p]
         L.ref_spar_ibp.argtypes = [C.c_int32, C.c_int64, DP, DP, DP, DP, C.c_double, C.c_int64, C.c_double,
                                    C.c_uint64, C.c_int, DP, C.POINTER(ref_ibp_result)]
 
@@ -474,6 +482,45 @@ class Reference:
                                           w.ctypes.data_as(DP), delta, max_iter, s, seed, int(strict),
                                           q.ctypes.data_as(DP), C.byref(res)))
         return q, {k: getattr(res, k) for k, _ in res._fields_}
+
+    # -- formats ---------------------------------------------------------------------
+    def save_triplet_csv(self, csr, path):
+        rp, ci, vv = (np.ascontiguousarray(csr[0], dtype=np.int64), np.ascontiguousarray(csr[1], dtype=np.uint32),
+                      np.ascontiguousarray(csr[2], dtype=np.float64))
+        self._check(self.lib.ref_save_triplet_csv(len(rp) - 1, rp.ctypes.data_as(I64P), ci.ctypes.data_as(U32P),
+                                                  vv.ctypes.data_as(DP), str(path).encode()))
+
+    def save_metadata_json(self, row_ptr, seed, s, theta, kind, path):
+        rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+        self._check(self.lib.ref_save_metadata_json(len(rp) - 1, rp.ctypes.data_as(I64P), seed, s, theta,
+                                                    {"ot": 0, "uot": 1, "barycenter": 2, "uniform": 3}[kind],
+                                                    str(path).encode()))
+
+    def report_json(self, objective, iterations, rr, rc, wall, sketch_nnz, converged, diverged, seed):
+        buf = C.create_string_buffer(4096)
+        self._check(self.lib.ref_report_json(objective, iterations, rr, rc, wall, sketch_nnz, int(converged),
+                                             int(diverged), seed, buf, len(buf)))
+        return buf.value.decode()
+
+    def write_measure_csv(self, w, x, path):
+        w = np.ascontiguousarray(w, dtype=np.float64)
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        self._check(self.lib.ref_write_measure_csv(w.ctypes.data_as(DP), x.ctypes.data_as(DP), len(w),
+                                                   x.size // len(w), str(path).encode()))
+
+    def read_measure_csv(self, path, simplex=False, cap=1 << 20):
+        w, x = np.empty(cap), np.empty(cap)
+        n, dim = np.zeros(1, np.int64), C.c_int(0)
+        self._check(self.lib.ref_read_measure_csv(str(path).encode(), int(simplex), w.ctypes.data_as(DP),
+                                                  x.ctypes.data_as(DP), cap, n.ctypes.data_as(I64P), C.byref(dim)))
+        nn, d = int(n[0]), dim.value
+        return w[:nn].copy(), x[:nn * d].reshape(nn, d).copy()
+
+    def matrix_save(self, a, bin_path=None, csv_path=None):
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        self._check(self.lib.ref_matrix_save(a.ctypes.data_as(DP), a.shape[0], a.shape[1],
+                                             str(bin_path).encode() if bin_path else None,
+                                             str(csv_path).encode() if csv_path else None))
 
     def predict_ed(self, d, t_es, lo, hi, t_true):
         d = np.ascontiguousarray(d, dtype=np.float64)

@@ -14,6 +14,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <chrono>
+#include <iostream>  // std::ios_base::Init for the statically linked libstdc++ (ofstream writers)
 #include <limits>
 #include <string>
 #include <vector>
@@ -484,6 +485,70 @@ int ref_spar_ibp(int32_t m, int64_t n, const double* K, const double* nnz_ratio,
     cfg.delta = delta;
     cfg.max_iter = (std::size_t)max_iter;
     fill_ibp(res, spar_ibp(kp, mp, std::vector<double>(w, w + m), cfg, s, seed, strict != 0), q);
+  });
+}
+
+
+// ---- formats (sparsify.cpp:236-263, solvers.cpp:227-242, measures.cpp:87-141, matrix.cpp) ----
+
+int ref_save_triplet_csv(int64_t n, const int64_t* rp, const uint32_t* ci, const double* val, const char* path) {
+  return guard([&] { sketch(n, rp, ci, val).save_triplet_csv(path); });
+}
+
+int ref_save_metadata_json(int64_t n, const int64_t* rp, uint64_t seed, double s, double theta, int kind,
+                           const char* path) {
+  return guard([&] {
+    SparseKernel sk;
+    sk.n = (std::size_t)n;
+    sk.seed = seed;
+    sk.realized_nnz = (std::size_t)rp[n];
+    sk.save_metadata_json(path, s, theta, static_cast<PlanKind>(kind));
+  });
+}
+
+// SolveReport::to_json into buf (sketch_nnz < 0: none)
+int ref_report_json(double objective, int64_t iterations, double rr, double rc, double wall, int64_t sketch_nnz,
+                    int converged, int diverged, uint64_t seed, char* buf, int64_t len) {
+  return guard([&] {
+    SolveReport r;
+    r.objective = objective;
+    r.iterations = (std::size_t)iterations;
+    r.marginal_residual_row = rr;
+    r.marginal_residual_col = rc;
+    r.wall_time_s = wall;
+    if (sketch_nnz >= 0) r.sketch_nnz = (std::size_t)sketch_nnz;
+    r.converged = converged != 0;
+    r.diverged = diverged != 0;
+    r.seed = seed;
+    std::snprintf(buf, (size_t)len, "%s", r.to_json().c_str());
+  });
+}
+
+int ref_write_measure_csv(const double* w, const double* x, int64_t n, int dim, const char* path) {
+  return guard([&] {
+    auto m = new_measure(std::vector<double>(w, w + n), points(x, n, dim), false);
+    write_measure_csv(m, path);
+  });
+}
+
+int ref_read_measure_csv(const char* path, int simplex, double* w, double* x, int64_t cap, int64_t* n, int* dim) {
+  return guard([&] {
+    auto m = read_measure_csv(path, simplex != 0);
+    *n = (int64_t)m.size();
+    *dim = (int)m.support.dim;
+    if (*n * *dim <= cap) {
+      std::memcpy(w, m.weights.data(), sizeof(double) * m.size());
+      std::memcpy(x, m.support.coords.data(), sizeof(double) * m.support.coords.size());
+    }
+  });
+}
+
+int ref_matrix_save(const double* a, int64_t r, int64_t c, const char* bin_path, const char* csv_path) {
+  return guard([&] {
+    Matrix m((std::size_t)r, (std::size_t)c);
+    std::memcpy(m.data().data(), a, sizeof(double) * r * c);
+    if (bin_path) m.save_binary(bin_path);
+    if (csv_path) m.save_csv(csv_path);
   });
 }
 
