@@ -409,6 +409,11 @@ class Reference:
         L.ref_write_measure_csv.argtypes = [DP, DP, C.c_int64, C.c_int, C.c_char_p]
         L.ref_read_measure_csv.argtypes = [C.c_char_p, C.c_int, DP, DP, C.c_int64, I64P, C.POINTER(C.c_int)]
         L.ref_matrix_save.argtypes = [DP, C.c_int64, C.c_int64, C.c_char_p, C.c_char_p]
+        L.ref_scenario.argtypes = [C.c_int, C.c_int64, C.c_int64, C.c_uint64, C.c_int, C.c_double, C.c_double,
+                                   C.c_int, C.c_double, C.c_double, C.c_int, DP, DP, DP, DP]
+        L.ref_rmae.argtypes = [C.c_int, C.c_int64, C.c_int64, C.c_uint64, C.c_int, C.c_double, C.c_double, C.c_int,
+                               C.c_double, C.c_double, C.c_int, C.c_int, DP, C.c_int64, C.c_int64, C.c_double,
+                               C.c_double, C.c_double, C.c_int64, DP, DP, I64P]
         L.ref_spar_ibp.argtypes = [C.c_int32, C.c_int64, DP, DP, DP, DP, C.c_double, C.c_int64, C.c_double,
                                    C.c_uint64, C.c_int, DP, C.POINTER(ref_ibp_result)]
 
@@ -482,6 +487,33 @@ class Reference:
                                           w.ctypes.data_as(DP), delta, max_iter, s, seed, int(strict),
                                           q.ctypes.data_as(DP), C.byref(res)))
         return q, {k: getattr(res, k) for k, _ in res._fields_}
+
+    # -- RMAE harness ----------------------------------------------------------------
+    def _spec(self, spec):
+        m = spec.get("masses")
+        t = spec.get("sparsity_target")
+        return ({"C1": 0, "C2": 1, "C3": 2}[spec.get("scenario", "C1")], spec.get("n", 1000), spec.get("d", 5),
+                spec.get("seed", 1), int(m is not None), m[0] if m else 1.0, m[1] if m else 1.0, int(t is not None),
+                t or 0.0, spec.get("scale_param", 0.05), int(spec.get("scale_is_sd", False)))
+
+    def scenario(self, spec):
+        sp = self._spec(spec)
+        n, d = sp[1], sp[2]
+        x, a, b, eta = np.empty(n * d), np.empty(n), np.empty(n), C.c_double()
+        self._check(self.lib.ref_scenario(*sp, x.ctypes.data_as(DP), a.ctypes.data_as(DP), b.ctypes.data_as(DP),
+                                          C.byref(eta)))
+        return x.reshape(n, d), a, b, eta.value
+
+    def rmae(self, spec, method, budgets, reps, eps, lam=math.inf, delta=1e-6, max_iter=1000):
+        sp = self._spec(spec)
+        bud = np.ascontiguousarray(budgets, dtype=np.float64)
+        exact = C.c_double()
+        errs = np.empty(len(bud) * reps)
+        retr = np.zeros(len(bud), np.int64)
+        self._check(self.lib.ref_rmae(*sp, 1 if method == "randsink" else 0, bud.ctypes.data_as(DP), len(bud), reps,
+                                      eps, lam, delta, max_iter, C.byref(exact), errs.ctypes.data_as(DP),
+                                      retr.ctypes.data_as(I64P)))
+        return exact.value, errs.reshape(len(bud), reps), retr
 
     # -- formats ---------------------------------------------------------------------
     def save_triplet_csv(self, csr, path):

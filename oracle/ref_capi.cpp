@@ -552,4 +552,56 @@ int ref_matrix_save(const double* a, int64_t r, int64_t c, const char* bin_path,
   });
 }
 
+
+// ---- RMAE harness (harness.cpp:85-232) ---------------------------------------------------
+
+static ScenarioSpec spec_of(int scenario, int64_t n, int64_t d, uint64_t seed, int has_masses, double ma, double mb,
+                            int has_target, double target, double scale_param, int scale_is_sd) {
+  ScenarioSpec sp;
+  sp.scenario = static_cast<Scenario>(scenario);
+  sp.n = (std::size_t)n;
+  sp.d = (std::size_t)d;
+  sp.seed = seed;
+  if (has_masses) sp.masses = std::make_pair(ma, mb);
+  if (has_target) sp.sparsity_target = target;
+  sp.scale_param = scale_param;
+  sp.scale_is_sd = scale_is_sd != 0;
+  return sp;
+}
+
+// generate_scenario (+ eta_for_sparsity when a target is set)
+int ref_scenario(int scenario, int64_t n, int64_t d, uint64_t seed, int has_masses, double ma, double mb,
+                 int has_target, double target, double scale_param, int scale_is_sd, double* support, double* a,
+                 double* b, double* eta) {
+  return guard([&] {
+    auto sp = spec_of(scenario, n, d, seed, has_masses, ma, mb, has_target, target, scale_param, scale_is_sd);
+    ScenarioData data = generate_scenario(sp);
+    std::memcpy(support, data.support.coords.data(), sizeof(double) * n * d);
+    std::memcpy(a, data.a.weights.data(), sizeof(double) * n);
+    std::memcpy(b, data.b.weights.data(), sizeof(double) * n);
+    *eta = has_target ? eta_for_sparsity(data.support, target) : 0.0;
+  });
+}
+
+int ref_rmae(int scenario, int64_t n, int64_t d, uint64_t seed, int has_masses, double ma, double mb, int has_target,
+             double target, double scale_param, int scale_is_sd, int method, const double* budgets, int64_t nb,
+             int64_t reps, double eps, double lambda, double delta, int64_t max_iter, double* exact, double* errors,
+             int64_t* retried) {
+  return guard([&] {
+    auto sp = spec_of(scenario, n, d, seed, has_masses, ma, mb, has_target, target, scale_param, scale_is_sd);
+    SolverConfig cfg;
+    cfg.epsilon = eps;
+    cfg.lambda = lambda;
+    cfg.delta = delta;
+    cfg.max_iter = (std::size_t)max_iter;
+    RmaeReport r = rmae_experiment(sp, method ? ApproxMethod::RandSink : ApproxMethod::SparSink,
+                                   std::vector<double>(budgets, budgets + nb), (std::size_t)reps, cfg);
+    *exact = r.exact_objective;
+    for (int64_t k = 0; k < nb; ++k) {
+      retried[k] = (int64_t)r.rows[k].retried;
+      for (int64_t q = 0; q < reps; ++q) errors[k * reps + q] = r.rows[k].errors[q];
+    }
+  });
+}
+
 }  // extern "C"
