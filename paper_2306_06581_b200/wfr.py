@@ -26,6 +26,7 @@ import math
 import numpy as np
 
 from .api import ERRORS, Context, Coords, SolverConfig, SparsinkError, frame_pairs, mix_seed
+from .harness import s0_budget  # noqa: F401 (harness.cpp:128-131; re-exported)
 
 
 def measure_from_image(pixels, height: int, width: int) -> tuple[np.ndarray, np.ndarray]:
@@ -57,11 +58,6 @@ def mean_pool(pixels, height: int, width: int, filt: int, stride: int) -> tuple[
         for dc in range(filt):
             out += img[dr:dr + stride * (oh - 1) + 1:stride, dc:dc + stride * (ow - 1) + 1:stride]
     return (out / float(filt * filt)).ravel(), oh, ow
-
-
-def s0_budget(n: int) -> float:
-    ln = math.log(n)
-    return 1e-3 * n * ln * ln * ln * ln
 
 
 def wfr_from_uot(value: float) -> float:
