@@ -14,6 +14,7 @@
 // in index order with contraction-free dadd/dmul, bit-identical to the CPU.
 #include <algorithm>
 #include <cmath>
+#include <type_traits>
 
 #include "common.cuh"
 #include "internal.h"
@@ -103,10 +104,15 @@ void run_t(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, double expon
   op.n = n;
   op.row_ptr = sk->row_ptr.as<long long>();
   op.col_idx = sk->col_idx.as<uint32_t>();
-  op.val = sk->values.as<VT>();
   op.col_ptr = sk->col_ptr.as<long long>();
   op.row_idx = sk->row_idx.as<uint32_t>();
-  op.val_t = sk->values_t.as<VT>();
+  if constexpr (std::is_same<VT, LogK>::value) {  // log K~ precomputed once per sketch
+    op.val = reinterpret_cast<const LogK*>(sk->log_values.p);
+    op.val_t = reinterpret_cast<const LogK*>(sk->log_values_t.p);
+  } else {
+    op.val = sk->values.as<VT>();
+    op.val_t = sk->values_t.as<VT>();
+  }
   const int64_t per_block = ctx->deterministic ? loopcore::kBlock : loopcore::kBlock / 32;
   const int64_t useful = (n + per_block - 1) / per_block;
   loopcore::run_core<LOG>(ctx, op, n, W, sk->cov_empty_rows, sk->cov_empty_cols, cfg, exponent, policy, st, useful,
@@ -170,6 +176,35 @@ void ensure_coverage(spk_ctx* ctx, spk_sketch* sk) {
   sk->cov_empty_cols = (long long)emp[1];
 }
 
+template <class VT>
+__global__ void log_values_kernel(const VT* v, int64_t m, double* out) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < m; k += (int64_t)gridDim.x * blockDim.x)
+    out[k] = log((double)v[k]);
+}
+
+// log K~ of the CSR and CSC values (fp64 logs of the stored values: the same
+// numbers the log-sum-exp took per entry before), built on the first
+// log-domain solve of a sketch.
+void ensure_log_values(spk_ctx* ctx, spk_sketch* sk) {
+  if (sk->log_values.p) return;
+  const int64_t m = std::max<int64_t>(sk->nnz, 1);
+  sk->log_values.alloc(sizeof(double) * m);
+  sk->log_values_t.alloc(sizeof(double) * m);
+  if (sk->nnz == 0) return;
+  const int g = loopcore::simple_grid(ctx, sk->nnz);
+  if (sk->value_type == SPK_VALUES_F32) {
+    log_values_kernel<float><<<g, 256, 0, ctx->stream>>>(sk->values.as<float>(), sk->nnz, sk->log_values.as<double>());
+    log_values_kernel<float><<<g, 256, 0, ctx->stream>>>(sk->values_t.as<float>(), sk->nnz,
+                                                         sk->log_values_t.as<double>());
+  } else {
+    log_values_kernel<double><<<g, 256, 0, ctx->stream>>>(sk->values.as<double>(), sk->nnz,
+                                                          sk->log_values.as<double>());
+    log_values_kernel<double><<<g, 256, 0, ctx->stream>>>(sk->values_t.as<double>(), sk->nnz,
+                                                          sk->log_values_t.as<double>());
+  }
+  ctx->launches += 2;
+}
+
 void run_sparse_loop(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, double exponent, int policy,
                      LoopState& st, LoopOut& out) {
   const bool log_domain = cfg.stabilize != 0;
@@ -179,12 +214,13 @@ void run_sparse_loop(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, do
   const bool try_blocked = ctx->use_blocked == 1 || (ctx->use_blocked == 2 && sk->n >= (int64_t(1) << 17));
   if (!ctx->deterministic && !log_domain && try_blocked && run_blocked(ctx, sk, cfg, exponent, policy, st, out))
     return;
-  if (sk->value_type == SPK_VALUES_F32) {
-    if (log_domain) run_t<true, float>(ctx, sk, cfg, exponent, policy, st, out);
-    else run_t<false, float>(ctx, sk, cfg, exponent, policy, st, out);
+  if (log_domain) {
+    ensure_log_values(ctx, sk);
+    run_t<true, LogK>(ctx, sk, cfg, exponent, policy, st, out);
+  } else if (sk->value_type == SPK_VALUES_F32) {
+    run_t<false, float>(ctx, sk, cfg, exponent, policy, st, out);
   } else {
-    if (log_domain) run_t<true, double>(ctx, sk, cfg, exponent, policy, st, out);
-    else run_t<false, double>(ctx, sk, cfg, exponent, policy, st, out);
+    run_t<false, double>(ctx, sk, cfg, exponent, policy, st, out);
   }
 }
 

@@ -7,12 +7,24 @@
 
 namespace spk {
 
+// A sketch value that already holds log K~ (the log-domain loop precomputes
+// them once per sketch instead of taking a log per entry per iteration).
+struct LogK {
+  double v;
+};
+__device__ __forceinline__ double log_of(double v) { return log(v); }
+__device__ __forceinline__ double log_of(float v) { return log((double)v); }
+__device__ __forceinline__ double log_of(LogK v) { return v.v; }
+__device__ __forceinline__ double ldg_val(const double* p) { return __ldg(p); }
+__device__ __forceinline__ float ldg_val(const float* p) { return __ldg(p); }
+__device__ __forceinline__ LogK ldg_val(const LogK* p) { return LogK{__ldg(&p->v)}; }
+
 // Row value of one half: sum_p val[p] * x[idx[p]] over [b, e) (linear), or
 // the log-sum-exp of log(val[p]) + x[idx[p]] skipping x = -inf (log).
 template <bool LOG, bool DET, class VT>
 __device__ __forceinline__ double row_apply(const VT* __restrict__ val, const uint32_t* __restrict__ idx, long long b,
                                             long long e, const double* x, int lane) {
-  if (!LOG) {
+  if constexpr (!LOG) {
     if (DET) {  // acc += v * x, j ascending, no FMA (sparsify.cpp:208-209)
       double acc = 0.0;
       for (long long p = b; p < e; ++p) acc = dadd(acc, dmul((double)val[p], __ldcg(x + idx[p])));
@@ -34,14 +46,14 @@ __device__ __forceinline__ double row_apply(const VT* __restrict__ val, const ui
       for (long long p = b; p < e; ++p) {
         const double xv = __ldcg(x + idx[p]);
         if (xv == -CUDART_INF) continue;
-        mx = fmax(mx, dadd(log((double)val[p]), xv));
+        mx = fmax(mx, dadd(log_of(val[p]), xv));
       }
       if (mx == -CUDART_INF) return -CUDART_INF;
       double acc = 0.0;
       for (long long p = b; p < e; ++p) {
         const double xv = __ldcg(x + idx[p]);
         if (xv == -CUDART_INF) continue;
-        acc = dadd(acc, exp(dsub(dadd(log((double)val[p]), xv), mx)));
+        acc = dadd(acc, exp(dsub(dadd(log_of(val[p]), xv), mx)));
       }
       return dadd(mx, log(acc));
     }
@@ -50,7 +62,7 @@ __device__ __forceinline__ double row_apply(const VT* __restrict__ val, const ui
     for (long long p = b + lane; p < e; p += 32) {
       const double xv = __ldcg(x + __ldg(idx + p));
       if (xv == -CUDART_INF) continue;
-      const double t = log((double)__ldg(val + p)) + xv;
+      const double t = log_of(ldg_val(val + p)) + xv;
       if (t == -CUDART_INF) continue;  // a zero K~ (e.g. fp32 underflow) adds nothing
       if (t > m) {
         s = s * exp(m - t) + 1.0;
