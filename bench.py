@@ -223,6 +223,10 @@ def run_ours(args, ws, rank, local):
         from paper_2306_06581_b200 import _lib as L
 
         ctx.set_option(L.OPT_BLOCKED_LOOP, int(os.environ["SPK_BLOCKED"]))
+    if os.environ.get("SPK_SPLIT") is not None:  # column parts per row slab (profiling)
+        from paper_2306_06581_b200 import _lib as L
+
+        ctx.set_option(L.OPT_BLOCKED_SPLIT, int(os.environ["SPK_SPLIT"]))
     stream = torch.cuda.current_stream()
     ctx.set_stream(stream.cuda_stream)
     kernel = spk.Coords(w.x, w.y, w.cost, w.eta, scale=w.scale, eps=w.eps)

@@ -8,27 +8,31 @@
 // entry stream (profiles/r1_c4_csr_loop_ncu.json: 9.5 GB L2 reads/iteration).
 //
 // Layout (built once per sketch, for the CSR and for the CSC mirror):
-//   output atoms (this half's rows) are cut into P = #SMs slabs of ~equal
-//   entry count, one per persistent CTA, each slab into 16 warp ranges;
-//   input atoms are cut into B blocks of W = 8192 atoms (one 64 KB x tile).
-//   Entries are ordered (slab, warp, block, row, col): each warp's whole half
-//   is ONE contiguous stream, and inside a row the columns still ascend, so
-//   every row is summed in the reference's j order (spmv,
-//   proj/src/sparsify.cpp:203-213; spmv_t :215-226 on the CSC). Each
-//   (slab, warp, block) segment is padded to 32 entries. An entry is packed
-//   (row_local << 16 | col_local) + value: no more bytes than a CSR entry.
-// Half-step (inside the persistent loop, loop_core.cuh), 17 warps per CTA:
-//   * producer warp: cp.async.bulk (TMA) of x tile b into stage b%2 as soon as
-//     every consumer released stage b-2 (empty mbarrier) -- 64 KB copies, the
-//     size at which 1-D bulk copies stream at full rate on B200
-//     (profiles/microbench/r1_tma_stream_b200.txt: 8 KB 2.3 TB/s, 64 KB 7.1 TB/s);
-//   * 16 consumer warps stream their entries with coalesced loads, 256
-//     entries double-buffered in registers ahead of use (independent of the
-//     tile pipeline), gather x from the shared tile, and fold each 32-entry
-//     chunk with a head-mask segmented scan (usually one shuffle step) into
-//     their own rows' shared accumulators (no atomics, deterministic).
-// L2->SM traffic per half: the entry stream + P tiles of x, instead of one
-// random 32-byte sector per entry.
+//   output atoms (this half's rows) are cut into Q row slabs of ~equal entry
+//   count; each slab is served by S CTAs (S = 2: a CTA pair, each reading
+//   one half of x, so every SM stages n/2 instead of n scalings per half);
+//   input atoms are cut into B blocks of W <= 4096 atoms (one 32 KB x tile).
+//   Inside a CTA the slab's rows are cut into 15 warp ranges of ~equal entry
+//   count. Entries are ordered (CTA, warp, block, chunk): each warp's half is
+//   ONE contiguous stream of 32-entry chunks, every chunk holding 32 DISTINCT
+//   rows (so lanes add into shared accumulators without atomics) spread over
+//   the shared-memory banks; inside a row the columns still ascend across
+//   chunks, so each part of a row is summed in the reference's j order
+//   (spmv, proj/src/sparsify.cpp:203-213; spmv_t :215-226 on the CSC).
+//   Entries are packed (row_local << 16 | col_local) + value, and four
+//   consecutive chunks are interleaved per lane, so one 16-byte load gives a
+//   lane its entries of 4 chunks: the stream goes HBM -> registers directly.
+// Half-step (inside the persistent loop, loop_core.cuh), 16 warps per CTA:
+//   * producer warp: cp.async.bulk (TMA) of the CTA's x tiles through a
+//     STG-deep ring (full/empty mbarriers);
+//   * 15 consumer warps stream their entries with coalesced 16-byte loads,
+//     kDepth groups (512 entries) in flight per warp, evict-first in L2 (the
+//     stream never fits; x must stay), gather x from the shared tile and add
+//     v * x into their rows' fp64 shared accumulators;
+//   * S = 2: the pair swaps the partial sums of each other's rows through L2
+//     (one flag per pair, no grid barrier) and each CTA finalizes half of the
+//     slab as p0 + p1.
+// L2->SM traffic per half: the entry stream + Q * n * 8 bytes of x tiles.
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -49,9 +53,7 @@ namespace {
 constexpr int kNW = 15;                 // consumer warps per CTA (+1 producer = 16 warps: 4 per SMSP, 128 registers)
 constexpr int kThreadsBlocked = 32 * (kNW + 1);
 constexpr int kTileW = 4096;            // x tile: 32 KB of fp64
-constexpr int kStages = 3;              // tile ring depth
-constexpr int kGE = 128;                // entries per cp.async group (4 chunks)
-constexpr int kGroup = 8;               // chunks of 32 entries per prefetch group
+constexpr int kGE = 128;                // entries per group (4 chunks; one 16-byte load per lane)
 constexpr uint32_t kPad = 0xffffffffu;  // padding entry (never a valid packed value)
 
 // ---- PTX helpers: mbarrier + 1-D bulk copy (TMA) ------------------------------
@@ -116,34 +118,87 @@ __device__ __forceinline__ void record_fault(unsigned int* fault, unsigned int c
   if (atomicCAS(fault, 0u, code) == 0u) fault[1] = blockIdx.x;
 }
 
+// Streaming 16-byte load of the entry stream: read-only, no L1 allocation,
+// evict-first in L2 (the 1.8 GB stream must not push the scalings out).
+__device__ __forceinline__ uint64_t evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint4 ldg_stream(const void* p, uint64_t pol) {
+  uint4 r;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+      : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+      : "l"(p), "l"(pol));
+  return r;
+}
+
 __host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
+// Stream position of (global chunk C, lane) -- 4-chunk groups interleaved per lane.
+__host__ __device__ __forceinline__ int64_t pos_packed(int64_t C, int lane) {
+  return (C >> 2) * kGE + 4 * lane + (C & 3);
+}
+__host__ __device__ __forceinline__ int64_t pos_f64(int64_t C, int lane) {
+  return (C >> 2) * kGE + ((C & 3) >> 1) * 64 + 2 * lane + (C & 1);
+}
+
 template <class VT>
+struct Group {  // one lane's entries of 4 consecutive chunks
+  uint4 k;
+  uint4 v0;
+  uint4 v1;  // f64 only
+};
+
+template <class VT, int S, int STG>
 struct BlockedOp {
   static constexpr int kThreads = kThreadsBlocked;
-  static constexpr int kMinBlocks = 1;  // one CTA per SM: full register file, ~190 KB shared
+  static constexpr int kMinBlocks = 1;  // one CTA per SM: full register file, up to 227 KB shared
+  static constexpr int kDepth = sizeof(VT) == 4 ? 3 : 2;  // groups in flight per consumer warp (registers)
   BlockedHalf L[2];
   int64_t n;
   int acc_rows;         // shared accumulator capacity (max rows of a slab over both halves)
   unsigned int* fault;  // [0] first fault code, [1] its CTA
-
-  static constexpr int kSlots = sizeof(VT) == 4 ? 5 : 3;  // entry-ring depth per consumer warp (groups)
+  double* xchg;         // S = 2: partial sums handed to the partner CTA (n doubles)
+  unsigned int* pair;   // S = 2: one arrival counter per row slab
 
   __host__ __device__ size_t head_bytes() const { return align16((size_t)(acc_rows + 1) * 8) + 128; }
-  __host__ __device__ size_t ring_offset() const { return head_bytes() + (size_t)kStages * kTileW * 8; }
-  __host__ __device__ size_t ring_packed_bytes() const { return (size_t)kNW * kSlots * kGE * sizeof(uint32_t); }
-  size_t smem_bytes() const { return ring_offset() + ring_packed_bytes() + (size_t)kNW * kSlots * kGE * sizeof(VT); }
+  size_t smem_bytes() const { return head_bytes() + (size_t)STG * kTileW * 8; }
+
+  __device__ __forceinline__ static double value(const Group<VT>& g, int k) {
+    if (sizeof(VT) == 4) {
+      const uint32_t b = k == 0 ? g.v0.x : k == 1 ? g.v0.y : k == 2 ? g.v0.z : g.v0.w;
+      return (double)__uint_as_float(b);
+    }
+    const uint4& q = k < 2 ? g.v0 : g.v1;
+    return (k & 1) ? __hiloint2double((int)q.w, (int)q.z) : __hiloint2double((int)q.y, (int)q.x);
+  }
+  __device__ __forceinline__ static uint32_t key(const Group<VT>& g, int k) {
+    return k == 0 ? g.k.x : k == 1 ? g.k.y : k == 2 ? g.k.z : g.k.w;
+  }
 
   // One 32-entry chunk: the layout guarantees its rows are distinct, so every
   // lane adds its product straight into its row's accumulator. A row's
   // entries arrive in column order (earlier chunks, earlier blocks), so each
-  // row is summed exactly like the reference's spmv / spmv_t loop
+  // row is summed like the reference's spmv / spmv_t loop
   // (sparsify.cpp:203-226): acc += v * x, no FMA.
   __device__ __forceinline__ static void fold(uint32_t u, double v, const double* xs, double* acc, uint32_t arows) {
     // padding (u = kPad, v = 0) lands in the sink row acc[acc_rows], never read
     const uint32_t rl = min(u >> 16, arows);
     acc[rl] = __dadd_rn(acc[rl], __dmul_rn(v, xs[u & (kTileW - 1)]));
     __syncwarp();  // the next chunk may revisit a row through another lane
+  }
+
+  __device__ __forceinline__ void load_group(const uint32_t* gk, const VT* gv, int g, int lane, uint64_t pol,
+                                             Group<VT>& r) const {
+    const int64_t e = (int64_t)g * kGE;
+    r.k = ldg_stream(gk + e + 4 * lane, pol);
+    if (sizeof(VT) == 4) {
+      r.v0 = ldg_stream(gv + e + 4 * lane, pol);
+    } else {
+      r.v0 = ldg_stream(gv + e + 2 * lane, pol);
+      r.v1 = ldg_stream(gv + e + 64 + 2 * lane, pol);
+    }
   }
 
   template <int ROLE, bool LOG, bool DET>
@@ -153,24 +208,27 @@ struct BlockedOp {
     extern __shared__ __align__(128) unsigned char dsm[];
     double* acc = reinterpret_cast<double*>(dsm);
     uint64_t* full = reinterpret_cast<uint64_t*>(dsm + align16((size_t)(acc_rows + 1) * 8));
-    uint64_t* empty = full + kStages;
-    uint32_t* ph = reinterpret_cast<uint32_t*>(empty + kStages);  // phases completed per stage
+    uint64_t* empty = full + STG;
+    uint32_t* ph = reinterpret_cast<uint32_t*>(empty + STG);  // phases completed per stage
     double* tiles = reinterpret_cast<double*>(dsm + head_bytes());
 
     const BlockedHalf& H = L[ROLE];
-    const int p = blockIdx.x;
+    const int cta = blockIdx.x;
+    const int q = cta / S;     // row slab
+    const int part = cta % S;  // column part
     const int lane = threadIdx.x & 31;
     const int w = threadIdx.x >> 5;
     const VT* gval = static_cast<const VT*>(H.val);
-    const int r0 = H.slab_row0[p];
-    const int nrows = H.slab_row0[p + 1] - r0;
-    const int B = H.B;
+    const int r0 = H.slab_row0[q];
+    const int nrows = H.slab_row0[q + 1] - r0;
+    const int bb0 = part * H.Bh;
+    const int nb = max(0, min(H.B, bb0 + H.Bh) - bb0);  // blocks of this CTA
 
     // Barriers are initialised once per launch (first half of iteration 1)
     // and never re-initialised; each stage's phase count carries over from
     // half to half in shared memory.
     if (ROLE == 0 && t == 1 && threadIdx.x == 0) {
-      for (int s = 0; s < kStages; ++s) {
+      for (int s = 0; s < STG; ++s) {
         mbar_init(&full[s], 1);
         mbar_init(&empty[s], kNW);
         ph[s] = 0u;
@@ -182,129 +240,139 @@ struct BlockedOp {
     // bit s: parity of the next phase of stage s; flipped after every wait on it
     uint32_t pmask = 0;
 #pragma unroll
-    for (int s = 0; s < kStages; ++s) pmask |= (ph[s] & 1u) << s;
-    uint32_t ph0[kStages];
+    for (int s = 0; s < STG; ++s) pmask |= (ph[s] & 1u) << s;
+    uint32_t ph0[STG];
 #pragma unroll
-    for (int s = 0; s < kStages; ++s) ph0[s] = ph[s];
+    for (int s = 0; s < STG; ++s) ph0[s] = ph[s];
 
     if (w == kNW) {
-      // ---- producer warp: x tiles through a kStages-deep ring ----
-      if (lane == 0) {
+      // ---- producer warp: x tiles through a STG-deep ring ----
+      if (lane == 0 && nb > 0) {
         fence_proxy_async();  // x was written with generic stores before the grid barrier
         int s = 0;
-        for (int b = 0; b < B; ++b) {
-          if (b >= kStages) {  // stage s last held block b - kStages: wait for its release
+        for (int b = 0; b < nb; ++b) {
+          if (b >= STG) {  // stage s last held block b - STG: wait for its release
             if (!mbar_wait(&empty[s], (pmask >> s) & 1u, fault))
               record_fault(fault, 0x10000000u | ((unsigned)ROLE << 24) | (unsigned)b);
             pmask ^= 1u << s;
           }
-          const int64_t c0 = (int64_t)b * H.W;
+          const int64_t c0 = (int64_t)(bb0 + b) * H.W;
           const int64_t cnt = min((int64_t)H.W, H.n_in - c0);
           const uint32_t bytes = (uint32_t)align16((size_t)cnt * 8);
           mbar_arrive_expect_tx(&full[s], bytes);
           bulk_copy_g2s(tiles + (size_t)s * kTileW, x + c0, bytes, &full[s]);
-          s = s + 1 == kStages ? 0 : s + 1;
+          s = s + 1 == STG ? 0 : s + 1;
         }
       }
       __syncwarp();
-    } else {
-      // ---- consumer warps: one contiguous entry stream per warp, streamed by
-      // cp.async into a per-warp shared ring of kSlots groups (kGE entries
-      // each), kSlots - 1 groups in flight ahead of the one being folded.
-      // Stream positions are 32-bit offsets from the warp's stream start. ----
-      const long long* ofs = H.off + ((int64_t)p * kNW + w) * (B + 1);  // block starts, padded, [B] = end
+    } else if (nb > 0) {
+      // ---- consumer warps: one contiguous stream per warp, kDepth groups of
+      // 4 chunks in flight in registers ahead of the group being folded ----
+      const long long* ofs = H.off + ((int64_t)cta * kNW + w) * (H.Bh + 1);  // block starts; [nb] = stream end
       const long long sbeg = ofs[0];
-      const int slen = (int)(ofs[B] - sbeg);
-      uint32_t* rp = reinterpret_cast<uint32_t*>(dsm + ring_offset()) + (size_t)w * kSlots * kGE;
-      VT* rv = reinterpret_cast<VT*>(dsm + ring_offset() + ring_packed_bytes()) + (size_t)w * kSlots * kGE;
-      const int ngroups = (slen + kGE - 1) / kGE;
-      constexpr int kVL = 16 / (int)sizeof(VT);  // values per 16-byte copy
-      const uint32_t* gp = H.packed + sbeg + lane * 4;
-      const VT* gq = gval + sbeg + lane * kVL;
-      int issue_slot = 0, issued = 0;
-      auto issue = [&]() {
-        if (issued < ngroups) {
-          cp_async16(rp + issue_slot * kGE + lane * 4, gp);
-          cp_async16(rv + issue_slot * kGE + lane * kVL, gq);
-          if (sizeof(VT) == 8) cp_async16(rv + issue_slot * kGE + 64 + lane * kVL, gq + 64);
-          gp += kGE;
-          gq += kGE;
-        }
-        ++issued;
-        cp_async_commit();  // (empty past the end: keeps the group count uniform)
-        issue_slot = issue_slot + 1 == kSlots ? 0 : issue_slot + 1;
-      };
+      const int nch = (int)((ofs[nb] - sbeg) >> 5);  // chunks in the stream
+      const int ngroups = (nch + 3) >> 2;
+      const uint32_t* gk = H.packed + sbeg;
+      const VT* gv = gval + sbeg;
+      const uint64_t pol = evict_first_policy();
+      // Loads are unconditional (clamped to the last group: streams are padded
+      // to whole groups) so no predicated register merge forces a wait.
+      const int glast = max(ngroups - 1, 0);
+      Group<VT> R[kDepth];
 #pragma unroll
-      for (int gi = 0; gi < kSlots - 1; ++gi) issue();
+      for (int d = 0; d < kDepth; ++d) load_group(gk, gv, min(d, glast), lane, pol, R[d]);
       int cb = 0, cs = 0;  // current block and its stage
-      int cb_end = (int)(ofs[1] - sbeg);
-      int cb_next = (int)((B > 1 ? ofs[2] : ofs[B]) - sbeg);  // next boundary, loaded one transition early
-      const double* xs = tiles;                               // tile of the current block
+      int cb_end = (int)((ofs[1] - sbeg) >> 5);
+      const double* xs = tiles;  // tile of the current block
       if (!mbar_wait(&full[0], pmask & 1u, fault)) record_fault(fault, 0x20000000u | ((unsigned)ROLE << 24));
       pmask ^= 1u;
-      int slot = 0;
       const uint32_t arows = (uint32_t)acc_rows;
-      for (int g = 0; g < ngroups; ++g) {
-        issue();
-        cp_async_wait_group<kSlots - 1>();  // group g has landed
-        __syncwarp();
-        const int gbase = g * kGE;
-        const uint32_t* up = rp + slot * kGE + lane;
-        const VT* vp = rv + slot * kGE + lane;
-        if (gbase + kGE <= cb_end && gbase + kGE <= slen) {
-          // the whole group lies inside the current block: no boundary checks
+      for (int g0 = 0; g0 < ngroups; g0 += kDepth) {
 #pragma unroll
-          for (int k = 0; k < kGE / 32; ++k) fold(up[32 * k], (double)vp[32 * k], xs, acc, arows);
-        } else {
+        for (int d = 0; d < kDepth; ++d) {
+          const int g = g0 + d;
+          const Group<VT> cur = R[d];
+          load_group(gk, gv, min(g + kDepth, glast), lane, pol, R[d]);
+          if (g < ngroups) {  // warp-uniform
+            const int c0 = 4 * g;
+            if (c0 + 4 <= cb_end && c0 + 4 <= nch) {
+              // the whole group lies inside the current block: no boundary checks
 #pragma unroll
-          for (int k = 0; k < kGE / 32; ++k) {
-            const int c = gbase + 32 * k;
-            if (c < slen) {  // warp-uniform
-              while (c >= cb_end && cb + 1 < B) {  // release tile cb, enter the next
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&empty[cs]);
-                ++cb;
-                cs = cs + 1 == kStages ? 0 : cs + 1;
-                cb_end = cb_next;
-                cb_next = (int)((cb + 2 <= B ? ofs[cb + 2] : ofs[B]) - sbeg);
-                xs = tiles + (size_t)cs * kTileW;
-                if (!mbar_wait(&full[cs], (pmask >> cs) & 1u, fault))
-                  record_fault(fault, 0x30000000u | ((unsigned)ROLE << 24) | (unsigned)cb);
-                pmask ^= 1u << cs;
+              for (int k = 0; k < 4; ++k) fold(key(cur, k), value(cur, k), xs, acc, arows);
+            } else {
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                const int c = c0 + k;
+                if (c < nch) {  // warp-uniform
+                  while (c >= cb_end && cb + 1 < nb) {  // release tile cb, enter the next
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&empty[cs]);
+                    ++cb;
+                    cs = cs + 1 == STG ? 0 : cs + 1;
+                    cb_end = (int)((ofs[cb + 1] - sbeg) >> 5);
+                    xs = tiles + (size_t)cs * kTileW;
+                    if (!mbar_wait(&full[cs], (pmask >> cs) & 1u, fault))
+                      record_fault(fault, 0x30000000u | ((unsigned)ROLE << 24) | (unsigned)cb);
+                    pmask ^= 1u << cs;
+                  }
+                  fold(key(cur, k), value(cur, k), xs, acc, arows);
+                }
               }
-              fold(up[32 * k], (double)vp[32 * k], xs, acc, arows);
             }
           }
         }
-        __syncwarp();  // every lane is done with this slot before it is refilled
-        slot = slot + 1 == kSlots ? 0 : slot + 1;
       }
-      cp_async_wait_group<0>();
       // release the remaining blocks in order (tile present before release)
       for (;;) {
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[cs]);
-        if (++cb >= B) break;
-        cs = cs + 1 == kStages ? 0 : cs + 1;
+        if (++cb >= nb) break;
+        cs = cs + 1 == STG ? 0 : cs + 1;
         if (!mbar_wait(&full[cs], (pmask >> cs) & 1u, fault))
           record_fault(fault, 0x40000000u | ((unsigned)ROLE << 24) | (unsigned)cb);
         pmask ^= 1u << cs;
       }
     }
     __syncthreads();
-    if (threadIdx.x == 0) {  // block b used stage b % kStages once
+    if (threadIdx.x == 0) {  // block b used stage b % STG once
 #pragma unroll
-      for (int s = 0; s < kStages; ++s) ph[s] = ph0[s] + (uint32_t)((B - s + kStages - 1) / kStages);
+      for (int s = 0; s < STG; ++s) ph[s] = ph0[s] + (uint32_t)((nb - s + STG - 1) / STG);
     }
-    // ---- finalize this slab's atoms ----
-    for (int r = threadIdx.x; r < nrows; r += blockDim.x) {
+    // ---- finalize this CTA's atoms of the slab ----
+    int fr0 = 0, fr1 = nrows;
+    if (S == 2) {
+      const int mid = nrows >> 1;
+      fr0 = part == 0 ? 0 : mid;
+      fr1 = part == 0 ? mid : nrows;
+      const int o0 = part == 0 ? mid : 0, o1 = part == 0 ? nrows : mid;  // the partner's rows
+      for (int r = o0 + threadIdx.x; r < o1; r += blockDim.x) __stcg(xchg + r0 + r, acc[r]);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned int target = 2u * (unsigned)(2 * (t - 1) + ROLE + 1);
+        atomicAdd(pair + q, 1u);
+        bool ok = false;
+        for (int spin = 0; spin < (1 << 22); ++spin) {
+          if (*(volatile unsigned int*)(pair + q) >= target) {
+            ok = true;
+            break;
+          }
+          if ((spin & 255) == 255 && __ldcg(fault)) break;
+        }
+        if (!ok) record_fault(fault, 0x50000000u | ((unsigned)ROLE << 24));
+        __threadfence();
+      }
+      __syncthreads();
+    }
+    for (int r = fr0 + threadIdx.x; r < fr1; r += blockDim.x) {
       const int64_t i = r0 + r;
       const double o = __ldcg(old + i);
       if (!ne[i]) {
         out[i] = o;
         continue;
       }
-      err += loopcore::finalize_atom<LOG>(i, acc[r], o, wgt[i], exponent, policy, t, ne, dyn, out, flag, masks);
+      const double tmp = S == 2 ? __dadd_rn(acc[r], __ldcg(xchg + i)) : acc[r];  // p0 + p1 (commutes exactly)
+      err += loopcore::finalize_atom<LOG>(i, tmp, o, wgt[i], exponent, policy, t, ne, dyn, out, flag, masks);
     }
     __syncthreads();
   }
@@ -312,22 +380,38 @@ struct BlockedOp {
 
 // ---- layout builder --------------------------------------------------------------
 
-// key = ((slab * NW + warp) * B + block): the warp's whole stream is contiguous
-// key = segment (slab, warp, block) | bank class of the row | row. Sorting by
+// Per row: entries whose column lies before `split` (columns ascend in a row).
+__global__ void split_count_kernel(const long long* ptr, const uint32_t* idx, int64_t n_out, uint32_t split,
+                                   int* cnt0) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_out; i += (int64_t)gridDim.x * blockDim.x) {
+    long long lo = ptr[i], hi = ptr[i + 1];
+    const long long b = lo;
+    while (lo < hi) {
+      const long long mid = (lo + hi) >> 1;
+      if (idx[mid] < split) lo = mid + 1;
+      else hi = mid;
+    }
+    cnt0[i] = (int)(lo - b);
+  }
+}
+
+// key = segment (CTA, warp, block) | bank class of the row | row. Sorting by
 // it (stably) lists each segment's rows grouped by shared-memory bank class,
 // every row's entries consecutive in column order; chunk c then takes list
 // positions c, c+C, ... and so spreads its rows over all banks.
 __global__ void key_kernel(const long long* ptr, const uint32_t* idx, int64_t n_out, const int* slab_of,
-                           const unsigned char* warp_of, const int* slab_row0_of_row, int W, int B, uint32_t* seg,
-                           unsigned long long* key) {
+                           const unsigned char* warp_of, const int* slab_row0_of_row, int W, int S, int Bh,
+                           uint32_t* seg, unsigned long long* key) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t i = warp; i < n_out; i += nw) {
-    const uint32_t base = ((uint32_t)slab_of[i] * kNW + warp_of[i]) * (uint32_t)B;
     const uint32_t rl = (uint32_t)(i - slab_row0_of_row[i]);
     for (long long q = ptr[i] + lane; q < ptr[i + 1]; q += 32) {
-      const uint32_t sg = base + idx[q] / (uint32_t)W;
+      const uint32_t blk = idx[q] / (uint32_t)W;
+      const uint32_t part = blk / (uint32_t)Bh;
+      const uint32_t cta = (uint32_t)slab_of[i] * (uint32_t)S + part;
+      const uint32_t sg = (cta * kNW + warp_of[part * n_out + i]) * (uint32_t)Bh + (blk - part * Bh);
       seg[q] = sg;
       key[q] = ((unsigned long long)sg << 20) | ((unsigned long long)(rl & 15u) << 16) | rl;
     }
@@ -390,10 +474,11 @@ __global__ void place_kernel(const uint32_t* keys_s, const uint32_t* perm, const
       pp = ps + (c - a);
     }
     const long long slot = pp / C;  // even slots -> lanes 0-15, odd -> 16-31: each half-warp spans the classes
-    const long long d = seg_base[key] + c * 32 + ((slot & 1) << 4) + (slot >> 1);
+    const int lane = (int)(((slot & 1) << 4) + (slot >> 1));
+    const int64_t Cg = (seg_base[key] >> 5) + c;  // global chunk index
     const uint32_t src = perm[q];
-    packed[d] = (rl[q] << 16) | (idx[src] % (uint32_t)W);
-    vout[d] = val[src];
+    packed[pos_packed(Cg, lane)] = (rl[q] << 16) | (idx[src] % (uint32_t)W);
+    vout[sizeof(VT) == 4 ? pos_packed(Cg, lane) : pos_f64(Cg, lane)] = val[src];
   }
 }
 
@@ -413,51 +498,73 @@ int grid_cap(spk_ctx* ctx, int64_t items) {
 
 }  // namespace
 
-// Build one half's layout from (ptr, idx, val). Returns false when the shape
-// does not fit (rows per slab >= 2^16).
-bool build_blocked(spk_ctx* ctx, int P, int W, int64_t n_out, int64_t n_in, int64_t m, const DBuf& ptr_d,
+// Build one half's layout from (ptr, idx, val) for P CTAs = Q slabs x S parts.
+// Returns false when the shape does not fit (rows per slab >= 2^16).
+bool build_blocked(spk_ctx* ctx, int P, int S, int W, int64_t n_out, int64_t n_in, int64_t m, const DBuf& ptr_d,
                    const DBuf& idx_d, const DBuf& val_d, int vbytes, BlockedHost& out) {
+  const int Q = P / S;
   std::vector<long long> ptr(n_out + 1);
   download(ctx, ptr.data(), ptr_d, sizeof(long long) * (n_out + 1));
-  std::vector<int> slab_row0(P + 1);
+  std::vector<int> slab_row0(Q + 1);
   slab_row0[0] = 0;
-  for (int k = 1; k < P; ++k) {
-    const long long target = (long long)((double)m * k / P);
+  for (int k = 1; k < Q; ++k) {
+    const long long target = (long long)((double)m * k / Q);
     int r = (int)(std::lower_bound(ptr.begin(), ptr.end(), target) - ptr.begin());
     slab_row0[k] = std::max<int>(std::min<int64_t>(r, n_out), slab_row0[k - 1]);
   }
-  slab_row0[P] = (int)n_out;
+  slab_row0[Q] = (int)n_out;
   int max_rows = 0;
-  for (int k = 0; k < P; ++k) max_rows = std::max(max_rows, slab_row0[k + 1] - slab_row0[k]);
+  for (int k = 0; k < Q; ++k) max_rows = std::max(max_rows, slab_row0[k + 1] - slab_row0[k]);
   if (max_rows >= 65535) return false;
   const int B = (int)((n_in + W - 1) / W);
+  const int Bh = (B + S - 1) / S;
+  cudaStream_t s = ctx->stream;
+  // entries of each row inside each column part
+  std::vector<int> cnt0(n_out);
+  if (S == 2) {
+    DBuf d_cnt0(sizeof(int) * std::max<int64_t>(n_out, 1));
+    split_count_kernel<<<grid_cap(ctx, n_out), 256, 0, s>>>(ptr_d.as<long long>(), idx_d.as<uint32_t>(), n_out,
+                                                             (uint32_t)std::min<int64_t>((int64_t)Bh * W, n_in),
+                                                             d_cnt0.as<int>());
+    ++ctx->launches;
+    download(ctx, cnt0.data(), d_cnt0, sizeof(int) * n_out);
+  }
   std::vector<int> slab_of(n_out), slab_row0_of_row(n_out);
-  std::vector<unsigned char> warp_of(n_out);
-  for (int k = 0; k < P; ++k) {
+  std::vector<unsigned char> warp_of((size_t)S * n_out);
+  std::vector<long long> pref(n_out + 1);
+  for (int k = 0; k < Q; ++k) {
     const int a = slab_row0[k], z = slab_row0[k + 1];
-    const long long e0 = ptr[a], e1 = ptr[z];
-    int prev = a;
-    for (int wv = 0; wv < kNW; ++wv) {
-      int r_end = z;
-      if (wv + 1 < kNW) {
-        const long long target = e0 + (long long)((double)(e1 - e0) * (wv + 1) / kNW);
-        r_end = std::max(prev, (int)(std::lower_bound(ptr.begin() + a, ptr.begin() + z, target) - ptr.begin()));
+    for (int r = a; r < z; ++r) {
+      slab_of[r] = k;
+      slab_row0_of_row[r] = a;
+    }
+    for (int part = 0; part < S; ++part) {
+      // entries of this part per row, prefix-summed over the slab
+      pref[a] = 0;
+      for (int r = a; r < z; ++r) {
+        const long long tot = ptr[r + 1] - ptr[r];
+        const long long e = S == 1 ? tot : (part == 0 ? cnt0[r] : tot - cnt0[r]);
+        pref[r + 1] = pref[r] + e;
       }
-      for (int r = prev; r < r_end; ++r) {
-        slab_of[r] = k;
-        warp_of[r] = (unsigned char)wv;
-        slab_row0_of_row[r] = a;
+      const long long e1 = pref[z];
+      int prev = a;
+      for (int wv = 0; wv < kNW; ++wv) {
+        int r_end = z;
+        if (wv + 1 < kNW) {
+          const long long target = (long long)((double)e1 * (wv + 1) / kNW);
+          r_end = std::max(prev, (int)(std::lower_bound(pref.begin() + a, pref.begin() + z, target) - pref.begin()));
+        }
+        for (int r = prev; r < r_end; ++r) warp_of[(size_t)part * n_out + r] = (unsigned char)wv;
+        prev = r_end;
       }
-      prev = r_end;
     }
   }
-  const int64_t nkeys = (int64_t)P * kNW * B;
+  const int64_t nkeys = (int64_t)Q * S * kNW * Bh;
   if (nkeys >= (1LL << 32)) return false;
-  cudaStream_t s = ctx->stream;
   const int64_t mm = std::max<int64_t>(m, 1);
   DBuf d_slab_of, d_warp_of, d_s0r;
   upload(ctx, d_slab_of, slab_of.data(), sizeof(int) * n_out);
-  upload(ctx, d_warp_of, warp_of.data(), n_out);
+  upload(ctx, d_warp_of, warp_of.data(), warp_of.size());
   upload(ctx, d_s0r, slab_row0_of_row.data(), sizeof(int) * n_out);
   DBuf keys(sizeof(uint32_t) * mm), keys_s(sizeof(uint32_t) * mm), iota(sizeof(uint32_t) * mm),
       perm(sizeof(uint32_t) * mm), hist(sizeof(unsigned long long) * nkeys),
@@ -465,7 +572,7 @@ bool build_blocked(spk_ctx* ctx, int P, int W, int64_t n_out, int64_t n_in, int6
   SPK_CUDA(cudaMemsetAsync(hist.p, 0, hist.bytes, s));
   key_kernel<<<grid_cap(ctx, n_out * 32), 256, 0, s>>>(ptr_d.as<long long>(), idx_d.as<uint32_t>(), n_out,
                                                         d_slab_of.as<int>(), d_warp_of.as<unsigned char>(),
-                                                        d_s0r.as<int>(), W, B, keys.as<uint32_t>(),
+                                                        d_s0r.as<int>(), W, S, Bh, keys.as<uint32_t>(),
                                                         key64.as<unsigned long long>());
   iota_u32<<<grid_cap(ctx, m), 256, 0, s>>>(iota.as<uint32_t>(), m);
   key_hist_kernel<<<grid_cap(ctx, m), 256, 0, s>>>(keys.as<uint32_t>(), m, hist.as<unsigned long long>());
@@ -503,31 +610,33 @@ bool build_blocked(spk_ctx* ctx, int P, int W, int64_t n_out, int64_t n_in, int6
   std::vector<unsigned int> mx(nkeys);
   download(ctx, h.data(), hist, sizeof(unsigned long long) * nkeys);
   download(ctx, mx.data(), maxrun, sizeof(unsigned int) * nkeys);
-  std::vector<long long> useg(nkeys), seg_base(nkeys), nch(nkeys), off((size_t)P * kNW * (B + 1));
+  // streams: one per (CTA, warp), group-aligned; segments chunk-aligned
+  std::vector<long long> useg(nkeys), seg_base(nkeys), nch(nkeys), off((size_t)P * kNW * (Bh + 1));
   long long u_acc = 0, p_acc = 0;
   for (int64_t sw = 0; sw < (int64_t)P * kNW; ++sw) {
-    for (int b = 0; b < B; ++b) {
-      const int64_t k = sw * B + b;
+    for (int b = 0; b < Bh; ++b) {
+      const int64_t k = sw * Bh + b;
       useg[k] = u_acc;
       u_acc += (long long)h[k];
       nch[k] = std::max<long long>(((long long)h[k] + 31) / 32, (long long)mx[k]);
       seg_base[k] = p_acc;
-      off[(size_t)sw * (B + 1) + b] = p_acc;
+      off[(size_t)sw * (Bh + 1) + b] = p_acc;
       p_acc += 32 * nch[k];
     }
-    off[(size_t)sw * (B + 1) + B] = p_acc;
+    off[(size_t)sw * (Bh + 1) + Bh] = p_acc;
+    p_acc = (p_acc + kGE - 1) / kGE * kGE;  // next stream starts on a group
   }
-  const int64_t total = p_acc + 2 * 32 * kGroup;  // unguarded prefetch runs up to 2 groups past a stream
+  const int64_t total = p_acc + kGE;  // an empty last stream still loads (and ignores) one group
   if (std::getenv("SPK_DEBUG_BLOCKED"))
-    std::fprintf(stderr, "[blocked] n_out %lld B %d W %d entries %lld padded %lld (x%.3f) max_rows %d\n",
-                 (long long)n_out, B, W, (long long)m, (long long)p_acc, (double)p_acc / std::max<int64_t>(m, 1),
+    std::fprintf(stderr, "[blocked] n_out %lld S %d B %d W %d entries %lld padded %lld (x%.3f) max_rows %d\n",
+                 (long long)n_out, S, B, W, (long long)m, (long long)p_acc, (double)p_acc / std::max<int64_t>(m, 1),
                  max_rows);
   DBuf d_useg, d_seg, d_nch;
   upload(ctx, d_useg, useg.data(), sizeof(long long) * nkeys);
   upload(ctx, d_seg, seg_base.data(), sizeof(long long) * nkeys);
   upload(ctx, d_nch, nch.data(), sizeof(long long) * nkeys);
   upload(ctx, out.off, off.data(), sizeof(long long) * off.size());
-  upload(ctx, out.slab_row0, slab_row0.data(), sizeof(int) * (P + 1));
+  upload(ctx, out.slab_row0, slab_row0.data(), sizeof(int) * (Q + 1));
   out.packed.alloc(sizeof(uint32_t) * total);
   out.val.alloc((size_t)vbytes * total);
   SPK_CUDA(cudaMemsetAsync(out.packed.p, 0xff, out.packed.bytes, s));  // padding = kPad
@@ -549,47 +658,30 @@ bool build_blocked(spk_ctx* ctx, int P, int W, int64_t n_out, int64_t n_in, int6
   SPK_CUDA(cudaStreamSynchronize(s));
   out.max_rows = max_rows;
   out.padded = p_acc;
-  out.ecap = 0;
   out.h.P = P;
+  out.h.S = S;
   out.h.B = B;
+  out.h.Bh = Bh;
   out.h.W = W;
   out.h.n_out = n_out;
   out.h.n_in = n_in;
   out.h.slab_row0 = out.slab_row0.as<int>();
-  out.h.warp_row0 = nullptr;
   out.h.off = out.off.as<long long>();
   out.h.packed = out.packed.as<uint32_t>();
   out.h.val = out.val.p;
   return true;
 }
 
-template <class VT>
-bool run_blocked_t(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, double exponent, int policy,
-                   LoopState& st, LoopOut& out) {
+namespace {
+
+// dynamic shared memory per CTA: 227 KB minus the loop kernel's static use
+constexpr size_t kSmemBudget = 232448 - 1024;
+
+template <class VT, int S, int STG>
+void launch_blocked(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, double exponent, int policy,
+                    LoopState& st, LoopOut& out) {
   const int64_t n = sk->n;
-  const int P = ctx->num_sms;
-  // dynamic shared memory per CTA: 227 KB minus the loop kernel's static use
-  const size_t budget = 232448 - 1024;
-  if (!sk->blocked_tried) {
-    sk->blocked_tried = true;
-    const int vb = sizeof(VT);
-    const int W = std::min(kTileW, std::max(16, ctx->blocked_max_w));
-    auto R = std::make_unique<BlockedHost>(), C = std::make_unique<BlockedHost>();
-    if (build_blocked(ctx, P, W, n, n, sk->nnz, sk->row_ptr, sk->col_idx, sk->values, vb, *R) &&
-        build_blocked(ctx, P, W, n, n, sk->nnz, sk->col_ptr, sk->row_idx, sk->values_t, vb, *C)) {
-      BlockedOp<VT> probe{};
-      probe.acc_rows = std::max(R->max_rows, C->max_rows);
-      // auto mode keeps the CSR loop when rows are too few per warp to fill
-      // conflict-free chunks (padding would outweigh the staged gathers)
-      const bool dense_pad = ctx->use_blocked == 2 && (double)(R->padded + C->padded) > 1.35 * 2.0 * (double)sk->nnz;
-      if (probe.smem_bytes() <= budget && !dense_pad) {
-        sk->blk_rows = std::move(R);
-        sk->blk_cols = std::move(C);
-      }
-    }
-  }
-  if (!sk->blk_rows) return false;
-  BlockedOp<VT> op{};
+  BlockedOp<VT, S, STG> op{};
   op.L[0] = sk->blk_rows->h;
   op.L[1] = sk->blk_cols->h;
   op.n = n;
@@ -598,23 +690,73 @@ bool run_blocked_t(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, doub
   W.scalar.ensure(sizeof(unsigned int) * 2);
   SPK_CUDA(cudaMemsetAsync(W.scalar.p, 0, sizeof(unsigned int) * 2, ctx->stream));
   op.fault = W.scalar.as<unsigned int>();
+  const int Q = op.L[0].P / S;
+  if (S == 2) {
+    W.xchg.ensure(sizeof(double) * n);
+    W.pair.ensure(sizeof(unsigned int) * Q);
+    SPK_CUDA(cudaMemsetAsync(W.pair.p, 0, sizeof(unsigned int) * Q, ctx->stream));
+    op.xchg = W.xchg.as<double>();
+    op.pair = W.pair.as<unsigned int>();
+  }
   W.row_ne.ensure(n);
   W.col_ne.ensure(n);
   SPK_CUDA(cudaMemcpyAsync(W.row_ne.p, sk->cov_row.p, n, cudaMemcpyDeviceToDevice, ctx->stream));
   SPK_CUDA(cudaMemcpyAsync(W.col_ne.p, sk->cov_col.p, n, cudaMemcpyDeviceToDevice, ctx->stream));
   loopcore::run_core<false>(ctx, op, n, W, sk->cov_empty_rows, sk->cov_empty_cols, cfg, exponent, policy, st,
-                            /*useful_blocks=*/P, out, /*exact_grid=*/P, op.smem_bytes());
+                            /*useful_blocks=*/op.L[0].P, out, /*exact_grid=*/op.L[0].P, op.smem_bytes());
   unsigned int fw[2] = {0u, 0u};
   download(ctx, fw, W.scalar, sizeof fw);
   if (fw[0]) {
-    // code: 1 producer / 2-4 consumer barrier wait timed out; then half and block
+    // code: 1 producer / 2-4 consumer barrier wait / 5 pair exchange timed out; then half and block
     const std::string msg = "blocked loop: a tile barrier timed out (site " + std::to_string(fw[0] >> 28) +
                             ", half " + std::to_string((fw[0] >> 24) & 15) + ", block " +
                             std::to_string(fw[0] & 0xffffff) + ", CTA " + std::to_string(fw[1]) + ")";
     fail_device(msg.c_str(), cudaErrorLaunchTimeout);
   }
+}
+
+// Ring depths: S = 1 keeps 4 tiles in flight; S = 2 doubles the accumulator
+// rows per CTA and keeps 3.
+constexpr int kStg1 = 4, kStg2 = 3;
+
+template <class VT>
+bool run_blocked_t(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, double exponent, int policy,
+                   LoopState& st, LoopOut& out) {
+  const int64_t n = sk->n;
+  if (!sk->blocked_tried) {
+    sk->blocked_tried = true;
+    const int vb = sizeof(VT);
+    const int W = std::min(kTileW, std::max(16, ctx->blocked_max_w));
+    // S = 2 when the pair split fits (even SM count, slab accumulators in
+    // shared memory); else one CTA per slab
+    for (int S = (ctx->blocked_split == 1 ? 1 : 2); S >= 1; --S) {
+      if (S == 2 && ctx->num_sms < 2) continue;
+      const int P = (ctx->num_sms / S) * S;
+      auto R = std::make_unique<BlockedHost>(), C = std::make_unique<BlockedHost>();
+      if (!build_blocked(ctx, P, S, W, n, n, sk->nnz, sk->row_ptr, sk->col_idx, sk->values, vb, *R) ||
+          !build_blocked(ctx, P, S, W, n, n, sk->nnz, sk->col_ptr, sk->row_idx, sk->values_t, vb, *C))
+        continue;
+      const int acc_rows = std::max(R->max_rows, C->max_rows);
+      const size_t smem = S == 2 ? BlockedOp<VT, 2, kStg2>{{}, 0, acc_rows}.smem_bytes()
+                                 : BlockedOp<VT, 1, kStg1>{{}, 0, acc_rows}.smem_bytes();
+      // auto mode keeps the CSR loop when rows are too few per warp to fill
+      // conflict-free chunks (padding would outweigh the staged gathers)
+      const bool dense_pad = ctx->use_blocked == 2 && (double)(R->padded + C->padded) > 1.35 * 2.0 * (double)sk->nnz;
+      if (smem <= kSmemBudget && !dense_pad) {
+        sk->blk_rows = std::move(R);
+        sk->blk_cols = std::move(C);
+        break;
+      }
+      if (ctx->blocked_split == 2) break;
+    }
+  }
+  if (!sk->blk_rows) return false;
+  if (sk->blk_rows->h.S == 2) launch_blocked<VT, 2, kStg2>(ctx, sk, cfg, exponent, policy, st, out);
+  else launch_blocked<VT, 1, kStg1>(ctx, sk, cfg, exponent, policy, st, out);
   return true;
 }
+
+}  // namespace
 
 bool run_blocked(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, double exponent, int policy, LoopState& st,
                  LoopOut& out) {

@@ -57,7 +57,7 @@ struct DBuf {
 // Reusable device scratch of one Sinkhorn loop / readout (kept per sketch so
 // repeated solves allocate nothing).
 struct LoopWs {
-  DBuf row_ne, col_ne, dyn_row, dyn_col, u2, v2, la, lb, absdiff, part, flag, status, scalar;
+  DBuf row_ne, col_ne, dyn_row, dyn_col, u2, v2, la, lb, absdiff, part, flag, status, scalar, xchg, pair;
 };
 struct ReadWs {
   DBuf row_m, col_m, row_c, row_h, terms, flag, tmp, sums, bad;
@@ -65,19 +65,20 @@ struct ReadWs {
 
 // Slab x block layout of one half of a sketch (blocked.cu).
 struct BlockedHalf {
-  int P, B, W;
+  int P;        // CTAs (= Q row slabs x S column parts)
+  int S;        // column parts per row slab (1, or 2 = pairs of CTAs split x)
+  int B, Bh;    // column blocks in all, per part
+  int W;        // columns per block (one staged x tile)
   int64_t n_out, n_in;
-  const int* slab_row0;    // [P+1] global row starts
-  const int* warp_row0;    // [P*(NW+1)] local row starts per warp
-  const long long* off;    // [P*B*(NW+1)] padded entry offsets of (slab, block, warp); [NW] = segment end
-  const uint32_t* packed;  // row_local << 16 | col_local
-  const void* val;         // f32 or f64
+  const int* slab_row0;    // [Q+1] global row starts
+  const long long* off;    // [P*NW*(Bh+1)] entry offsets of (CTA, warp, block); [Bh] = stream end
+  const uint32_t* packed;  // row_local << 16 | col_local, 4-chunk groups interleaved per lane
+  const void* val;         // f32 or f64, same order
 };
 struct BlockedHost {
   BlockedHalf h{};
-  DBuf slab_row0, warp_row0, off, packed, val;
+  DBuf slab_row0, off, packed, val;
   int max_rows = 0;
-  int ecap = 0;  // largest padded (slab, block) entry segment
   int64_t padded = 0;  // entries after chunk padding
 };
 
@@ -131,6 +132,7 @@ struct spk_ctx {
   int otf_fp32 = 1;            // dense on-the-fly comparator computes K in fp32
   int use_blocked = 2;         // fast sparse loop layout: 0 CSR/CSC, 1 slab x block, 2 auto (large n)
   int blocked_max_w = 16384;   // cap on the shared tile width (tests force many blocks)
+  int blocked_split = 0;       // column parts per row slab: 0 auto, 1, 2
   int force_two_pass = 0;      // sampler: skip the single-pass tiled path (testing)
   int64_t launches = 0;
   // last error

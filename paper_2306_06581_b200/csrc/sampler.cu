@@ -403,6 +403,18 @@ __device__ __forceinline__ uint32_t sm_finalize_hi(uint64_t x) {
   return zh ^ (zh >> 31);
 }
 
+// Screen word of the fast scan: the high word zh of the last product, before
+// the final xor-shift. out_hi = zh ^ (zh >> 31) differs from zh only when
+// zh >= 2^31, and then both exceed any bound below 2^31; so for th < 2^31,
+// out_hi <= th <=> zh <= th (rows with a larger bound use th2 = 2^32 - 1,
+// i.e. always take the exact path).
+__device__ __forceinline__ uint32_t sm_screen_hi(uint64_t x) {
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  x = x ^ (x >> 27);
+  const uint32_t lo = (uint32_t)x, hi = (uint32_t)(x >> 32);
+  return __umulhi(lo, 0x133111ebu) + lo * 0x94d049bbu + hi * 0x133111ebu;
+}
+
 // The grid entry / prob of a supported entry, given its row and column
 // weights (same operations as grid_raw / plan_prob).
 __device__ __forceinline__ double plan_prob_w(const DPlan& P, double rw, double cw, double k) {
@@ -433,7 +445,7 @@ __device__ __forceinline__ uint32_t row_threshold(const TiledArgs& A, double rw)
 }
 
 template <int DIM, bool SAMPLE, bool NEEDK, class VT>
-__global__ void __launch_bounds__(256) tiled_kernel(TiledArgs A) {
+__global__ void __launch_bounds__(256, 2) tiled_kernel(TiledArgs A) {
   __shared__ float yfs[DIM][kTileJ];  // the screen's fp32 columns (exact paths read y from L2)
   __shared__ float yns[kTileJ];
   const int lane = threadIdx.x & 31;
@@ -449,6 +461,8 @@ __global__ void __launch_bounds__(256) tiled_kernel(TiledArgs A) {
     double rw[kRPW];
     uint64_t st0[kRPW];
     uint32_t th[kRPW];
+    uint32_t th2[kRPW];  // fast-scan bound on zh (see sm_screen_hi)
+    uint64_t lb[kRPW];   // stream base of the lane's draw: st0 + (lane + 1) * golden
     uint32_t tcnt[kRPW], cnt[kRPW];
     double racc[kRPW];
     int64_t row[kRPW];
@@ -472,6 +486,8 @@ __global__ void __launch_bounds__(256) tiled_kernel(TiledArgs A) {
       rw[q] = valid ? A.P.row_w[gi] : 0.0;
       st0[q] = mix_seed(A.seed, (uint64_t)gi);
       th[q] = SAMPLE ? row_threshold(A, rw[q]) : 0u;
+      th2[q] = th[q] < 0x80000000u ? th[q] : 0xffffffffu;
+      lb[q] = st0[q] + (uint64_t)(lane + 1) * kGolden;
       tcnt[q] = 0;
       cnt[q] = 0;
       racc[q] = 0.0;
@@ -501,6 +517,21 @@ __global__ void __launch_bounds__(256) tiled_kernel(TiledArgs A) {
       }
       if (!SAMPLE && !NEEDK && tile_all) continue;  // nothing off the support in this tile
       for (int c = 0; c < jend; c += 32) {
+        if (SAMPLE && tile_all) {
+          // every pair of the tile is supported: draw t of row q at lane l is
+          // tcnt + l + 1. Scan 32-column steps with the 4 rows' screens
+          // evaluated independently (no short-circuit: 4 hash chains in
+          // flight per warp) until some lane may keep an entry.
+          for (; c + 32 <= jend; c += 32) {
+            bool cand = false;
+#pragma unroll
+            for (int q = 0; q < kRPW; ++q) cand |= sm_screen_hi(lb[q] + (uint64_t)tcnt[q] * kGolden) <= th2[q];
+            if (__any_sync(0xffffffffu, cand)) break;
+#pragma unroll
+            for (int q = 0; q < kRPW; ++q) tcnt[q] += 32u;
+          }
+          if (c >= jend) break;
+        }
         const int jj = c + lane;
         const bool jvalid = jj < jend;
         const int64_t j = j0 + jj;
