@@ -448,6 +448,7 @@ template <int DIM, bool SAMPLE, bool NEEDK, class VT>
 __global__ void __launch_bounds__(256, 2) tiled_kernel(TiledArgs A) {
   __shared__ float yfs[DIM][kTileJ];  // the screen's fp32 columns (exact paths read y from L2)
   __shared__ float yns[kTileJ];
+  __shared__ double xmx[8];
   const int lane = threadIdx.x & 31;
   const int w = threadIdx.x >> 5;
   const unsigned lt_mask = (1u << lane) - 1u;
@@ -494,26 +495,43 @@ __global__ void __launch_bounds__(256, 2) tiled_kernel(TiledArgs A) {
       base[q] = (SAMPLE && valid) ? A.slot_off[row[q]] : 0;
       cap[q] = (SAMPLE && valid) ? A.slot_cap[row[q]] : 0;
     }
-    for (int64_t j0 = 0; j0 < A.n; j0 += kTileJ) {
-      __syncthreads();
-      for (int e = threadIdx.x; e < kTileJ * DIM; e += blockDim.x) {
-        const int jj = e / DIM, k = e - jj * DIM;
-        const int64_t j = j0 + jj;
-        yfs[k][jj] = j < A.n ? A.yf[j * DIM + k] : 0.f;
-      }
-      for (int jj = threadIdx.x; jj < kTileJ; jj += blockDim.x) yns[jj] = j0 + jj < A.n ? A.yn[j0 + jj] : 0.f;
-      __syncthreads();
-      const int jend = (int)min((int64_t)kTileJ, A.n - j0);
-      // |x_i - y_j| <= |x_i| + max_tile |y_j|: when that bound is inside the
-      // support for all 4 rows, every pair of the tile is supported
-      bool tile_all = true;
-      {
-        const double R = A.ytile_r[j0 / kTileJ];
+    // largest |x_i| of the CTA's 32 rows (inf if any row is padding)
+    double xmax_cta;
+    {
+      double m = xnorm[0];
 #pragma unroll
-        for (int q = 0; q < kRPW; ++q) {
-          const double b = xnorm[q] + R;
-          tile_all = tile_all && b * b * (1.0 + 1e-12) < A.lo;
+      for (int q = 1; q < kRPW; ++q) m = fmax(m, xnorm[q]);
+      __syncthreads();  // the previous group's readers of xmx are done
+      if (lane == 0) xmx[w] = m;
+      __syncthreads();
+      xmax_cta = xmx[0];
+#pragma unroll
+      for (int k = 1; k < 8; ++k) xmax_cta = fmax(xmax_cta, xmx[k]);
+    }
+    for (int64_t j0 = 0; j0 < A.n; j0 += kTileJ) {
+      // |x_i - y_j| <= |x_i| + max_tile |y_j|: when that bound is inside the
+      // support, every pair of the tile is supported. When it holds for all
+      // 32 rows of the CTA no path reads the staged fp32 tile (the screen is
+      // skipped; exact paths read y from L2), so the staging and both CTA
+      // barriers are skipped too (every thread takes the same decision).
+      const double R = A.ytile_r[j0 / kTileJ];
+      const bool cta_all = (xmax_cta + R) * (xmax_cta + R) * (1.0 + 1e-12) < A.lo;
+      if (!cta_all) {
+        __syncthreads();
+        for (int e = threadIdx.x; e < kTileJ * DIM; e += blockDim.x) {
+          const int jj = e / DIM, k = e - jj * DIM;
+          const int64_t j = j0 + jj;
+          yfs[k][jj] = j < A.n ? A.yf[j * DIM + k] : 0.f;
         }
+        for (int jj = threadIdx.x; jj < kTileJ; jj += blockDim.x) yns[jj] = j0 + jj < A.n ? A.yn[j0 + jj] : 0.f;
+        __syncthreads();
+      }
+      const int jend = (int)min((int64_t)kTileJ, A.n - j0);
+      bool tile_all = true;
+#pragma unroll
+      for (int q = 0; q < kRPW; ++q) {
+        const double b = xnorm[q] + R;
+        tile_all = tile_all && b * b * (1.0 + 1e-12) < A.lo;
       }
       if (!SAMPLE && !NEEDK && tile_all) continue;  // nothing off the support in this tile
       for (int c = 0; c < jend; c += 32) {
@@ -522,6 +540,25 @@ __global__ void __launch_bounds__(256, 2) tiled_kernel(TiledArgs A) {
           // tcnt + l + 1. Scan 32-column steps with the 4 rows' screens
           // evaluated independently (no short-circuit: 4 hash chains in
           // flight per warp) until some lane may keep an entry.
+          for (; c + 64 <= jend; c += 64) {  // two steps per pass: 8 independent chains
+            bool c0 = false, c1 = false;
+#pragma unroll
+            for (int q = 0; q < kRPW; ++q) {
+              c0 |= sm_screen_hi(lb[q] + (uint64_t)tcnt[q] * kGolden) <= th2[q];
+              c1 |= sm_screen_hi(lb[q] + (uint64_t)(tcnt[q] + 32u) * kGolden) <= th2[q];
+            }
+            const bool a0 = __any_sync(0xffffffffu, c0), a1 = __any_sync(0xffffffffu, c1);
+            if (a0 || a1) {
+              if (!a0) {  // the first step keeps nothing: stop at the second
+#pragma unroll
+                for (int q = 0; q < kRPW; ++q) tcnt[q] += 32u;
+                c += 32;
+              }
+              break;
+            }
+#pragma unroll
+            for (int q = 0; q < kRPW; ++q) tcnt[q] += 64u;
+          }
           for (; c + 32 <= jend; c += 32) {
             bool cand = false;
 #pragma unroll
