@@ -408,10 +408,30 @@ __device__ __forceinline__ uint32_t sm_finalize_hi(uint64_t x) {
 // zh >= 2^31, and then both exceed any bound below 2^31; so for th < 2^31,
 // out_hi <= th <=> zh <= th (rows with a larger bound use th2 = 2^32 - 1,
 // i.e. always take the exact path).
+// 17 integer instructions: the 64x64 product as one wide multiply plus two
+// accumulating low multiplies (ptxas otherwise adds a fourth).
+__device__ __forceinline__ uint32_t mulhi_pipe(uint32_t a, uint32_t b) {  // a * b >> 32 on the FMA pipe
+  uint32_t r;
+  asm("mul.hi.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+  return r;
+}
 __device__ __forceinline__ uint32_t sm_screen_hi(uint64_t x) {
-  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
-  x = x ^ (x >> 27);
-  const uint32_t lo = (uint32_t)x, hi = (uint32_t)(x >> 32);
+  // the high words' right shifts run as IMAD.HI (FMA pipe): the hash is
+  // otherwise ALU-pipe bound (shifts, xors, compares)
+  uint32_t lo = (uint32_t)x, hi = (uint32_t)(x >> 32);
+  lo = lo ^ __funnelshift_r(lo, hi, 30);
+  hi = hi ^ mulhi_pipe(hi, 4u);
+  uint32_t plo, phi;
+  asm("{\n\t.reg .u64 p;\n\t"
+      "mul.wide.u32 p, %2, 0x1ce4e5b9;\n\t"
+      "mov.b64 {%0, %1}, p;\n\t"
+      "mad.lo.u32 %1, %2, 0xbf58476d, %1;\n\t"
+      "mad.lo.u32 %1, %3, 0x1ce4e5b9, %1;\n\t}"
+      : "=r"(plo), "=r"(phi)
+      : "r"(lo), "r"(hi));
+  // x ^ (x >> 27) on (phi:plo)
+  lo = plo ^ __funnelshift_r(plo, phi, 27);
+  hi = phi ^ mulhi_pipe(phi, 32u);
   return __umulhi(lo, 0x133111ebu) + lo * 0x94d049bbu + hi * 0x133111ebu;
 }
 
@@ -540,12 +560,15 @@ __global__ void __launch_bounds__(256, 2) tiled_kernel(TiledArgs A) {
           // tcnt + l + 1. Scan 32-column steps with the 4 rows' screens
           // evaluated independently (no short-circuit: 4 hash chains in
           // flight per warp) until some lane may keep an entry.
+          uint64_t xq[kRPW];  // draw input of the lane at tcnt (advanced by 64 golden per pass)
+#pragma unroll
+          for (int q = 0; q < kRPW; ++q) xq[q] = lb[q] + (uint64_t)tcnt[q] * kGolden;
           for (; c + 64 <= jend; c += 64) {  // two steps per pass: 8 independent chains
             bool c0 = false, c1 = false;
 #pragma unroll
             for (int q = 0; q < kRPW; ++q) {
-              c0 |= sm_screen_hi(lb[q] + (uint64_t)tcnt[q] * kGolden) <= th2[q];
-              c1 |= sm_screen_hi(lb[q] + (uint64_t)(tcnt[q] + 32u) * kGolden) <= th2[q];
+              c0 |= sm_screen_hi(xq[q]) <= th2[q];
+              c1 |= sm_screen_hi(xq[q] + 32ull * kGolden) <= th2[q];
             }
             const bool a0 = __any_sync(0xffffffffu, c0), a1 = __any_sync(0xffffffffu, c1);
             if (a0 || a1) {
@@ -557,7 +580,10 @@ __global__ void __launch_bounds__(256, 2) tiled_kernel(TiledArgs A) {
               break;
             }
 #pragma unroll
-            for (int q = 0; q < kRPW; ++q) tcnt[q] += 64u;
+            for (int q = 0; q < kRPW; ++q) {
+              tcnt[q] += 64u;
+              xq[q] += 64ull * kGolden;
+            }
           }
           for (; c + 32 <= jend; c += 32) {
             bool cand = false;
