@@ -17,6 +17,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <memory>
 #include <cmath>
 #include <cstring>
 
@@ -416,7 +417,7 @@ __device__ __forceinline__ uint32_t mulhi_pipe(uint32_t a, uint32_t b) {  // a *
   return r;
 }
 __device__ __forceinline__ uint32_t sm_screen_hi(uint64_t x) {
-  // the high words' right shifts run as IMAD.HI (FMA pipe): the hash is
+  // one high-word right shift runs as IMAD.HI (FMA pipe): the hash is
   // otherwise ALU-pipe bound (shifts, xors, compares)
   uint32_t lo = (uint32_t)x, hi = (uint32_t)(x >> 32);
   lo = lo ^ __funnelshift_r(lo, hi, 30);
@@ -431,7 +432,7 @@ __device__ __forceinline__ uint32_t sm_screen_hi(uint64_t x) {
       : "r"(lo), "r"(hi));
   // x ^ (x >> 27) on (phi:plo)
   lo = plo ^ __funnelshift_r(plo, phi, 27);
-  hi = phi ^ mulhi_pipe(phi, 32u);
+  hi = phi ^ (phi >> 27);  // (ALU: IMAD runs on the heavy FMA half only, measured 74% busy with both on it)
   return __umulhi(lo, 0x133111ebu) + lo * 0x94d049bbu + hi * 0x133111ebu;
 }
 
@@ -465,7 +466,7 @@ __device__ __forceinline__ uint32_t row_threshold(const TiledArgs& A, double rw)
 }
 
 template <int DIM, bool SAMPLE, bool NEEDK, class VT>
-__global__ void __launch_bounds__(256, 2) tiled_kernel(TiledArgs A) {
+__global__ void __launch_bounds__(256, 3) tiled_kernel(TiledArgs A) {
   __shared__ float yfs[DIM][kTileJ];  // the screen's fp32 columns (exact paths read y from L2)
   __shared__ float yns[kTileJ];
   __shared__ double xmx[8];
@@ -814,6 +815,8 @@ __global__ void int_to_ll_kernel(const int* a, int64_t n, long long* b) {
 template <bool SAMPLE, bool NEEDK, class VT>
 void launch_tiled(spk_ctx* ctx, const TiledArgs& A) {
   const int64_t groups = (A.n_rows + kTileRows - 1) / kTileRows;
+  static const bool dbg = std::getenv("SPK_DEBUG_TIMING") != nullptr;
+  std::unique_ptr<Timer> tm(dbg ? new Timer(ctx->stream) : nullptr);
 #define SPK_TILED_CASE(D)                                                                                    \
   case D: {                                                                                                  \
     int occ = 0;                                                                                             \
@@ -837,6 +840,7 @@ void launch_tiled(spk_ctx* ctx, const TiledArgs& A) {
 #undef SPK_TILED_CASE
   ++ctx->launches;
   SPK_CUDA(cudaGetLastError());
+  if (tm) std::fprintf(stderr, "[timing] tiled_kernel<%s> %.4f s\n", SAMPLE ? "sample" : "plan", tm->stop());
 }
 
 bool tiled_dim_ok(int dim) { return dim == 1 || dim == 2 || dim == 3 || dim == 4 || dim == 5 || dim == 6 || dim == 8 || dim == 10; }
