@@ -227,6 +227,10 @@ def run_ours(args, ws, rank, local):
         from paper_2306_06581_b200 import _lib as L
 
         ctx.set_option(L.OPT_BLOCKED_SPLIT, int(os.environ["SPK_SPLIT"]))
+    if os.environ.get("SPK_SPREAD") is not None:  # column-bank spreading of the layout (profiling)
+        from paper_2306_06581_b200 import _lib as L
+
+        ctx.set_option(L.OPT_BLOCKED_SPREAD, int(os.environ["SPK_SPREAD"]))
     stream = torch.cuda.current_stream()
     ctx.set_stream(stream.cuda_stream)
     kernel = spk.Coords(w.x, w.y, w.cost, w.eta, scale=w.scale, eps=w.eps)

@@ -24,6 +24,7 @@ VALUES_F64, VALUES_F32 = 0, 1
 OPT_DETERMINISTIC, OPT_LOOP_BLOCKS_PER_SM, OPT_OTF_FP32, OPT_BLOCKED_LOOP, OPT_BLOCKED_MAX_W = 1, 2, 3, 4, 5
 OPT_TWO_PASS_SAMPLER = 6
 OPT_BLOCKED_SPLIT = 7
+OPT_BLOCKED_SPREAD = 8
 
 ERROR_CLASSES = {
     1: "Error", 2: "NegativeWeight", 3: "LengthMismatch", 4: "NotNormalized", 5: "AllBlack",

@@ -453,11 +453,93 @@ __global__ void runlen_kernel(const uint32_t* keys_s, const uint32_t* rl, const 
 // A row's m <= C consecutive positions hit m distinct chunks, so no chunk
 // holds a row twice; its entries then take those chunks in ascending order,
 // so the row is still summed in column order when the chunks run in order.
+//
+// Column spreading (slot_kernel, one thread per segment): the placement fixes,
+// per row bank class, a set of list positions (hence (chunk, half-warp)
+// slots); any permutation of the class's entries over its own positions
+// keeps the row-bank spread. The x gather costs the worst column-bank
+// multiplicity of a half-warp (~6 wavefronts per chunk at random, 4.9 per
+// LDS.64 measured with the accumulator loads), so each class's entries are
+// dealt greedily to the free position whose half-warp holds the fewest
+// entries of the entry's column class (rows with several entries first, each
+// in distinct chunks). Simulated at config 4: 6.1 -> 3.8 gather wavefronts
+// per chunk, no extra padding. newpos[q] = chosen list position, or -1 where
+// a segment keeps the plain placement.
+__global__ void __launch_bounds__(64) slot_kernel(int64_t nkeys, const long long* useg,
+                                                  const unsigned long long* cnt, const long long* nchunk,
+                                                  const uint32_t* rl, const uint32_t* idx, const uint32_t* perm,
+                                                  int W, const uint32_t* start, const uint32_t* runlen,
+                                                  int* newpos) {
+  __shared__ unsigned long long cc[64][64];  // per thread: [chunk][half] -> 16 x 4-bit column-class counts
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= nkeys) return;
+  const int E = (int)cnt[k];
+  const int C = (int)nchunk[k];
+  if (E == 0 || C > 32) return;
+  const long long u0 = useg[k];
+  unsigned long long* my = cc[threadIdx.x];
+  for (int i = 0; i < 2 * C; ++i) my[i] = 0ull;
+  bool ok = true;
+  int p = 0;
+  for (int cls = 0; cls < 16 && ok; ++cls) {
+    const int ps = p;
+    while (p < E && (int)(rl[u0 + p] & 15u) == cls) ++p;
+    const int nk = p - ps;
+    if (nk == 0) continue;
+    if (nk > 64) {
+      ok = false;
+      break;
+    }
+    unsigned long long freem = nk == 64 ? ~0ull : ((1ull << nk) - 1ull);
+    for (int pass = 0; pass < 2 && ok; ++pass) {
+      for (int o = 0; o < nk; ++o) {
+        const long long q = u0 + ps + o;
+        const long long rs = start[q];
+        const int rn = (int)runlen[rs];
+        if ((rn > 1) != (pass == 0)) continue;
+        const int cc4 = 4 * (int)((idx[perm[q]] % (uint32_t)W) & 15u);
+        int best = -1, bc = 1 << 30;
+        for (unsigned long long fm = freem; fm; fm &= fm - 1) {
+          const int f = __ffsll((long long)fm) - 1;
+          const int pos = ps + f;
+          const int ch = pos % C, hf = (pos / C) & 1;
+          bool clash = false;
+          for (int j = 0; j < rn && rn > 1; ++j) {
+            const int np = newpos[rs + j];
+            if (rs + j != q && np >= 0 && np % C == ch) {
+              clash = true;
+              break;
+            }
+          }
+          if (clash) continue;
+          const int c = (int)((my[2 * ch + hf] >> cc4) & 15ull);
+          if (c < bc) {
+            bc = c;
+            best = f;
+            if (c == 0) break;
+          }
+        }
+        if (best < 0) {
+          ok = false;
+          break;
+        }
+        const int pos = ps + best;
+        newpos[q] = pos;
+        freem &= ~(1ull << best);
+        const int ch = pos % C, hf = (pos / C) & 1;
+        if (((my[2 * ch + hf] >> cc4) & 15ull) < 15ull) my[2 * ch + hf] += 1ull << cc4;
+      }
+    }
+  }
+  if (!ok)
+    for (int e = 0; e < E; ++e) newpos[u0 + e] = -1;
+}
+
 template <class VT>
 __global__ void place_kernel(const uint32_t* keys_s, const uint32_t* perm, const uint32_t* rl, const uint32_t* start,
                              const uint32_t* runlen, const long long* useg, const long long* seg_base,
                              const long long* nchunk, const uint32_t* idx, const VT* val, int W, int64_t m,
-                             uint32_t* packed, VT* vout) {
+                             const int* newpos, uint32_t* packed, VT* vout) {
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < m; q += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t key = keys_s[q];
     const long long C = nchunk[key];
@@ -466,7 +548,10 @@ __global__ void place_kernel(const uint32_t* keys_s, const uint32_t* perm, const
     const long long mr = runlen[start[q]];
     const long long a = ps % C, wrap = a + mr - C;
     long long c, pp;
-    if (wrap > 0 && kk < wrap) {
+    if (newpos[q] >= 0) {  // column-spread position (slot_kernel)
+      pp = newpos[q];
+      c = pp % C;
+    } else if (wrap > 0 && kk < wrap) {
       c = kk;
       pp = ps + (C - a) + c;
     } else {
@@ -642,17 +727,24 @@ bool build_blocked(spk_ctx* ctx, int P, int S, int W, int64_t n_out, int64_t n_i
   SPK_CUDA(cudaMemsetAsync(out.packed.p, 0xff, out.packed.bytes, s));  // padding = kPad
   SPK_CUDA(cudaMemsetAsync(out.val.p, 0, out.val.bytes, s));
   if (m > 0) {
+    DBuf newpos(sizeof(int) * mm);
+    SPK_CUDA(cudaMemsetAsync(newpos.p, 0xff, newpos.bytes, s));
+    if (ctx->blocked_spread)
+      slot_kernel<<<(int)((nkeys + 63) / 64), 64, 0, s>>>(nkeys, d_useg.as<long long>(), hist.as<unsigned long long>(),
+                                                        d_nch.as<long long>(), rl.as<uint32_t>(), idx_d.as<uint32_t>(),
+                                                        perm.as<uint32_t>(), W, start.as<uint32_t>(),
+                                                        runlen.as<uint32_t>(), newpos.as<int>());
     if (vbytes == 4)
       place_kernel<float><<<grid_cap(ctx, m), 256, 0, s>>>(
           keys_s.as<uint32_t>(), perm.as<uint32_t>(), rl.as<uint32_t>(), start.as<uint32_t>(), runlen.as<uint32_t>(),
           d_useg.as<long long>(), d_seg.as<long long>(), d_nch.as<long long>(), idx_d.as<uint32_t>(),
-          val_d.as<float>(), W, m, out.packed.as<uint32_t>(), out.val.as<float>());
+          val_d.as<float>(), W, m, newpos.as<int>(), out.packed.as<uint32_t>(), out.val.as<float>());
     else
       place_kernel<double><<<grid_cap(ctx, m), 256, 0, s>>>(
           keys_s.as<uint32_t>(), perm.as<uint32_t>(), rl.as<uint32_t>(), start.as<uint32_t>(), runlen.as<uint32_t>(),
           d_useg.as<long long>(), d_seg.as<long long>(), d_nch.as<long long>(), idx_d.as<uint32_t>(),
-          val_d.as<double>(), W, m, out.packed.as<uint32_t>(), out.val.as<double>());
-    ++ctx->launches;
+          val_d.as<double>(), W, m, newpos.as<int>(), out.packed.as<uint32_t>(), out.val.as<double>());
+    ctx->launches += ctx->blocked_spread ? 2 : 1;
   }
   SPK_CUDA(cudaGetLastError());
   SPK_CUDA(cudaStreamSynchronize(s));
