@@ -283,6 +283,7 @@ struct BlockedOp {
       for (int d = 0; d < kDepth; ++d) load_group(gk, gv, min(d, glast), lane, pol, R[d]);
       int cb = 0, cs = 0;  // current block and its stage
       int cb_end = (int)((ofs[1] - sbeg) >> 5);
+      int cb_next = (int)((ofs[nb > 1 ? 2 : 1] - sbeg) >> 5);  // next boundary, loaded one transition early
       const double* xs = tiles;  // tile of the current block
       if (!mbar_wait(&full[0], pmask & 1u, fault)) record_fault(fault, 0x20000000u | ((unsigned)ROLE << 24));
       pmask ^= 1u;
@@ -309,7 +310,8 @@ struct BlockedOp {
                     if (lane == 0) mbar_arrive(&empty[cs]);
                     ++cb;
                     cs = cs + 1 == STG ? 0 : cs + 1;
-                    cb_end = (int)((ofs[cb + 1] - sbeg) >> 5);
+                    cb_end = cb_next;
+                    cb_next = (int)((ofs[min(cb + 2, nb)] - sbeg) >> 5);
                     xs = tiles + (size_t)cs * kTileW;
                     if (!mbar_wait(&full[cs], (pmask >> cs) & 1u, fault))
                       record_fault(fault, 0x30000000u | ((unsigned)ROLE << 24) | (unsigned)cb);
