@@ -133,6 +133,12 @@ __device__ __forceinline__ uint4 ldg_stream(const void* p, uint64_t pol) {
   return r;
 }
 
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 __host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
 // Stream position of (global chunk C, lane) -- 4-chunk groups interleaved per lane.
@@ -161,6 +167,7 @@ struct BlockedOp {
   unsigned int* fault;  // [0] first fault code, [1] its CTA
   double* xchg;         // S = 2: partial sums handed to the partner CTA (n doubles)
   unsigned int* pair;   // S = 2: one arrival counter per row slab
+  unsigned long long* trace;  // SPK_TRACE_BLOCKED: globaltimer stamps of the first 4 iterations
 
   __host__ __device__ size_t head_bytes() const { return align16((size_t)(acc_rows + 1) * 8) + 128; }
   size_t smem_bytes() const { return head_bytes() + (size_t)STG * kTileW * 8; }
@@ -235,6 +242,8 @@ struct BlockedOp {
       }
       fence_mbar_init();
     }
+    unsigned long long* tr = (trace && t <= 4) ? trace + (((size_t)(t - 1) * 2 + ROLE) * gridDim.x + cta) * 20 : nullptr;
+    if (tr && threadIdx.x == 0) tr[0] = globaltimer();
     for (int r = threadIdx.x; r < nrows; r += blockDim.x) acc[r] = 0.0;
     __syncthreads();
     // bit s: parity of the next phase of stage s; flipped after every wait on it
@@ -324,6 +333,7 @@ struct BlockedOp {
           }
         }
       }
+      if (tr && lane == 0) tr[1 + w] = globaltimer();
       // release the remaining blocks in order (tile present before release)
       for (;;) {
         __syncwarp();
@@ -336,6 +346,7 @@ struct BlockedOp {
       }
     }
     __syncthreads();
+    if (tr && threadIdx.x == 0) tr[16] = globaltimer();
     if (threadIdx.x == 0) {  // block b used stage b % STG once
 #pragma unroll
       for (int s = 0; s < STG; ++s) ph[s] = ph0[s] + (uint32_t)((nb - s + STG - 1) / STG);
@@ -349,6 +360,7 @@ struct BlockedOp {
       const int o0 = part == 0 ? mid : 0, o1 = part == 0 ? nrows : mid;  // the partner's rows
       for (int r = o0 + threadIdx.x; r < o1; r += blockDim.x) __stcg(xchg + r0 + r, acc[r]);
       __syncthreads();
+      if (tr && threadIdx.x == 0) tr[17] = globaltimer();
       if (threadIdx.x == 0) {
         __threadfence();
         const unsigned int target = 2u * (unsigned)(2 * (t - 1) + ROLE + 1);
@@ -366,17 +378,41 @@ struct BlockedOp {
       }
       __syncthreads();
     }
-    for (int r = fr0 + threadIdx.x; r < fr1; r += blockDim.x) {
-      const int64_t i = r0 + r;
-      const double o = __ldcg(old + i);
-      if (!ne[i]) {
-        out[i] = o;
-        continue;
+    if (tr && threadIdx.x == 0) tr[18] = globaltimer();
+    // Latency-bound (~13 rows per thread at config 4): the loads of the next
+    // rows are issued before the current row is finalized (software
+    // pipeline: out/ne/dyn never alias old/wgt/xchg).
+    {
+      int r = fr0 + threadIdx.x;
+      double o = 0.0, wv = 0.0, px = 0.0;
+      unsigned char nv = 0;
+      if (r < fr1) {
+        o = __ldcg(old + r0 + r);
+        nv = ne[r0 + r];
+        wv = __ldg(wgt + r0 + r);
+        if (S == 2) px = __ldcg(xchg + r0 + r);
       }
-      const double tmp = S == 2 ? __dadd_rn(acc[r], __ldcg(xchg + i)) : acc[r];  // p0 + p1 (commutes exactly)
-      err += loopcore::finalize_atom<LOG>(i, tmp, o, wgt[i], exponent, policy, t, ne, dyn, out, flag, masks);
+      for (; r < fr1; r += blockDim.x) {
+        const int64_t i = r0 + r;
+        const double oc = o, wc = wv, pc = px;
+        const unsigned char nc = nv;
+        const int rn = r + (int)blockDim.x;
+        if (rn < fr1) {  // next row's loads in flight while this one finishes
+          o = __ldcg(old + r0 + rn);
+          nv = ne[r0 + rn];
+          wv = __ldg(wgt + r0 + rn);
+          if (S == 2) px = __ldcg(xchg + r0 + rn);
+        }
+        if (!nc) {
+          out[i] = oc;
+          continue;
+        }
+        const double tmp = S == 2 ? __dadd_rn(acc[r], pc) : acc[r];  // p0 + p1 (commutes exactly)
+        err += loopcore::finalize_atom<LOG>(i, tmp, oc, wc, exponent, policy, t, ne, dyn, out, flag, masks);
+      }
     }
     __syncthreads();
+    if (tr && threadIdx.x == 0) tr[19] = globaltimer();
   }
 };
 
@@ -784,6 +820,13 @@ void launch_blocked(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, dou
   W.scalar.ensure(sizeof(unsigned int) * 2);
   SPK_CUDA(cudaMemsetAsync(W.scalar.p, 0, sizeof(unsigned int) * 2, ctx->stream));
   op.fault = W.scalar.as<unsigned int>();
+  static const bool trace = std::getenv("SPK_TRACE_BLOCKED") != nullptr;
+  DBuf tbuf;
+  if (trace) {
+    tbuf.alloc(sizeof(unsigned long long) * 4 * 2 * op.L[0].P * 20);
+    SPK_CUDA(cudaMemsetAsync(tbuf.p, 0, tbuf.bytes, ctx->stream));
+    op.trace = tbuf.as<unsigned long long>();
+  }
   const int Q = op.L[0].P / S;
   if (S == 2) {
     W.xchg.ensure(sizeof(double) * n);
@@ -798,6 +841,53 @@ void launch_blocked(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, dou
   SPK_CUDA(cudaMemcpyAsync(W.col_ne.p, sk->cov_col.p, n, cudaMemcpyDeviceToDevice, ctx->stream));
   loopcore::run_core<false>(ctx, op, n, W, sk->cov_empty_rows, sk->cov_empty_cols, cfg, exponent, policy, st,
                             /*useful_blocks=*/op.L[0].P, out, /*exact_grid=*/op.L[0].P, op.smem_bytes());
+  if (trace) {  // per (iteration, half, CTA): half start, 15 warps' stream ends, finalize end (ns)
+    std::vector<unsigned long long> h(tbuf.bytes / 8);
+    download(ctx, h.data(), tbuf, tbuf.bytes);
+    const int P = op.L[0].P;
+    for (int it = 0; it < 4; ++it)
+      for (int role = 0; role < 2; ++role) {
+        unsigned long long t0 = ~0ull, t1 = 0, smin = ~0ull, smax = 0, fmax = 0;
+        long double smean = 0;
+        int cntw = 0;
+        for (int c = 0; c < P; ++c) {
+          const unsigned long long* e = h.data() + (((size_t)it * 2 + role) * P + c) * 20;
+          if (!e[0]) continue;
+          t0 = std::min(t0, e[0]);
+          t1 = std::max(t1, e[0]);
+          fmax = std::max(fmax, e[19]);
+          for (int w = 0; w < kNW; ++w)
+            if (e[1 + w]) {
+              smin = std::min(smin, e[1 + w]);
+              smax = std::max(smax, e[1 + w]);
+              smean += (long double)(e[1 + w] - e[0]);
+              ++cntw;
+            }
+        }
+        if (t0 == ~0ull) continue;
+        std::fprintf(stderr,
+                     "[trace] it %d half %d: start spread %.1f us, stream end min %.1f mean %.1f max %.1f us, "
+                     "finalize end %.1f us\n",
+                     it + 1, role, (t1 - t0) * 1e-3, (smin - t0) * 1e-3, (double)(smean / cntw) * 1e-3,
+                     (smax - t0) * 1e-3, (fmax - t0) * 1e-3);
+        // per-CTA phase durations averaged: stream end (last warp) -> released, -> xchg written, -> pair met, -> final
+        double d1 = 0, d2 = 0, d3 = 0, d4 = 0;
+        int nc = 0;
+        for (int c = 0; c < P; ++c) {
+          const unsigned long long* e = h.data() + (((size_t)it * 2 + role) * P + c) * 20;
+          if (!e[0] || !e[16]) continue;
+          unsigned long long se = 0;
+          for (int w = 0; w < kNW; ++w) se = std::max(se, e[1 + w]);
+          d1 += (double)(e[16] - se);
+          if (e[17]) d2 += (double)(e[17] - e[16]);
+          d3 += (double)(e[18] - (e[17] ? e[17] : e[16]));
+          d4 += (double)(e[19] - e[18]);
+          ++nc;
+        }
+        std::fprintf(stderr, "[trace]   per CTA: release %.2f us, xchg %.2f us, pair wait %.2f us, finalize %.2f us\n",
+                     d1 / nc * 1e-3, d2 / nc * 1e-3, d3 / nc * 1e-3, d4 / nc * 1e-3);
+      }
+  }
   unsigned int fw[2] = {0u, 0u};
   download(ctx, fw, W.scalar, sizeof fw);
   if (fw[0]) {
