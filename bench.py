@@ -231,6 +231,10 @@ def run_ours(args, ws, rank, local):
         from paper_2306_06581_b200 import _lib as L
 
         ctx.set_option(L.OPT_BLOCKED_SPREAD, int(os.environ["SPK_SPREAD"]))
+    if os.environ.get("SPK_CLUSTER") is not None:  # CTA pairs as clusters (profiling)
+        from paper_2306_06581_b200 import _lib as L
+
+        ctx.set_option(L.OPT_BLOCKED_CLUSTER, int(os.environ["SPK_CLUSTER"]))
     stream = torch.cuda.current_stream()
     ctx.set_stream(stream.cuda_stream)
     kernel = spk.Coords(w.x, w.y, w.cost, w.eta, scale=w.scale, eps=w.eps)

@@ -169,7 +169,8 @@ enum spk_option {
   SPK_OPT_BLOCKED_MAX_W = 5, /* cap on the staged tile width (testing) */
   SPK_OPT_TWO_PASS_SAMPLER = 6, /* sampler: always the exact two-pass kernels (testing) */
   SPK_OPT_BLOCKED_SPLIT = 7,    /* slab x block loop: column parts per row slab (0 auto, 1, 2 = CTA pairs) */
-  SPK_OPT_BLOCKED_SPREAD = 8    /* slab x block loop: spread each half-warp's gathered columns over the banks (1, default) */
+  SPK_OPT_BLOCKED_SPREAD = 8,   /* slab x block loop: spread each half-warp's gathered columns over the banks (1, default) */
+  SPK_OPT_BLOCKED_CLUSTER = 9   /* slab x block loop: CTA pairs as 2-CTA clusters sharing partial sums (1, default, when they fit) */
 };
 int spk_ctx_set_option(spk_ctx* ctx, int key, int64_t value);
 /* Status of the last failed call on ctx: category (spk_status), class

@@ -25,6 +25,7 @@ OPT_DETERMINISTIC, OPT_LOOP_BLOCKS_PER_SM, OPT_OTF_FP32, OPT_BLOCKED_LOOP, OPT_B
 OPT_TWO_PASS_SAMPLER = 6
 OPT_BLOCKED_SPLIT = 7
 OPT_BLOCKED_SPREAD = 8
+OPT_BLOCKED_CLUSTER = 9
 
 ERROR_CLASSES = {
     1: "Error", 2: "NegativeWeight", 3: "LengthMismatch", 4: "NotNormalized", 5: "AllBlack",

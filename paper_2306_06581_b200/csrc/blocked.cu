@@ -139,6 +139,17 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   return t;
 }
 
+// Cluster barrier with release/acquire semantics (shared::cluster writes of
+// each CTA visible to the other after it) and the peer's view of a shared address.
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ const double* map_peer(const double* p, unsigned rank) {
+  const double* q;
+  asm volatile("mapa.u64 %0, %1, %2;" : "=l"(q) : "l"(p), "r"(rank));
+  return q;
+}
+
 __host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
 // Stream position of (global chunk C, lane) -- 4-chunk groups interleaved per lane.
@@ -156,9 +167,12 @@ struct Group {  // one lane's entries of 4 consecutive chunks
   uint4 v1;  // f64 only
 };
 
-template <class VT, int S, int STG>
+// CL: the CTA pair is a 2-CTA cluster and reads the partner's partial sums
+// from its shared memory (DSMEM) instead of swapping them through L2.
+template <class VT, int S, int STG, bool CL = false>
 struct BlockedOp {
   static constexpr int kThreads = kThreadsBlocked;
+  static constexpr int kCluster = CL ? 2 : 1;
   static constexpr int kMinBlocks = 1;  // one CTA per SM: full register file, up to 227 KB shared
   static constexpr int kDepth = sizeof(VT) == 4 ? 3 : 2;  // groups in flight per consumer warp (registers)
   BlockedHalf L[2];
@@ -353,7 +367,15 @@ struct BlockedOp {
     }
     // ---- finalize this CTA's atoms of the slab ----
     int fr0 = 0, fr1 = nrows;
-    if (S == 2) {
+    const double* pacc = nullptr;  // CL: the partner's accumulators (DSMEM)
+    if (S == 2 && CL) {
+      const int mid = nrows >> 1;
+      fr0 = part == 0 ? 0 : mid;
+      fr1 = part == 0 ? mid : nrows;
+      if (tr && threadIdx.x == 0) tr[17] = globaltimer();
+      cluster_sync();  // both CTAs' sums complete (release/acquire at cluster scope)
+      pacc = map_peer(acc, (unsigned)(part ^ 1));
+    } else if (S == 2) {
       const int mid = nrows >> 1;
       fr0 = part == 0 ? 0 : mid;
       fr1 = part == 0 ? mid : nrows;
@@ -390,7 +412,7 @@ struct BlockedOp {
         o = __ldcg(old + r0 + r);
         nv = ne[r0 + r];
         wv = __ldg(wgt + r0 + r);
-        if (S == 2) px = __ldcg(xchg + r0 + r);
+        if (S == 2) px = CL ? pacc[r] : __ldcg(xchg + r0 + r);
       }
       for (; r < fr1; r += blockDim.x) {
         const int64_t i = r0 + r;
@@ -401,7 +423,7 @@ struct BlockedOp {
           o = __ldcg(old + r0 + rn);
           nv = ne[r0 + rn];
           wv = __ldg(wgt + r0 + rn);
-          if (S == 2) px = __ldcg(xchg + r0 + rn);
+          if (S == 2) px = CL ? pacc[rn] : __ldcg(xchg + r0 + rn);
         }
         if (!nc) {
           out[i] = oc;
@@ -807,11 +829,11 @@ namespace {
 // dynamic shared memory per CTA: 227 KB minus the loop kernel's static use
 constexpr size_t kSmemBudget = 232448 - 1024;
 
-template <class VT, int S, int STG>
+template <class VT, int S, int STG, bool CL = false>
 void launch_blocked(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, double exponent, int policy,
                     LoopState& st, LoopOut& out) {
   const int64_t n = sk->n;
-  BlockedOp<VT, S, STG> op{};
+  BlockedOp<VT, S, STG, CL> op{};
   op.L[0] = sk->blk_rows->h;
   op.L[1] = sk->blk_cols->h;
   op.n = n;
@@ -828,7 +850,7 @@ void launch_blocked(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, dou
     op.trace = tbuf.as<unsigned long long>();
   }
   const int Q = op.L[0].P / S;
-  if (S == 2) {
+  if (S == 2 && !CL) {
     W.xchg.ensure(sizeof(double) * n);
     W.pair.ensure(sizeof(unsigned int) * Q);
     SPK_CUDA(cudaMemsetAsync(W.pair.p, 0, sizeof(unsigned int) * Q, ctx->stream));
@@ -903,6 +925,39 @@ void launch_blocked(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, dou
 // rows per CTA and keeps 3.
 constexpr int kStg1 = 4, kStg2 = 3;
 
+// The cluster variant needs every CTA pair co-resident as a 2-CTA cluster
+// (a GPC with an odd number of free SMs loses one); else the L2 swap is used.
+template <class VT>
+bool cluster_pairs_fit(spk_ctx* ctx, spk_sketch* sk) {
+  if (!ctx->blocked_cluster) return false;
+  const int P = sk->blk_rows->h.P;
+  BlockedOp<VT, 2, kStg2, true> probe{};
+  probe.acc_rows = std::max(sk->blk_rows->max_rows, sk->blk_cols->max_rows);
+  const size_t smem = probe.smem_bytes();
+  auto kern = loopcore::loop_kernel<false, false, BlockedOp<VT, 2, kStg2, true>>;
+  if (cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return false;
+  }
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = dim3(P);
+  lc.blockDim = dim3(kThreadsBlocked);
+  lc.dynamicSmemBytes = smem;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  int nclusters = 0;
+  if (cudaOccupancyMaxActiveClusters(&nclusters, (const void*)kern, &lc) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return false;
+  }
+  return nclusters >= P / 2;
+}
+
 template <class VT>
 bool run_blocked_t(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, double exponent, int policy,
                    LoopState& st, LoopOut& out) {
@@ -935,7 +990,10 @@ bool run_blocked_t(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, doub
     }
   }
   if (!sk->blk_rows) return false;
-  if (sk->blk_rows->h.S == 2) launch_blocked<VT, 2, kStg2>(ctx, sk, cfg, exponent, policy, st, out);
+  if (sk->blk_rows->h.S == 2 && cluster_pairs_fit<VT>(ctx, sk))
+    launch_blocked<VT, 2, kStg2, true>(ctx, sk, cfg, exponent, policy, st, out);
+  else if (sk->blk_rows->h.S == 2)
+    launch_blocked<VT, 2, kStg2>(ctx, sk, cfg, exponent, policy, st, out);
   else launch_blocked<VT, 1, kStg1>(ctx, sk, cfg, exponent, policy, st, out);
   return true;
 }

@@ -134,6 +134,7 @@ struct spk_ctx {
   int blocked_max_w = 16384;   // cap on the shared tile width (tests force many blocks)
   int blocked_split = 0;       // column parts per row slab: 0 auto, 1, 2
   int blocked_spread = 1;      // slab x block layout: spread gathered columns over banks (slot_kernel)
+  int blocked_cluster = 1;     // CTA pairs as 2-CTA clusters (DSMEM partial sums) when they all fit
   int force_two_pass = 0;      // sampler: skip the single-pass tiled path (testing)
   int64_t launches = 0;
   // last error

@@ -18,6 +18,7 @@
 #include <algorithm>
 #include <cmath>
 #include <string>
+#include <type_traits>
 
 #include "common.cuh"
 #include "internal.h"
@@ -334,6 +335,16 @@ inline int simple_grid(spk_ctx* ctx, int64_t n) {
   return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)ctx->num_sms * 8));
 }
 
+// Cluster size an operator asks for (Op::kCluster, default 1).
+template <class Op, class = void>
+struct cluster_of {
+  static constexpr int value = 1;
+};
+template <class Op>
+struct cluster_of<Op, std::void_t<decltype(Op::kCluster)>> {
+  static constexpr int value = Op::kCluster;
+};
+
 // Host driver shared by every operator. row_ne / col_ne hold the structural
 // coverage (kernel_coverage, solvers.cpp:138-163); masked_rows/cols their
 // zero counts. Fills st.u/st.v (and st.lu/st.lv in the log domain).
@@ -435,7 +446,25 @@ void run_core(spk_ctx* ctx, const Op& op, int64_t n, LoopWs& W, long long masked
   Op op_copy = op;
   void* args[] = {&P, &op_copy};
   Timer tm(s);
-  SPK_CUDA(cudaLaunchCooperativeKernel((void*)kern, dim3(grid), dim3(Op::kThreads), args, dyn_smem, s));
+  if (cluster_of<Op>::value > 1) {  // cooperative launch of 2-CTA clusters (grid.sync + DSMEM)
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3(grid);
+    lc.blockDim = dim3(Op::kThreads);
+    lc.dynamicSmemBytes = dyn_smem;
+    lc.stream = s;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    at[1].id = cudaLaunchAttributeClusterDimension;
+    at[1].val.clusterDim.x = cluster_of<Op>::value;
+    at[1].val.clusterDim.y = 1;
+    at[1].val.clusterDim.z = 1;
+    lc.attrs = at;
+    lc.numAttrs = 2;
+    SPK_CUDA(cudaLaunchKernelExC(&lc, (const void*)kern, args));
+  } else {
+    SPK_CUDA(cudaLaunchCooperativeKernel((void*)kern, dim3(grid), dim3(Op::kThreads), args, dyn_smem, s));
+  }
   ++ctx->launches;
   out.loop_s = tm.stop();
   SPK_CUDA(cudaGetLastError());

@@ -257,6 +257,7 @@ int spk_ctx_set_option(spk_ctx* ctx, int key, int64_t value) {
     case 4: ctx->use_blocked = (int)std::max<int64_t>(0, std::min<int64_t>(value, 2)); return SPK_OK;
     case 5: ctx->blocked_max_w = (int)std::max<int64_t>(16, std::min<int64_t>(value, 16384)); return SPK_OK;
     case 6: ctx->force_two_pass = value ? 1 : 0; return SPK_OK;
+    case 9: ctx->blocked_cluster = value ? 1 : 0; return SPK_OK;
     case 8: ctx->blocked_spread = value ? 1 : 0; return SPK_OK;
     case 7: ctx->blocked_split = (int)std::max<int64_t>(0, std::min<int64_t>(value, 2)); return SPK_OK;
     default: return SPK_STATUS_INPUT;
