@@ -421,7 +421,7 @@ __device__ __forceinline__ uint32_t sm_screen_hi(uint64_t x) {
   // otherwise ALU-pipe bound (shifts, xors, compares)
   uint32_t lo = (uint32_t)x, hi = (uint32_t)(x >> 32);
   lo = lo ^ __funnelshift_r(lo, hi, 30);
-  hi = hi ^ mulhi_pipe(hi, 4u);
+  hi = hi ^ (hi >> 30);
   uint32_t plo, phi;
   asm("{\n\t.reg .u64 p;\n\t"
       "mul.wide.u32 p, %2, 0x1ce4e5b9;\n\t"
