@@ -45,6 +45,7 @@
 #include "common.cuh"
 #include "internal.h"
 #include "loop_core.cuh"
+#include "shard_core.cuh"
 
 namespace spk {
 
@@ -182,6 +183,7 @@ struct BlockedOp {
   double* xchg;         // S = 2: partial sums handed to the partner CTA (n doubles)
   unsigned int* pair;   // S = 2: one arrival counter per row slab
   unsigned long long* trace;  // SPK_TRACE_BLOCKED: globaltimer stamps of the first 4 iterations
+  bool fresh;                 // one launch per half (sharded): initialise the barriers on every call
 
   __host__ __device__ size_t head_bytes() const { return align16((size_t)(acc_rows + 1) * 8) + 128; }
   size_t smem_bytes() const { return head_bytes() + (size_t)STG * kTileW * 8; }
@@ -248,7 +250,7 @@ struct BlockedOp {
     // Barriers are initialised once per launch (first half of iteration 1)
     // and never re-initialised; each stage's phase count carries over from
     // half to half in shared memory.
-    if (ROLE == 0 && t == 1 && threadIdx.x == 0) {
+    if ((fresh || (ROLE == 0 && t == 1)) && threadIdx.x == 0) {
       for (int s = 0; s < STG; ++s) {
         mbar_init(&full[s], 1);
         mbar_init(&empty[s], kNW);
@@ -935,10 +937,7 @@ bool cluster_pairs_fit(spk_ctx* ctx, spk_sketch* sk) {
   probe.acc_rows = std::max(sk->blk_rows->max_rows, sk->blk_cols->max_rows);
   const size_t smem = probe.smem_bytes();
   auto kern = loopcore::loop_kernel<false, false, BlockedOp<VT, 2, kStg2, true>>;
-  if (cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
-    (void)cudaGetLastError();
-    return false;
-  }
+  loopcore::allow_max_dyn_smem((const void*)kern);
   cudaLaunchConfig_t lc{};
   lc.gridDim = dim3(P);
   lc.blockDim = dim3(kThreadsBlocked);
@@ -999,6 +998,116 @@ bool run_blocked_t(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, doub
 }
 
 }  // namespace
+
+// ---- sharded half-steps (shard.cu's state machine, this file's operator) -----------
+
+namespace {
+
+template <class VT, int S, int STG, bool CL>
+__global__ void __launch_bounds__(kThreadsBlocked, 1) shard_half_kernel(shard::HalfArgs A, BlockedOp<VT, S, STG, CL> op) {
+  __shared__ shard::State St;
+  if (threadIdx.x == 0) {
+    St = *A.st_in;
+    shard::decide<false>(A, St);
+  }
+  __syncthreads();
+  if (blockIdx.x == 0 && threadIdx.x == 0) *A.st_out = St;
+  if (St.stopped) return;  // the same decision in every CTA (same gathered tails)
+  double err = 0.0;
+  long long masks = 0;
+  if (A.half == 0)
+    op.template half<0, false, false>(A.x, A.w, A.old, A.out, A.ne, A.dyn, A.exponent, A.policy, (int)A.t, A.flag,
+                                      nullptr, err, masks);
+  else
+    op.template half<1, false, false>(A.x, A.w, A.old, A.out, A.ne, A.dyn, A.exponent, A.policy, (int)A.t, A.flag,
+                                      nullptr, err, masks);
+  shard::finish_half(A, err, masks);
+}
+
+template <class VT>
+void launch_shard_half(spk_ctx* ctx, const shard::HalfArgs& A, shard::BlockedShard& B) {
+  const BlockedHalf& h = B.R->h;
+  const int acc_rows = std::max(B.R->max_rows, B.C->max_rows);
+  if (h.S == 2) {  // CTA pairs as 2-CTA clusters (independent clusters: no co-residency needed)
+    BlockedOp<VT, 2, kStg2, true> op{};
+    op.L[0] = B.R->h;
+    op.L[1] = B.C->h;
+    op.n = h.n_out;
+    op.acc_rows = acc_rows;
+    op.fault = B.fault.as<unsigned int>();
+    op.fresh = true;
+    auto kern = shard_half_kernel<VT, 2, kStg2, true>;
+    const size_t smem = op.smem_bytes();
+    loopcore::allow_max_dyn_smem((const void*)kern);
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3(h.P);
+    lc.blockDim = dim3(kThreadsBlocked);
+    lc.dynamicSmemBytes = smem;
+    lc.stream = ctx->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    shard::HalfArgs a = A;
+    void* args[] = {&a, &op};
+    SPK_CUDA(cudaLaunchKernelExC(&lc, (const void*)kern, args));
+  } else {
+    BlockedOp<VT, 1, kStg1> op{};
+    op.L[0] = B.R->h;
+    op.L[1] = B.C->h;
+    op.n = h.n_out;
+    op.acc_rows = acc_rows;
+    op.fault = B.fault.as<unsigned int>();
+    op.fresh = true;
+    auto kern = shard_half_kernel<VT, 1, kStg1, false>;
+    const size_t smem = op.smem_bytes();
+    loopcore::allow_max_dyn_smem((const void*)kern);
+    kern<<<h.P, kThreadsBlocked, smem, ctx->stream>>>(A, op);
+  }
+  ++ctx->launches;
+  SPK_CUDA(cudaGetLastError());
+}
+
+}  // namespace
+
+namespace shard {
+
+bool blocked_shard_build(spk_ctx* ctx, int64_t m_own, int64_t n_in, int64_t nnz_r, const DBuf& row_ptr,
+                         const DBuf& col_idx, const DBuf& vals, int64_t nnz_c, const DBuf& col_ptr,
+                         const DBuf& row_idx, const DBuf& vals_t, int vbytes, BlockedShard& out) {
+  const int W = std::min(kTileW, std::max(16, ctx->blocked_max_w));
+  for (int S = (ctx->blocked_split == 1 || !ctx->blocked_cluster ? 1 : 2); S >= 1; --S) {
+    if (S == 2 && ctx->num_sms < 2) continue;
+    const int P = (ctx->num_sms / S) * S;
+    auto R = std::make_unique<BlockedHost>(), C = std::make_unique<BlockedHost>();
+    if (!build_blocked(ctx, P, S, W, m_own, n_in, nnz_r, row_ptr, col_idx, vals, vbytes, *R) ||
+        !build_blocked(ctx, P, S, W, m_own, n_in, nnz_c, col_ptr, row_idx, vals_t, vbytes, *C))
+      continue;
+    const int acc_rows = std::max(R->max_rows, C->max_rows);
+    const size_t smem = S == 2 ? (vbytes == 4 ? BlockedOp<float, 2, kStg2, true>{{}, 0, acc_rows}.smem_bytes()
+                                              : BlockedOp<double, 2, kStg2, true>{{}, 0, acc_rows}.smem_bytes())
+                               : (vbytes == 4 ? BlockedOp<float, 1, kStg1>{{}, 0, acc_rows}.smem_bytes()
+                                              : BlockedOp<double, 1, kStg1>{{}, 0, acc_rows}.smem_bytes());
+    if (smem > kSmemBudget) continue;
+    out.R = std::move(R);
+    out.C = std::move(C);
+    out.vbytes = vbytes;
+    out.fault.alloc(sizeof(unsigned int) * 2);
+    SPK_CUDA(cudaMemsetAsync(out.fault.p, 0, out.fault.bytes, ctx->stream));
+    return true;
+  }
+  return false;
+}
+
+void blocked_shard_half(spk_ctx* ctx, const HalfArgs& A, BlockedShard& B) {
+  if (B.vbytes == 4) launch_shard_half<float>(ctx, A, B);
+  else launch_shard_half<double>(ctx, A, B);
+}
+
+}  // namespace shard
 
 bool run_blocked(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, double exponent, int policy, LoopState& st,
                  LoopOut& out) {

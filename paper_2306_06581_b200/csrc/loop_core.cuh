@@ -335,6 +335,19 @@ inline int simple_grid(spk_ctx* ctx, int64_t n) {
   return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)ctx->num_sms * 8));
 }
 
+// Opt a kernel into the largest dynamic shared memory the device allows
+// (not the launch's own size: contexts on other host threads launch the same
+// kernel with other sizes, and a smaller attribute set between another
+// thread's set and launch would fail that launch).
+inline void allow_max_dyn_smem(const void* kern) {
+  int dev = 0, optin = 0;
+  SPK_CUDA(cudaGetDevice(&dev));
+  SPK_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  cudaFuncAttributes fa{};
+  SPK_CUDA(cudaFuncGetAttributes(&fa, kern));
+  SPK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes));
+}
+
 // Cluster size an operator asks for (Op::kCluster, default 1).
 template <class Op, class = void>
 struct cluster_of {
@@ -398,7 +411,7 @@ void run_core(spk_ctx* ctx, const Op& op, int64_t n, LoopWs& W, long long masked
   const bool det = ctx->deterministic != 0;
   auto kern = det ? loop_kernel<LOG, true, Op> : loop_kernel<LOG, false, Op>;
   if (dyn_smem > 0)
-    SPK_CUDA(cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_smem));
+    allow_max_dyn_smem((const void*)kern);
   int per_sm = 0;
   SPK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, Op::kThreads, dyn_smem));
   if (per_sm < 1) fail_device("loop_kernel occupancy", cudaErrorLaunchOutOfResources);

@@ -29,116 +29,10 @@
 #include "ksrc.cuh"
 #include "loop_core.cuh"
 #include "rowdot.cuh"
+#include "shard_core.cuh"
 
 namespace spk {
 namespace shard {
-
-constexpr int kT = SPK_SHARD_TAIL;
-constexpr int kThreads = 512;
-constexpr unsigned long long kNone = ~0ull;
-
-struct State {
-  long long t;           // accepted iterations
-  long long iterations;  // reported count (includes a failing iteration)
-  int stopped, converged, diverged, error_kind, error_half, final_par;
-  long long error_index;
-  long long masked_rows, masked_cols;
-  long long masks_u_pending;
-  double err_u_pending;
-};
-
-struct HalfArgs {
-  int half;       // 0: rows (u from v), 1: columns (v from u)
-  int compute;    // 0 = decision only (finish)
-  long long t;    // iteration of this half
-  int64_t m_own;  // atoms in this rank's slab
-  int64_t base;   // global index of slab atom 0
-  int64_t m, stride;
-  int world;
-  long long n, max_iter;
-  double delta, exponent;
-  int policy;
-  const long long* ptr;
-  const uint32_t* idx;
-  const void* val;
-  const double* x;    // gathered input vector (previous half's output, tails inside)
-  const double* old;  // own block of the previous iterate of this side
-  double* out;        // own block of the new iterate (tail at out + m)
-  const double* w;    // own weights (a or b; log weights in the log domain)
-  unsigned char* ne;
-  int* dyn;
-  const State* st_in;
-  State* st_out;
-  loopcore::Part* part;
-  unsigned int* ticket;
-  unsigned long long* flag;
-};
-
-// The previous half's outcome, from the W tails of the gathered vector x
-// (scaling_loop's divergence / ZeroDenominator / mask / stop rules).
-template <bool LOG>
-__device__ void decide(const HalfArgs& A, State& S) {
-  if (S.stopped) return;
-  if (A.half == 0 && A.t == 1) return;  // nothing ran before iteration 1
-  int rstar = -1;
-  double err = 0.0, masks = 0.0, before = 0.0, fidx = 0.0;
-  for (int r = 0; r < A.world; ++r) {
-    const double* tail = A.x + (int64_t)r * A.stride + A.m;
-    if (rstar < 0 && tail[2] > 0.0) {
-      rstar = r;
-      fidx = tail[2] - 1.0;
-      before += tail[3];  // this rank's masks below its first failing atom
-    } else if (rstar < 0) {
-      before += tail[1];
-    }
-    err += tail[0];
-    masks += tail[1];
-  }
-  const long long tprev = A.half == 0 ? A.t - 1 : A.t;  // iteration of the half being judged
-  const int judged = A.half == 0 ? 1 : 0;               // which half produced x
-  if (rstar >= 0) {
-    S.stopped = 1;
-    S.iterations = tprev;
-    if (A.policy == SPK_POLICY_MASK && !LOG) {  // restore the previous iterate (:321-325, :352-356)
-      S.diverged = 1;
-      S.final_par = (int)((tprev - 1) & 1);
-      if (judged == 0) {
-        S.masked_rows += (long long)before;
-      } else {
-        S.masked_rows += S.masks_u_pending;
-        S.masked_cols += (long long)before;
-      }
-    } else {
-      S.error_kind = SPK_E_ZERO_DENOMINATOR;
-      S.error_half = judged;
-      S.error_index = (long long)fidx;
-    }
-    return;
-  }
-  if (judged == 0) {  // u-half of iteration t accepted; v-half runs next
-    S.masks_u_pending = (long long)masks;
-    S.err_u_pending = err;
-    return;
-  }
-  // both halves of iteration tprev accepted
-  S.masked_rows += S.masks_u_pending;
-  S.masked_cols += (long long)masks;
-  S.masks_u_pending = 0;
-  S.t = tprev;
-  S.iterations = tprev;
-  S.final_par = (int)(tprev & 1);
-  if (S.masked_rows == A.n || S.masked_cols == A.n) {  // solvers.hpp:357-358 / :465-466
-    S.stopped = 1;
-    S.error_kind = SPK_E_DEGENERATE_SKETCH_ERROR;
-    return;
-  }
-  if (tprev >= 2 && S.err_u_pending + err <= A.delta) {  // :360-364
-    S.stopped = 1;
-    S.converged = 1;
-    return;
-  }
-  if (tprev >= A.max_iter) S.stopped = 1;
-}
 
 template <bool LOG, class VT>
 __global__ void __launch_bounds__(kThreads) half_kernel(HalfArgs A) {
@@ -167,41 +61,7 @@ __global__ void __launch_bounds__(kThreads) half_kernel(HalfArgs A) {
       err += loopcore::finalize_atom<LOG>(i, tmp, __ldcg(A.old + i), __ldg(A.w + i), A.exponent, A.policy, (int)A.t,
                                           A.ne, A.dyn, A.out, A.flag, masks);
   }
-  loopcore::block_partial(err, masks, A.part);
-
-  // last CTA to finish reduces the partials in a fixed order and writes the tail
-  __shared__ bool last;
-  __threadfence();
-  if (threadIdx.x == 0) last = atomicAdd(A.ticket, 1u) == gridDim.x - 1;
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-  double e_tot;
-  long long m_tot;
-  loopcore::reduce_parts(A.part, gridDim.x, e_tot, m_tot);
-  const unsigned long long f = __ldcg(A.flag);
-  long long before = m_tot;
-  if (f != kNone) {  // only masks met before the first failing atom count (:306-307)
-    __shared__ long long cnt;
-    if (threadIdx.x == 0) cnt = 0;
-    __syncthreads();
-    long long c = 0;
-    for (int64_t i = threadIdx.x; i < (int64_t)f; i += blockDim.x) c += (__ldcg(A.dyn + i) == (int)A.t) ? 1 : 0;
-    c = warp_sum_ll(c);
-    if (lane == 0) atomicAdd(reinterpret_cast<unsigned long long*>(&cnt), (unsigned long long)c);
-    __syncthreads();
-    before = cnt;
-  }
-  if (threadIdx.x == 0) {
-    double* tail = A.out + A.m;
-    tail[0] = e_tot;
-    tail[1] = (double)m_tot;
-    tail[2] = f == kNone ? 0.0 : (double)(A.base + (int64_t)f) + 1.0;
-    tail[3] = (double)before;
-    for (int k = 4; k < kT; ++k) tail[k] = 0.0;
-    *A.ticket = 0u;
-    *A.flag = kNone;
-  }
+  finish_half(A, err, masks);
 }
 
 // j (global) -> position in the gathered layout
@@ -462,6 +322,8 @@ struct spk_shard {
   int64_t kernel_nnz = 0;
   int factorized = 0;
   spk::DBuf rd_row_m, rd_col_m, rd_row_c, rd_row_h, rd_flags, rd_out;
+  spk::shard::BlockedShard blk;  // slab x block layouts of both halves (fast linear loop)
+  bool blk_tried = false;
 };
 
 using namespace spk;
@@ -753,6 +615,21 @@ int spk_shard_begin(spk_shard* sh, const spk_solver_cfg* cfg, int uot, int polic
       sh->part.alloc(sizeof(loopcore::Part) * g);
       sh->part_cap = g;
     }
+    // fast path: slab x block layouts of the row and column slabs, indices
+    // already in the gathered layout (x of a half = W blocks of stride doubles)
+    const bool want_blk = !sh->log_domain && !ctx->deterministic && sh->m_own > 0 &&
+                          (ctx->use_blocked == 1 || (ctx->use_blocked == 2 && n >= (int64_t(1) << 17)));
+    if (want_blk && !sh->blk_tried) {
+      sh->blk_tried = true;
+      if (!shard::blocked_shard_build(ctx, sh->m_own, (int64_t)sh->world * sh->stride, sh->rows.nnz, sh->rows.row_ptr,
+                                      sh->rows.col_idx, sh->rows.values, sh->col_nnz, sh->col_ptr, sh->row_idx,
+                                      sh->vals_t, (int)sh->vbytes, sh->blk))
+        sh->blk.R.reset();
+    }
+    if (sh->blk.R && sh->blk.R->h.P > sh->part_cap) {
+      sh->part.alloc(sizeof(loopcore::Part) * sh->blk.R->h.P);
+      sh->part_cap = sh->blk.R->h.P;
+    }
     shard::state_init_kernel<<<1, 1, 0, ctx->stream>>>(sh->state.as<shard::State>(), empty_rows_total,
                                                        empty_cols_total);
     shard::reset_kernel<<<1, 1, 0, ctx->stream>>>(sh->ticket.as<unsigned int>(), sh->flag.as<unsigned long long>());
@@ -803,6 +680,13 @@ static int shard_step(spk_shard* sh, int half, int compute, int64_t t, const dou
     A.flag = sh->flag.as<unsigned long long>();
     const int grid = A.compute ? shard::grid_rows(ctx, sh->m_own) : 1;
     const bool f32 = sh->value_type == SPK_VALUES_F32;
+    const bool blk = A.compute && !sh->log_domain && sh->blk.R && !ctx->deterministic &&
+                     (ctx->use_blocked == 1 || (ctx->use_blocked == 2 && sh->n >= (int64_t(1) << 17)));
+    if (blk) {
+      shard::blocked_shard_half(ctx, A, sh->blk);
+      ++sh->calls;
+      return;
+    }
     if (sh->log_domain) {
       if (f32) launch_half<true, float>(sh, A, grid);
       else launch_half<true, double>(sh, A, grid);
@@ -833,6 +717,11 @@ int spk_shard_status(spk_shard* sh, spk_report* rep, int32_t* stopped, int32_t* 
     SPK_CUDA(cudaMemcpyAsync(&S, sh->state.as<shard::State>() + (sh->calls & 1), sizeof S, cudaMemcpyDeviceToHost,
                              sh->ctx->stream));
     SPK_CUDA(cudaStreamSynchronize(sh->ctx->stream));
+    if (sh->blk.R) {  // slab x block halves record a barrier timeout instead of hanging
+      unsigned int fw[2] = {0u, 0u};
+      download(sh->ctx, fw, sh->blk.fault, sizeof fw);
+      if (fw[0]) fail_device("sharded blocked half: a tile barrier timed out", cudaErrorLaunchTimeout);
+    }
     if (stopped) *stopped = S.stopped;
     if (final_parity) *final_parity = S.final_par;
     if (rep) {

@@ -156,7 +156,7 @@ class ThreadComm(Comm):
 class CudaShard:
     """spk_shard_* on one GPU; tensors are CUDA tensors on `device`."""
 
-    def __init__(self, device: int = 0):
+    def __init__(self, device: int = 0, options: dict | None = None):
         self.lib = L.load()
         self.device = torch.device("cuda", device)
         p = C.c_void_p()
@@ -165,6 +165,8 @@ class CudaShard:
             raise RuntimeError(f"spk_ctx_create(device={device}) failed with status {rc}")
         self.ctx = p
         self.sh = None
+        for k, v in (options or {}).items():  # spk_ctx_set_option keys (L.OPT_*)
+            _raise(self.ctx, self.lib.spk_ctx_set_option(self.ctx, int(k), int(v)))
 
     def close(self):
         if self.sh:
@@ -420,9 +422,10 @@ def spar_sink_sharded(comm: Comm, shard, kernel: Coords, a, b, cfg: SolverConfig
     return sk.solve(cfg, uot, check_every, on_loop)
 
 
-def run_emulated(world: int, fn, device: int = 0):
+def run_emulated(world: int, fn, device: int = 0, options: dict | None = None):
     """Run fn(comm, shard) for `world` emulated ranks (threads) on one GPU and
-    return the per-rank results (exceptions re-raised)."""
+    return the per-rank results (exceptions re-raised). `options` are context
+    options (L.OPT_* -> value) applied to every rank."""
     comms = ThreadComm.make(world)
     out: list = [None] * world
     err: list = [None] * world
@@ -432,7 +435,7 @@ def run_emulated(world: int, fn, device: int = 0):
         try:
             torch.cuda.set_device(device)
             with torch.cuda.stream(torch.cuda.Stream(device)):
-                shard = CudaShard(device)
+                shard = CudaShard(device, options)
                 out[r] = fn(comms[r], shard)
                 torch.cuda.current_stream(device).synchronize()
         except BaseException as e:  # noqa: BLE001 -- re-raised below

@@ -103,6 +103,41 @@ def test_sharded_ot_matches_single_gpu(ctx, world):
         np.testing.assert_array_equal(r.u, outs[0].u)
 
 
+@pytest.mark.parametrize("world,max_w", [(1, 256), (2, 256), (3, 64), (4, 4096)])
+def test_sharded_blocked_matches_single_gpu(ctx, world, max_w):
+    """The slab x block half-steps (CTA-pair clusters, TMA-staged tiles of the
+    gathered vector, tails skipped) on every rank, forced at a small n, against
+    the single-GPU solve."""
+    from paper_2306_06581_b200 import _lib as L
+
+    x, y, a, q = _c4_like()
+    kern = spk.Coords(x, y, scale=q, eps=0.05)
+    n = len(a)
+    cfg = spk.SolverConfig(0.05, math.inf, -1.0, 40)
+    s = 8 * n * math.log(n)
+    opts = spk.SparSinkOptions(values="f32")
+    ref = ctx.spar_sink(kern, a, a, cfg, s, 5, opts)
+    o = {L.OPT_BLOCKED_LOOP: 1, L.OPT_BLOCKED_MAX_W: max_w}
+    outs = S.run_emulated(world, lambda comm, shard: S.spar_sink_sharded(comm, shard, kern, a, a, cfg, s, 5, opts),
+                          options=o)
+    for r in outs:
+        np.testing.assert_allclose(r.u, ref.u, rtol=1e-9)
+        np.testing.assert_allclose(r.v, ref.v, rtol=1e-9)
+        assert r.report["iterations"] == ref.report["iterations"] == 40
+        assert r.report["objective"] == pytest.approx(ref.report["objective"], rel=1e-9)
+    # UOT with a convergence stop
+    b = a * 1.5
+    cfg = spk.SolverConfig(0.05, 1.0, 1e-9, 500)
+    ref = ctx.spar_sink(kern, a, b, cfg, s, 9, uot=True)
+    outs = S.run_emulated(world, lambda comm, shard: S.spar_sink_sharded(comm, shard, kern, a, b, cfg, s, 9, uot=True,
+                                                                           check_every=8), options=o)
+    for r in outs:
+        assert r.report["converged"] == ref.report["converged"] == 1
+        assert abs(r.report["iterations"] - ref.report["iterations"]) <= 1
+        np.testing.assert_allclose(r.u, ref.u, rtol=1e-6)
+        np.testing.assert_allclose(r.v, ref.v, rtol=1e-6)
+
+
 @pytest.mark.parametrize("stabilize", [False, True])
 def test_sharded_uot_converges_like_single_gpu(ctx, stabilize):
     x, y, a, q = _c4_like(2000, 13)
