@@ -435,6 +435,10 @@ struct BlockedOp {
         err += loopcore::finalize_atom<LOG>(i, tmp, oc, wc, exponent, policy, t, ne, dyn, out, flag, masks);
       }
     }
+    // one launch per half: the partner may still read this CTA's accumulators,
+    // and a CTA must not exit under a DSMEM reader (the persistent loop's grid
+    // barrier already orders this)
+    if (S == 2 && CL && fresh) cluster_sync();
     __syncthreads();
     if (tr && threadIdx.x == 0) tr[19] = globaltimer();
   }
