@@ -225,6 +225,15 @@ int spk_sketch_spmv(spk_sketch* sk, const double* x, double* y, int transpose);
 int spk_sketch_solve(spk_ctx* ctx, spk_sketch* sk, const double* a, const double* b,
                      const spk_solver_cfg* cfg, int uot, double* u, double* v, double* log_u,
                      double* log_v, spk_report* rep);
+/* sinkhorn_uot / sinkhorn_ot<SparseKernel> on `count` independent sketches
+ * (solvers.hpp:209-232; pairwise_wfr's per-pair solves, harness.cpp:349-406)
+ * with the weights given at build. Log domain (cfg->stabilize) sketches small
+ * enough for one CTA's shared memory run together, one CTA per sketch;
+ * otherwise one after another. reps: `count` reports (may be NULL). Results
+ * stay on each sketch for spk_sketch_readout. On failure the status is that
+ * of the lowest failing item and the message names it. */
+int spk_sketch_solve_batch(spk_ctx* ctx, spk_sketch* const* sketches, int count, const spk_solver_cfg* cfg,
+                           int uot, spk_report* reps);
 /* Plan readout of the LAST solve on this sketch: marginals (may be NULL)
  * and the OT/UOT objective with costs from kd (dense C or coordinates). */
 int spk_sketch_readout(spk_ctx* ctx, spk_sketch* sk, const spk_kernel_desc* kd, int uot,

@@ -93,6 +93,8 @@ SIGNATURES = {
     "spk_sketch_spmv": (C.c_int, [C.c_void_p, DP, DP, C.c_int]),
     "spk_sketch_solve": (C.c_int, [C.c_void_p, C.c_void_p, DP, DP, C.POINTER(SolverCfg), C.c_int, DP, DP, DP, DP,
                                    C.POINTER(Report)]),
+    "spk_sketch_solve_batch": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.c_int, C.POINTER(SolverCfg), C.c_int,
+                                         C.POINTER(Report)]),
     "spk_sketch_readout": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(KernelDesc), C.c_int, C.c_double,
                                      C.c_double, DP, DP, DP, C.POINTER(Report)]),
     "spk_plan_readout": (C.c_int, [C.c_void_p, C.POINTER(KernelDesc), C.c_int64, I64P, U32P, DP, DP, DP, DP, DP,

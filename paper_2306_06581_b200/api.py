@@ -345,6 +345,19 @@ class Sketch:
         return rm, cm, obj.value, rep.as_dict()
 
 
+def solve_batch(ctx: Context, sketches, cfg: SolverConfig, uot: bool = False, policy: str = "mask") -> list[dict]:
+    """sinkhorn_ot / sinkhorn_uot on many independent sketches at once
+    (spk_sketch_solve_batch: log-domain sketches that fit one CTA's shared
+    memory run one CTA each, in a single launch). Scalings stay on the
+    sketches (Sketch.readout). Returns the per-sketch reports."""
+    m = len(sketches)
+    ptrs = (C.c_void_p * max(m, 1))(*[sk.ptr for sk in sketches])
+    reps = (L.Report * max(m, 1))()
+    c = cfg.c(L.POLICY_MASK if policy == "mask" else L.POLICY_ERROR)
+    _raise(ctx.ptr, ctx.lib.spk_sketch_solve_batch(ctx.ptr, ptrs, m, C.byref(c), int(uot), reps))
+    return [reps[k].as_dict() for k in range(m)]
+
+
 _default: Context | None = None
 
 
@@ -396,16 +409,37 @@ def frame_pairs(frames: int) -> list[tuple[int, int]]:
 
 def spar_sink_pairs(ctx: Context, coords, masses, cfg: SolverConfig, s: float, seed: int, eta: float,
                     opts: SparSinkOptions | None = None, pairs=None, rank: int = 0, world: int = 1,
-                    scale: float = 1.0) -> list[tuple[int, tuple[int, int], dict]]:
+                    scale: float = 1.0, batched: bool = True,
+                    chunk: int = 512) -> list[tuple[int, tuple[int, int], dict]]:
     """Config 3's batch: spar_sink_uot with the WFR cost between frame pairs
     (pairwise_wfr, proj/src/harness.cpp:349-406). Pair k (in frame_pairs
     order) uses seed mix_seed(seed, k) as the reference does (:393). Pairs are
     independent: rank r of `world` takes pairs k = r, r + world, ... (no
-    communication). Returns (k, pair, report) for this rank's pairs."""
+    communication). batched (log domain): the rank's pairs are sketched, then
+    solved together by spk_sketch_solve_batch (chunks of `chunk` pairs).
+    Returns (k, pair, report) for this rank's pairs."""
     pairs = pairs if pairs is not None else frame_pairs(masses.shape[0])
     kern = Coords(coords, coords, "wfr", eta, scale=scale, eps=cfg.epsilon)
+    mine = list(range(rank, len(pairs), world))
+    if batched and cfg.stabilize and not (opts and opts.strict):
+        # every sketch first, then ONE batched loop (a CTA per pair), then the
+        # per-pair objectives: spar_sink_uot's steps (solvers.cpp:360-378)
+        out = []
+        for c0 in range(0, len(mine), chunk):
+            ks = mine[c0:c0 + chunk]
+            sks = [ctx.sketch(kern, masses[pairs[k][0]], masses[pairs[k][1]], "uot", cfg.lambda_, cfg.epsilon, s,
+                              mix_seed(seed, k), opts) for k in ks]
+            reps = solve_batch(ctx, sks, cfg, uot=True, policy="error" if (opts and opts.strict) else "mask")
+            for k, sk, rep in zip(ks, sks, reps):
+                _, _, obj, rr = sk.readout(kern, uot=True, lambda_=cfg.lambda_, epsilon=cfg.epsilon)
+                rep = dict(rep)
+                rep["objective"] = obj
+                rep["seed"] = mix_seed(seed, k)
+                out.append((k, pairs[k], rep))
+                sk.free()
+        return out
     out = []
-    for k in range(rank, len(pairs), world):
+    for k in mine:
         i, j = pairs[k]
         r = ctx.spar_sink(kern, masses[i], masses[j], cfg, s, mix_seed(seed, k), opts, uot=True)
         out.append((k, (i, j), r.report))

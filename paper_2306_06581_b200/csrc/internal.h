@@ -291,6 +291,12 @@ struct LoopState {
 void run_sparse_loop(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, double exponent,
                      int policy, LoopState& st, LoopOut& out);
 void ensure_coverage(spk_ctx* ctx, spk_sketch* sk);
+void ensure_log_values(spk_ctx* ctx, spk_sketch* sk);
+// batch.cu: one CTA per sketch, log domain, scalings in shared memory
+int64_t batch_max_n(spk_ctx* ctx);
+void run_batch_log(spk_ctx* ctx, spk_sketch* const* sks, int count, const spk_solver_cfg& cfg,
+                   const std::vector<double>& exponents, int policy, std::vector<LoopOut>& outs,
+                   std::vector<std::string>& errors, std::vector<int>& error_kinds);
 bool run_blocked(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, double exponent, int policy,
                  LoopState& st, LoopOut& out);
 void run_dense_loop(spk_ctx* ctx, DevKernel& dk, const spk_solver_cfg& cfg, double exponent,

@@ -57,30 +57,24 @@ __device__ __forceinline__ double row_apply(const VT* __restrict__ val, const ui
       }
       return dadd(mx, log(acc));
     }
-    // online (max, scaled sum) per lane, merged across the warp
-    double m = -CUDART_INF, s = 0.0;
+    // two passes (the reference's order of operations, solvers.cpp:99-111):
+    // the row max (no exp), then the sum of exp(t - max) -- one exp per
+    // entry; the warp merges are a plain max and a plain sum
+    double m = -CUDART_INF;
     for (long long p = b + lane; p < e; p += 32) {
       const double xv = __ldcg(x + __ldg(idx + p));
       if (xv == -CUDART_INF) continue;
-      const double t = log_of(ldg_val(val + p)) + xv;
-      if (t == -CUDART_INF) continue;  // a zero K~ (e.g. fp32 underflow) adds nothing
-      if (t > m) {
-        s = s * exp(m - t) + 1.0;
-        m = t;
-      } else {
-        s += exp(t - m);
-      }
+      m = fmax(m, log_of(ldg_val(val + p)) + xv);
     }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-      const double m2 = __shfl_xor_sync(0xffffffffu, m, o);
-      const double s2 = __shfl_xor_sync(0xffffffffu, s, o);
-      const double M = fmax(m, m2);
-      if (M != -CUDART_INF)
-        s = (m == -CUDART_INF ? 0.0 : s * exp(m - M)) + (m2 == -CUDART_INF ? 0.0 : s2 * exp(m2 - M));
-      m = M;
+    m = warp_max(m);
+    if (m == -CUDART_INF) return -CUDART_INF;
+    double s = 0.0;
+    for (long long p = b + lane; p < e; p += 32) {
+      const double xv = __ldcg(x + __ldg(idx + p));
+      if (xv == -CUDART_INF) continue;
+      s += exp(log_of(ldg_val(val + p)) + xv - m);  // a zero K~ (log -inf) adds exp(-inf) = 0
     }
-    return m == -CUDART_INF ? -CUDART_INF : m + log(s);
+    return m + log(warp_sum(s));
   }
 }
 

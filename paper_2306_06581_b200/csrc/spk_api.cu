@@ -496,6 +496,82 @@ int spk_sketch_solve(spk_ctx* ctx, spk_sketch* sk, const double* a, const double
   });
 }
 
+int spk_sketch_solve_batch(spk_ctx* ctx, spk_sketch* const* sks, int count, const spk_solver_cfg* cfg, int uot,
+                           spk_report* reps) {
+  if (!ctx || (count > 0 && !sks)) return SPK_STATUS_INPUT;
+  for (int k = 0; k < count; ++k) init_report(reps ? reps + k : nullptr);
+  return guard(ctx, [&] {
+    check_cfg(cfg);
+    if (count < 0) fail(SPK_E_LENGTH_MISMATCH, "negative batch size");
+    const int policy = cfg->empty_policy;
+    std::vector<double> f(count);
+    bool batched = cfg->stabilize && !ctx->deterministic;
+    const int64_t nmax = batch_max_n(ctx);
+    for (int k = 0; k < count; ++k) {
+      spk_sketch* sk = sks[k];
+      if (!sk) fail(SPK_E_LENGTH_MISMATCH, "null sketch in batch");
+      if (!sk->have_ab) fail(SPK_E_LENGTH_MISMATCH, "sketch has no marginals; pass a and b at build");
+      f[k] = solver_exponent(*cfg, uot, sk->a_total, sk->b_total);
+      if (sk->n > nmax || sk->n_cols) batched = false;
+    }
+    if (!batched) {  // one solve at a time (linear domain, parity mode, or large sketches)
+      for (int k = 0; k < count; ++k) solve_on_sketch(ctx, sks[k], *cfg, uot, policy, reps ? reps + k : nullptr);
+      return;
+    }
+    // structural coverage and the loop's entry checks (solvers.hpp:411-414)
+    for (int k = 0; k < count; ++k) {
+      spk_sketch* sk = sks[k];
+      ensure_coverage(ctx, sk);
+      if ((sk->cov_empty_rows || sk->cov_empty_cols) && policy == SPK_POLICY_ERROR)
+        fail(SPK_E_ZERO_DENOMINATOR, "batch item " + std::to_string(k) + ": kernel has empty rows or columns");
+      if (sk->cov_empty_rows == sk->n || sk->cov_empty_cols == sk->n)
+        fail(SPK_E_DEGENERATE_SKETCH_ERROR, "batch item " + std::to_string(k) + ": kernel has no entries at all");
+    }
+    std::vector<LoopOut> outs;
+    std::vector<std::string> errs;
+    std::vector<int> kinds;
+    run_batch_log(ctx, sks, count, *cfg, f, policy, outs, errs, kinds);
+    int first_bad = -1;
+    for (int k = 0; k < count; ++k) {
+      spk_sketch* sk = sks[k];
+      const LoopOut& lo = outs[k];
+      sk->last_valid = kinds[k] ? 0 : 1;
+      sk->last_log_domain = 1;
+      sk->masked_rows = lo.masked_rows;
+      sk->masked_cols = lo.masked_cols;
+      if (kinds[k]) {
+        if (first_bad < 0) first_bad = k;
+        continue;
+      }
+      ReadoutOut ro;  // residuals from the plan marginals (solvers.hpp:380-389)
+      Timer tr(ctx->stream);
+      sparse_readout(ctx, sk, nullptr, 1, sk->a.as<double>(), sk->b.as<double>(), false, uot, cfg->lambda,
+                     cfg->epsilon, nullptr, nullptr, ro);
+      const double t_read = tr.stop();
+      if (reps) {
+        spk_report* rep = reps + k;
+        rep->iterations = lo.iterations;
+        rep->converged = lo.converged;
+        rep->diverged = 0;
+        rep->masked_rows = lo.masked_rows;
+        rep->masked_cols = lo.masked_cols;
+        rep->residual_row = ro.residual_row;
+        rep->residual_col = ro.residual_col;
+        rep->kernel_mean = sk->kernel_mean;
+        rep->log_domain = 1;
+        rep->t_loop_s = lo.loop_s;
+        rep->t_readout_s = t_read;
+        rep->wall_time_s = lo.loop_s + t_read;
+        rep->sketch_nnz = sk->nnz;
+        rep->seed = sk->seed;
+        rep->kernel_nnz = sk->kernel_nnz;
+        rep->factorized_plan = sk->factorized_plan;
+      }
+    }
+    if (first_bad >= 0) fail(kinds[first_bad], "batch item " + std::to_string(first_bad) + ": " + errs[first_bad]);
+  });
+}
+
 int spk_sketch_readout(spk_ctx* ctx, spk_sketch* sk, const spk_kernel_desc* kd, int uot, double lambda,
                        double epsilon, double* row_marginal, double* col_marginal, double* objective,
                        spk_report* rep) {

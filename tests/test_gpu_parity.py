@@ -583,5 +583,5 @@ def test_config3_pairs_batch_split_across_ranks(ctx):
     kern = spk.Coords(coords, coords, "wfr", 0.1, scale=1.0, eps=0.01)
     for k, (i, j) in enumerate(pairs):
         one = ctx.spar_sink(kern, masses[i], masses[j], cfg, s, api.mix_seed(3, k), uot=True)
-        assert one.report["objective"] == got[k]["objective"]
+        assert one.report["objective"] == pytest.approx(got[k]["objective"], rel=1e-10)  # batched: other sum order
         assert one.report["sketch_nnz"] == got[k]["sketch_nnz"]
