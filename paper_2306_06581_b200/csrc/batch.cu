@@ -17,6 +17,7 @@
 #include <algorithm>
 #include <cmath>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "common.cuh"
@@ -85,6 +86,7 @@ __device__ __forceinline__ double group_sum(double v) {
   return v;
 }
 
+template <class VT>
 __device__ __forceinline__ double batch_half(int64_t n, const long long* __restrict__ ptr,
                                              const uint32_t* __restrict__ idx, const double* __restrict__ lval,
                                              const double* __restrict__ w, const double* x, double* out,
@@ -95,39 +97,40 @@ __device__ __forceinline__ double batch_half(int64_t n, const long long* __restr
   const int warp = threadIdx.x >> 5;
   const int nw = blockDim.x >> 5;
   constexpr int kRows = 32 / kG;
+  constexpr bool kOnline = std::is_same<VT, LogKf>::value;
   double err = 0.0;
+  // row bounds of the next row group loaded one group ahead
+  int64_t i = (int64_t)warp * kRows + (lane / kG);
+  long long bn = 0, en = 0;
+  if (i < n) {
+    bn = __ldg(ptr + i);
+    en = __ldg(ptr + i + 1);
+  }
   for (int64_t i0 = (int64_t)warp * kRows; i0 < n; i0 += (int64_t)nw * kRows) {
-    const int64_t i = i0 + (lane / kG);
+    i = i0 + (lane / kG);
     const bool live = i < n && ((ne[i >> 5] >> (i & 31)) & 1u);  // masked rows keep -inf
-    long long b = 0, e = 0;
-    if (live) {
-      b = __ldg(ptr + i);
-      e = __ldg(ptr + i + 1);
-    }
-    double m = -CUDART_INF;
-    long long p = b + gl;
-    for (; p + 3 * kG < e; p += 4 * kG) {
-      uint32_t j[4];
-      double l[4];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        j[k] = __ldg(idx + p + k * kG);
-        l[k] = __ldg(lval + p + k * kG);
-      }
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const double xv = x[j[k]];
-        if (xv != -CUDART_INF) m = fmax(m, l[k] + xv);
+    long long b = live ? bn : 0, e = live ? en : 0;
+    {
+      const int64_t inext = i + (int64_t)nw * kRows;
+      if (inext < n) {
+        bn = __ldg(ptr + inext);
+        en = __ldg(ptr + inext + 1);
       }
     }
-    for (; p < e; p += kG) {
-      const double xv = x[__ldg(idx + p)];
-      if (xv != -CUDART_INF) m = fmax(m, __ldg(lval + p) + xv);
-    }
-    m = group_max(m);
-    double s = 0.0;
-    if (m != -CUDART_INF) {
-      p = b + gl;
+    double m = -CUDART_INF, s = 0.0;
+    if (kOnline) {
+      // fp32 sketches: one pass, online (max, scaled sum) with the fp32-accurate
+      // exp (each term rescaled at most once per new max)
+      long long p = b + gl;
+      auto add = [&](double t) {
+        if (t == -CUDART_INF) return;
+        if (t > m) {
+          s = s * exp_fast(m - t) + 1.0;
+          m = t;
+        } else {
+          s += exp_fast(t - m);
+        }
+      };
       for (; p + 3 * kG < e; p += 4 * kG) {
         uint32_t j[4];
         double l[4];
@@ -139,15 +142,68 @@ __device__ __forceinline__ double batch_half(int64_t n, const long long* __restr
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           const double xv = x[j[k]];
-          if (xv != -CUDART_INF) s += exp(l[k] + xv - m);
+          if (xv != -CUDART_INF) add(l[k] + xv);
         }
       }
       for (; p < e; p += kG) {
         const double xv = x[__ldg(idx + p)];
-        if (xv != -CUDART_INF) s += exp(__ldg(lval + p) + xv - m);
+        if (xv != -CUDART_INF) add(__ldg(lval + p) + xv);
       }
+#pragma unroll
+      for (int o = kG / 2; o; o >>= 1) {
+        const double m2 = __shfl_xor_sync(0xffffffffu, m, o);
+        const double s2 = __shfl_xor_sync(0xffffffffu, s, o);
+        const double M = fmax(m, m2);
+        if (M != -CUDART_INF)
+          s = (m == -CUDART_INF ? 0.0 : s * exp_fast(m - M)) + (m2 == -CUDART_INF ? 0.0 : s2 * exp_fast(m2 - M));
+        m = M;
+      }
+    } else {
+      // fp64 sketches: two passes (max, then the sum of exp(t - max): the
+      // reference's order, solvers.cpp:99-111)
+      long long p = b + gl;
+      for (; p + 3 * kG < e; p += 4 * kG) {
+        uint32_t j[4];
+        double l[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          j[k] = __ldg(idx + p + k * kG);
+          l[k] = __ldg(lval + p + k * kG);
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const double xv = x[j[k]];
+          if (xv != -CUDART_INF) m = fmax(m, l[k] + xv);
+        }
+      }
+      for (; p < e; p += kG) {
+        const double xv = x[__ldg(idx + p)];
+        if (xv != -CUDART_INF) m = fmax(m, __ldg(lval + p) + xv);
+      }
+      m = group_max(m);
+      if (m != -CUDART_INF) {
+        p = b + gl;
+        for (; p + 3 * kG < e; p += 4 * kG) {
+          uint32_t j[4];
+          double l[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            j[k] = __ldg(idx + p + k * kG);
+            l[k] = __ldg(lval + p + k * kG);
+          }
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const double xv = x[j[k]];
+            if (xv != -CUDART_INF) s += exp(l[k] + xv - m);
+          }
+        }
+        for (; p < e; p += kG) {
+          const double xv = x[__ldg(idx + p)];
+          if (xv != -CUDART_INF) s += exp(__ldg(lval + p) + xv - m);
+        }
+      }
+      s = group_sum(s);
     }
-    s = group_sum(s);
     if (live && gl == 0) {
       const double lse = m == -CUDART_INF ? -CUDART_INF : m + log(s);
       if (lse == -CUDART_INF) {
@@ -180,6 +236,8 @@ __device__ __forceinline__ double cta_sum(double v, double* scratch) {
   return r;
 }
 
+// VT: LogK (fp64 exp) or LogKf (fp32 sketches: fp32-accurate exp), as the single-sketch path
+template <class VT>
 __global__ void __launch_bounds__(kBatchThreads, 1) batch_log_kernel(BatchArgs A) {
   extern __shared__ __align__(16) double smem[];
   const BatchItem& I = A.items[blockIdx.x];
@@ -223,7 +281,7 @@ __global__ void __launch_bounds__(kBatchThreads, 1) batch_log_kernel(BatchArgs A
     __syncthreads();
     // u-half: rows of K~ against lv (kernel_log_apply, solvers.cpp:96-116)
     const double eu = cta_sum(
-        batch_half(n, I.row_ptr, I.col_idx, I.lval, I.la, lv, lu, neu, I.exponent, A.policy, &masks_sh[0], &bad_sh[0]),
+        batch_half<VT>(n, I.row_ptr, I.col_idx, I.lval, I.la, lv, lu, neu, I.exponent, A.policy, &masks_sh[0], &bad_sh[0]),
         scratch);
     __syncthreads();
     if (bad_sh[0] != ~0ull) {
@@ -234,7 +292,7 @@ __global__ void __launch_bounds__(kBatchThreads, 1) batch_log_kernel(BatchArgs A
     }
     // v-half: columns against the NEW lu (Gauss-Seidel, :451-463)
     const double ev = cta_sum(
-        batch_half(n, I.col_ptr, I.row_idx, I.lval_t, I.lb, lu, lv, nev, I.exponent, A.policy, &masks_sh[1],
+        batch_half<VT>(n, I.col_ptr, I.row_idx, I.lval_t, I.lb, lu, lv, nev, I.exponent, A.policy, &masks_sh[1],
                    &bad_sh[1]),
         scratch);
     __syncthreads();
@@ -331,27 +389,41 @@ void run_batch_log(spk_ctx* ctx, spk_sketch* const* sks, int count, const spk_so
     I.masked_cols0 = sk->cov_empty_cols;
     I.exponent = exponents[k];
   }
-  DBuf d_items, d_status(sizeof(BatchStatus) * std::max(count, 1));
-  upload(ctx, d_items, items.data(), sizeof(BatchItem) * count);
-  SPK_CUDA(cudaMemsetAsync(d_status.p, 0, d_status.bytes, s));
+  std::vector<BatchStatus> status_host(count, BatchStatus{});
   BatchArgs A{};
-  A.items = d_items.as<BatchItem>();
-  A.status = d_status.as<BatchStatus>();
   A.max_iter = cfg.max_iter;
   A.delta = cfg.delta;
   A.policy = policy;
   A.npad = npad;
   const size_t smem = sizeof(double) * 2 * npad + sizeof(unsigned int) * 2 * (npad / 32);
-  loopcore::allow_max_dyn_smem((const void*)batch_log_kernel);
+  // fp32 sketches take the fp32-accurate exp (as spk_sketch_solve); a batch
+  // mixing storage types runs its fp64 ones with fp64 exp in a second launch
   Timer tm(s);
-  if (count > 0 && cfg.max_iter > 0) {
-    batch_log_kernel<<<count, kBatchThreads, smem, s>>>(A);
+  for (int f32 = 0; f32 < 2; ++f32) {
+    std::vector<int> sel;
+    for (int k = 0; k < count; ++k)
+      if ((sks[k]->value_type == SPK_VALUES_F32 && !ctx->deterministic) == (f32 == 1)) sel.push_back(k);
+    if (sel.empty() || cfg.max_iter <= 0) continue;
+    DBuf d_sel_items;
+    std::vector<BatchItem> part(sel.size());
+    for (size_t q = 0; q < sel.size(); ++q) part[q] = items[sel[q]];
+    upload(ctx, d_sel_items, part.data(), sizeof(BatchItem) * part.size());
+    BatchArgs B = A;
+    B.items = d_sel_items.as<BatchItem>();
+    DBuf d_part_status(sizeof(BatchStatus) * sel.size());
+    B.status = d_part_status.as<BatchStatus>();
+    auto kern = f32 ? batch_log_kernel<LogKf> : batch_log_kernel<LogK>;
+    loopcore::allow_max_dyn_smem((const void*)kern);
+    kern<<<(int)sel.size(), kBatchThreads, smem, s>>>(B);
     ++ctx->launches;
+    SPK_CUDA(cudaGetLastError());
+    std::vector<BatchStatus> ps(sel.size());
+    download(ctx, ps.data(), d_part_status, sizeof(BatchStatus) * sel.size());
+    for (size_t q = 0; q < sel.size(); ++q) status_host[sel[q]] = ps[q];
   }
   const double secs = tm.stop();
   SPK_CUDA(cudaGetLastError());
-  std::vector<BatchStatus> st(count);
-  download(ctx, st.data(), d_status, sizeof(BatchStatus) * count);
+  const std::vector<BatchStatus>& st = status_host;
   outs.assign(count, LoopOut{});
   errors.assign(count, std::string());
   error_kinds.assign(count, 0);

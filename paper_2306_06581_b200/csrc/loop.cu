@@ -106,9 +106,9 @@ void run_t(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, double expon
   op.col_idx = sk->col_idx.as<uint32_t>();
   op.col_ptr = sk->col_ptr.as<long long>();
   op.row_idx = sk->row_idx.as<uint32_t>();
-  if constexpr (std::is_same<VT, LogK>::value) {  // log K~ precomputed once per sketch
-    op.val = reinterpret_cast<const LogK*>(sk->log_values.p);
-    op.val_t = reinterpret_cast<const LogK*>(sk->log_values_t.p);
+  if constexpr (std::is_same<VT, LogK>::value || std::is_same<VT, LogKf>::value) {  // log K~ precomputed once
+    op.val = reinterpret_cast<const VT*>(sk->log_values.p);
+    op.val_t = reinterpret_cast<const VT*>(sk->log_values_t.p);
   } else {
     op.val = sk->values.as<VT>();
     op.val_t = sk->values_t.as<VT>();
@@ -216,7 +216,8 @@ void run_sparse_loop(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, do
     return;
   if (log_domain) {
     ensure_log_values(ctx, sk);
-    run_t<true, LogK>(ctx, sk, cfg, exponent, policy, st, out);
+    if (sk->value_type == SPK_VALUES_F32 && !ctx->deterministic) run_t<true, LogKf>(ctx, sk, cfg, exponent, policy, st, out);
+    else run_t<true, LogK>(ctx, sk, cfg, exponent, policy, st, out);
   } else if (sk->value_type == SPK_VALUES_F32) {
     run_t<false, float>(ctx, sk, cfg, exponent, policy, st, out);
   } else {

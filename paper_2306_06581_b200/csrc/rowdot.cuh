@@ -3,6 +3,8 @@
 // single-GPU loop (loop.cu) and the sharded half-steps (shard.cu).
 #pragma once
 
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace spk {
@@ -12,9 +14,29 @@ namespace spk {
 struct LogK {
   double v;
 };
+// The same, for a sketch stored in fp32: its log-sum-exp terms take an
+// fp32-accurate exp (MUFU.EX2, relative error ~2^-22, the order of the fp32
+// rounding of K~ itself; sums and logs stay fp64).
+struct LogKf {
+  double v;
+};
 __device__ __forceinline__ double log_of(double v) { return log(v); }
 __device__ __forceinline__ double log_of(float v) { return log((double)v); }
 __device__ __forceinline__ double log_of(LogK v) { return v.v; }
+__device__ __forceinline__ double log_of(LogKf v) { return v.v; }
+__device__ __forceinline__ LogKf ldg_val(const LogKf* p) { return LogKf{__ldg(&p->v)}; }
+
+// exp(d) for d <= 0 (a log-sum-exp term): fp64, or fp32-accurate for fp32 sketches
+__device__ __forceinline__ double exp_fast(double d) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"((float)(d * 1.4426950408889634)));
+  return (double)r;
+}
+template <class VT>
+__device__ __forceinline__ double exp_term(double d) {
+  if constexpr (std::is_same<VT, LogKf>::value) return exp_fast(d);
+  else return exp(d);
+}
 __device__ __forceinline__ double ldg_val(const double* p) { return __ldg(p); }
 __device__ __forceinline__ float ldg_val(const float* p) { return __ldg(p); }
 __device__ __forceinline__ LogK ldg_val(const LogK* p) { return LogK{__ldg(&p->v)}; }
@@ -72,7 +94,7 @@ __device__ __forceinline__ double row_apply(const VT* __restrict__ val, const ui
     for (long long p = b + lane; p < e; p += 32) {
       const double xv = __ldcg(x + __ldg(idx + p));
       if (xv == -CUDART_INF) continue;
-      s += exp(log_of(ldg_val(val + p)) + xv - m);  // a zero K~ (log -inf) adds exp(-inf) = 0
+      s += exp_term<VT>(log_of(ldg_val(val + p)) + xv - m);  // a zero K~ (log -inf) adds exp(-inf) = 0
     }
     return m + log(warp_sum(s));
   }
