@@ -30,6 +30,18 @@ struct Failure : std::runtime_error {
     if (e_ != cudaSuccess) ::spk::fail_device(#x, e_); \
   } while (0)
 
+// Stream that device buffers are allocated / freed on: the context stream of
+// the C ABI call in progress (set by guard() and the free functions).
+// Buffers come from the device's stream-ordered memory pool (kept, not
+// returned to the driver: repeated solves allocate nothing new), and every
+// use of a context's buffers is ordered on that same stream.
+extern thread_local cudaStream_t g_alloc_stream;
+struct AllocStreamScope {
+  cudaStream_t prev;
+  explicit AllocStreamScope(cudaStream_t s) : prev(g_alloc_stream) { g_alloc_stream = s; }
+  ~AllocStreamScope() { g_alloc_stream = prev; }
+};
+
 // Device buffer with RAII.
 struct DBuf {
   void* p = nullptr;
@@ -47,10 +59,14 @@ struct DBuf {
   void alloc(size_t b) {
     release();
     bytes = b;
-    if (b) SPK_CUDA(cudaMalloc(&p, b));
+    if (b) SPK_CUDA(cudaMallocAsync(&p, b, g_alloc_stream));
   }
   void ensure(size_t b) { if (b > bytes) alloc(b); }
-  void release() { if (p) cudaFree(p); p = nullptr; bytes = 0; }
+  void release() {
+    if (p) cudaFreeAsync(p, g_alloc_stream);
+    p = nullptr;
+    bytes = 0;
+  }
   template <class T> T* as() const { return static_cast<T*>(p); }
 };
 
@@ -180,6 +196,7 @@ double solver_exponent(const spk_solver_cfg& cfg, int uot, double a_total, doubl
 // context's last-error record.
 template <class F>
 int guard(spk_ctx* ctx, F&& f) {
+  AllocStreamScope scope(ctx ? ctx->stream : g_alloc_stream);
   try {
     if (ctx) SPK_CUDA(cudaSetDevice(ctx->device));
     (void)cudaGetLastError();  // drop stale non-sticky errors from other callers

@@ -429,7 +429,11 @@ int spk_shard_create(spk_ctx* ctx, const spk_kernel_desc* kd, const double* a, c
 void spk_shard_free(spk_shard* sh) {
   if (!sh) return;
   cudaSetDevice(sh->device);
-  delete sh;
+  cudaDeviceSynchronize();  // as spk_sketch_free: the buffers return to the pool once idle
+  {
+    AllocStreamScope scope(nullptr);
+    delete sh;
+  }
   (void)cudaGetLastError();
 }
 

@@ -184,6 +184,8 @@ double solver_exponent(const spk_solver_cfg& cfg, int uot, double a_total, doubl
                 std::string("CUDA error ") + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ") in " + what);
 }
 
+thread_local cudaStream_t g_alloc_stream = nullptr;
+
 void upload(spk_ctx* ctx, DBuf& dst, const void* src, size_t bytes) {
   dst.ensure(bytes ? bytes : 1);
   if (bytes) SPK_CUDA(cudaMemcpyAsync(dst.p, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
@@ -223,6 +225,12 @@ int spk_ctx_create(int device, spk_ctx** out) {
     if (!coop) fail_device("device lacks cooperative launch", cudaErrorNotSupported);
     SPK_CUDA(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));
     ctx->stream = ctx->own_stream;
+    // device buffers come from the stream-ordered pool; keep freed memory in
+    // it (a repeated solve then allocates nothing from the driver)
+    cudaMemPool_t pool;
+    SPK_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t keep = ~0ull;
+    SPK_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
   });
   if (rc != SPK_OK) {
     std::fprintf(stderr, "spk_ctx_create: %s\n", ctx->err_msg.c_str());
@@ -235,7 +243,11 @@ int spk_ctx_create(int device, spk_ctx** out) {
 void spk_ctx_destroy(spk_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
-  ctx->scratch.release();
+  {
+    AllocStreamScope scope(ctx->stream);
+    ctx->scratch.release();
+  }
+  cudaStreamSynchronize(ctx->stream);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   delete ctx;
 }
@@ -422,9 +434,14 @@ int spk_sketch_from_csr(spk_ctx* ctx, int64_t n, const int64_t* row_ptr, const u
 
 void spk_sketch_free(spk_sketch* sk) {
   if (!sk) return;
-  // the owning context may already be gone: only the device id is used
+  // the owning context (and its stream) may already be gone: only the device
+  // id is used; once the device is idle the buffers go back to the pool
   cudaSetDevice(sk->device);
-  delete sk;
+  cudaDeviceSynchronize();
+  {
+    AllocStreamScope scope(nullptr);
+    delete sk;
+  }
   (void)cudaGetLastError();
 }
 
