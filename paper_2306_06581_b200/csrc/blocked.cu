@@ -816,6 +816,12 @@ bool build_blocked(spk_ctx* ctx, int P, int S, int W, int64_t n_out, int64_t n_i
   SPK_CUDA(cudaStreamSynchronize(s));
   out.max_rows = max_rows;
   out.padded = p_acc;
+  out.cta_entries.assign(P, 0);
+  for (int c = 0; c < P; ++c)
+    for (int wv = 0; wv < kNW; ++wv) {
+      const size_t o = ((size_t)c * kNW + wv) * (Bh + 1);
+      out.cta_entries[c] += off[o + Bh] - off[o];
+    }
   out.h.P = P;
   out.h.S = S;
   out.h.B = B;
@@ -911,6 +917,30 @@ void launch_blocked(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, dou
           d3 += (double)(e[18] - (e[17] ? e[17] : e[16]));
           d4 += (double)(e[19] - e[18]);
           ++nc;
+        }
+        {  // stream time per CTA against its padded entries (and its slowest warp against the mean warp)
+          const std::vector<long long>& ce = role == 0 ? sk->blk_rows->cta_entries : sk->blk_cols->cta_entries;
+          double sx = 0, sy = 0, sxx = 0, syy = 0, sxy = 0, wspread = 0;
+          int cnt = 0;
+          for (int c = 0; c < P && c < (int)ce.size(); ++c) {
+            const unsigned long long* e = h.data() + (((size_t)it * 2 + role) * P + c) * 20;
+            if (!e[0]) continue;
+            unsigned long long se = 0, smn = ~0ull;
+            for (int w = 0; w < kNW; ++w)
+              if (e[1 + w]) {
+                se = std::max(se, e[1 + w]);
+                smn = std::min(smn, e[1 + w]);
+              }
+            const double x = (double)ce[c], y = (double)(se - e[0]);
+            sx += x; sy += y; sxx += x * x; syy += y * y; sxy += x * y;
+            wspread += (double)(se - smn);
+            ++cnt;
+          }
+          const double cov = sxy / cnt - sx / cnt * sy / cnt, vx = sxx / cnt - sx / cnt * sx / cnt,
+                       vy = syy / cnt - sy / cnt * sy / cnt;
+          std::fprintf(stderr, "[trace]   CTA stream time vs padded entries: corr %.3f, entries cv %.4f, time cv %.4f; "
+                       "warp spread in a CTA %.1f us\n", cov / std::sqrt(vx * vy + 1e-30), std::sqrt(vx) / (sx / cnt),
+                       std::sqrt(vy) / (sy / cnt), wspread / cnt * 1e-3);
         }
         std::fprintf(stderr, "[trace]   per CTA: release %.2f us, xchg %.2f us, pair wait %.2f us, finalize %.2f us\n",
                      d1 / nc * 1e-3, d2 / nc * 1e-3, d3 / nc * 1e-3, d4 / nc * 1e-3);

@@ -96,6 +96,7 @@ struct BlockedHost {
   DBuf slab_row0, off, packed, val;
   int max_rows = 0;
   int64_t padded = 0;  // entries after chunk padding
+  std::vector<long long> cta_entries;  // padded entries per CTA (load-balance diagnostics)
 };
 
 }  // namespace spk
