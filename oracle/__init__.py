@@ -394,6 +394,8 @@ class Reference:
         L.ref_time_scaling_iters.argtypes = [C.c_int64, I64P, U32P, DP, DP, DP, C.c_int64, DP, DP]
         L.ref_sparse_loop_timed.argtypes = [C.c_int64, I64P, U32P, DP, DP, DP, C.c_double, C.c_double, C.c_int64,
                                             C.c_int, DP, C.POINTER(ref_result)]
+        L.ref_sparse_loop_timed_stab.argtypes = [C.c_int64, I64P, U32P, DP, DP, DP, C.c_double, C.c_double,
+                                                 C.c_int64, C.c_int, C.c_int, DP, C.POINTER(ref_result)]
         L.ref_measure_from_image.argtypes = [DP, C.c_int64, C.c_int64, DP, DP]
         L.ref_mean_pool.argtypes = [DP, C.c_int64, C.c_int64, C.c_int64, C.c_int64, DP, I64P, I64P]
         L.ref_pairwise_wfr.argtypes = [DP, C.c_int64, C.c_int64, C.c_int64, C.c_double, C.c_double, C.c_double,
@@ -670,13 +672,14 @@ class Reference:
                                          C.byref(obj)))
         return rm, cm, obj.value
 
-    def sparse_loop_seconds(self, csr, a, b, eps, iters, lambda_=math.inf, uot=False):
-        """The reference's own sinkhorn_ot/uot<SparseKernel> for `iters` fixed iterations (delta=-1)."""
+    def sparse_loop_seconds(self, csr, a, b, eps, iters, lambda_=math.inf, uot=False, stabilize=False):
+        """The reference's own sinkhorn_ot/uot<SparseKernel> for `iters` fixed iterations (delta=-1),
+        linear or log domain (SolverConfig::stabilize)."""
         rp, ci, vv = self._csr(csr)
         n = len(rp) - 1
         secs = C.c_double()
         res = ref_result()
-        self._check(self.lib.ref_sparse_loop_timed(n, rp.ctypes.data_as(I64P), ci.ctypes.data_as(U32P),
-                                                   vv.ctypes.data_as(DP), _d(a), _d(b), eps, lambda_, iters,
-                                                   int(uot), C.byref(secs), C.byref(res)))
+        self._check(self.lib.ref_sparse_loop_timed_stab(n, rp.ctypes.data_as(I64P), ci.ctypes.data_as(U32P),
+                                                        vv.ctypes.data_as(DP), _d(a), _d(b), eps, lambda_, iters,
+                                                        int(uot), int(stabilize), C.byref(secs), C.byref(res)))
         return secs.value, res.as_dict()

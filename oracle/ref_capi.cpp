@@ -349,6 +349,21 @@ double ref_time_scaling_iters(int64_t n, const int64_t* rp, const uint32_t* ci,
 
 // sinkhorn_ot<SparseKernel> wall time for `iters` fixed iterations
 // (delta = -1 so the t>=2 stop never fires): the reference's own loop.
+int ref_sparse_loop_timed_stab(int64_t n, const int64_t* rp, const uint32_t* ci, const double* val,
+                               const double* a, const double* b, double eps, double lambda,
+                               int64_t iters, int uot, int stabilize, double* seconds, ref_result* res) {
+  return guard([&] {
+    auto sk = sketch(n, rp, ci, val);
+    auto da = measure(a, n), db = measure(b, n);
+    auto cfg = config(eps, lambda, -1.0, iters, stabilize);
+    const auto t0 = std::chrono::steady_clock::now();
+    SolveResult r = uot ? sinkhorn_uot(sk, da, db, cfg, EmptyPolicy::Mask)
+                        : sinkhorn_ot(sk, da, db, cfg, EmptyPolicy::Mask);
+    *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    fill(res, r);
+  });
+}
+
 int ref_sparse_loop_timed(int64_t n, const int64_t* rp, const uint32_t* ci, const double* val,
                           const double* a, const double* b, double eps, double lambda,
                           int64_t iters, int uot, double* seconds, ref_result* res) {
