@@ -520,7 +520,7 @@ __global__ void runlen_kernel(const uint32_t* keys_s, const uint32_t* rl, const 
 // holds a row twice; its entries then take those chunks in ascending order,
 // so the row is still summed in column order when the chunks run in order.
 //
-// Column spreading (slot_kernel, one thread per segment): the placement fixes,
+// Column spreading (slot_warp_kernel, one warp per segment): the placement fixes,
 // per row bank class, a set of list positions (hence (chunk, half-warp)
 // slots); any permutation of the class's entries over its own positions
 // keeps the row-bank spread. The x gather costs the worst column-bank
@@ -531,26 +531,38 @@ __global__ void runlen_kernel(const uint32_t* keys_s, const uint32_t* rl, const 
 // in distinct chunks). Simulated at config 4: 6.1 -> 3.8 gather wavefronts
 // per chunk, no extra padding. newpos[q] = chosen list position, or -1 where
 // a segment keeps the plain placement.
-__global__ void __launch_bounds__(64) slot_kernel(int64_t nkeys, const long long* useg,
-                                                  const unsigned long long* cnt, const long long* nchunk,
-                                                  const uint32_t* rl, const uint32_t* idx, const uint32_t* perm,
-                                                  int W, const uint32_t* start, const uint32_t* runlen,
-                                                  int* newpos) {
-  __shared__ unsigned long long cc[64][64];  // per thread: [chunk][half] -> 16 x 4-bit column-class counts
-  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+// Column bank class of each sorted entry (coalesced; read by slot_warp_kernel).
+__global__ void colclass_kernel(const uint32_t* perm, const uint32_t* idx, int W, int64_t m, unsigned char* cc) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < m; q += (int64_t)gridDim.x * blockDim.x)
+    cc[q] = (unsigned char)((idx[perm[q]] % (uint32_t)W) & 15u);
+}
+
+// The free positions of a class are scored by the lanes in parallel (cost =
+// the column class's count in that position's half-warp, ties to the lowest
+// position): one warp argmin per entry.
+constexpr int kSlotWarps = 8;
+__global__ void __launch_bounds__(32 * kSlotWarps) slot_warp_kernel(
+    int64_t nkeys, const long long* useg, const unsigned long long* cnt, const long long* nchunk, const uint32_t* rl,
+    const unsigned char* colc, const uint32_t* start, const uint32_t* runlen, int* newpos) {
+  __shared__ unsigned char counts[kSlotWarps][32 * 2 * 16];  // [chunk][half][column class]
+  __shared__ int cls_n[kSlotWarps][17];
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  const int64_t k = (int64_t)blockIdx.x * kSlotWarps + wl;
   if (k >= nkeys) return;
   const int E = (int)cnt[k];
   const int C = (int)nchunk[k];
   if (E == 0 || C > 32) return;
   const long long u0 = useg[k];
-  unsigned long long* my = cc[threadIdx.x];
-  for (int i = 0; i < 2 * C; ++i) my[i] = 0ull;
+  unsigned char* ct = counts[wl];
+  for (int i = lane; i < C * 32; i += 32) ct[i] = 0;
+  if (lane < 17) cls_n[wl][lane] = 0;
+  __syncwarp();
+  for (int e = lane; e < E; e += 32) atomicAdd(&cls_n[wl][rl[u0 + e] & 15u], 1);
+  __syncwarp();
   bool ok = true;
-  int p = 0;
-  for (int cls = 0; cls < 16 && ok; ++cls) {
-    const int ps = p;
-    while (p < E && (int)(rl[u0 + p] & 15u) == cls) ++p;
-    const int nk = p - ps;
+  int ps = 0;
+  for (int c = 0; c < 16 && ok; ++c) {
+    const int nk = cls_n[wl][c];
     if (nk == 0) continue;
     if (nk > 64) {
       ok = false;
@@ -563,42 +575,47 @@ __global__ void __launch_bounds__(64) slot_kernel(int64_t nkeys, const long long
         const long long rs = start[q];
         const int rn = (int)runlen[rs];
         if ((rn > 1) != (pass == 0)) continue;
-        const int cc4 = 4 * (int)((idx[perm[q]] % (uint32_t)W) & 15u);
-        int best = -1, bc = 1 << 30;
-        for (unsigned long long fm = freem; fm; fm &= fm - 1) {
-          const int f = __ffsll((long long)fm) - 1;
-          const int pos = ps + f;
-          const int ch = pos % C, hf = (pos / C) & 1;
-          bool clash = false;
-          for (int j = 0; j < rn && rn > 1; ++j) {
-            const int np = newpos[rs + j];
-            if (rs + j != q && np >= 0 && np % C == ch) {
-              clash = true;
-              break;
+        const int cc = colc[q];
+        unsigned int key = 0xffffffffu;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int f = lane + 32 * h;
+          if (f < nk && ((freem >> f) & 1ull)) {
+            const int pos = ps + f;
+            const int ch = pos % C, hf = (pos / C) & 1;
+            bool clash = false;
+            for (int j = 0; j < rn && rn > 1; ++j) {
+              const int np = newpos[rs + j];
+              if (rs + j != q && np >= 0 && np % C == ch) {
+                clash = true;
+                break;
+              }
             }
-          }
-          if (clash) continue;
-          const int c = (int)((my[2 * ch + hf] >> cc4) & 15ull);
-          if (c < bc) {
-            bc = c;
-            best = f;
-            if (c == 0) break;
+            if (!clash) key = min(key, ((unsigned int)ct[(ch * 2 + hf) * 16 + cc] << 8) | (unsigned int)f);
           }
         }
-        if (best < 0) {
+#pragma unroll
+        for (int o2 = 16; o2; o2 >>= 1) key = min(key, __shfl_xor_sync(0xffffffffu, key, o2));
+        if (key == 0xffffffffu) {
           ok = false;
           break;
         }
-        const int pos = ps + best;
-        newpos[q] = pos;
-        freem &= ~(1ull << best);
+        const int f = (int)(key & 255u);
+        const int pos = ps + f;
         const int ch = pos % C, hf = (pos / C) & 1;
-        if (((my[2 * ch + hf] >> cc4) & 15ull) < 15ull) my[2 * ch + hf] += 1ull << cc4;
+        if (lane == 0) {
+          newpos[q] = pos;
+          unsigned char& v = ct[(ch * 2 + hf) * 16 + cc];
+          if (v < 255) ++v;
+        }
+        freem &= ~(1ull << f);
+        __syncwarp();
       }
     }
+    ps += nk;
   }
   if (!ok)
-    for (int e = 0; e < E; ++e) newpos[u0 + e] = -1;
+    for (int e = lane; e < E; e += 32) newpos[u0 + e] = -1;
 }
 
 template <class VT>
@@ -653,6 +670,13 @@ int grid_cap(spk_ctx* ctx, int64_t items) {
 // Returns false when the shape does not fit (rows per slab >= 2^16).
 bool build_blocked(spk_ctx* ctx, int P, int S, int W, int64_t n_out, int64_t n_in, int64_t m, const DBuf& ptr_d,
                    const DBuf& idx_d, const DBuf& val_d, int vbytes, BlockedHost& out) {
+  static const bool dbg = std::getenv("SPK_DEBUG_TIMING") != nullptr;
+  std::unique_ptr<Timer> tph(dbg ? new Timer(ctx->stream) : nullptr);
+  auto phase = [&](const char* what) {
+    if (!tph) return;
+    std::fprintf(stderr, "[timing]   build_blocked %s %.4f s\n", what, tph->stop());
+    tph.reset(new Timer(ctx->stream));
+  };
   const int Q = P / S;
   std::vector<long long> ptr(n_out + 1);
   download(ctx, ptr.data(), ptr_d, sizeof(long long) * (n_out + 1));
@@ -721,6 +745,7 @@ bool build_blocked(spk_ctx* ctx, int P, int S, int W, int64_t n_out, int64_t n_i
       perm(sizeof(uint32_t) * mm), hist(sizeof(unsigned long long) * nkeys),
       key64(sizeof(unsigned long long) * mm), key64_s(sizeof(unsigned long long) * mm);
   SPK_CUDA(cudaMemsetAsync(hist.p, 0, hist.bytes, s));
+  phase("host cuts");
   key_kernel<<<grid_cap(ctx, n_out * 32), 256, 0, s>>>(ptr_d.as<long long>(), idx_d.as<uint32_t>(), n_out,
                                                         d_slab_of.as<int>(), d_warp_of.as<unsigned char>(),
                                                         d_s0r.as<int>(), W, S, Bh, keys.as<uint32_t>(),
@@ -754,6 +779,7 @@ bool build_blocked(spk_ctx* ctx, int P, int S, int W, int64_t n_out, int64_t n_i
   ctx->scratch.ensure(tb);
   SPK_CUDA(cub::DeviceScan::InclusiveScan(ctx->scratch.p, tb, start.as<uint32_t>(), start.as<uint32_t>(), cub::Max(),
                                           (int)m, s));
+  phase("keys + sort");
   runlen_kernel<<<grid_cap(ctx, m), 256, 0, s>>>(keys_s.as<uint32_t>(), rl.as<uint32_t>(), start.as<uint32_t>(), m,
                                                  runlen.as<uint32_t>(), maxrun.as<unsigned int>());
   ctx->launches += 2;
@@ -795,11 +821,16 @@ bool build_blocked(spk_ctx* ctx, int P, int S, int W, int64_t n_out, int64_t n_i
   if (m > 0) {
     DBuf newpos(sizeof(int) * mm);
     SPK_CUDA(cudaMemsetAsync(newpos.p, 0xff, newpos.bytes, s));
-    if (ctx->blocked_spread)
-      slot_kernel<<<(int)((nkeys + 63) / 64), 64, 0, s>>>(nkeys, d_useg.as<long long>(), hist.as<unsigned long long>(),
-                                                        d_nch.as<long long>(), rl.as<uint32_t>(), idx_d.as<uint32_t>(),
-                                                        perm.as<uint32_t>(), W, start.as<uint32_t>(),
-                                                        runlen.as<uint32_t>(), newpos.as<int>());
+    phase("runs + host offsets");
+    if (ctx->blocked_spread) {
+      DBuf colc(mm);
+      colclass_kernel<<<grid_cap(ctx, m), 256, 0, s>>>(perm.as<uint32_t>(), idx_d.as<uint32_t>(), W, m,
+                                                       colc.as<unsigned char>());
+      slot_warp_kernel<<<(int)((nkeys + kSlotWarps - 1) / kSlotWarps), 32 * kSlotWarps, 0, s>>>(
+          nkeys, d_useg.as<long long>(), hist.as<unsigned long long>(), d_nch.as<long long>(), rl.as<uint32_t>(),
+          colc.as<unsigned char>(), start.as<uint32_t>(), runlen.as<uint32_t>(), newpos.as<int>());
+      ++ctx->launches;
+    }
     if (vbytes == 4)
       place_kernel<float><<<grid_cap(ctx, m), 256, 0, s>>>(
           keys_s.as<uint32_t>(), perm.as<uint32_t>(), rl.as<uint32_t>(), start.as<uint32_t>(), runlen.as<uint32_t>(),
@@ -814,6 +845,7 @@ bool build_blocked(spk_ctx* ctx, int P, int S, int W, int64_t n_out, int64_t n_i
   }
   SPK_CUDA(cudaGetLastError());
   SPK_CUDA(cudaStreamSynchronize(s));
+  phase("spread + place");
   out.max_rows = max_rows;
   out.padded = p_acc;
   out.cta_entries.assign(P, 0);
@@ -1001,6 +1033,8 @@ bool run_blocked_t(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, doub
     const int W = std::min(kTileW, std::max(16, ctx->blocked_max_w));
     // S = 2 when the pair split fits (even SM count, slab accumulators in
     // shared memory); else one CTA per slab
+    static const bool dbg = std::getenv("SPK_DEBUG_TIMING") != nullptr;
+    Timer tb(ctx->stream);
     for (int S = (ctx->blocked_split == 1 ? 1 : 2); S >= 1; --S) {
       if (S == 2 && ctx->num_sms < 2) continue;
       const int P = (ctx->num_sms / S) * S;
@@ -1021,6 +1055,7 @@ bool run_blocked_t(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, doub
       }
       if (ctx->blocked_split == 2) break;
     }
+    if (dbg) std::fprintf(stderr, "[timing] blocked layouts %.4f s\n", tb.stop());
   }
   if (!sk->blk_rows) return false;
   if (sk->blk_rows->h.S == 2 && cluster_pairs_fit<VT>(ctx, sk))
