@@ -116,6 +116,39 @@ def test_sampler_unbiased_monte_carlo(ctx, oracle):
     assert np.sum(np.abs(mean - K) <= 3 * se + 1e-15) >= 61
 
 
+def test_tiled_sampler_inclusion_frequencies(ctx, oracle):
+    """inclusion frequencies of the coordinate (tiled) sampler are
+    consistent with p*_ij = min(1, s p_ij) for the factorized OT plan
+    p_ij = ra_i cb_j (ra = sqrt(a) / sum sqrt(a), sparsify.cpp:71-91): 3000
+    seeds, every entry's frequency within 4 standard errors (a 4-sigma miss
+    has probability 6e-5 per entry), and the mean sketch size within 4 se of
+    sum p*."""
+    n, s, reps = 16, 60.0, 3000
+    x = oracle.rng_doubles(23, 0, 2 * n).reshape(n, 2)
+    y = oracle.rng_doubles(23, 1, 2 * n).reshape(n, 2)
+    w = 0.1 + oracle.rng_doubles(23, 2, 2 * n)
+    a, b = w[:n] / w[:n].sum(), w[n:] / w[n:].sum()
+    kern = spk.Coords(x, y, "sqeuclid", scale=1.0, eps=1.0)  # K > 0 everywhere: factorized plan
+    counts = np.zeros((n, n))
+    sizes = np.zeros(reps)
+    for rep in range(reps):
+        sk = ctx.sketch(kern, a, b, "ot", math.inf, 1.0, s, 5000 + rep)
+        assert sk.factorized_plan
+        rp, ci, _ = sk.csr()
+        rows = np.repeat(np.arange(n), np.diff(rp))
+        np.add.at(counts, (rows, ci.astype(np.int64)), 1.0)
+        sizes[rep] = len(ci)
+        sk.free()
+    ra = np.sqrt(a) / np.sqrt(a).sum()
+    cb = np.sqrt(b) / np.sqrt(b).sum()
+    pstar = np.minimum(1.0, s * np.outer(ra, cb))
+    freq = counts / reps
+    se = np.sqrt(pstar * (1 - pstar) / reps)
+    assert np.all(np.abs(freq - pstar) <= 4 * se + 1e-12)
+    tot_se = np.sqrt(np.sum(pstar * (1 - pstar)) / reps)
+    assert abs(sizes.mean() - pstar.sum()) <= 4 * tot_se
+
+
 def test_sampler_errors(ctx, oracle):
     n = 10
     x = oracle.rng_doubles(1, 0, 2 * n).reshape(n, 2)
