@@ -465,6 +465,40 @@ __device__ __forceinline__ uint32_t row_threshold(const TiledArgs& A, double rw)
   return t >= 4294967295.0 ? 0xffffffffu : (uint32_t)t;
 }
 
+// Upper bound of K^g_k (UOT plan exponent) at squared distance >= d2lo, in
+// fp32 with a 1e-4 relative slack (>> fp32 cos/log/exp error): K^g is
+// decreasing in the distance, so the bound is evaluated at d2lo.
+__device__ __forceinline__ double kg_upper(const TiledArgs& A, float d2lo) {
+  const double gk = A.P.g_k;
+  if (!(d2lo > 0.f) || gk <= 0.0) return 1.0;
+  const float coef = (float)(gk / (A.scale * A.eps)) * (1.f - 1e-6f);  // rounded down
+  float e;  // log2 of the bound
+  if (A.kind == 0) {
+    e = -coef * 1.44269504f * d2lo;
+  } else if (A.kind == 1) {
+    e = -coef * 1.44269504f * sqrtf(d2lo);
+  } else {
+    const float arg = sqrtf(d2lo) / (float)(2.0 * A.eta) * (1.f - 1e-6f);
+    if (!(arg < 1.5707f)) return 1.0;  // at the support edge: no tightening
+    const float c = cosf(arg);
+    e = coef * log2f(c * c);
+  }
+  return (double)exp2f(e) * (1.0 + 1e-4);
+}
+
+// Draw-screen threshold of one UOT entry: p* <= s (pa_i pb_j K^g_k) inv, with
+// K^g_k bounded above (theta mixing as SamplingPlan::prob).
+__device__ __forceinline__ uint32_t entry_threshold(const TiledArgs& A, double rw, double cw, float d2lo) {
+  const DPlan& P = A.P;
+  if (P.kind != SPK_PLAN_UOT) return 0xffffffffu;
+  double b = rw * cw * kg_upper(A, d2lo) * P.inv;
+  if (P.theta_mode) b = P.omt * b + P.unif;
+  const double Pi = A.s * b * (1.0 + 0x1p-30);
+  if (!(Pi < 1.0)) return 0xffffffffu;
+  const double t = floor(Pi * 4294967296.0) + 1.0;
+  return t >= 4294967295.0 ? 0xffffffffu : (uint32_t)t;
+}
+
 template <int DIM, bool SAMPLE, bool NEEDK, class VT>
 __global__ void __launch_bounds__(256, 3) tiled_kernel(TiledArgs A) {
   __shared__ float yfs[DIM][kTileJ];  // the screen's fp32 columns (exact paths read y from L2)
@@ -683,7 +717,15 @@ __global__ void __launch_bounds__(256, 3) tiled_kernel(TiledArgs A) {
           double ps = 0.0;
           if (nz) {
             const uint64_t x0 = st0[q] + (uint64_t)t * kGolden;
-            if (sm_finalize_hi(x0) <= th[q]) {  // may be kept: exact draw, K and p*
+            // UOT: the row bound assumes K^g_k <= 1 and the largest column
+            // factor; this entry's own bound (its pb_j, K^g_k at a lower
+            // bound of its distance) rejects most far entries before the
+            // fp64 cost / exp / pow of the exact path
+            // (no screen ran on an all-supported tile: its staged y, and so
+            // ymg, may be stale -- no distance bound there)
+            const float d2lo = tile_all ? 0.f : fmaxf(d2s[q] - (xmg[q] + ymg), 0.f);
+            const uint32_t th_e = NEEDK ? min(th[q], entry_threshold(A, rw[q], cw, d2lo)) : th[q];
+            if (sm_finalize_hi(x0) <= th_e) {  // may be kept: exact draw, K and p*
               if (kv < 0.0) kv = exact_k(A, exact_d2<DIM>(xp, A.y + j * DIM));
               ps = min1(dmul(A.s, plan_prob_w(A.P, rw[q], cw, kv)));
               if (ps > 0.0) keep = ps >= 1.0 || u64_to_unit(sm_finalize(x0)) < ps;
