@@ -465,6 +465,19 @@ __device__ __forceinline__ uint32_t row_threshold(const TiledArgs& A, double rw)
   return t >= 4294967295.0 ? 0xffffffffu : (uint32_t)t;
 }
 
+// The exact decision of one screened entry (sparsify.cpp:188-197): K from the
+// reference-order fp64 distance when not known yet, p* = min(1, s prob), keep
+// iff the full draw falls below p*. Out of line: taken by a small fraction of
+// entries, and inlined four times (one per row) it overflows the instruction
+// cache (ncu: "no instruction" stalls dominated the UOT sample pass).
+template <int DIM>
+__device__ __noinline__ bool exact_keep(const TiledArgs& A, const double* xp, int64_t j, double rw, double cw,
+                                        uint64_t x0, double& kv, double& ps) {
+  if (kv < 0.0) kv = exact_k(A, exact_d2<DIM>(xp, A.y + j * DIM));
+  ps = min1(dmul(A.s, plan_prob_w(A.P, rw, cw, kv)));
+  return ps > 0.0 && (ps >= 1.0 || u64_to_unit(sm_finalize(x0)) < ps);
+}
+
 // Upper bound of K^g_k (UOT plan exponent) at squared distance >= d2lo, in
 // fp32 with a 1e-4 relative slack (>> fp32 cos/log/exp error): K^g is
 // decreasing in the distance, so the bound is evaluated at d2lo.
@@ -480,8 +493,11 @@ __device__ __forceinline__ double kg_upper(const TiledArgs& A, float d2lo) {
   } else {
     const float arg = sqrtf(d2lo) / (float)(2.0 * A.eta) * (1.f - 1e-6f);
     if (!(arg < 1.5707f)) return 1.0;  // at the support edge: no tightening
-    const float c = cosf(arg);
-    e = coef * log2f(c * c);
+    // MUFU cos / lg2 / ex2: absolute error of __cosf ~4e-7 on [0, pi/2], so
+    // the bound keeps its 1e-4 slack only where cos >= 0.01
+    const float c = __cosf(arg);
+    if (!(c >= 0.01f)) return 1.0;
+    e = coef * __log2f(c * c);
   }
   return (double)exp2f(e) * (1.0 + 1e-4);
 }
@@ -725,11 +741,8 @@ __global__ void __launch_bounds__(256, 3) tiled_kernel(TiledArgs A) {
             // ymg, may be stale -- no distance bound there)
             const float d2lo = tile_all ? 0.f : fmaxf(d2s[q] - (xmg[q] + ymg), 0.f);
             const uint32_t th_e = NEEDK ? min(th[q], entry_threshold(A, rw[q], cw, d2lo)) : th[q];
-            if (sm_finalize_hi(x0) <= th_e) {  // may be kept: exact draw, K and p*
-              if (kv < 0.0) kv = exact_k(A, exact_d2<DIM>(xp, A.y + j * DIM));
-              ps = min1(dmul(A.s, plan_prob_w(A.P, rw[q], cw, kv)));
-              if (ps > 0.0) keep = ps >= 1.0 || u64_to_unit(sm_finalize(x0)) < ps;
-            }
+            if (sm_finalize_hi(x0) <= th_e)  // may be kept: exact draw, K and p* (out of line)
+              keep = exact_keep<DIM>(A, xp, j, rw[q], cw, x0, kv, ps);
           }
           const unsigned km = __ballot_sync(0xffffffffu, keep);
           if (keep) {
