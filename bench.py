@@ -470,8 +470,8 @@ def run_c3_batch(args, ws, rank, local):
     stream = torch.cuda.current_stream()
     ctx.set_stream(stream.cuda_stream)
     t0 = time.perf_counter()
-    sks = [ctx.sketch(kern, masses[pairs[k][0]], masses[pairs[k][1]], "uot", 1.0, 0.01, s, api.mix_seed(3, k), opts)
-           for k in mine]
+    sks = ctx.sketch_batch(kern, masses[[pairs[k][0] for k in mine]], masses[[pairs[k][1] for k in mine]], "uot",
+                           1.0, 0.01, s, [api.mix_seed(3, k) for k in mine], opts)
     torch.cuda.synchronize()
     setup_s = time.perf_counter() - t0
     for _ in range(args.warmup):

@@ -204,6 +204,13 @@ int spk_sinkhorn(spk_ctx* ctx, const spk_kernel_desc* kd, const double* a, const
 int spk_sketch_build(spk_ctx* ctx, const spk_kernel_desc* kd, const double* a, const double* b,
                      int plan_kind, double lambda, double epsilon, double s, uint64_t seed,
                      const spk_sketch_opts* opts, spk_sketch** out);
+/* spk_sketch_build for `count` measure pairs on ONE kernel (pairwise_wfr's
+ * frame pairs, harness.cpp:349-406): a and b are count x n row-major, seeds
+ * count values; the kernel's coordinates, screen copies and support
+ * threshold are prepared once. out: count sketches (all or none on error). */
+int spk_sketch_build_batch(spk_ctx* ctx, const spk_kernel_desc* kd, int count, const double* a, const double* b,
+                           int plan_kind, double lambda, double epsilon, double s, const uint64_t* seeds,
+                           const spk_sketch_opts* opts, spk_sketch** out);
 /* Upload a host CSR (SparseKernel layout, sparsify.hpp:57-71). */
 int spk_sketch_from_csr(spk_ctx* ctx, int64_t n, const int64_t* row_ptr, const uint32_t* col_idx,
                         const double* values, int value_type, spk_sketch** out);

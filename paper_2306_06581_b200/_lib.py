@@ -84,6 +84,9 @@ SIGNATURES = {
                                DP, DP, C.POINTER(Report)]),
     "spk_sketch_build": (C.c_int, [C.c_void_p, C.POINTER(KernelDesc), DP, DP, C.c_int, C.c_double, C.c_double,
                                    C.c_double, C.c_uint64, C.POINTER(SketchOpts), C.POINTER(C.c_void_p)]),
+    "spk_sketch_build_batch": (C.c_int, [C.c_void_p, C.POINTER(KernelDesc), C.c_int, DP, DP, C.c_int, C.c_double,
+                                         C.c_double, C.c_double, C.POINTER(C.c_uint64), C.POINTER(SketchOpts),
+                                         C.POINTER(C.c_void_p)]),
     "spk_sketch_from_csr": (C.c_int, [C.c_void_p, C.c_int64, I64P, U32P, DP, C.c_int, C.POINTER(C.c_void_p)]),
     "spk_sketch_free": (None, [C.c_void_p]),
     "spk_sketch_info": (C.c_int, [C.c_void_p, I64P, I64P, I64P, C.POINTER(C.c_int32), DP]),

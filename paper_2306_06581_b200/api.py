@@ -224,6 +224,23 @@ class Context:
         _raise(self.ptr, rc)
         return Sketch(self, p)
 
+    def sketch_batch(self, kernel, A, B, plan: str, lambda_: float, epsilon: float, s: float, seeds,
+                     opts: SparSinkOptions | None = None) -> list["Sketch"]:
+        """spk_sketch_build for many measure pairs on one kernel (rows of A, B:
+        count x n), preparing the kernel once."""
+        A = np.ascontiguousarray(A, dtype=np.float64)
+        B = np.ascontiguousarray(B, dtype=np.float64)
+        m = A.shape[0]
+        kd, keep = kernel.desc()
+        kind = {"ot": L.PLAN_OT, "uot": L.PLAN_UOT, "uniform": L.PLAN_UNIFORM, "barycenter": L.PLAN_BARYCENTER}[plan]
+        o = (opts or SparSinkOptions()).c()
+        sd = (C.c_uint64 * max(m, 1))(*[int(x) & 0xFFFFFFFFFFFFFFFF for x in seeds])
+        out = (C.c_void_p * max(m, 1))()
+        rc = self.lib.spk_sketch_build_batch(self.ptr, C.byref(kd), m, L.dptr(A), L.dptr(B), kind, float(lambda_),
+                                             float(epsilon), float(s), sd, C.byref(o), out)
+        _raise(self.ptr, rc)
+        return [Sketch(self, C.c_void_p(out[k])) for k in range(m)]
+
     def sketch_from_csr(self, row_ptr, col_idx, values, values_type: str = "f64") -> "Sketch":
         rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
         ci = np.ascontiguousarray(col_idx, dtype=np.uint32)
@@ -427,8 +444,8 @@ def spar_sink_pairs(ctx: Context, coords, masses, cfg: SolverConfig, s: float, s
         out = []
         for c0 in range(0, len(mine), chunk):
             ks = mine[c0:c0 + chunk]
-            sks = [ctx.sketch(kern, masses[pairs[k][0]], masses[pairs[k][1]], "uot", cfg.lambda_, cfg.epsilon, s,
-                              mix_seed(seed, k), opts) for k in ks]
+            sks = ctx.sketch_batch(kern, masses[[pairs[k][0] for k in ks]], masses[[pairs[k][1] for k in ks]], "uot",
+                                   cfg.lambda_, cfg.epsilon, s, [mix_seed(seed, k) for k in ks], opts)
             reps = solve_batch(ctx, sks, cfg, uot=True, policy="error" if (opts and opts.strict) else "mask")
             for k, sk, rep in zip(ks, sks, reps):
                 _, _, obj, rr = sk.readout(kern, uot=True, lambda_=cfg.lambda_, epsilon=cfg.epsilon)

@@ -247,6 +247,8 @@ struct DevKernel {
   double max_abs = 0.0;         // largest |coordinate| (enables the fp32 support screen)
   DBuf xf, yf, xn, yn;          // fp32 coordinates + squared norms (built on first use)
   DBuf ytr;                     // per sampler column tile: max |y_j|
+  double d0 = 0.0;              // support threshold on d^2 (threshold_kernel), once per kernel
+  bool have_d0 = false;
 };
 
 void make_dev_kernel(spk_ctx* ctx, const spk_kernel_desc* kd, double default_eps, DevKernel& dk,

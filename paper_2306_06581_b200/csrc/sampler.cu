@@ -945,11 +945,14 @@ TiledArgs tiled_args(spk_ctx* ctx, DevKernel& dk) {
   A.eta = dk.eta;
   A.scale = dk.scale;
   A.eps = dk.eps;
-  DBuf d0(sizeof(double));
-  threshold_kernel<<<1, 32, 0, ctx->stream>>>(A, d0.as<double>());
-  ++ctx->launches;
-  double D0 = 0.0;
-  download(ctx, &D0, d0, sizeof D0);
+  if (!dk.have_d0) {  // a property of the kernel (kind, eta, scale, eps): once per DevKernel
+    DBuf d0(sizeof(double));
+    threshold_kernel<<<1, 32, 0, ctx->stream>>>(A, d0.as<double>());
+    ++ctx->launches;
+    download(ctx, &dk.d0, d0, sizeof dk.d0);
+    dk.have_d0 = true;
+  }
+  const double D0 = dk.d0;
   // exact-path band around the threshold (absorbs any non-monotone ULP effects)
   A.lo = D0 * (1.0 - 1e-12);
   A.hi = std::isinf(D0) ? D0 : D0 * (1.0 + 1e-12);

@@ -403,6 +403,32 @@ int spk_sketch_build(spk_ctx* ctx, const spk_kernel_desc* kd, const double* a, c
   });
 }
 
+int spk_sketch_build_batch(spk_ctx* ctx, const spk_kernel_desc* kd, int count, const double* a, const double* b,
+                           int plan_kind, double lambda, double epsilon, double s, const uint64_t* seeds,
+                           const spk_sketch_opts* opts, spk_sketch** out) {
+  if (!ctx || !out || (count > 0 && (!a || !b || !seeds))) return SPK_STATUS_INPUT;
+  for (int k = 0; k < count; ++k) out[k] = nullptr;
+  return guard(ctx, [&] {
+    spk_sketch_opts o{};
+    if (opts) o = *opts;
+    DevKernel dk;  // coordinates, fp32 screen copies and the support threshold: once for the batch
+    make_dev_kernel(ctx, kd, epsilon, dk, /*need_cost=*/false);
+    const int64_t n = dk.n;
+    std::vector<std::unique_ptr<spk_sketch>> made;
+    for (int k = 0; k < count; ++k) {
+      auto sk = std::make_unique<spk_sketch>();
+      sk->ctx = ctx;
+      sk->device = ctx->device;
+      double tp = 0, ts = 0;
+      build_sketch(ctx, dk, a + (int64_t)k * n, b + (int64_t)k * n, plan_kind, lambda, epsilon, o.theta, s, seeds[k],
+                   o.value_type, sk.get(), &tp, &ts);
+      if (o.strict) strict_coverage(ctx, sk.get());
+      made.push_back(std::move(sk));
+    }
+    for (int k = 0; k < count; ++k) out[k] = made[k].release();
+  });
+}
+
 int spk_sketch_from_csr(spk_ctx* ctx, int64_t n, const int64_t* row_ptr, const uint32_t* col_idx,
                         const double* values, int value_type, spk_sketch** out) {
   if (!ctx || !out) return SPK_STATUS_INPUT;

@@ -88,3 +88,23 @@ def test_batch_error_policy_and_linear_fallback(ctx, oracle):
     reps = api.solve_batch(ctx, [good, bad], lin)
     one = good.solve(lin)
     assert reps[0]["iterations"] == one.report["iterations"]
+
+
+def test_sketch_batch_equals_one_at_a_time(ctx):
+    """spk_sketch_build_batch (the kernel prepared once) draws the same sketches
+    bit for bit as spk_sketch_build per pair."""
+    coords, masses = W.c3_frames(7, frames=5, side=48)
+    n = coords.shape[0]
+    s = 10 * n * math.log(n)
+    kern = spk.Coords(coords, coords, "wfr", 0.1, scale=1.0, eps=0.01)
+    pairs = api.frame_pairs(5)
+    seeds = [api.mix_seed(7, k) for k in range(len(pairs))]
+    opts = spk.SparSinkOptions(values="f32")
+    batch = ctx.sketch_batch(kern, masses[[i for i, _ in pairs]], masses[[j for _, j in pairs]], "uot", 1.0, 0.01, s,
+                             seeds, opts)
+    for (i, j), sd, sb in zip(pairs, seeds, batch):
+        one = ctx.sketch(kern, masses[i], masses[j], "uot", 1.0, 0.01, s, sd, opts)
+        for x, y in zip(sb.csr(), one.csr()):
+            assert np.array_equal(x, y)
+        one.free()
+        sb.free()
