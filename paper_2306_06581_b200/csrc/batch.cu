@@ -204,6 +204,18 @@ __device__ __forceinline__ double batch_half(int64_t n, const long long* __restr
       }
       s = group_sum(s);
     }
+    {  // the next row's entry ranges into L2 while this row finishes (its bounds have arrived by now)
+      const int64_t inext = i + (int64_t)nw * kRows;
+      if (inext < n && en > bn) {
+        const char* i0p = reinterpret_cast<const char*>(idx + bn);
+        const char* l0p = reinterpret_cast<const char*>(lval + bn);
+        const long long li = ((long long)(en - bn) * 4 + 127) >> 7, ll = ((long long)(en - bn) * 8 + 127) >> 7;
+        for (long long q = gl; q < li + ll; q += kG) {
+          const char* a = q < li ? i0p + (q << 7) : l0p + ((q - li) << 7);
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
+        }
+      }
+    }
     if (live && gl == 0) {
       const double lse = m == -CUDART_INF ? -CUDART_INF : m + log(s);
       if (lse == -CUDART_INF) {
