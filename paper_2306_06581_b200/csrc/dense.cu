@@ -169,7 +169,7 @@ constexpr int kOtfChunk = 256; // columns per fp32 partial
 // K_ij = exp2(bias_i + bias_j + <p_i, y_j>) = exp(-|x_i - y_j|^2/(scale*eps)).
 struct OtfFastOp {
   static constexpr int kThreads = loopcore::kBlock;
-  static constexpr int kMinBlocks = 2;
+  static constexpr int kMinBlocks = 1;  // 128 registers (at 64 the point records spilled)
   int64_t n;
   int dim;
   const float4* out_rec[2];  // [role] output-side records (2 float4 per atom)
@@ -211,10 +211,13 @@ struct OtfFastOp {
         float part[kOtfRows];
 #pragma unroll
         for (int r = 0; r < kOtfRows; ++r) part[r] = 0.f;
-        for (int64_t j = c0; j < c1; ++j) {
-          const float4 qa = __ldg(irec + 2 * j);
-          const float4 qb = __ldg(irec + 2 * j + 1);
-          const float xj = (float)__ldcg(x + j);
+        const float4* qp = irec + 2 * c0;
+        const double* xp = x + c0;
+        const int len = (int)(c1 - c0);
+        for (int jj = 0; jj < len; ++jj) {  // 32-bit induction: no 64-bit counter arithmetic per column
+          const float4 qa = __ldg(qp + 2 * jj);
+          const float4 qb = __ldg(qp + 2 * jj + 1);
+          const float xj = (float)__ldcg(xp + jj);
 #pragma unroll
           for (int r = 0; r < kOtfRows; ++r) {
             // bias_i (p[r][dim] slot) + bias_j (qb.w) + <p_i, y_j>
