@@ -167,6 +167,15 @@ constexpr int kOtfChunk = 256; // columns per fp32 partial
 // p = -2*alpha*x_i and bias = alpha*|x_i|^2; input side p = y_j, bias =
 // alpha*|y_j|^2, with alpha = -log2(e)/(scale*eps), so
 // K_ij = exp2(bias_i + bias_j + <p_i, y_j>) = exp(-|x_i - y_j|^2/(scale*eps)).
+// MUFU.EX2 with subnormal results flushed to zero: K values below 2^-126
+// (the fp32 comparator's own floor is 2^-149) count as zero. Saves the
+// range test and two multiplies exp2f spends per kernel evaluation.
+__device__ __forceinline__ float ex2_ftz(float e) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(e));
+  return r;
+}
+
 struct OtfFastOp {
   static constexpr int kThreads = loopcore::kBlock;
   static constexpr int kMinBlocks = 1;  // 128 registers (at 64 the point records spilled)
@@ -229,7 +238,7 @@ struct OtfFastOp {
             e = fmaf(p[r][4], qb.x, e);
             e = fmaf(p[r][5], qb.y, e);
             e = fmaf(p[r][6], qb.z, e);
-            part[r] = fmaf(exp2f(e), xj, part[r]);
+            part[r] = fmaf(ex2_ftz(e), xj, part[r]);
           }
         }
 #pragma unroll
