@@ -467,6 +467,11 @@ def run_c3_batch(args, ws, rank, local):
     kern = spk.Coords(coords, coords, "wfr", 0.1, scale=1.0, eps=0.01)
     opts = spk.SparSinkOptions(values="f32")
     ctx = spk.Context(local)
+    from paper_2306_06581_b200 import _lib as L
+
+    for env, key in (("SPK_BATCH_CS", L.OPT_BATCH_CLUSTER), ("SPK_BATCH_U", L.OPT_BATCH_UNROLL)):
+        if os.environ.get(env) is not None:  # batched-loop variant override (profiling)
+            ctx.set_option(key, int(os.environ[env]))
     stream = torch.cuda.current_stream()
     ctx.set_stream(stream.cuda_stream)
     t0 = time.perf_counter()
@@ -492,9 +497,10 @@ def run_c3_batch(args, ws, rank, local):
     elapsed = max_over_ranks(ev0.elapsed_time(ev1) * 1e-3, ws)
     total_iters = sum_over_ranks(iters_done, ws)
     value = total_iters / elapsed
-    # algorithmic bytes: the batched loop streams u32 indices + fp64 log K~ per entry
+    # algorithmic bytes: V + I = 8 bytes per entry and half (fp32
+    # sketch: log K~ and the index travel as one u64 per entry)
     nnz = [sk.nnz for sk in sks]
-    b_pair_iter = [W.bytes_per_iteration(n, z, 8) for z in nnz]
+    b_pair_iter = [W.bytes_per_iteration(n, z, 4) for z in nnz]
     per_step_bytes = sum(b * r["iterations"] for b, r in zip(b_pair_iter, reps))
     achieved = sum_over_ranks(per_step_bytes, ws) * args.steps / elapsed / 1e9
     peak, peak_src = peaks()
@@ -534,12 +540,14 @@ def run_c3_batch(args, ws, rank, local):
         "warmup": args.warmup, "ms_per_step": 1e3 * elapsed / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": "C3", "n": n, "pairs": len(pairs), "pairs_this_rank": len(mine), "epsilon": 0.01,
-                   "lambda": 1.0, "iterations_max": iters, "sketch_values": "f32 (log K~ streamed as fp64)",
+                   "lambda": 1.0, "iterations_max": iters,
+                   "sketch_values": "f32 (streamed as one u64 per entry: log K~ with a 37-bit mantissa | 16-bit index)",
+                   "batch_cluster": ctx.get_option(L.OPT_BATCH_CLUSTER), "batch_unroll": ctx.get_option(L.OPT_BATCH_UNROLL),
                    "scalings": "f64 (shared memory)", "parallelism": f"pairs-round-robin{ws}" if ws > 1 else "single",
                    "l2": "inputs larger than L2: 496 sketches ~10 GB"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": None, "kernel": "batch_log_kernel (one CTA per pair)",
-                     "bytes_per_iter": "per pair: 2 nnz (8+4) + 2 (n+1) 8 + 64 n", "peak_source": peak_src},
+                     "traffic": None, "kernel": "batch_log_kernel (one cluster of CTAs per pair)",
+                     "bytes_per_iter": "per pair: 2 nnz (4+4) + 2 (n+1) 8 + 64 n", "peak_source": peak_src},
         "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": ctx.launches - launches0, "clocks": clk.summary(),
         "extra": {"setup_s": setup_s, "iterations_per_step": total_iters / args.steps,
                   "converged_last_step": sum(r["converged"] for r in reps)},

@@ -170,9 +170,13 @@ enum spk_option {
   SPK_OPT_TWO_PASS_SAMPLER = 6, /* sampler: always the exact two-pass kernels (testing) */
   SPK_OPT_BLOCKED_SPLIT = 7,    /* slab x block loop: column parts per row slab (0 auto, 1, 2 = CTA pairs) */
   SPK_OPT_BLOCKED_SPREAD = 8,   /* slab x block loop: spread each half-warp's gathered columns over the banks (1, default) */
-  SPK_OPT_BLOCKED_CLUSTER = 9   /* slab x block loop: CTA pairs as 2-CTA clusters sharing partial sums (1, default, when they fit) */
+  SPK_OPT_BLOCKED_CLUSTER = 9,  /* slab x block loop: CTA pairs as 2-CTA clusters sharing partial sums (1, default, when they fit) */
+  SPK_OPT_BATCH_CLUSTER = 10,   /* batched log loop: CTAs (SMs) per sketch as one cluster: 1, 2 (default) or 4 */
+  SPK_OPT_BATCH_UNROLL = 11     /* batched log loop: entry loads in flight per lane: 4 (default) or 8 */
 };
 int spk_ctx_set_option(spk_ctx* ctx, int key, int64_t value);
+/* Current value of an option key (SPK_STATUS_INPUT for an unknown key). */
+int spk_ctx_get_option(const spk_ctx* ctx, int key, int64_t* value);
 /* Status of the last failed call on ctx: category (spk_status), class
  * (spk_error_kind) and message. Returns the category. */
 int spk_last_error(const spk_ctx* ctx, int* category, int* kind, char* msg, size_t len);
@@ -237,10 +241,18 @@ int spk_sketch_solve(spk_ctx* ctx, spk_sketch* sk, const double* a, const double
  * with the weights given at build. Log domain (cfg->stabilize) sketches small
  * enough for one CTA's shared memory run together, one CTA per sketch;
  * otherwise one after another. reps: `count` reports (may be NULL). Results
- * stay on each sketch for spk_sketch_readout. On failure the status is that
- * of the lowest failing item and the message names it. */
+ * stay on each sketch for spk_sketch_readout / spk_sketch_scalings.
+ * item_error NULL: on failure the status is that of the lowest failing item
+ * and the message names it. item_error non-NULL (`count` entries): each
+ * item's outcome is recorded there (0, or the SPK_E_* class of its failure:
+ * ZeroDenominator, DegenerateSketchError, ...) and the call succeeds unless
+ * the device faults -- pairwise_wfr's per-pair NaN (harness.cpp:395-401). */
 int spk_sketch_solve_batch(spk_ctx* ctx, spk_sketch* const* sketches, int count, const spk_solver_cfg* cfg,
-                           int uot, spk_report* reps);
+                           int uot, spk_report* reps, int32_t* item_error);
+/* Scalings of the LAST solve on this sketch (n doubles each; any may be
+ * NULL; log_u/log_v only after a log-domain solve) -- TransportPlan::u/v
+ * (solvers.hpp:34-59). */
+int spk_sketch_scalings(spk_sketch* sk, double* u, double* v, double* log_u, double* log_v);
 /* Plan readout of the LAST solve on this sketch: marginals (may be NULL)
  * and the OT/UOT objective with costs from kd (dense C or coordinates). */
 int spk_sketch_readout(spk_ctx* ctx, spk_sketch* sk, const spk_kernel_desc* kd, int uot,

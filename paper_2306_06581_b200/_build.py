@@ -48,15 +48,24 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     build_dir = PKG / "_obj"
     build_dir.mkdir(exist_ok=True)
     if force or _stale(LIB, deps):
-        objs = []
+        from concurrent.futures import ThreadPoolExecutor
+
+        objs, todo = [], []
         for src in CUDA_SOURCES:
             obj = build_dir / (Path(src).stem + ".o")
             if force or _stale(obj, deps):
-                _run([NVCC, *ARCH, *NVCC_FLAGS, "-c", str(CSRC / src), "-o", str(obj)],
-                     log=build_dir / (Path(src).stem + ".ptxas.txt"))
-                if verbose:
-                    print("compiled", src)
+                todo.append((src, obj))
             objs.append(str(obj))
+
+        def compile_one(item):
+            src, obj = item
+            _run([NVCC, *ARCH, *NVCC_FLAGS, "-c", str(CSRC / src), "-o", str(obj)],
+                 log=build_dir / (Path(src).stem + ".ptxas.txt"))
+            if verbose:
+                print("compiled", src)
+
+        with ThreadPoolExecutor(max_workers=min(len(todo), os.cpu_count() or 4) or 1) as ex:
+            list(ex.map(compile_one, todo))
         _run([NVCC, *ARCH, "-shared", "-o", str(LIB), *objs, "-lcudart_static", "-lrt", "-ldl", "-lpthread"])
     shim_src = CSRC / "host" / "sparsink_b200.cpp"
     if shim_src.exists():

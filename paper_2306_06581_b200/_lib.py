@@ -26,6 +26,8 @@ OPT_TWO_PASS_SAMPLER = 6
 OPT_BLOCKED_SPLIT = 7
 OPT_BLOCKED_SPREAD = 8
 OPT_BLOCKED_CLUSTER = 9
+OPT_BATCH_CLUSTER = 10
+OPT_BATCH_UNROLL = 11
 
 ERROR_CLASSES = {
     1: "Error", 2: "NegativeWeight", 3: "LengthMismatch", 4: "NotNormalized", 5: "AllBlack",
@@ -76,6 +78,7 @@ SIGNATURES = {
     "spk_ctx_set_stream": (C.c_int, [C.c_void_p, C.c_void_p]),
     "spk_ctx_stream": (C.c_void_p, [C.c_void_p]),
     "spk_ctx_set_option": (C.c_int, [C.c_void_p, C.c_int, C.c_int64]),
+    "spk_ctx_get_option": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_int64)]),
     "spk_last_error": (C.c_int, [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int), C.c_char_p, C.c_size_t]),
     "spk_ctx_launch_count": (C.c_int64, [C.c_void_p]),
     "spk_spar_sink": (C.c_int, [C.c_void_p, C.POINTER(KernelDesc), DP, DP, C.POINTER(SolverCfg), C.c_double,
@@ -97,7 +100,8 @@ SIGNATURES = {
     "spk_sketch_solve": (C.c_int, [C.c_void_p, C.c_void_p, DP, DP, C.POINTER(SolverCfg), C.c_int, DP, DP, DP, DP,
                                    C.POINTER(Report)]),
     "spk_sketch_solve_batch": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.c_int, C.POINTER(SolverCfg), C.c_int,
-                                         C.POINTER(Report)]),
+                                         C.POINTER(Report), C.POINTER(C.c_int32)]),
+    "spk_sketch_scalings": (C.c_int, [C.c_void_p, DP, DP, DP, DP]),
     "spk_sketch_readout": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(KernelDesc), C.c_int, C.c_double,
                                      C.c_double, DP, DP, DP, C.POINTER(Report)]),
     "spk_plan_readout": (C.c_int, [C.c_void_p, C.POINTER(KernelDesc), C.c_int64, I64P, U32P, DP, DP, DP, DP, DP,

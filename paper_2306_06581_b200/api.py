@@ -170,6 +170,11 @@ class Context:
     def set_option(self, key: int, value: int) -> None:
         _raise(self.ptr, self.lib.spk_ctx_set_option(self.ptr, key, int(value)))
 
+    def get_option(self, key: int) -> int:
+        v = C.c_int64()
+        _raise(self.ptr, self.lib.spk_ctx_get_option(self.ptr, key, C.byref(v)))
+        return v.value
+
     def set_stream(self, stream_ptr: int | None) -> None:
         _raise(self.ptr, self.lib.spk_ctx_set_stream(self.ptr, C.c_void_p(stream_ptr) if stream_ptr else None))
 
@@ -344,6 +349,13 @@ class Sketch:
         log = bool(rep.log_domain)
         return Result(u, v, lu if log else None, lv if log else None, rep.as_dict())
 
+    def scalings(self):
+        """(u, v, log_u, log_v) of the last solve (log_* None after a linear-domain solve)."""
+        n = self.n
+        u, v, lu, lv = (np.empty(n) for _ in range(4))
+        _raise(self.ctx.ptr, self.lib.spk_sketch_scalings(self.ptr, L.dptr(u), L.dptr(v), L.dptr(lu), L.dptr(lv)))
+        return u, v, lu, lv
+
     def readout(self, kernel=None, uot: bool = False, lambda_: float = math.inf, epsilon: float = 1.0,
                 objective: bool = True):
         """Marginals + ot_objective / uot_objective of the last solve."""
@@ -362,17 +374,28 @@ class Sketch:
         return rm, cm, obj.value, rep.as_dict()
 
 
-def solve_batch(ctx: Context, sketches, cfg: SolverConfig, uot: bool = False, policy: str = "mask") -> list[dict]:
+def solve_batch(ctx: Context, sketches, cfg: SolverConfig, uot: bool = False, policy: str = "mask",
+                per_item: bool = False) -> list[dict]:
     """sinkhorn_ot / sinkhorn_uot on many independent sketches at once
     (spk_sketch_solve_batch: log-domain sketches that fit one CTA's shared
     memory run one CTA each, in a single launch). Scalings stay on the
-    sketches (Sketch.readout). Returns the per-sketch reports."""
+    sketches (Sketch.readout / Sketch.scalings). Returns the per-sketch
+    reports. per_item=False: the first failing item raises (its class);
+    per_item=True: a failing item gets report["error"] = its exception class
+    name and the others complete (pairwise_wfr, harness.cpp:395-401)."""
     m = len(sketches)
     ptrs = (C.c_void_p * max(m, 1))(*[sk.ptr for sk in sketches])
     reps = (L.Report * max(m, 1))()
+    errs = (C.c_int32 * max(m, 1))()
     c = cfg.c(L.POLICY_MASK if policy == "mask" else L.POLICY_ERROR)
-    _raise(ctx.ptr, ctx.lib.spk_sketch_solve_batch(ctx.ptr, ptrs, m, C.byref(c), int(uot), reps))
-    return [reps[k].as_dict() for k in range(m)]
+    _raise(ctx.ptr, ctx.lib.spk_sketch_solve_batch(ctx.ptr, ptrs, m, C.byref(c), int(uot), reps,
+                                                   errs if per_item else None))
+    out = []
+    for k in range(m):
+        d = reps[k].as_dict()
+        d["error"] = L.ERROR_CLASSES.get(errs[k]) if errs[k] else None
+        out.append(d)
+    return out
 
 
 _default: Context | None = None
@@ -446,21 +469,39 @@ def spar_sink_pairs(ctx: Context, coords, masses, cfg: SolverConfig, s: float, s
             ks = mine[c0:c0 + chunk]
             sks = ctx.sketch_batch(kern, masses[[pairs[k][0] for k in ks]], masses[[pairs[k][1] for k in ks]], "uot",
                                    cfg.lambda_, cfg.epsilon, s, [mix_seed(seed, k) for k in ks], opts)
-            reps = solve_batch(ctx, sks, cfg, uot=True, policy="error" if (opts and opts.strict) else "mask")
-            for k, sk, rep in zip(ks, sks, reps):
-                _, _, obj, rr = sk.readout(kern, uot=True, lambda_=cfg.lambda_, epsilon=cfg.epsilon)
-                rep = dict(rep)
-                rep["objective"] = obj
-                rep["seed"] = mix_seed(seed, k)
-                out.append((k, pairs[k], rep))
-                sk.free()
+            try:
+                reps = solve_batch(ctx, sks, cfg, uot=True, policy="mask", per_item=True)
+                for k, sk, rep in zip(ks, sks, reps):
+                    rep = dict(rep)
+                    if rep["error"] is None:
+                        _, _, obj, rr = sk.readout(kern, uot=True, lambda_=cfg.lambda_, epsilon=cfg.epsilon)
+                        rep["objective"] = obj
+                    else:  # the reference records a failed pair as NaN (harness.cpp:395-401)
+                        rep["objective"] = math.nan
+                    rep["seed"] = mix_seed(seed, k)
+                    out.append((k, pairs[k], rep))
+            finally:
+                for sk in sks:
+                    sk.free()
         return out
     out = []
     for k in mine:
         i, j = pairs[k]
-        r = ctx.spar_sink(kern, masses[i], masses[j], cfg, s, mix_seed(seed, k), opts, uot=True)
-        out.append((k, (i, j), r.report))
+        try:
+            r = ctx.spar_sink(kern, masses[i], masses[j], cfg, s, mix_seed(seed, k), opts, uot=True)
+            rep = dict(r.report)
+            rep["error"] = None
+        except SparsinkError as e:
+            if isinstance(e, ERRORS["DeviceError"]):
+                raise
+            rep = {"objective": math.nan, "error": type(e).__name__, "seed": mix_seed(seed, k)}
+        out.append((k, (i, j), rep))
     return out
+
+
+def failed_pairs(results) -> int:
+    """Pairs whose solve failed (NaN objective), as pairwise_wfr's failed_pairs."""
+    return sum(1 for _, _, rep in results if rep.get("error"))
 
 
 # ---- barycenters (ibp / spar_ibp, include/sparsink/barycenter.hpp) ------------------

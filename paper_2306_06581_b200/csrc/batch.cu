@@ -2,18 +2,34 @@
 // 496 WFR frame pairs of n = 12,544, each run by pairwise_wfr,
 // proj/src/harness.cpp:349-406, one spar_sink_uot at a time).
 //
-// One CTA owns one sketch for its whole solve: both log scalings (lu, lv:
-// 2 n fp64 = 196 KB at n = 12,544) live in shared memory for every
-// iteration, so the gathered x of a half is a shared-memory read and the
-// only HBM traffic is the sketch stream (indices + log K~). CTAs are
-// independent (no grid barrier): the grid is the batch, run in waves.
+// A cluster of CS CTAs (CS = 2 by default: two SMs) owns one sketch for its
+// whole solve. Every CTA keeps BOTH log scalings (lu, lv: 2 n fp64 = 196 KB at
+// n = 12,544) in its own shared memory, so the gathered x of a half is a
+// shared-memory read and the only HBM traffic is the sketch stream. A half
+// is split over the cluster's CTAs by entry count; each CTA writes the new
+// values of its rows into its own copy and, through DSMEM, into its peers'
+// copies; one cluster barrier per half publishes them. Residual partials,
+// mask counts and the first failing atom are exchanged through DSMEM after
+// the same barrier and combined in rank order, so every CTA takes the same
+// stop / failure decision. Clusters are independent (no grid barrier). Two
+// SMs per pair also evens out the waves: 496 pairs = 3.35 waves of 148 SMs
+// one CTA per pair (4 waves run), 6.7 waves as CTA pairs (7 run).
 //
-// Semantics: detail::log_scaling_loop (include/sparsink/solvers.hpp:397-513),
-// as the single-sketch fast path (two-pass log-sum-exp; the sums run in
-// another lane order, so scalings agree to rounding): lu = f (log a - LSE_j(log K~ +
-// lv)); a row whose LSE is -inf is masked (Mask) or raises ZeroDenominator
-// (Error); the stop rule sums |d lu| + |d lv| over unmasked atoms for t >= 2;
-// all rows or all columns masked raises DegenerateSketchError.
+// Entry stream: fp32 sketches (config 3) stream ONE u64 per entry -- log K~
+// as an fp64 rounded to a 37-bit mantissa (relative error 2^-37, far below
+// the fp32 rounding of K~ itself) with the 16-bit column (row) index in the
+// low mantissa bits (n <= 65,536: the batch limit is ~14k). 8 bytes per entry,
+// SURVEY 8(d)'s V + I. fp64 sketches stream u32 indices + fp64 log K~ (12 B).
+//
+// Semantics: detail::log_scaling_loop (include/sparsink/solvers.hpp:397-513):
+// lu = f (log a - LSE_j(log K~ + lv)); a row whose LSE is -inf is masked
+// (Mask) or raises ZeroDenominator (Error); the stop rule sums |d lu| + |d lv|
+// over unmasked atoms for t >= 2; all rows or all columns masked raises
+// DegenerateSketchError. The LSE is one online pass (running max, rescaled
+// sum) over blocks of U entries per lane, with the fp32-accurate exp for fp32
+// sketches (as spk_sketch_solve) and fp64 exp for fp64 sketches; the single-
+// sketch path sums in another order, so results agree to rounding
+// (tests/test_gpu_batch.py, tests/test_gpu_fullsize.py quantify it).
 #include <algorithm>
 #include <cmath>
 #include <string>
@@ -30,16 +46,20 @@ namespace spk {
 namespace {
 
 constexpr int kBatchThreads = 1024;
+constexpr int kG = 8;      // lanes per row (config 3 rows: ~94 entries)
+constexpr int kRows = 32 / kG;
 
 struct BatchItem {
   int64_t n;
   const long long* row_ptr;
-  const uint32_t* col_idx;
-  const double* lval;  // log K~ of the CSR values
+  const uint32_t* col_idx;            // split stream (fp64 sketches)
+  const double* lval;
+  const unsigned long long* lpack;    // packed stream (fp32 sketches)
   const long long* col_ptr;
   const uint32_t* row_idx;
-  const double* lval_t;  // log K~ of the CSC values
-  const double* la;      // log a (-inf where a = 0)
+  const double* lval_t;
+  const unsigned long long* lpack_t;
+  const double* la;  // log a (-inf where a = 0)
   const double* lb;
   const unsigned char* cov_row;  // structural coverage (kernel_coverage)
   const unsigned char* cov_col;
@@ -65,178 +85,188 @@ struct BatchArgs {
   int npad;  // shared doubles per vector
 };
 
-// One half: out[i] for every unmasked output atom i from the row/column
-// [ptr[i], ptr[i+1]) against the shared vector x. Returns this thread's
-// residual share; masks and the first failing atom go through shared counters.
-// Rows are short (config 3: ~94 entries), so 8 lanes share a row (4 rows per
-// warp) and each lane keeps 4 independent entry loads in flight: the pass is
-// bound by the latency of the sketch stream, not by its exp()s.
-// Two-pass log-sum-exp (max, then the sum of exp(t - max): the reference's
-// order, solvers.cpp:99-111).
-constexpr int kG = 8;  // lanes per row
+// Per-CTA values every CTA of the cluster reads after the half's barrier.
+struct Xch {
+  double err[2];
+  long long masks[2];
+  unsigned long long bad[2];
+};
 
-__device__ __forceinline__ double group_max(double v) {
-#pragma unroll
-  for (int o = kG / 2; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
-}
-__device__ __forceinline__ double group_sum(double v) {
-#pragma unroll
-  for (int o = kG / 2; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
+// Entry stream of one half: packed u64 (PACKED) or u32 index + fp64 log K~.
+template <bool PACKED>
+struct Stream {
+  const unsigned long long* pk;
+  const uint32_t* idx;
+  const double* lv;
+  __device__ __forceinline__ void load(long long p, uint32_t& j, double& l) const {
+    if constexpr (PACKED) {
+      const unsigned long long w = __ldg(pk + p);
+      j = (uint32_t)(w & 0xffffull);
+      l = __longlong_as_double((long long)(w & ~0xffffull));
+    } else {
+      j = __ldg(idx + p);
+      l = __ldg(lv + p);
+    }
+  }
+  __device__ __forceinline__ void prefetch_l2(long long b, long long e, int gl) const {
+    const long long nb = (e - b) * (PACKED ? 8 : 12);
+    const long long lines = (nb + 127) >> 7;
+    for (long long q = gl; q < lines + (PACKED ? 0 : 1); q += kG) {
+      const char* a;
+      if constexpr (PACKED) {
+        a = reinterpret_cast<const char*>(pk + b) + (q << 7);
+      } else {
+        const long long li = ((e - b) * 4 + 127) >> 7;
+        a = q < li ? reinterpret_cast<const char*>(idx + b) + (q << 7)
+                   : reinterpret_cast<const char*>(lv + b) + ((q - li) << 7);
+      }
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
+    }
+  }
+};
+
+template <bool FAST>
+__device__ __forceinline__ double lse_exp(double d) {
+  if constexpr (FAST) return exp_fast(d);
+  else return exp(d);
 }
 
-template <class VT>
-__device__ __forceinline__ double batch_half(int64_t n, const long long* __restrict__ ptr,
-                                             const uint32_t* __restrict__ idx, const double* __restrict__ lval,
-                                             const double* __restrict__ w, const double* x, double* out,
-                                             unsigned int* ne, double exponent, int policy, long long* masks,
-                                             unsigned long long* bad) {
+__device__ __forceinline__ double* peer_ptr(double* p, unsigned rank) {
+  double* q;
+  asm volatile("mapa.u64 %0, %1, %2;" : "=l"(q) : "l"(p), "r"(rank));
+  return q;
+}
+__device__ __forceinline__ const Xch* peer_xch(const Xch* p, unsigned rank) {
+  const Xch* q;
+  asm volatile("mapa.u64 %0, %1, %2;" : "=l"(q) : "l"(p), "r"(rank));
+  return q;
+}
+__device__ __forceinline__ void cluster_barrier() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ unsigned cluster_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+// First output atom of cluster rank r's share of a half: rows split by entry
+// count (binary search on the row pointer).
+__device__ __forceinline__ int64_t split_point(const long long* ptr, int64_t n, int r, int CS) {
+  if (r <= 0) return 0;
+  if (r >= CS) return n;
+  const long long target = (long long)((__ldg(ptr + n) * (double)r) / CS);
+  int64_t lo = 0, hi = n;  // first i with ptr[i] >= target
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (__ldg(ptr + mid) < target) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// One half over output atoms [i_lo, i_hi): out[i] for every unmasked atom from
+// the row/column [ptr[i], ptr[i+1]) against the shared vector x. Writes the
+// new value into this CTA's copy and into the CS-1 peers' copies. Returns
+// this thread's residual share; masks and the first failing atom go through
+// shared counters. 8 lanes share a row (4 rows per warp); each lane keeps U
+// independent entry loads in flight; the next row group's entries are
+// prefetched into L2 while this one finishes.
+template <int CS, int U, bool PACKED, bool FAST>
+__device__ __forceinline__ double batch_half(int64_t i_lo, int64_t i_hi, const long long* __restrict__ ptr,
+                                             Stream<PACKED> st, const double* __restrict__ w, const double* x,
+                                             double* out, unsigned int* ne, double exponent, int policy,
+                                             long long* masks, unsigned long long* bad, unsigned my_rank) {
   const int lane = threadIdx.x & 31;
   const int gl = lane & (kG - 1);
   const int warp = threadIdx.x >> 5;
   const int nw = blockDim.x >> 5;
-  constexpr int kRows = 32 / kG;
-  constexpr bool kOnline = std::is_same<VT, LogKf>::value;
   double err = 0.0;
-  // row bounds of the next row group loaded one group ahead
-  int64_t i = (int64_t)warp * kRows + (lane / kG);
+  int64_t i = i_lo + (int64_t)warp * kRows + (lane / kG);
   long long bn = 0, en = 0;
-  if (i < n) {
+  if (i < i_hi) {
     bn = __ldg(ptr + i);
     en = __ldg(ptr + i + 1);
   }
-  for (int64_t i0 = (int64_t)warp * kRows; i0 < n; i0 += (int64_t)nw * kRows) {
+  for (int64_t i0 = i_lo + (int64_t)warp * kRows; i0 < i_hi; i0 += (int64_t)nw * kRows) {
     i = i0 + (lane / kG);
-    const bool live = i < n && ((ne[i >> 5] >> (i & 31)) & 1u);  // masked rows keep -inf
-    long long b = live ? bn : 0, e = live ? en : 0;
+    const bool live = i < i_hi && ((ne[i >> 5] >> (i & 31)) & 1u);  // masked rows keep -inf
+    const long long b = live ? bn : 0, e = live ? en : 0;
     {
       const int64_t inext = i + (int64_t)nw * kRows;
-      if (inext < n) {
+      if (inext < i_hi) {
         bn = __ldg(ptr + inext);
         en = __ldg(ptr + inext + 1);
       }
     }
     double m = -CUDART_INF, s = 0.0;
-    if (kOnline) {
-      // fp32 sketches: one pass, online (max, scaled sum) with the fp32-accurate
-      // exp (each term rescaled at most once per new max)
-      long long p = b + gl;
-      auto add = [&](double t) {
-        if (t == -CUDART_INF) return;
-        if (t > m) {
-          s = s * exp_fast(m - t) + 1.0;
-          m = t;
-        } else {
-          s += exp_fast(t - m);
-        }
-      };
-      for (; p + 3 * kG < e; p += 4 * kG) {
-        uint32_t j[4];
-        double l[4];
+    for (long long p = b + gl; p < e; p += U * kG) {
+      uint32_t j[U];
+      double l[U];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          j[k] = __ldg(idx + p + k * kG);
-          l[k] = __ldg(lval + p + k * kG);
-        }
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const double xv = x[j[k]];
-          if (xv != -CUDART_INF) add(l[k] + xv);
+      for (int k = 0; k < U; ++k) {
+        if (p + k * kG < e) st.load(p + k * kG, j[k], l[k]);
+        else {
+          j[k] = 0;
+          l[k] = -CUDART_INF;
         }
       }
-      for (; p < e; p += kG) {
-        const double xv = x[__ldg(idx + p)];
-        if (xv != -CUDART_INF) add(__ldg(lval + p) + xv);
-      }
+      double t[U];
+      double M = m;
 #pragma unroll
-      for (int o = kG / 2; o; o >>= 1) {
-        const double m2 = __shfl_xor_sync(0xffffffffu, m, o);
-        const double s2 = __shfl_xor_sync(0xffffffffu, s, o);
-        const double M = fmax(m, m2);
-        if (M != -CUDART_INF)
-          s = (m == -CUDART_INF ? 0.0 : s * exp_fast(m - M)) + (m2 == -CUDART_INF ? 0.0 : s2 * exp_fast(m2 - M));
+      for (int k = 0; k < U; ++k) {
+        t[k] = l[k] == -CUDART_INF ? -CUDART_INF : l[k] + x[j[k]];  // x = -inf: masked column
+        M = fmax(M, t[k]);
+      }
+      if (M != -CUDART_INF) {
+        double acc = (m == -CUDART_INF) ? 0.0 : s * lse_exp<FAST>(m - M);
+#pragma unroll
+        for (int k = 0; k < U; ++k) acc += (t[k] == -CUDART_INF) ? 0.0 : lse_exp<FAST>(t[k] - M);
+        s = acc;
         m = M;
       }
-    } else {
-      // fp64 sketches: two passes (max, then the sum of exp(t - max): the
-      // reference's order, solvers.cpp:99-111)
-      long long p = b + gl;
-      for (; p + 3 * kG < e; p += 4 * kG) {
-        uint32_t j[4];
-        double l[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          j[k] = __ldg(idx + p + k * kG);
-          l[k] = __ldg(lval + p + k * kG);
-        }
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const double xv = x[j[k]];
-          if (xv != -CUDART_INF) m = fmax(m, l[k] + xv);
-        }
-      }
-      for (; p < e; p += kG) {
-        const double xv = x[__ldg(idx + p)];
-        if (xv != -CUDART_INF) m = fmax(m, __ldg(lval + p) + xv);
-      }
-      m = group_max(m);
-      if (m != -CUDART_INF) {
-        p = b + gl;
-        for (; p + 3 * kG < e; p += 4 * kG) {
-          uint32_t j[4];
-          double l[4];
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            j[k] = __ldg(idx + p + k * kG);
-            l[k] = __ldg(lval + p + k * kG);
-          }
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const double xv = x[j[k]];
-            if (xv != -CUDART_INF) s += exp(l[k] + xv - m);
-          }
-        }
-        for (; p < e; p += kG) {
-          const double xv = x[__ldg(idx + p)];
-          if (xv != -CUDART_INF) s += exp(__ldg(lval + p) + xv - m);
-        }
-      }
-      s = group_sum(s);
     }
-    {  // the next row's entry ranges into L2 while this row finishes (its bounds have arrived by now)
+#pragma unroll
+    for (int o = kG / 2; o; o >>= 1) {
+      const double m2 = __shfl_xor_sync(0xffffffffu, m, o);
+      const double s2 = __shfl_xor_sync(0xffffffffu, s, o);
+      const double M = fmax(m, m2);
+      if (M != -CUDART_INF)
+        s = (m == -CUDART_INF ? 0.0 : s * lse_exp<FAST>(m - M)) + (m2 == -CUDART_INF ? 0.0 : s2 * lse_exp<FAST>(m2 - M));
+      m = M;
+    }
+    {  // the next row group's entries into L2 while this one finishes
       const int64_t inext = i + (int64_t)nw * kRows;
-      if (inext < n && en > bn) {
-        const char* i0p = reinterpret_cast<const char*>(idx + bn);
-        const char* l0p = reinterpret_cast<const char*>(lval + bn);
-        const long long li = ((long long)(en - bn) * 4 + 127) >> 7, ll = ((long long)(en - bn) * 8 + 127) >> 7;
-        for (long long q = gl; q < li + ll; q += kG) {
-          const char* a = q < li ? i0p + (q << 7) : l0p + ((q - li) << 7);
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
-        }
-      }
+      if (inext < i_hi && en > bn) st.prefetch_l2(bn, en, gl);
     }
     if (live && gl == 0) {
       const double lse = m == -CUDART_INF ? -CUDART_INF : m + log(s);
+      double nv;
+      bool write = true;
       if (lse == -CUDART_INF) {
         if (policy == SPK_POLICY_MASK) {  // :440-446 (masked atoms leave the residual)
           atomicAnd(ne + (i >> 5), ~(1u << (i & 31)));
-          out[i] = -CUDART_INF;
+          nv = -CUDART_INF;
           atomicAdd(reinterpret_cast<unsigned long long*>(masks), 1ull);
         } else {
           atomicMin(bad, (unsigned long long)i);
+          write = false;
         }
       } else {
-        const double ln = exponent * (__ldg(w + i) - lse);  // :449
-        err += fabs(ln - out[i]);
-        out[i] = ln;
+        nv = exponent * (__ldg(w + i) - lse);  // :449
+        err += fabs(nv - out[i]);
+      }
+      if (write) {
+        out[i] = nv;
+#pragma unroll
+        for (int r = 1; r < CS; ++r) *peer_ptr(out + i, (my_rank + r) % CS) = nv;
       }
     }
   }
   return err;
 }
 
-// Fixed-order CTA sum (warp sums, then warp 0 over the warps in order).
+// Fixed-order CTA sum (warp sums, then every thread over the warps in order).
 __device__ __forceinline__ double cta_sum(double v, double* scratch) {
   v = warp_sum(v);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -248,11 +278,11 @@ __device__ __forceinline__ double cta_sum(double v, double* scratch) {
   return r;
 }
 
-// VT: LogK (fp64 exp) or LogKf (fp32 sketches: fp32-accurate exp), as the single-sketch path
-template <class VT>
+template <int CS, int U, bool PACKED, bool FAST>
 __global__ void __launch_bounds__(kBatchThreads, 1) batch_log_kernel(BatchArgs A) {
   extern __shared__ __align__(16) double smem[];
-  const BatchItem& I = A.items[blockIdx.x];
+  const unsigned rank = CS > 1 ? cluster_rank() : 0u;
+  const BatchItem& I = A.items[blockIdx.x / CS];
   const int64_t n = I.n;
   double* lu = smem;
   double* lv = smem + A.npad;
@@ -261,6 +291,7 @@ __global__ void __launch_bounds__(kBatchThreads, 1) batch_log_kernel(BatchArgs A
   __shared__ double scratch[32];
   __shared__ long long masks_sh[2];
   __shared__ unsigned long long bad_sh[2];
+  __shared__ Xch xch;
   // u = v = 1 (log 0) on covered atoms, masked atoms -inf (:424-428)
   for (int64_t w = threadIdx.x; w < (A.npad >> 5); w += blockDim.x) {
     unsigned int bu = 0u, bv = 0u;
@@ -278,11 +309,37 @@ __global__ void __launch_bounds__(kBatchThreads, 1) batch_log_kernel(BatchArgs A
     lu[i] = I.cov_row[i] ? 0.0 : -CUDART_INF;
     lv[i] = I.cov_col[i] ? 0.0 : -CUDART_INF;
   }
+  // this CTA's share of the rows (u-half) and of the columns (v-half)
+  const int64_t r0 = split_point(I.row_ptr, n, (int)rank, CS), r1 = split_point(I.row_ptr, n, (int)rank + 1, CS);
+  const int64_t c0 = split_point(I.col_ptr, n, (int)rank, CS), c1 = split_point(I.col_ptr, n, (int)rank + 1, CS);
+  const Stream<PACKED> srow{I.lpack, I.col_idx, I.lval};
+  const Stream<PACKED> scol{I.lpack_t, I.row_idx, I.lval_t};
   long long mr = I.masked_rows0, mc = I.masked_cols0;
   long long t = 0;
   int converged = 0, ekind = 0, ehalf = 0;
   long long eidx = 0;
-  __syncthreads();
+  if (CS > 1) cluster_barrier();  // peers' shared memory initialised before any DSMEM write
+  else __syncthreads();
+  // the half's cluster-wide outcome: residual, new masks, first failing atom
+  auto exchange = [&](int h, double e_cta, double& e_all, long long& m_all, unsigned long long& b_all) {
+    if (threadIdx.x == 0) {
+      xch.err[h] = e_cta;
+      xch.masks[h] = masks_sh[h];
+      xch.bad[h] = bad_sh[h];
+    }
+    if (CS > 1) cluster_barrier();  // new values + partials visible cluster-wide
+    else __syncthreads();
+    e_all = 0.0;
+    m_all = 0;
+    b_all = ~0ull;
+#pragma unroll
+    for (int r = 0; r < CS; ++r) {  // rank order: the same sum on every CTA
+      const Xch* px = (r == (int)rank || CS == 1) ? &xch : peer_xch(&xch, (unsigned)r);
+      e_all += px->err[h];
+      m_all += px->masks[h];
+      b_all = min(b_all, px->bad[h]);
+    }
+  };
   while (t < A.max_iter) {
     ++t;
     __syncthreads();  // every thread has read last iteration's counters
@@ -292,30 +349,34 @@ __global__ void __launch_bounds__(kBatchThreads, 1) batch_log_kernel(BatchArgs A
     }
     __syncthreads();
     // u-half: rows of K~ against lv (kernel_log_apply, solvers.cpp:96-116)
-    const double eu = cta_sum(
-        batch_half<VT>(n, I.row_ptr, I.col_idx, I.lval, I.la, lv, lu, neu, I.exponent, A.policy, &masks_sh[0], &bad_sh[0]),
-        scratch);
-    __syncthreads();
-    if (bad_sh[0] != ~0ull) {
+    double eu, ev;
+    long long mu, mv;
+    unsigned long long bu, bv;
+    exchange(0,
+             cta_sum(batch_half<CS, U, PACKED, FAST>(r0, r1, I.row_ptr, srow, I.la, lv, lu, neu, I.exponent, A.policy,
+                                                     &masks_sh[0], &bad_sh[0], rank),
+                     scratch),
+             eu, mu, bu);
+    if (bu != ~0ull) {
       ekind = SPK_E_ZERO_DENOMINATOR;
       ehalf = 0;
-      eidx = (long long)bad_sh[0];
+      eidx = (long long)bu;
       break;
     }
     // v-half: columns against the NEW lu (Gauss-Seidel, :451-463)
-    const double ev = cta_sum(
-        batch_half<VT>(n, I.col_ptr, I.row_idx, I.lval_t, I.lb, lu, lv, nev, I.exponent, A.policy, &masks_sh[1],
-                   &bad_sh[1]),
-        scratch);
-    __syncthreads();
-    if (bad_sh[1] != ~0ull) {
+    exchange(1,
+             cta_sum(batch_half<CS, U, PACKED, FAST>(c0, c1, I.col_ptr, scol, I.lb, lu, lv, nev, I.exponent, A.policy,
+                                                     &masks_sh[1], &bad_sh[1], rank),
+                     scratch),
+             ev, mv, bv);
+    if (bv != ~0ull) {
       ekind = SPK_E_ZERO_DENOMINATOR;
       ehalf = 1;
-      eidx = (long long)bad_sh[1];
+      eidx = (long long)bv;
       break;
     }
-    mr += masks_sh[0];
-    mc += masks_sh[1];
+    mr += mu;
+    mc += mv;
     if (mr == n || mc == n) {  // :465-466
       ekind = SPK_E_DEGENERATE_SKETCH_ERROR;
       break;
@@ -325,12 +386,12 @@ __global__ void __launch_bounds__(kBatchThreads, 1) batch_log_kernel(BatchArgs A
       break;
     }
   }
-  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
-    I.lu[i] = lu[i];
-    I.lv[i] = lv[i];
-  }
-  if (threadIdx.x == 0) {
-    BatchStatus& S = A.status[blockIdx.x];
+  if (CS > 1) cluster_barrier();  // no CTA leaves while a peer may still read its Xch
+  // every CTA holds the full vectors: each stores its own share
+  for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) I.lu[i] = lu[i];
+  for (int64_t i = c0 + threadIdx.x; i < c1; i += blockDim.x) I.lv[i] = lv[i];
+  if (threadIdx.x == 0 && rank == 0) {
+    BatchStatus& S = A.status[blockIdx.x / CS];
     S.iterations = t;
     S.masked_rows = mr;
     S.masked_cols = mc;
@@ -338,6 +399,18 @@ __global__ void __launch_bounds__(kBatchThreads, 1) batch_log_kernel(BatchArgs A
     S.error_kind = ekind;
     S.error_half = ehalf;
     S.error_index = eidx;
+  }
+}
+
+// Packed entry stream of an fp32 sketch: log K~ (fp64 log of the stored fp32
+// value, rounded to a 37-bit mantissa; -inf stays -inf) | 16-bit index.
+__global__ void pack_log_kernel(const float* __restrict__ v, const uint32_t* __restrict__ idx, int64_t m,
+                                unsigned long long* __restrict__ out) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < m; k += (int64_t)gridDim.x * blockDim.x) {
+    const double l = log((double)v[k]);
+    unsigned long long b = (unsigned long long)__double_as_longlong(l);
+    if (isfinite(l)) b += 0x8000ull;  // round to nearest on the kept bits
+    out[k] = (b & ~0xffffull) | (unsigned long long)(idx[k] & 0xffffu);
   }
 }
 
@@ -359,6 +432,58 @@ int64_t batch_max_n(spk_ctx* ctx) {
   return std::max<int64_t>(0, (avail * 8 / (2 * 64 + 2)) / 32 * 32 - 32);
 }
 
+// The packed (log K~ | index) streams of an fp32 sketch, built once.
+static void ensure_log_packed(spk_ctx* ctx, spk_sketch* sk) {
+  if (sk->log_packed.p) return;
+  const int64_t m = std::max<int64_t>(sk->nnz, 1);
+  sk->log_packed.alloc(sizeof(unsigned long long) * m);
+  sk->log_packed_t.alloc(sizeof(unsigned long long) * m);
+  if (sk->nnz == 0) return;
+  const int g = loopcore::simple_grid(ctx, sk->nnz);
+  pack_log_kernel<<<g, 256, 0, ctx->stream>>>(sk->values.as<float>(), sk->col_idx.as<uint32_t>(), sk->nnz,
+                                              sk->log_packed.as<unsigned long long>());
+  pack_log_kernel<<<g, 256, 0, ctx->stream>>>(sk->values_t.as<float>(), sk->row_idx.as<uint32_t>(), sk->nnz,
+                                              sk->log_packed_t.as<unsigned long long>());
+  ctx->launches += 2;
+}
+
+template <int CS, int U, bool PACKED, bool FAST>
+static void launch_batch(spk_ctx* ctx, const BatchArgs& B, int count, size_t smem) {
+  auto kern = batch_log_kernel<CS, U, PACKED, FAST>;
+  loopcore::allow_max_dyn_smem((const void*)kern);
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = dim3((unsigned)(count * CS));
+  lc.blockDim = dim3(kBatchThreads);
+  lc.dynamicSmemBytes = smem;
+  lc.stream = ctx->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CS;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  BatchArgs a = B;
+  void* args[] = {&a};
+  SPK_CUDA(cudaLaunchKernelExC(&lc, (const void*)kern, args));
+}
+
+template <bool PACKED, bool FAST>
+static void launch_batch_cs(spk_ctx* ctx, const BatchArgs& B, int count, size_t smem) {
+  const int cs = ctx->batch_cluster;
+  const int u = ctx->batch_unroll;
+  if (cs == 1) {
+    if (u == 8) launch_batch<1, 8, PACKED, FAST>(ctx, B, count, smem);
+    else launch_batch<1, 4, PACKED, FAST>(ctx, B, count, smem);
+  } else if (cs == 4) {
+    if (u == 8) launch_batch<4, 8, PACKED, FAST>(ctx, B, count, smem);
+    else launch_batch<4, 4, PACKED, FAST>(ctx, B, count, smem);
+  } else {
+    if (u == 8) launch_batch<2, 8, PACKED, FAST>(ctx, B, count, smem);
+    else launch_batch<2, 4, PACKED, FAST>(ctx, B, count, smem);
+  }
+}
+
 // The batched loop over sks[0..count); returns per-item loop outcomes.
 void run_batch_log(spk_ctx* ctx, spk_sketch* const* sks, int count, const spk_solver_cfg& cfg,
                    const std::vector<double>& exponents, int policy, std::vector<LoopOut>& outs,
@@ -371,8 +496,11 @@ void run_batch_log(spk_ctx* ctx, spk_sketch* const* sks, int count, const spk_so
   for (int k = 0; k < count; ++k) {
     spk_sketch* sk = sks[k];
     const int64_t n = sk->n;
+    if (n > 65536) fail(SPK_E_LENGTH_MISMATCH, "batched loop: dimension above 65536");
+    const bool packed = sk->value_type == SPK_VALUES_F32;
     ensure_coverage(ctx, sk);
-    ensure_log_values(ctx, sk);
+    if (packed) ensure_log_packed(ctx, sk);
+    else ensure_log_values(ctx, sk);
     LoopWs& W = sk->ws;
     W.la.ensure(sizeof(double) * n);
     W.lb.ensure(sizeof(double) * n);
@@ -384,13 +512,19 @@ void run_batch_log(spk_ctx* ctx, spk_sketch* const* sks, int count, const spk_so
     sk->lu.ensure(sizeof(double) * n);
     sk->lv.ensure(sizeof(double) * n);
     BatchItem& I = items[k];
+    I = BatchItem{};
     I.n = n;
     I.row_ptr = sk->row_ptr.as<long long>();
-    I.col_idx = sk->col_idx.as<uint32_t>();
-    I.lval = sk->log_values.as<double>();
     I.col_ptr = sk->col_ptr.as<long long>();
-    I.row_idx = sk->row_idx.as<uint32_t>();
-    I.lval_t = sk->log_values_t.as<double>();
+    if (packed) {
+      I.lpack = sk->log_packed.as<unsigned long long>();
+      I.lpack_t = sk->log_packed_t.as<unsigned long long>();
+    } else {
+      I.col_idx = sk->col_idx.as<uint32_t>();
+      I.lval = sk->log_values.as<double>();
+      I.row_idx = sk->row_idx.as<uint32_t>();
+      I.lval_t = sk->log_values_t.as<double>();
+    }
     I.la = W.la.as<double>();
     I.lb = W.lb.as<double>();
     I.cov_row = sk->cov_row.as<unsigned char>();
@@ -408,13 +542,13 @@ void run_batch_log(spk_ctx* ctx, spk_sketch* const* sks, int count, const spk_so
   A.policy = policy;
   A.npad = npad;
   const size_t smem = sizeof(double) * 2 * npad + sizeof(unsigned int) * 2 * (npad / 32);
-  // fp32 sketches take the fp32-accurate exp (as spk_sketch_solve); a batch
-  // mixing storage types runs its fp64 ones with fp64 exp in a second launch
+  // fp32 sketches: packed stream + fp32-accurate exp (as spk_sketch_solve);
+  // fp64 sketches: u32 + fp64 stream, fp64 exp -- one launch per storage type
   Timer tm(s);
   for (int f32 = 0; f32 < 2; ++f32) {
     std::vector<int> sel;
     for (int k = 0; k < count; ++k)
-      if ((sks[k]->value_type == SPK_VALUES_F32 && !ctx->deterministic) == (f32 == 1)) sel.push_back(k);
+      if ((sks[k]->value_type == SPK_VALUES_F32) == (f32 == 1)) sel.push_back(k);
     if (sel.empty() || cfg.max_iter <= 0) continue;
     DBuf d_sel_items;
     std::vector<BatchItem> part(sel.size());
@@ -424,9 +558,8 @@ void run_batch_log(spk_ctx* ctx, spk_sketch* const* sks, int count, const spk_so
     B.items = d_sel_items.as<BatchItem>();
     DBuf d_part_status(sizeof(BatchStatus) * sel.size());
     B.status = d_part_status.as<BatchStatus>();
-    auto kern = f32 ? batch_log_kernel<LogKf> : batch_log_kernel<LogK>;
-    loopcore::allow_max_dyn_smem((const void*)kern);
-    kern<<<(int)sel.size(), kBatchThreads, smem, s>>>(B);
+    if (f32) launch_batch_cs<true, true>(ctx, B, (int)sel.size(), smem);
+    else launch_batch_cs<false, false>(ctx, B, (int)sel.size(), smem);
     ++ctx->launches;
     SPK_CUDA(cudaGetLastError());
     std::vector<BatchStatus> ps(sel.size());

@@ -114,6 +114,8 @@ struct spk_sketch {
   spk::DBuf row_ptr, col_idx, values;   // int64[n+1], u32[nnz], f64|f32[nnz]
   spk::DBuf col_ptr, row_idx, values_t; // CSC
   spk::DBuf log_values, log_values_t;   // lazily built log K~ (same dtype)
+  spk::DBuf log_packed, log_packed_t;   // batched loop, fp32 sketches: u64 per entry = log K~ (fp64, 37-bit
+                                        // mantissa) with the 16-bit column / row index in the low bits
   spk::DBuf a, b;                       // f64[n] weights given at build
   bool have_ab = false;
   double a_total = 0.0, b_total = 0.0;
@@ -152,6 +154,8 @@ struct spk_ctx {
   int blocked_split = 0;       // column parts per row slab: 0 auto, 1, 2
   int blocked_spread = 1;      // slab x block layout: spread gathered columns over banks (slot_kernel)
   int blocked_cluster = 1;     // CTA pairs as 2-CTA clusters (DSMEM partial sums) when they all fit
+  int batch_cluster = 2;       // batched log loop: CTAs (SMs) per sketch, 1 / 2 / 4
+  int batch_unroll = 4;        // batched log loop: entry loads in flight per lane, 4 / 8
   int force_two_pass = 0;      // sampler: skip the single-pass tiled path (testing)
   int64_t launches = 0;
   // last error

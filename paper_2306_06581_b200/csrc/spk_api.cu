@@ -267,11 +267,39 @@ int spk_ctx_set_option(spk_ctx* ctx, int key, int64_t value) {
     case SPK_OPT_LOOP_BLOCKS_PER_SM: ctx->loop_blocks_per_sm = (int)value; return SPK_OK;
     case 3: ctx->otf_fp32 = value ? 1 : 0; return SPK_OK;
     case 4: ctx->use_blocked = (int)std::max<int64_t>(0, std::min<int64_t>(value, 2)); return SPK_OK;
-    case 5: ctx->blocked_max_w = (int)std::max<int64_t>(16, std::min<int64_t>(value, 16384)); return SPK_OK;
+    case 5:  // multiple of 16 elements: every tile's TMA source stays 16-byte aligned
+      ctx->blocked_max_w = (int)(std::max<int64_t>(16, std::min<int64_t>(value, 16384)) & ~int64_t(15));
+      return SPK_OK;
     case 6: ctx->force_two_pass = value ? 1 : 0; return SPK_OK;
     case 9: ctx->blocked_cluster = value ? 1 : 0; return SPK_OK;
+    case 10:
+      if (value != 1 && value != 2 && value != 4) return SPK_STATUS_INPUT;
+      ctx->batch_cluster = (int)value;
+      return SPK_OK;
+    case 11:
+      if (value != 4 && value != 8) return SPK_STATUS_INPUT;
+      ctx->batch_unroll = (int)value;
+      return SPK_OK;
     case 8: ctx->blocked_spread = value ? 1 : 0; return SPK_OK;
     case 7: ctx->blocked_split = (int)std::max<int64_t>(0, std::min<int64_t>(value, 2)); return SPK_OK;
+    default: return SPK_STATUS_INPUT;
+  }
+}
+
+int spk_ctx_get_option(const spk_ctx* ctx, int key, int64_t* value) {
+  if (!ctx || !value) return SPK_STATUS_INPUT;
+  switch (key) {
+    case SPK_OPT_DETERMINISTIC: *value = ctx->deterministic; return SPK_OK;
+    case SPK_OPT_LOOP_BLOCKS_PER_SM: *value = ctx->loop_blocks_per_sm; return SPK_OK;
+    case 3: *value = ctx->otf_fp32; return SPK_OK;
+    case 4: *value = ctx->use_blocked; return SPK_OK;
+    case 5: *value = ctx->blocked_max_w; return SPK_OK;
+    case 6: *value = ctx->force_two_pass; return SPK_OK;
+    case 7: *value = ctx->blocked_split; return SPK_OK;
+    case 8: *value = ctx->blocked_spread; return SPK_OK;
+    case 9: *value = ctx->blocked_cluster; return SPK_OK;
+    case 10: *value = ctx->batch_cluster; return SPK_OK;
+    case 11: *value = ctx->batch_unroll; return SPK_OK;
     default: return SPK_STATUS_INPUT;
   }
 }
@@ -540,9 +568,12 @@ int spk_sketch_solve(spk_ctx* ctx, spk_sketch* sk, const double* a, const double
 }
 
 int spk_sketch_solve_batch(spk_ctx* ctx, spk_sketch* const* sks, int count, const spk_solver_cfg* cfg, int uot,
-                           spk_report* reps) {
+                           spk_report* reps, int32_t* item_error) {
   if (!ctx || (count > 0 && !sks)) return SPK_STATUS_INPUT;
-  for (int k = 0; k < count; ++k) init_report(reps ? reps + k : nullptr);
+  for (int k = 0; k < count; ++k) {
+    init_report(reps ? reps + k : nullptr);
+    if (item_error) item_error[k] = 0;
+  }
   return guard(ctx, [&] {
     check_cfg(cfg);
     if (count < 0) fail(SPK_E_LENGTH_MISMATCH, "negative batch size");
@@ -557,33 +588,74 @@ int spk_sketch_solve_batch(spk_ctx* ctx, spk_sketch* const* sks, int count, cons
       f[k] = solver_exponent(*cfg, uot, sk->a_total, sk->b_total);
       if (sk->n > nmax || sk->n_cols) batched = false;
     }
+    // per-item outcome: with item_error the batch carries on past a failing
+    // item (pairwise_wfr marks that pair NaN, harness.cpp:395-401); without it
+    // the call fails with the lowest failing item
+    int first_bad = -1;
+    std::vector<std::string> pre_errs(count);
+    std::vector<int> pre_kinds(count, 0);
+    auto item_failed = [&](int k, int kind, const std::string& msg) {
+      pre_kinds[k] = kind;
+      pre_errs[k] = msg;
+      sks[k]->last_valid = 0;
+      if (item_error) item_error[k] = kind;
+      if (first_bad < 0) first_bad = k;
+    };
     if (!batched) {  // one solve at a time (linear domain, parity mode, or large sketches)
-      for (int k = 0; k < count; ++k) solve_on_sketch(ctx, sks[k], *cfg, uot, policy, reps ? reps + k : nullptr);
+      for (int k = 0; k < count; ++k) {
+        try {
+          solve_on_sketch(ctx, sks[k], *cfg, uot, policy, reps ? reps + k : nullptr);
+        } catch (const Failure& e) {
+          if (!item_error || e.kind == SPK_E_DEVICE) throw;
+          item_failed(k, e.kind, e.what());
+        }
+      }
       return;
     }
     // structural coverage and the loop's entry checks (solvers.hpp:411-414)
+    std::vector<spk_sketch*> run;
+    std::vector<int> run_k;
+    std::vector<double> run_f;
     for (int k = 0; k < count; ++k) {
       spk_sketch* sk = sks[k];
       ensure_coverage(ctx, sk);
-      if ((sk->cov_empty_rows || sk->cov_empty_cols) && policy == SPK_POLICY_ERROR)
-        fail(SPK_E_ZERO_DENOMINATOR, "batch item " + std::to_string(k) + ": kernel has empty rows or columns");
-      if (sk->cov_empty_rows == sk->n || sk->cov_empty_cols == sk->n)
-        fail(SPK_E_DEGENERATE_SKETCH_ERROR, "batch item " + std::to_string(k) + ": kernel has no entries at all");
+      int kind = 0;
+      std::string msg;
+      if ((sk->cov_empty_rows || sk->cov_empty_cols) && policy == SPK_POLICY_ERROR) {
+        kind = SPK_E_ZERO_DENOMINATOR;
+        msg = "kernel has empty rows or columns";
+      }
+      if (sk->cov_empty_rows == sk->n || sk->cov_empty_cols == sk->n) {
+        kind = SPK_E_DEGENERATE_SKETCH_ERROR;
+        msg = "kernel has no entries at all";
+      }
+      if (kind) {
+        if (!item_error) fail(kind, "batch item " + std::to_string(k) + ": " + msg);
+        item_failed(k, kind, msg);
+        continue;
+      }
+      run.push_back(sk);
+      run_k.push_back(k);
+      run_f.push_back(f[k]);
     }
     std::vector<LoopOut> outs;
     std::vector<std::string> errs;
     std::vector<int> kinds;
-    run_batch_log(ctx, sks, count, *cfg, f, policy, outs, errs, kinds);
-    int first_bad = -1;
-    for (int k = 0; k < count; ++k) {
+    run_batch_log(ctx, run.data(), (int)run.size(), *cfg, run_f, policy, outs, errs, kinds);
+    for (size_t q = 0; q < run.size(); ++q) {
+      const int k = run_k[q];
       spk_sketch* sk = sks[k];
-      const LoopOut& lo = outs[k];
-      sk->last_valid = kinds[k] ? 0 : 1;
+      const LoopOut& lo = outs[q];
+      sk->last_valid = kinds[q] ? 0 : 1;
       sk->last_log_domain = 1;
       sk->masked_rows = lo.masked_rows;
       sk->masked_cols = lo.masked_cols;
-      if (kinds[k]) {
-        if (first_bad < 0) first_bad = k;
+      if (kinds[q]) {
+        sk->last_valid = 0;
+        pre_kinds[k] = kinds[q];
+        pre_errs[k] = errs[q];
+        if (item_error) item_error[k] = kinds[q];
+        if (first_bad < 0 || k < first_bad) first_bad = k;
         continue;
       }
       ReadoutOut ro;  // residuals from the plan marginals (solvers.hpp:380-389)
@@ -611,7 +683,16 @@ int spk_sketch_solve_batch(spk_ctx* ctx, spk_sketch* const* sks, int count, cons
         rep->factorized_plan = sk->factorized_plan;
       }
     }
-    if (first_bad >= 0) fail(kinds[first_bad], "batch item " + std::to_string(first_bad) + ": " + errs[first_bad]);
+    if (first_bad >= 0 && !item_error)
+      fail(pre_kinds[first_bad], "batch item " + std::to_string(first_bad) + ": " + pre_errs[first_bad]);
+  });
+}
+
+int spk_sketch_scalings(spk_sketch* sk, double* u, double* v, double* log_u, double* log_v) {
+  if (!sk) return SPK_STATUS_INPUT;
+  return guard(sk->ctx, [&] {
+    if (!sk->last_valid) fail(SPK_E_LENGTH_MISMATCH, "no solve has run on this sketch");
+    copy_scalings(sk->ctx, sk, sk->n, sk->last_log_domain, u, v, log_u, log_v);
   });
 }
 

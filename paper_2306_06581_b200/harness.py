@@ -49,6 +49,7 @@ def rmae_experiment(ctx: Context, support, a, b, cfg: SolverConfig, budgets, rep
     x = np.ascontiguousarray(support, dtype=np.float64)
     uot = eta is not None
     kern = Coords(x, x, "wfr" if uot else "sqeuclid", eta or 0.0, scale=1.0, eps=cfg.epsilon)
+    prev_fp32 = ctx.get_option(L.OPT_OTF_FP32)
     ctx.set_option(L.OPT_OTF_FP32, 0)  # the exact baseline is the fp64 dense solve
     try:
         base = ctx.sinkhorn(kern, a, b, cfg, uot=uot)
@@ -56,7 +57,7 @@ def rmae_experiment(ctx: Context, support, a, b, cfg: SolverConfig, budgets, rep
         from .api import ERRORS
         raise ERRORS["BaselineFailed"](f"BaselineFailed: {e}")
     finally:
-        ctx.set_option(L.OPT_OTF_FP32, 1)
+        ctx.set_option(L.OPT_OTF_FP32, prev_fp32)  # the caller's setting, not a default
     exact = base.report["objective"]
     if exact == 0.0:
         from .api import ERRORS
@@ -81,6 +82,8 @@ def rmae_experiment(ctx: Context, support, a, b, cfg: SolverConfig, budgets, rep
                         raise
                     retried += 1
             errors.append(abs(approx - exact) / abs(exact))
+        if world > 1:  # every rank computed a disjoint subset: merge before the statistics
+            errors, retried = _merge_ranks(errors, retried, world)
         e = np.asarray([v for v in errors if not math.isnan(v)])
         mean = float(e.sum() / len(e)) if len(e) else math.nan
         var = float(((e - mean) ** 2).sum()) if len(e) else math.nan
@@ -88,3 +91,17 @@ def rmae_experiment(ctx: Context, support, a, b, cfg: SolverConfig, budgets, rep
         rows.append({"budget": s, "errors": errors, "mean": mean, "std_error": se, "retried": retried})
     return {"exact_objective": exact, "rows": rows, "replications": replications,
             "method": method}
+
+
+def _merge_ranks(errors: list[float], retried: int, world: int) -> tuple[list[float], int]:
+    """Replication r was run by rank r % world: gather every rank's errors
+    (torch.distributed, any backend) so mean / std_error cover all
+    replications as the reference's single loop does (harness.cpp:213-225)."""
+    import torch.distributed as dist
+
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() != world:
+        raise RuntimeError("rmae_experiment with world > 1 needs an initialised torch.distributed group of that size")
+    gathered: list = [None] * world
+    dist.all_gather_object(gathered, (errors, retried))
+    merged = [gathered[r % world][0][r] for r in range(len(errors))]
+    return merged, int(sum(g[1] for g in gathered))

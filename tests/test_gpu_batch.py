@@ -88,6 +88,17 @@ def test_batch_error_policy_and_linear_fallback(ctx, oracle):
     reps = api.solve_batch(ctx, [good, bad], lin)
     one = good.solve(lin)
     assert reps[0]["iterations"] == one.report["iterations"]
+    # per-item outcomes (pairwise_wfr, harness.cpp:395-401): the failing item is
+    # recorded, the others complete and keep their scalings
+    for c in (cfg, lin):
+        reps = api.solve_batch(ctx, [bad, good, bad], c, policy="error", per_item=True)
+        assert [r["error"] for r in reps] == ["ZeroDenominator", None, "ZeroDenominator"]
+        ref = good.solve(c)
+        u, v, _, _ = api.solve_batch(ctx, [bad, good], c, policy="error", per_item=True) and good.scalings()
+        np.testing.assert_allclose(u, ref.u, rtol=1e-12)
+        np.testing.assert_allclose(v, ref.v, rtol=1e-12)
+        with pytest.raises(spk.ERRORS["LengthMismatch"]):
+            bad.scalings()  # no valid solve on the failed item
 
 
 def test_sketch_batch_equals_one_at_a_time(ctx):

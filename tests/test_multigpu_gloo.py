@@ -94,3 +94,31 @@ def test_sharded_driver_gloo_matches_oracle(tmp_path, case, world):
     for d in outs[1:]:
         np.testing.assert_array_equal(d["u"], outs[0]["u"])
         np.testing.assert_array_equal(d["rep"], outs[0]["rep"])
+
+
+def _rmae_merge_worker(rank, world, port, outdir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    sys.path.insert(0, str(ROOT))
+    import torch.distributed as dist
+
+    from paper_2306_06581_b200.harness import _merge_ranks
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    reps = 7
+    # rank r ran replications r, r + world, ... (rmae_experiment's split)
+    errors = [0.1 * (k + 1) if k % world == rank else math.nan for k in range(reps)]
+    merged, retried = _merge_ranks(errors, rank + 1, world)
+    np.save(Path(outdir) / f"m{rank}.npy", np.asarray(merged + [retried]))
+    dist.destroy_process_group()
+
+
+def test_rmae_ranks_merge_before_statistics(tmp_path):
+    """rmae_experiment at world > 1: every rank ends with ALL replications'
+    errors (so mean / std_error match the reference's single loop)."""
+    import torch.multiprocessing as mp
+
+    mp.spawn(_rmae_merge_worker, args=(2, _free_port(), str(tmp_path)), nprocs=2, join=True)
+    for r in range(2):
+        m = np.load(tmp_path / f"m{r}.npy")
+        np.testing.assert_allclose(m[:-1], 0.1 * np.arange(1, 8))
+        assert m[-1] == 3  # retried counts summed over ranks
