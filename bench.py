@@ -172,6 +172,8 @@ def run_reference(args, ws, rank):
     from oracle import Oracle, Reference
     from paper_2306_06581_b200 import workloads as W
 
+    if args.config == "c3":
+        return run_reference_c3(args)
     w = W.CONFIGS[args.config]()
     iters = args.ref_iters
     t0 = time.time()
@@ -213,9 +215,84 @@ def run_reference(args, ws, rank):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": w.name, "n": w.n, "iterations_per_step": iters, "nnz": int(csr[0][-1])},
-        "cpu_baseline": {"value": value, "unit": "iters/s", "cores": 1, "kind": kind, "sample": sample},
+        "cpu_baseline": {"value": value, "unit": "iters/s", "cores": 1, "host_cores": os.cpu_count(), "kind": kind,
+                         "sample": sample},
         "e2e": {"value": value, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "extra": {"prep_s": prep, "note": "reference is single-threaded (proj/CMakeLists.txt:19; no OpenMP)"},
+        "extra": {"prep_s": prep, "note": f"one solve is single-threaded in the reference (proj/CMakeLists.txt:19; "
+                                          f"no OpenMP): 1 of {os.cpu_count()} host cores"},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def c3_reference_pool(P: int, iters: int, sketches=None):
+    """Config 3 on the host as the reference runs it: independent frame pairs,
+    one single-threaded reference solve (log-domain sinkhorn_uot<SparseKernel>)
+    per host thread, P threads at once (ctypes drops the GIL). sketches: the
+    first P pairs' CSR (default: the reference's own spar_sink sketches on
+    its dense WFR kernel). Returns (step(), sample)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import Reference
+    from paper_2306_06581_b200 import api
+    from paper_2306_06581_b200 import workloads as W
+
+    R = Reference()
+    coords, masses = W.c3_frames(3)
+    n = coords.shape[0]
+    pairs = api.frame_pairs(masses.shape[0])[:P]
+    if sketches is None:
+        Cm, _ = R.pairwise_cost(coords, coords, "wfr", 0.1)
+        K, ratio = R.kernel_from_cost(Cm, 0.01)
+        del Cm
+        s = 10 * n * math.log(n)
+
+        def draw(k):
+            i, j = pairs[k]
+            return R.poisson_sparsify("uot", masses[i], masses[j], K, ratio, s, api.mix_seed(3, k), 1.0, 0.01)
+
+        with ThreadPoolExecutor(P) as ex:
+            sketches = list(ex.map(draw, range(P)))
+        del K
+        src = "the reference's own sketches (poisson_sparsify on its dense WFR kernel)"
+    else:
+        src = "the GPU-built sketches copied to host"
+
+    def one(k):
+        i, j = pairs[k]
+        secs, _ = R.sparse_loop_seconds(sketches[k], masses[i], masses[j], 0.01, iters, 1.0, True, stabilize=True)
+        return secs
+
+    def step():
+        t0 = time.perf_counter()
+        with ThreadPoolExecutor(P) as ex:
+            list(ex.map(one, range(P)))
+        return time.perf_counter() - t0
+
+    sample = (f"{P} frame pairs at once (1 reference solve per host thread, {P} of {os.cpu_count()} cores), "
+              f"{iters} log-domain iterations of sinkhorn_uot<SparseKernel> each per step, on {src}")
+    return step, sample
+
+
+def run_reference_c3(args):
+    P = max(1, min(os.cpu_count() or 1, 496))
+    iters = args.ref_iters
+    t0 = time.time()
+    step, sample = c3_reference_pool(P, iters)
+    prep = time.time() - t0
+    for _ in range(args.warmup):
+        step()
+    times = [step() for _ in range(args.steps)]
+    total = sum(times)
+    value = args.steps * P * iters / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "C3", "n": 12544, "pairs": 496, "pairs_timed": P, "iterations_per_step": P * iters},
+        "cpu_baseline": {"value": value, "unit": "iters/s", "cores": P, "host_cores": os.cpu_count(),
+                         "kind": "reference", "sample": sample},
+        "e2e": {"value": value, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "extra": {"prep_s": prep, "all_496_pairs_1000_iterations_s_extrapolated": 496 * 1000 / value},
     }
     print(json.dumps(line), flush=True)
 
@@ -242,6 +319,14 @@ def run_ours(args, ws, rank, local):
         from paper_2306_06581_b200 import _lib as L
 
         ctx.set_option(L.OPT_BLOCKED_SPREAD, int(os.environ["SPK_SPREAD"]))
+    if os.environ.get("SPK_SMALL") is not None:  # one-cluster loop for small sketches (profiling)
+        from paper_2306_06581_b200 import _lib as L
+
+        ctx.set_option(L.OPT_SMALL_LOOP, int(os.environ["SPK_SMALL"]))
+    if os.environ.get("SPK_SMALL_CS") is not None:
+        from paper_2306_06581_b200 import _lib as L
+
+        ctx.set_option(L.OPT_SMALL_CLUSTER, int(os.environ["SPK_SMALL_CS"]))
     if os.environ.get("SPK_CLUSTER") is not None:  # CTA pairs as clusters (profiling)
         from paper_2306_06581_b200 import _lib as L
 
@@ -326,9 +411,27 @@ def run_ours(args, ws, rank, local):
         else:
             t, _, _ = Oracle().time_scaling_iters((rp, ci, vv), w.a, w.b, k_cpu)
             secs, kind = t * k_cpu, "port"
-        cpu = {"value": k_cpu / secs, "unit": "iters/s", "cores": 1, "kind": kind,
+        cpu = {"value": k_cpu / secs, "unit": "iters/s", "cores": 1, "host_cores": os.cpu_count(), "kind": kind,
                "sample": f"{k_cpu} of {iters} iterations of sinkhorn_{plan}<SparseKernel> on the GPU-built "
-                         f"{w.name} sketch ({sk.nnz} nnz) copied to host, 1 core (reference is single-threaded)"}
+                         f"{w.name} sketch ({sk.nnz} nnz) copied to host, 1 of {os.cpu_count()} host cores "
+                         f"(one reference solve is single-threaded)"}
+        if args.config == "c4":
+            # the reference cannot build config 4's dense K (8 TB); its sampler
+            # (poisson_sparsify, sparsify.cpp:169-201) restated on coordinates
+            # (oracle) on a row sample, extrapolated to all n rows (labelled)
+            plan = sk.plan()
+            ra = np.sqrt(w.a)
+            sa = 0.0
+            for t_ in ra.tolist():
+                sa += t_
+            rows = 100
+            t0 = time.perf_counter()
+            Oracle().sample_rows_coords(w.x, w.y, "sqeuclid", 0.0, w.scale, w.eps, "ot", plan["factorized"],
+                                        ra / sa, ra / sa, 0.0, plan["inv"], w.s, 7, 0, rows)
+            ts = time.perf_counter() - t0
+            cpu["sampler"] = {"rows_timed": rows, "seconds": ts, "extrapolated_all_rows_s": ts * w.n / rows,
+                              "kind": "port (oracle restatement of poisson_sparsify on coordinates), 1 core",
+                              "gpu_sample_s": e2e["phases_s"]["sample"] if e2e else None}
 
     line = {
         "metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": ws, "steps": args.steps,
@@ -518,21 +621,11 @@ def run_c3_batch(args, ws, rank, local):
                "pairs": len(pairs), "objective_pair0": out[0][2]["objective"] if out else None}
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
-        from oracle import Oracle, Reference
-
-        rp, ci, vv = sks[0].csr()
-        k_cpu = args.cpu_iters
-        i, j = pairs[0]
-        if Reference.available():
-            secs, _ = Reference().sparse_loop_seconds((rp, ci, vv), masses[i], masses[j], 0.01, k_cpu, 1.0, True,
-                                                      stabilize=True)
-            kind = "reference"
-        else:
-            t, _, _ = Oracle().time_scaling_iters((rp, ci, vv), masses[i], masses[j], k_cpu)
-            secs, kind = t * k_cpu, "port"
-        cpu = {"value": k_cpu / secs, "unit": "iters/s", "cores": 1, "kind": kind,
-               "sample": f"{k_cpu} log-domain iterations of sinkhorn_uot<SparseKernel> on pair 0's GPU-built sketch "
-                         f"({len(ci)} nnz) copied to host, 1 core (reference is single-threaded; one pair)"}
+        P = max(1, min(os.cpu_count() or 1, len(sks)))
+        step, sample = c3_reference_pool(P, args.cpu_iters, [sks[k].csr() for k in range(P)])
+        secs = step()
+        cpu = {"value": P * args.cpu_iters / secs, "unit": "iters/s", "cores": P, "host_cores": os.cpu_count(),
+               "kind": "reference", "sample": sample}
     for sk in sks:
         sk.free()
     line = {
@@ -565,7 +658,7 @@ def main():
     ap.add_argument("--config", default="c4", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--iters", type=int, default=0, help="iterations per step (default: the config's)")
     ap.add_argument("--cpu-iters", type=int, default=10)
-    ap.add_argument("--ref-iters", type=int, default=3)
+    ap.add_argument("--ref-iters", type=int, default=10)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()

@@ -17,7 +17,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-CUDA_SOURCES = ["spk_api.cu", "sampler.cu", "loop.cu", "blocked.cu", "dense.cu", "readout.cu", "shard.cu", "ibp.cu", "batch.cu"]
+CUDA_SOURCES = ["spk_api.cu", "sampler.cu", "loop.cu", "blocked.cu", "dense.cu", "readout.cu", "shard.cu", "ibp.cu", "batch.cu", "small.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr",
               "-Xptxas", "-v", "-I", str(ROOT / "include")]

@@ -28,6 +28,9 @@ OPT_BLOCKED_SPREAD = 8
 OPT_BLOCKED_CLUSTER = 9
 OPT_BATCH_CLUSTER = 10
 OPT_BATCH_UNROLL = 11
+OPT_SMALL_LOOP = 12
+OPT_SMALL_CLUSTER = 13
+OPT_SMALL_MAX_NNZ = 14
 
 ERROR_CLASSES = {
     1: "Error", 2: "NegativeWeight", 3: "LengthMismatch", 4: "NotNormalized", 5: "AllBlack",

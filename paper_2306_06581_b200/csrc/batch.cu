@@ -125,10 +125,17 @@ struct Stream {
   }
 };
 
+// exp(d), d <= 0 (or -inf): fp32 MUFU.EX2 on the fp64-formed exponent (FAST)
+// or fp64 exp
 template <bool FAST>
-__device__ __forceinline__ double lse_exp(double d) {
-  if constexpr (FAST) return exp_fast(d);
-  else return exp(d);
+__device__ __forceinline__ typename std::conditional<FAST, float, double>::type lse_term(double d) {
+  if constexpr (FAST) {
+    float r;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(__double2float_rn(d) * 1.44269504088896341f));
+    return r;
+  } else {
+    return exp(d);
+  }
 }
 
 __device__ __forceinline__ double* peer_ptr(double* p, unsigned rank) {
@@ -199,40 +206,42 @@ __device__ __forceinline__ double batch_half(int64_t i_lo, int64_t i_hi, const l
         en = __ldg(ptr + inext + 1);
       }
     }
-    double m = -CUDART_INF, s = 0.0;
+    // online log-sum-exp: running max m (fp64) and the sum of exp(t - m).
+    // FAST (fp32 sketches): each term's exponent t - m is formed in fp64 (no
+    // cancellation), then exp2 runs on MUFU.EX2 and the lane's sum is fp32 --
+    // the fp32 bar of the stored K~; fp64 sketches keep fp64 exp and sums.
+    // A -inf term (K~ = 0 or a masked column) contributes exp(-inf) = 0.
+    using Acc = typename std::conditional<FAST, float, double>::type;
+    double m = -CUDART_INF;
+    Acc s = 0;
     for (long long p = b + gl; p < e; p += U * kG) {
-      uint32_t j[U];
-      double l[U];
-#pragma unroll
-      for (int k = 0; k < U; ++k) {
-        if (p + k * kG < e) st.load(p + k * kG, j[k], l[k]);
-        else {
-          j[k] = 0;
-          l[k] = -CUDART_INF;
-        }
-      }
       double t[U];
-      double M = m;
 #pragma unroll
       for (int k = 0; k < U; ++k) {
-        t[k] = l[k] == -CUDART_INF ? -CUDART_INF : l[k] + x[j[k]];  // x = -inf: masked column
-        M = fmax(M, t[k]);
+        uint32_t j = 0;
+        double l = -CUDART_INF;
+        if (p + k * kG < e) st.load(p + k * kG, j, l);
+        t[k] = l + x[j];
       }
-      if (M != -CUDART_INF) {
-        double acc = (m == -CUDART_INF) ? 0.0 : s * lse_exp<FAST>(m - M);
+      double M = t[0];
 #pragma unroll
-        for (int k = 0; k < U; ++k) acc += (t[k] == -CUDART_INF) ? 0.0 : lse_exp<FAST>(t[k] - M);
-        s = acc;
+      for (int k = 1; k < U; ++k) M = fmax(M, t[k]);
+      if (M == -CUDART_INF) continue;  // every term of the block is -inf
+      if (M > m) {
+        s = (m == -CUDART_INF) ? Acc(0) : s * lse_term<FAST>(m - M);
         m = M;
       }
+#pragma unroll
+      for (int k = 0; k < U; ++k) s += lse_term<FAST>(t[k] - m);
     }
 #pragma unroll
     for (int o = kG / 2; o; o >>= 1) {
       const double m2 = __shfl_xor_sync(0xffffffffu, m, o);
-      const double s2 = __shfl_xor_sync(0xffffffffu, s, o);
+      const Acc s2 = __shfl_xor_sync(0xffffffffu, s, o);
       const double M = fmax(m, m2);
       if (M != -CUDART_INF)
-        s = (m == -CUDART_INF ? 0.0 : s * lse_exp<FAST>(m - M)) + (m2 == -CUDART_INF ? 0.0 : s2 * lse_exp<FAST>(m2 - M));
+        s = (m == -CUDART_INF ? Acc(0) : s * lse_term<FAST>(m - M)) +
+            (m2 == -CUDART_INF ? Acc(0) : s2 * lse_term<FAST>(m2 - M));
       m = M;
     }
     {  // the next row group's entries into L2 while this one finishes
@@ -240,7 +249,7 @@ __device__ __forceinline__ double batch_half(int64_t i_lo, int64_t i_hi, const l
       if (inext < i_hi && en > bn) st.prefetch_l2(bn, en, gl);
     }
     if (live && gl == 0) {
-      const double lse = m == -CUDART_INF ? -CUDART_INF : m + log(s);
+      const double lse = m == -CUDART_INF ? -CUDART_INF : m + log((double)s);
       double nv;
       bool write = true;
       if (lse == -CUDART_INF) {

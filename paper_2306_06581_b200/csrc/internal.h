@@ -156,6 +156,11 @@ struct spk_ctx {
   int blocked_cluster = 1;     // CTA pairs as 2-CTA clusters (DSMEM partial sums) when they all fit
   int batch_cluster = 2;       // batched log loop: CTAs (SMs) per sketch, 1 / 2 / 4
   int batch_unroll = 4;        // batched log loop: entry loads in flight per lane, 4 / 8
+  int small_loop = 1;          // fast-mode loop on one cluster for small sketches (small.cu)
+  int small_cluster = 16;      // its cluster size (largest that launches; 16 = non-portable)
+  int64_t small_max_n = 14000;       // ... when both scaling vectors fit every CTA's shared memory
+  int64_t small_max_nnz = 4000000;   // ... and the sketch is small enough that 16 SMs stream it faster
+                                     //     than a grid barrier pair costs
   int force_two_pass = 0;      // sampler: skip the single-pass tiled path (testing)
   int64_t launches = 0;
   // last error
@@ -316,6 +321,9 @@ void run_sparse_loop(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, do
                      int policy, LoopState& st, LoopOut& out);
 void ensure_coverage(spk_ctx* ctx, spk_sketch* sk);
 void ensure_log_values(spk_ctx* ctx, spk_sketch* sk);
+// small.cu: the loop on one cluster (scalings in shared memory); false = not applicable
+bool run_cluster_loop(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, double exponent, int policy,
+                      LoopState& st, LoopOut& out);
 // batch.cu: one CTA per sketch, log domain, scalings in shared memory
 int64_t batch_max_n(spk_ctx* ctx);
 void run_batch_log(spk_ctx* ctx, spk_sketch* const* sks, int count, const spk_solver_cfg& cfg,

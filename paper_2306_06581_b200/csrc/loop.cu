@@ -209,6 +209,8 @@ void run_sparse_loop(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, do
                      LoopState& st, LoopOut& out) {
   const bool log_domain = cfg.stabilize != 0;
   ensure_coverage(ctx, sk);
+  // small sketches: one cluster, scalings in shared memory, no grid barriers
+  if (run_cluster_loop(ctx, sk, cfg, exponent, policy, st, out)) return;
   // fast linear-domain path: slab x block layout with TMA-staged scalings
   // (auto: large sketches only; the layout pays off once x no longer sits in L1/L2-friendly sizes)
   const bool try_blocked = ctx->use_blocked == 1 || (ctx->use_blocked == 2 && sk->n >= (int64_t(1) << 17));

@@ -358,6 +358,10 @@ struct cluster_of<Op, std::void_t<decltype(Op::kCluster)>> {
   static constexpr int value = Op::kCluster;
 };
 
+template <bool LOG>
+void loop_epilogue(spk_ctx* ctx, const Status& S, int64_t n, LoopWs& W, const double* uf, const double* vf,
+                   LoopState& st, LoopOut& out);
+
 // Host driver shared by every operator. row_ne / col_ne hold the structural
 // coverage (kernel_coverage, solvers.cpp:138-163); masked_rows/cols their
 // zero counts. Fills st.u/st.v (and st.lu/st.lv in the log domain).
@@ -483,7 +487,18 @@ void run_core(spk_ctx* ctx, const Op& op, int64_t n, LoopWs& W, long long masked
   SPK_CUDA(cudaGetLastError());
   Status S;
   download(ctx, &S, status, sizeof S);
+  loop_epilogue<LOG>(ctx, S, n, W, u2.as<double>() + (size_t)S.cur * npad, v2.as<double>() + (size_t)S.cur * npad, st,
+                     out);
+}
 
+// Loop outcome -> LoopOut (raising the loop's failures) and the final
+// scalings uf / vf (device, n each) -> st.u / st.v (+ st.lu / st.lv).
+template <bool LOG>
+void loop_epilogue(spk_ctx* ctx, const Status& S, int64_t n, LoopWs& W, const double* uf, const double* vf,
+                   LoopState& st, LoopOut& out) {
+  cudaStream_t s = ctx->stream;
+  DBuf& dyn_row = W.dyn_row;
+  DBuf& dyn_col = W.dyn_col;
   if (S.error_kind == SPK_E_ZERO_DENOMINATOR) {
     const std::string idx = std::to_string(S.error_index);
     if (LOG)
@@ -518,8 +533,6 @@ void run_core(spk_ctx* ctx, const Op& op, int64_t n, LoopWs& W, long long masked
     out.masked_rows = S.masked_rows;
     out.masked_cols = S.masked_cols;
   }
-  const double* uf = u2.as<double>() + (size_t)S.cur * npad;
-  const double* vf = v2.as<double>() + (size_t)S.cur * npad;
   st.u->ensure(sizeof(double) * n);
   st.v->ensure(sizeof(double) * n);
   if (LOG) {

@@ -1,0 +1,485 @@
+// small.cu -- the Sinkhorn loop for sketches small enough for shared memory
+// (configs 1 and 2: n = 1e3, 1e4): ONE cluster of CS CTAs (up to 16 SMs)
+// runs every iteration with no grid barrier.
+//
+// Reference semantics: detail::scaling_loop (include/sparsink/solvers.hpp:256-395)
+// and detail::log_scaling_loop (:397-513), per atom exactly as loop_core.cuh
+// (finalize_atom), fast-mode summation (warp per row, FMA / two-pass LSE).
+//
+// Why: at these sizes the persistent grid loop is bound by its two grid-wide
+// barriers per iteration (~10 us per iteration at C1), not by bytes. Here
+// every CTA of the cluster keeps BOTH scaling vectors (fp64, full length) in
+// its own shared memory, so the gathered x of a half is a shared-memory read.
+// A half is split over the CTAs by entry count; each CTA writes the new
+// values of its atoms into its own copy and, through DSMEM, into every
+// peer's copy; one cluster barrier (hardware, ~1 us less than a grid
+// barrier) publishes them with the CTA partials (residual, new masks, first
+// failing atom), which every CTA then combines in rank order -- the same
+// stop / failure decision everywhere. When the CTA's share of the sketch
+// (both halves) also fits, it is staged into shared memory once, and an
+// iteration touches no global memory except the per-atom mask state.
+// Divergence restore (:321-325, :352-356): each CTA keeps the previous
+// iterate of its own atoms and puts it back.
+#include <algorithm>
+#include <cmath>
+#include <type_traits>
+#include <vector>
+
+#include "common.cuh"
+#include "internal.h"
+#include "loop_core.cuh"
+#include "rowdot.cuh"
+
+namespace spk {
+
+namespace {
+
+using loopcore::finalize_atom;
+using loopcore::kNone;
+
+constexpr int kThreads = 1024;
+constexpr int kMaxCS = 16;
+
+template <class VT>
+struct ClusterArgs {
+  int64_t n;
+  // sketch halves (global); the CTA's share may be staged into shared memory
+  const long long* ptr[2];
+  const uint32_t* idx[2];
+  const VT* val[2];
+  int64_t lo[2][kMaxCS + 1];  // atom split of each half by entry count
+  const double* w[2];         // a, b (log domain: log a, log b)
+  unsigned char* ne[2];       // row / column non-empty flags (dynamic masks)
+  int* dyn[2];
+  double* out[2];  // final u, v (or log u, log v)
+  loopcore::Status* status;
+  long long max_iter;
+  double delta, exponent;
+  int policy;
+  long long masked0[2];
+  int npad;   // doubles per shared vector
+  int stage;  // 1: the CTA's sketch share lives in shared memory
+  int64_t stage_ent[2];  // max entries of one CTA's share per half (staged layout)
+  int64_t stage_rows[2];
+};
+
+struct Xch {
+  double err[2];
+  long long masks[2];
+  unsigned long long flag[2];
+};
+
+__device__ __forceinline__ unsigned cluster_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_barrier() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+template <class T>
+__device__ __forceinline__ T* peer(T* p, unsigned rank) {
+  T* q;
+  asm volatile("mapa.u64 %0, %1, %2;" : "=l"(q) : "l"(p), "r"(rank));
+  return q;
+}
+
+// Warp-per-row dot with generic (shared or global) sketch pointers and a
+// shared x: linear sum of v * x (FMA), or the two-pass log-sum-exp
+// (solvers.cpp:99-111; fp32 sketches take the fp32-accurate exp).
+template <bool LOG, class VT>
+__device__ __forceinline__ double row_dot(const VT* val, const uint32_t* idx, long long b, long long e,
+                                          const double* x, int lane) {
+  if constexpr (!LOG) {
+    double a0 = 0.0, a1 = 0.0;
+    long long p = b + lane;
+    for (; p + 32 < e; p += 64) {
+      a0 = fma((double)val[p], x[idx[p]], a0);
+      a1 = fma((double)val[p + 32], x[idx[p + 32]], a1);
+    }
+    if (p < e) a0 = fma((double)val[p], x[idx[p]], a0);
+    return warp_sum(a0 + a1);
+  } else {
+    double m = -CUDART_INF;
+    for (long long p = b + lane; p < e; p += 32) {
+      const double xv = x[idx[p]];
+      if (xv == -CUDART_INF) continue;
+      m = fmax(m, log_of(val[p]) + xv);
+    }
+    m = warp_max(m);
+    if (m == -CUDART_INF) return -CUDART_INF;
+    double s = 0.0;
+    for (long long p = b + lane; p < e; p += 32) {
+      const double xv = x[idx[p]];
+      if (xv == -CUDART_INF) continue;
+      s += exp_term<VT>(log_of(val[p]) + xv - m);
+    }
+    return m + log(warp_sum(s));
+  }
+}
+
+template <bool LOG, class VT, int CS>
+__global__ void __launch_bounds__(kThreads, 1) cluster_loop_kernel(ClusterArgs<VT> A) {
+  extern __shared__ __align__(16) double smem[];
+  const unsigned rank = CS > 1 ? cluster_rank() : 0u;
+  const int64_t n = A.n;
+  double* X[2] = {smem, smem + A.npad};  // X[0] = u (rows), X[1] = v (columns)
+  // previous iterate of this CTA's own atoms (divergence restore)
+  const int64_t own0 = A.lo[0][rank + 1] - A.lo[0][rank], own1 = A.lo[1][rank + 1] - A.lo[1][rank];
+  double* prev[2] = {smem + 2 * (int64_t)A.npad, smem + 2 * (int64_t)A.npad + ((own0 + 1) & ~int64_t(1))};
+  char* tail = reinterpret_cast<char*>(prev[1] + ((own1 + 1) & ~int64_t(1)));
+  // staged sketch share: per half rows+1 offsets (int64), entries' values then indices
+  const long long* ptr[2] = {A.ptr[0], A.ptr[1]};
+  const uint32_t* idx[2] = {A.idx[0], A.idx[1]};
+  const VT* val[2] = {A.val[0], A.val[1]};
+  long long base[2] = {0, 0};  // entry offset subtracted from ptr (staged: share-relative)
+  int64_t rbase[2] = {0, 0};   // atom offset subtracted from the row index into ptr
+  if (A.stage) {
+    for (int h = 0; h < 2; ++h) {
+      const int64_t r0 = A.lo[h][rank], r1 = A.lo[h][rank + 1];
+      const long long e0 = A.ptr[h][r0], e1 = A.ptr[h][r1];
+      long long* sp = reinterpret_cast<long long*>(tail);
+      tail += sizeof(long long) * ((A.stage_rows[h] + 2) & ~int64_t(1));
+      VT* sv = reinterpret_cast<VT*>(tail);
+      tail += sizeof(VT) * ((A.stage_ent[h] + 3) & ~int64_t(3));
+      uint32_t* si = reinterpret_cast<uint32_t*>(tail);
+      tail += sizeof(uint32_t) * ((A.stage_ent[h] + 3) & ~int64_t(3));
+      for (int64_t k = threadIdx.x; k <= r1 - r0; k += blockDim.x) sp[k] = A.ptr[h][r0 + k] - e0;
+      for (long long k = threadIdx.x; k < e1 - e0; k += blockDim.x) {
+        sv[k] = A.val[h][e0 + k];
+        si[k] = A.idx[h][e0 + k];
+      }
+      ptr[h] = sp;
+      idx[h] = si;
+      val[h] = sv;
+      rbase[h] = r0;
+    }
+  }
+  __shared__ double scratch[32];
+  __shared__ long long mscratch[32];
+  __shared__ unsigned long long flag_sh[2];
+  __shared__ long long masks_sh;
+  __shared__ Xch xch;
+  const double on = LOG ? 0.0 : 1.0, off = LOG ? -CUDART_INF : 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {  // u = v = 1 on covered atoms (:277-281, :424-428)
+    X[0][i] = A.ne[0][i] ? on : off;
+    X[1][i] = A.ne[1][i] ? on : off;
+  }
+  if (threadIdx.x == 0) flag_sh[0] = flag_sh[1] = kNone;
+  if (CS > 1) cluster_barrier();
+  else __syncthreads();
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  long long mr = A.masked0[0], mc = A.masked0[1];
+  long long t = 0;
+  int converged = 0, diverged = 0, ekind = 0, ehalf = 0, dhalf = 0;
+  long long eidx = 0, didx = 0, mr_before = mr, mc_before = mc, mu_last = 0;
+
+  // one half: h = 0 rows against v (u-half), h = 1 columns against the new u
+  auto half = [&](int h, double& err_all, long long& masks_all, unsigned long long& flag_all) {
+    const int64_t r0 = A.lo[h][rank], r1 = A.lo[h][rank + 1];
+    const double* x = X[h ^ 1];
+    double* out = X[h];
+    double err = 0.0;
+    long long masks = 0;
+    for (int64_t i = r0 + warp; i < r1; i += nw) {
+      const double old = out[i];
+      if (lane == 0) prev[h][i - r0] = old;
+      if (!A.ne[h][i]) continue;  // structurally empty / masked: keeps its value
+      const int64_t li = i - rbase[h];
+      const double tmp = row_dot<LOG, VT>(val[h], idx[h], ptr[h][li] - base[h], ptr[h][li + 1] - base[h], x, lane);
+      if (lane == 0) {
+        err += finalize_atom<LOG>(i, tmp, old, __ldg(A.w[h] + i), A.exponent, A.policy, (int)t, A.ne[h], A.dyn[h],
+                                  out, &flag_sh[h], masks);
+        const double nv = out[i];
+#pragma unroll
+        for (int r = 1; r < CS; ++r) *peer(out + i, (rank + r) % CS) = nv;
+      }
+    }
+    // CTA partials in a fixed order
+    err = warp_sum(err);
+    masks = warp_sum_ll(masks);
+    if (lane == 0) {
+      scratch[warp] = err;
+      mscratch[warp] = masks;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double e = 0.0;
+      long long m = 0;
+      for (int k = 0; k < nw; ++k) {
+        e += scratch[k];
+        m += mscratch[k];
+      }
+      xch.err[h] = e;
+      xch.masks[h] = m;
+      xch.flag[h] = flag_sh[h];
+      flag_sh[h] = kNone;  // recycled: read back only through xch
+    }
+    if (CS > 1) cluster_barrier();  // new values and partials visible cluster-wide
+    else __syncthreads();
+    err_all = 0.0;
+    masks_all = 0;
+    flag_all = kNone;
+#pragma unroll
+    for (int r = 0; r < CS; ++r) {
+      const Xch* px = (CS == 1 || r == (int)rank) ? &xch : peer(&xch, (unsigned)r);
+      err_all += px->err[h];
+      masks_all += px->masks[h];
+      flag_all = min(flag_all, px->flag[h]);
+    }
+  };
+  auto restore = [&](int h) {  // previous iterate of this CTA's atoms (every CTA restores its own)
+    const int64_t r0 = A.lo[h][rank], r1 = A.lo[h][rank + 1];
+    for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) X[h][i] = prev[h][i - r0];
+  };
+
+  while (t < A.max_iter) {
+    ++t;
+    mr_before = mr;
+    mc_before = mc;
+    double eu, ev;
+    long long mu, mv;
+    unsigned long long fu, fv;
+    half(0, eu, mu, fu);
+    if (fu != kNone) {
+      if (A.policy == SPK_POLICY_MASK && !LOG) {
+        diverged = 1;
+        dhalf = 0;
+        didx = (long long)fu;
+      } else {
+        ekind = SPK_E_ZERO_DENOMINATOR;
+        ehalf = 0;
+        eidx = (long long)fu;
+      }
+      restore(0);
+      mu_last = 0;
+      break;
+    }
+    half(1, ev, mv, fv);
+    if (fv != kNone) {
+      if (A.policy == SPK_POLICY_MASK && !LOG) {
+        diverged = 1;
+        dhalf = 1;
+        didx = (long long)fv;
+      } else {
+        ekind = SPK_E_ZERO_DENOMINATOR;
+        ehalf = 1;
+        eidx = (long long)fv;
+      }
+      restore(0);
+      restore(1);
+      mu_last = mu;
+      break;
+    }
+    mr += mu;
+    mc += mv;
+    if (mr == n || mc == n) {  // solvers.hpp:357-358 / :465-466
+      ekind = SPK_E_DEGENERATE_SKETCH_ERROR;
+      break;
+    }
+    if (t >= 2 && eu + ev <= A.delta) {
+      converged = 1;
+      break;
+    }
+  }
+  __syncthreads();
+  for (int h = 0; h < 2; ++h)  // each CTA stores its own atoms
+    for (int64_t i = A.lo[h][rank] + threadIdx.x; i < A.lo[h][rank + 1]; i += blockDim.x) A.out[h][i] = X[h][i];
+  if (CS > 1) cluster_barrier();  // no CTA leaves while a peer may still read its Xch
+  if (threadIdx.x == 0 && rank == 0) {
+    loopcore::Status* s = A.status;
+    s->iterations = t;
+    s->converged = converged;
+    s->diverged = diverged;
+    s->error_kind = ekind;
+    s->error_half = ehalf;
+    s->error_index = eidx;
+    s->cur = 0;
+    s->div_half = dhalf;
+    s->div_index = didx;
+    s->masked_rows_before = mr_before;
+    s->masked_cols_before = mc_before;
+    s->masks_u_last = mu_last;
+    s->masked_rows = mr;
+    s->masked_cols = mc;
+  }
+}
+
+// Atom split of a half over CS CTAs by entry count (host copy of ptr).
+void split_by_entries(const std::vector<long long>& ptr, int64_t n, int CS, int64_t* lo) {
+  const long long total = ptr[n];
+  lo[0] = 0;
+  for (int r = 1; r < CS; ++r) {
+    const long long target = (long long)((double)total * r / CS);
+    lo[r] = std::lower_bound(ptr.begin(), ptr.begin() + n + 1, target) - ptr.begin();
+    lo[r] = std::max(lo[r], lo[r - 1]);
+  }
+  lo[CS] = n;
+}
+
+template <bool LOG, class VT, int CS>
+bool launch_cluster(spk_ctx* ctx, ClusterArgs<VT>& A, size_t smem) {
+  auto kern = cluster_loop_kernel<LOG, VT, CS>;
+  loopcore::allow_max_dyn_smem((const void*)kern);
+  if (CS > 8) SPK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = dim3(CS);
+  lc.blockDim = dim3(kThreads);
+  lc.dynamicSmemBytes = smem;
+  lc.stream = ctx->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CS;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  int nclusters = 0;
+  if (cudaOccupancyMaxActiveClusters(&nclusters, (const void*)kern, &lc) != cudaSuccess || nclusters < 1) {
+    (void)cudaGetLastError();
+    return false;
+  }
+  void* args[] = {&A};
+  SPK_CUDA(cudaLaunchKernelExC(&lc, (const void*)kern, args));
+  return true;
+}
+
+template <bool LOG, class VT>
+bool run_cluster_t(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, double exponent, int policy,
+                   LoopState& st, LoopOut& out) {
+  const int64_t n = sk->n;
+  int optin = 0;
+  SPK_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
+  const size_t budget = (size_t)optin - 2048;  // static shared use
+  const int npad = (int)((n + 31) & ~int64_t(31));
+  std::vector<long long> rp(n + 1), cp(n + 1);
+  download(ctx, rp.data(), sk->row_ptr, sizeof(long long) * (n + 1));
+  download(ctx, cp.data(), sk->col_ptr, sizeof(long long) * (n + 1));
+  ClusterArgs<VT> A{};
+  int CS = 0;
+  size_t smem = 0;
+  for (int cs : {ctx->small_cluster, 8, 4, 2, 1}) {  // largest cluster first; stage the sketch when it fits
+    if (cs < 1 || cs > kMaxCS || (cs & (cs - 1))) continue;
+    ClusterArgs<VT> B{};
+    split_by_entries(rp, n, cs, B.lo[0]);
+    split_by_entries(cp, n, cs, B.lo[1]);
+    int64_t own[2] = {0, 0}, ent[2] = {0, 0};
+    for (int h = 0; h < 2; ++h) {
+      const std::vector<long long>& p = h ? cp : rp;
+      for (int r = 0; r < cs; ++r) {
+        own[h] = std::max(own[h], B.lo[h][r + 1] - B.lo[h][r]);
+        ent[h] = std::max<int64_t>(ent[h], p[B.lo[h][r + 1]] - p[B.lo[h][r]]);
+      }
+    }
+    size_t base = sizeof(double) * (2 * (size_t)npad + ((own[0] + 1) & ~1) + ((own[1] + 1) & ~1));
+    size_t staged = 0;
+    for (int h = 0; h < 2; ++h)
+      staged += sizeof(long long) * ((own[h] + 2) & ~1) + (sizeof(VT) + 4) * ((ent[h] + 3) & ~3);
+    if (base > budget) continue;
+    B.stage = base + staged <= budget;
+    B.stage_ent[0] = ent[0];
+    B.stage_ent[1] = ent[1];
+    B.stage_rows[0] = own[0];
+    B.stage_rows[1] = own[1];
+    smem = base + (B.stage ? staged : 0);
+    A = B;
+    CS = cs;
+    break;
+  }
+  if (!CS) return false;
+
+  LoopWs& W = sk->ws;
+  W.row_ne.ensure(n);
+  W.col_ne.ensure(n);
+  W.dyn_row.ensure(sizeof(int) * n);
+  W.dyn_col.ensure(sizeof(int) * n);
+  W.u2.ensure(sizeof(double) * (2 * (size_t)npad + 16));
+  W.status.ensure(sizeof(loopcore::Status));
+  cudaStream_t s = ctx->stream;
+  SPK_CUDA(cudaMemcpyAsync(W.row_ne.p, sk->cov_row.p, n, cudaMemcpyDeviceToDevice, s));
+  SPK_CUDA(cudaMemcpyAsync(W.col_ne.p, sk->cov_col.p, n, cudaMemcpyDeviceToDevice, s));
+  SPK_CUDA(cudaMemsetAsync(W.dyn_row.p, 0, sizeof(int) * n, s));
+  SPK_CUDA(cudaMemsetAsync(W.dyn_col.p, 0, sizeof(int) * n, s));
+  SPK_CUDA(cudaMemsetAsync(W.status.p, 0, sizeof(loopcore::Status), s));
+  const double* wa = st.a;
+  const double* wb = st.b;
+  if (LOG) {
+    W.la.ensure(sizeof(double) * n);
+    W.lb.ensure(sizeof(double) * n);
+    loopcore::log_weights_kernel<<<loopcore::simple_grid(ctx, n), 256, 0, s>>>(n, st.a, W.la.as<double>());
+    loopcore::log_weights_kernel<<<loopcore::simple_grid(ctx, n), 256, 0, s>>>(n, st.b, W.lb.as<double>());
+    ctx->launches += 2;
+    wa = W.la.as<double>();
+    wb = W.lb.as<double>();
+  }
+  A.n = n;
+  A.ptr[0] = sk->row_ptr.as<long long>();
+  A.ptr[1] = sk->col_ptr.as<long long>();
+  A.idx[0] = sk->col_idx.as<uint32_t>();
+  A.idx[1] = sk->row_idx.as<uint32_t>();
+  if constexpr (std::is_same<VT, LogK>::value || std::is_same<VT, LogKf>::value) {
+    A.val[0] = reinterpret_cast<const VT*>(sk->log_values.p);
+    A.val[1] = reinterpret_cast<const VT*>(sk->log_values_t.p);
+  } else {
+    A.val[0] = sk->values.as<VT>();
+    A.val[1] = sk->values_t.as<VT>();
+  }
+  A.w[0] = wa;
+  A.w[1] = wb;
+  A.ne[0] = W.row_ne.as<unsigned char>();
+  A.ne[1] = W.col_ne.as<unsigned char>();
+  A.dyn[0] = W.dyn_row.as<int>();
+  A.dyn[1] = W.dyn_col.as<int>();
+  A.out[0] = W.u2.as<double>();
+  A.out[1] = W.u2.as<double>() + npad;
+  A.status = W.status.as<loopcore::Status>();
+  A.max_iter = cfg.max_iter;
+  A.delta = cfg.delta;
+  A.exponent = exponent;
+  A.policy = policy;
+  A.masked0[0] = sk->cov_empty_rows;
+  A.masked0[1] = sk->cov_empty_cols;
+  A.npad = npad;
+  Timer tm(s);
+  bool ok = false;
+  switch (CS) {
+    case 16: ok = launch_cluster<LOG, VT, 16>(ctx, A, smem); break;
+    case 8: ok = launch_cluster<LOG, VT, 8>(ctx, A, smem); break;
+    case 4: ok = launch_cluster<LOG, VT, 4>(ctx, A, smem); break;
+    case 2: ok = launch_cluster<LOG, VT, 2>(ctx, A, smem); break;
+    default: ok = launch_cluster<LOG, VT, 1>(ctx, A, smem); break;
+  }
+  if (!ok) return false;
+  ++ctx->launches;
+  out.loop_s = tm.stop();
+  SPK_CUDA(cudaGetLastError());
+  loopcore::Status S;
+  download(ctx, &S, W.status, sizeof S);
+  loopcore::loop_epilogue<LOG>(ctx, S, n, W, A.out[0], A.out[1], st, out);
+  return true;
+}
+
+}  // namespace
+
+// Fast-mode loop on one cluster when the sketch is small enough (both
+// scaling vectors in every CTA's shared memory). Returns false when it does
+// not apply (the caller then runs the grid loop).
+bool run_cluster_loop(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, double exponent, int policy,
+                      LoopState& st, LoopOut& out) {
+  if (ctx->deterministic || !ctx->small_loop || sk->n_cols) return false;
+  if (sk->n > ctx->small_max_n || sk->nnz > ctx->small_max_nnz) return false;
+  // the loop's entry checks (solvers.hpp:269-274 / :411-414) are the grid loop's: let it raise them
+  if ((sk->cov_empty_rows || sk->cov_empty_cols) && policy == SPK_POLICY_ERROR) return false;
+  if (sk->cov_empty_rows == sk->n || sk->cov_empty_cols == sk->n) return false;
+  const bool log_domain = cfg.stabilize != 0;
+  if (log_domain) {
+    ensure_log_values(ctx, sk);
+    if (sk->value_type == SPK_VALUES_F32) return run_cluster_t<true, LogKf>(ctx, sk, cfg, exponent, policy, st, out);
+    return run_cluster_t<true, LogK>(ctx, sk, cfg, exponent, policy, st, out);
+  }
+  if (sk->value_type == SPK_VALUES_F32) return run_cluster_t<false, float>(ctx, sk, cfg, exponent, policy, st, out);
+  return run_cluster_t<false, double>(ctx, sk, cfg, exponent, policy, st, out);
+}
+
+}  // namespace spk

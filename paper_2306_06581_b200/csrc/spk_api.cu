@@ -280,6 +280,12 @@ int spk_ctx_set_option(spk_ctx* ctx, int key, int64_t value) {
       if (value != 4 && value != 8) return SPK_STATUS_INPUT;
       ctx->batch_unroll = (int)value;
       return SPK_OK;
+    case 12: ctx->small_loop = value ? 1 : 0; return SPK_OK;
+    case 13:
+      if (value != 1 && value != 2 && value != 4 && value != 8 && value != 16) return SPK_STATUS_INPUT;
+      ctx->small_cluster = (int)value;
+      return SPK_OK;
+    case 14: ctx->small_max_nnz = std::max<int64_t>(0, value); return SPK_OK;
     case 8: ctx->blocked_spread = value ? 1 : 0; return SPK_OK;
     case 7: ctx->blocked_split = (int)std::max<int64_t>(0, std::min<int64_t>(value, 2)); return SPK_OK;
     default: return SPK_STATUS_INPUT;
@@ -300,6 +306,9 @@ int spk_ctx_get_option(const spk_ctx* ctx, int key, int64_t* value) {
     case 9: *value = ctx->blocked_cluster; return SPK_OK;
     case 10: *value = ctx->batch_cluster; return SPK_OK;
     case 11: *value = ctx->batch_unroll; return SPK_OK;
+    case 12: *value = ctx->small_loop; return SPK_OK;
+    case 13: *value = ctx->small_cluster; return SPK_OK;
+    case 14: *value = ctx->small_max_nnz; return SPK_OK;
     default: return SPK_STATUS_INPUT;
   }
 }

@@ -217,9 +217,9 @@ def test_config3_batch_vs_reference(reference):
         print(f"C3 pair {k} ({i},{j}): {rres['iterations']} it; batch vs reference |dlog u| {du:.2e} |dlog v| "
               f"{dv:.2e}; objective {objs[q]!r} vs {oobj!r} (rel {abs(objs[q] - oobj) / abs(oobj):.2e}); "
               f"batch vs single |dlog u| {du1:.2e}, objective rel {abs(objs[q] - obj1) / abs(obj1):.2e}")
-        assert objs[q] == pytest.approx(oobj, rel=1e-4)
+        assert objs[q] == pytest.approx(oobj, rel=1e-6)  # measured ~6e-9
         assert objs[q] == pytest.approx(obj1, rel=1e-5)
-        assert du <= 1e-3 and dv <= 1e-3
+        assert du <= 2e-5 and dv <= 2e-5  # measured ~2.3e-6 (fp32 K~ values, fp32-accurate exp)
 
 
 def oracle_readout(csr, lu, lv, a, b, coords):
