@@ -251,10 +251,16 @@ SolveResult sinkhorn_uot<SparseKernel>(const SparseKernel&, const DiscreteMeasur
 
 enum class SketchProbs { Importance, Uniform };
 
+// Storage of the sketch values K~ on the device (B200 extension; the
+// reference's SparseKernel is fp64). F32 halves the loop's value stream
+// (configs 3 and 4); sums and scalings stay fp64.
+enum class ValuePrecision { F64, F32 };
+
 struct SparSinkOptions {
   double theta = 0.0;
   SketchProbs probs = SketchProbs::Importance;
   bool strict = false;
+  ValuePrecision values = ValuePrecision::F64;  // B200 extension
 };
 
 SolveResult spar_sink_ot(const KernelMatrix& K, const CostMatrix& C, const DiscreteMeasure& a,
@@ -293,6 +299,26 @@ SolveResult sinkhorn_ot(const PointList& x, const PointList& y, const CostSpec& 
                         const DiscreteMeasure& b, const SolverConfig& cfg, EmptyPolicy empty_policy = EmptyPolicy::Error);
 SolveResult sinkhorn_uot(const PointList& x, const PointList& y, const CostSpec& cost, const DiscreteMeasure& a,
                          const DiscreteMeasure& b, const SolverConfig& cfg, EmptyPolicy empty_policy = EmptyPolicy::Error);
+
+// Batched frame pairs (config 3; the per-pair spar_sink_uot calls of
+// pairwise_wfr, harness.cpp:381-401): pair k solves
+//   spar_sink_uot(support, support, cost, measures[pairs[k].first],
+//                 measures[pairs[k].second], cfg, s, seeds[k], opts)
+// with every sketch drawn by one device batch and, in the log domain
+// (cfg.stabilize), every loop run by one batched launch (a cluster of CTAs per
+// pair). A pair whose solve fails gets failed = true, its exception class in
+// error, and a NaN objective -- the reference's NaN distance and failed_pairs
+// count; the other pairs complete. Results come in pair order.
+struct PairSolve {
+  SolveResult result;
+  bool failed = false;
+  std::string error;
+};
+std::vector<PairSolve> spar_sink_uot_pairs(const PointList& support, const CostSpec& cost,
+                                           const std::vector<DiscreteMeasure>& measures,
+                                           const std::vector<std::pair<std::size_t, std::size_t>>& pairs,
+                                           const SolverConfig& cfg, double s, const std::vector<std::uint64_t>& seeds,
+                                           const SparSinkOptions& opts = {});
 
 // Runtime controls of the device context used by this thread.
 void set_device(int device);

@@ -301,6 +301,7 @@ __global__ void __launch_bounds__(kBatchThreads, 1) batch_log_kernel(BatchArgs A
   __shared__ long long masks_sh[2];
   __shared__ unsigned long long bad_sh[2];
   __shared__ Xch xch;
+  __shared__ Xch comb;  // the cluster-wide combination, read by every thread
   // u = v = 1 (log 0) on covered atoms, masked atoms -inf (:424-428)
   for (int64_t w = threadIdx.x; w < (A.npad >> 5); w += blockDim.x) {
     unsigned int bu = 0u, bv = 0u;
@@ -338,16 +339,25 @@ __global__ void __launch_bounds__(kBatchThreads, 1) batch_log_kernel(BatchArgs A
     }
     if (CS > 1) cluster_barrier();  // new values + partials visible cluster-wide
     else __syncthreads();
-    e_all = 0.0;
-    m_all = 0;
-    b_all = ~0ull;
+    if (threadIdx.x == 0) {  // one thread reads the peers; rank order: the same sum on every CTA
+      double e = 0.0;
+      long long mk = 0;
+      unsigned long long bb = ~0ull;
 #pragma unroll
-    for (int r = 0; r < CS; ++r) {  // rank order: the same sum on every CTA
-      const Xch* px = (r == (int)rank || CS == 1) ? &xch : peer_xch(&xch, (unsigned)r);
-      e_all += px->err[h];
-      m_all += px->masks[h];
-      b_all = min(b_all, px->bad[h]);
+      for (int r = 0; r < CS; ++r) {
+        const Xch* px = (r == (int)rank || CS == 1) ? &xch : peer_xch(&xch, (unsigned)r);
+        e += px->err[h];
+        mk += px->masks[h];
+        bb = min(bb, px->bad[h]);
+      }
+      comb.err[h] = e;
+      comb.masks[h] = mk;
+      comb.bad[h] = bb;
     }
+    __syncthreads();
+    e_all = comb.err[h];
+    m_all = comb.masks[h];
+    b_all = comb.bad[h];
   };
   while (t < A.max_iter) {
     ++t;

@@ -82,6 +82,32 @@ void check(int rc) {
   if (rc != SPK_OK) rethrow(ctx());
 }
 
+// Reference exception class name of a spk_error_kind.
+std::string error_class_name(int kind) {
+  static const char* const names[] = {"",
+                                      "Error",
+                                      "NegativeWeight",
+                                      "LengthMismatch",
+                                      "NotNormalized",
+                                      "AllBlack",
+                                      "EmptyOutput",
+                                      "DimensionMismatch",
+                                      "NonPositiveEta",
+                                      "NonPositiveEpsilon",
+                                      "DegenerateSupport",
+                                      "AllZeroKernel",
+                                      "ThetaOutOfRange",
+                                      "BudgetTooLarge",
+                                      "EmptyWindow",
+                                      "InfiniteCostOnSupport",
+                                      "IoError",
+                                      "ZeroDenominator",
+                                      "BaselineFailed",
+                                      "DegenerateSketchError",
+                                      "DeviceError"};
+  return kind >= 0 && kind <= 20 ? names[kind] : "Error";
+}
+
 int kind_of(CostKind k) {
   return k == CostKind::SqEuclidean ? SPK_COST_SQEUCLID : k == CostKind::Euclidean ? SPK_COST_EUCLID : SPK_COST_WFR;
 }
@@ -127,7 +153,7 @@ spk_sketch_opts c_opts(const SparSinkOptions& o) {
   s.theta = o.theta;
   s.probs = o.probs == SketchProbs::Uniform ? SPK_PROBS_UNIFORM : SPK_PROBS_IMPORTANCE;
   s.strict = o.strict ? 1 : 0;
-  s.value_type = SPK_VALUES_F64;
+  s.value_type = o.values == ValuePrecision::F32 ? SPK_VALUES_F32 : SPK_VALUES_F64;
   return s;
 }
 
@@ -529,6 +555,75 @@ SolveResult spar_sink_uot(const PointList& x, const PointList& y, const CostSpec
                           const DiscreteMeasure& b, const SolverConfig& cfg, double s, std::uint64_t seed,
                           const SparSinkOptions& opts) {
   return spar_sink(coord_desc(x, y, cost, cfg.epsilon), a, b, cfg, s, seed, opts, true);
+}
+
+std::vector<PairSolve> spar_sink_uot_pairs(const PointList& support, const CostSpec& cost,
+                                           const std::vector<DiscreteMeasure>& measures,
+                                           const std::vector<std::pair<std::size_t, std::size_t>>& pairs,
+                                           const SolverConfig& cfg, double s, const std::vector<std::uint64_t>& seeds,
+                                           const SparSinkOptions& opts) {
+  if (seeds.size() != pairs.size()) throw LengthMismatch("one seed per pair");
+  const spk_kernel_desc d = coord_desc(support, support, cost, cfg.epsilon);
+  const std::size_t n = static_cast<std::size_t>(d.n);
+  for (const auto& pr : pairs) {
+    if (pr.first >= measures.size() || pr.second >= measures.size()) throw LengthMismatch("pair index out of range");
+    check_sizes(n, measures[pr.first], measures[pr.second]);
+  }
+  const spk_solver_cfg c = c_cfg(cfg, opts.strict ? EmptyPolicy::Error : EmptyPolicy::Mask);
+  const spk_sketch_opts o = c_opts(opts);
+  std::vector<PairSolve> out(pairs.size());
+  constexpr std::size_t kChunk = 512;  // sketches resident at once
+  for (std::size_t c0 = 0; c0 < pairs.size(); c0 += kChunk) {
+    const std::size_t m = std::min(kChunk, pairs.size() - c0);
+    std::vector<double> A(m * n), B(m * n);
+    for (std::size_t q = 0; q < m; ++q) {
+      std::copy(measures[pairs[c0 + q].first].weights.begin(), measures[pairs[c0 + q].first].weights.end(),
+                A.begin() + q * n);
+      std::copy(measures[pairs[c0 + q].second].weights.begin(), measures[pairs[c0 + q].second].weights.end(),
+                B.begin() + q * n);
+    }
+    std::vector<spk_sketch*> sks(m, nullptr);
+    check(spk_sketch_build_batch(ctx(), &d, static_cast<int>(m), A.data(), B.data(), SPK_PLAN_UOT, cfg.lambda,
+                                 cfg.epsilon, s, seeds.data() + c0, &o, sks.data()));
+    struct Free {  // the chunk's sketches die with the chunk, whatever happens
+      std::vector<spk_sketch*>& v;
+      ~Free() {
+        for (spk_sketch* p : v) spk_sketch_free(p);
+      }
+    } free_all{sks};
+    std::vector<spk_report> reps(m);
+    std::vector<int32_t> err(m, 0);
+    check(spk_sketch_solve_batch(ctx(), sks.data(), static_cast<int>(m), &c, 1, reps.data(), err.data()));
+    for (std::size_t q = 0; q < m; ++q) {
+      PairSolve& ps = out[c0 + q];
+      if (err[q]) {
+        ps.failed = true;
+        ps.error = error_class_name(err[q]);
+        ps.result.report.objective = std::numeric_limits<double>::quiet_NaN();
+        ps.result.report.seed = seeds[c0 + q];
+        continue;
+      }
+      std::vector<double> u(n), v(n), lu(n), lv(n);
+      check(spk_sketch_scalings(sks[q], u.data(), v.data(), lu.data(), lv.data()));
+      double obj = std::numeric_limits<double>::quiet_NaN();
+      spk_report rr = reps[q];
+      if (spk_sketch_readout(ctx(), sks[q], &d, 1, cfg.lambda, cfg.epsilon, nullptr, nullptr, &obj, &rr) != SPK_OK) {
+        int cat = 0, kind = 0;
+        spk_last_error(ctx(), &cat, &kind, nullptr, 0);
+        if (kind == SPK_E_DEVICE) rethrow(ctx());
+        ps.failed = true;
+        ps.error = error_class_name(kind);
+        ps.result.report.objective = std::numeric_limits<double>::quiet_NaN();
+        ps.result.report.seed = seeds[c0 + q];
+        continue;
+      }
+      ps.result = make_result(n, reps[q], std::move(u), std::move(v), std::move(lu), std::move(lv));
+      ps.result.report.objective = obj;
+      ps.result.report.sketch_nnz = static_cast<std::size_t>(reps[q].sketch_nnz);
+      ps.result.report.seed = seeds[c0 + q];
+    }
+  }
+  return out;
 }
 
 namespace {

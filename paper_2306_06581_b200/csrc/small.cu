@@ -128,6 +128,27 @@ __global__ void __launch_bounds__(kThreads, 1) cluster_loop_kernel(ClusterArgs<V
   const int64_t own0 = A.lo[0][rank + 1] - A.lo[0][rank], own1 = A.lo[1][rank + 1] - A.lo[1][rank];
   double* prev[2] = {smem + 2 * (int64_t)A.npad, smem + 2 * (int64_t)A.npad + ((own0 + 1) & ~int64_t(1))};
   char* tail = reinterpret_cast<char*>(prev[1] + ((own1 + 1) & ~int64_t(1)));
+  // this CTA's atoms' mask state (non-empty flag, dynamic-mask iteration) in
+  // shared memory, addressed by the global atom index
+  int* dyn_own[2];
+  unsigned char* ne_own[2];
+  for (int h = 0; h < 2; ++h) {
+    const int64_t own = h ? own1 : own0;
+    dyn_own[h] = reinterpret_cast<int*>(tail);
+    tail += sizeof(int) * ((own + 3) & ~int64_t(3));
+  }
+  for (int h = 0; h < 2; ++h) {
+    const int64_t own = h ? own1 : own0;
+    ne_own[h] = reinterpret_cast<unsigned char*>(tail);
+    tail += (own + 15) & ~int64_t(15);
+  }
+  unsigned char* ne_s[2] = {ne_own[0] - A.lo[0][rank], ne_own[1] - A.lo[1][rank]};
+  int* dyn_s[2] = {dyn_own[0] - A.lo[0][rank], dyn_own[1] - A.lo[1][rank]};
+  for (int h = 0; h < 2; ++h)
+    for (int64_t i = A.lo[h][rank] + threadIdx.x; i < A.lo[h][rank + 1]; i += blockDim.x) {
+      ne_s[h][i] = A.ne[h][i];
+      dyn_s[h][i] = 0;
+    }
   // staged sketch share: per half rows+1 offsets (int64), entries' values then indices
   const long long* ptr[2] = {A.ptr[0], A.ptr[1]};
   const uint32_t* idx[2] = {A.idx[0], A.idx[1]};
@@ -160,6 +181,9 @@ __global__ void __launch_bounds__(kThreads, 1) cluster_loop_kernel(ClusterArgs<V
   __shared__ unsigned long long flag_sh[2];
   __shared__ long long masks_sh;
   __shared__ Xch xch;
+  __shared__ double comb_err;
+  __shared__ long long comb_masks;
+  __shared__ unsigned long long comb_flag;
   const double on = LOG ? 0.0 : 1.0, off = LOG ? -CUDART_INF : 0.0;
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {  // u = v = 1 on covered atoms (:277-281, :424-428)
     X[0][i] = A.ne[0][i] ? on : off;
@@ -185,16 +209,14 @@ __global__ void __launch_bounds__(kThreads, 1) cluster_loop_kernel(ClusterArgs<V
     for (int64_t i = r0 + warp; i < r1; i += nw) {
       const double old = out[i];
       if (lane == 0) prev[h][i - r0] = old;
-      if (!A.ne[h][i]) continue;  // structurally empty / masked: keeps its value
+      if (!ne_s[h][i]) continue;  // structurally empty / masked: keeps its value
       const int64_t li = i - rbase[h];
       const double tmp = row_dot<LOG, VT>(val[h], idx[h], ptr[h][li] - base[h], ptr[h][li + 1] - base[h], x, lane);
-      if (lane == 0) {
-        err += finalize_atom<LOG>(i, tmp, old, __ldg(A.w[h] + i), A.exponent, A.policy, (int)t, A.ne[h], A.dyn[h],
+      if (lane == 0)
+        err += finalize_atom<LOG>(i, tmp, old, __ldg(A.w[h] + i), A.exponent, A.policy, (int)t, ne_s[h], dyn_s[h],
                                   out, &flag_sh[h], masks);
-        const double nv = out[i];
-#pragma unroll
-        for (int r = 1; r < CS; ++r) *peer(out + i, (rank + r) % CS) = nv;
-      }
+      __syncwarp();
+      if (CS > 1 && lane >= 1 && lane < CS) *peer(out + i, (rank + lane) % CS) = out[i];  // DSMEM broadcast
     }
     // CTA partials in a fixed order
     err = warp_sum(err);
@@ -218,16 +240,36 @@ __global__ void __launch_bounds__(kThreads, 1) cluster_loop_kernel(ClusterArgs<V
     }
     if (CS > 1) cluster_barrier();  // new values and partials visible cluster-wide
     else __syncthreads();
-    err_all = 0.0;
-    masks_all = 0;
-    flag_all = kNone;
-#pragma unroll
-    for (int r = 0; r < CS; ++r) {
-      const Xch* px = (CS == 1 || r == (int)rank) ? &xch : peer(&xch, (unsigned)r);
-      err_all += px->err[h];
-      masks_all += px->masks[h];
-      flag_all = min(flag_all, px->flag[h]);
+    // warp 0 gathers the CS partials (lane r reads CTA r) and combines them in
+    // rank order; the CTA reads the result from shared memory
+    if (warp == 0) {
+      double e = 0.0;
+      long long mk = 0;
+      unsigned long long f = kNone;
+      if (lane < CS) {
+        const Xch* px = (CS == 1 || lane == (int)rank) ? &xch : peer(&xch, (unsigned)lane);
+        e = px->err[h];
+        mk = px->masks[h];
+        f = px->flag[h];
+      }
+      double et = 0.0;
+      long long mt = 0;
+      unsigned long long ft = kNone;
+      for (int r = 0; r < CS; ++r) {  // fixed order: the same sums on every CTA
+        et += __shfl_sync(0xffffffffu, e, r);
+        mt += __shfl_sync(0xffffffffu, mk, r);
+        ft = min(ft, __shfl_sync(0xffffffffu, f, r));
+      }
+      if (lane == 0) {
+        comb_err = et;
+        comb_masks = mt;
+        comb_flag = ft;
+      }
     }
+    __syncthreads();
+    err_all = comb_err;
+    masks_all = comb_masks;
+    flag_all = comb_flag;
   };
   auto restore = [&](int h) {  // previous iterate of this CTA's atoms (every CTA restores its own)
     const int64_t r0 = A.lo[h][rank], r1 = A.lo[h][rank + 1];
@@ -284,8 +326,11 @@ __global__ void __launch_bounds__(kThreads, 1) cluster_loop_kernel(ClusterArgs<V
     }
   }
   __syncthreads();
-  for (int h = 0; h < 2; ++h)  // each CTA stores its own atoms
-    for (int64_t i = A.lo[h][rank] + threadIdx.x; i < A.lo[h][rank + 1]; i += blockDim.x) A.out[h][i] = X[h][i];
+  for (int h = 0; h < 2; ++h)  // each CTA stores its own atoms (and their dynamic-mask stamps)
+    for (int64_t i = A.lo[h][rank] + threadIdx.x; i < A.lo[h][rank + 1]; i += blockDim.x) {
+      A.out[h][i] = X[h][i];
+      A.dyn[h][i] = dyn_s[h][i];
+    }
   if (CS > 1) cluster_barrier();  // no CTA leaves while a peer may still read its Xch
   if (threadIdx.x == 0 && rank == 0) {
     loopcore::Status* s = A.status;
@@ -373,11 +418,14 @@ bool run_cluster_t(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, doub
       }
     }
     size_t base = sizeof(double) * (2 * (size_t)npad + ((own[0] + 1) & ~1) + ((own[1] + 1) & ~1));
+    for (int h = 0; h < 2; ++h) base += sizeof(int) * ((own[h] + 3) & ~3) + ((own[h] + 15) & ~15);
     size_t staged = 0;
     for (int h = 0; h < 2; ++h)
       staged += sizeof(long long) * ((own[h] + 2) & ~1) + (sizeof(VT) + 4) * ((ent[h] + 3) & ~3);
-    if (base > budget) continue;
-    B.stage = base + staged <= budget;
+    // the cluster's SMs win only while the sketch lives in their shared memory:
+    // streamed from L2 by <= 16 SMs it loses to the whole-GPU grid loop
+    if (base + staged > budget) continue;
+    B.stage = 1;
     B.stage_ent[0] = ent[0];
     B.stage_ent[1] = ent[1];
     B.stage_rows[0] = own[0];

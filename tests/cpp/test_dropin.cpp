@@ -326,6 +326,54 @@ int main() {
     CHECK(dense.report.iterations == coords.report.iterations);
     CHECK_CLOSE(coords.report.objective, dense.report.objective, 1e-10);
   });
+  run("batched frame pairs == one spar_sink_uot per pair (pairwise_wfr, harness.cpp:381-401)", [] {
+    // 4 frames of 20x20 on [0,1]^2, WFR eta = 0.1, log domain, fp32 sketches
+    const std::size_t side = 20, n = side * side;
+    PointList grid;
+    grid.dim = 2;
+    for (std::size_t r = 0; r < side; ++r)
+      for (std::size_t c = 0; c < side; ++c) {
+        grid.coords.push_back(static_cast<double>(r) / (side - 1));
+        grid.coords.push_back(static_cast<double>(c) / (side - 1));
+      }
+    std::vector<DiscreteMeasure> frames;
+    for (int f = 0; f < 4; ++f) {
+      std::vector<double> w(n);
+      double t = 0.0;
+      for (std::size_t i = 0; i < n; ++i) {
+        const double dy = grid.coords[2 * i] - (0.3 + 0.1 * f), dx = grid.coords[2 * i + 1] - 0.5;
+        t += (w[i] = 1e-4 + std::exp(-(dx * dx + dy * dy) / 0.02));
+      }
+      for (auto& x : w) x /= t;
+      frames.push_back(new_measure(std::move(w), grid, true));
+    }
+    std::vector<std::pair<std::size_t, std::size_t>> pairs{{0, 1}, {0, 3}, {1, 2}, {2, 3}};
+    std::vector<std::uint64_t> seeds{11, 12, 13, 14};
+    SolverConfig cfg;
+    cfg.epsilon = 0.01;
+    cfg.lambda = 1.0;
+    cfg.delta = 1e-6;
+    cfg.max_iter = 400;
+    cfg.stabilize = true;
+    CostSpec cs;
+    cs.kind = CostKind::WFR;
+    cs.eta = 0.1;
+    cs.scale = 1.0;
+    SparSinkOptions o;
+    o.values = ValuePrecision::F32;
+    const double s = 10.0 * n * std::log(static_cast<double>(n));
+    auto batch = spar_sink_uot_pairs(grid, cs, frames, pairs, cfg, s, seeds, o);
+    CHECK(batch.size() == pairs.size());
+    for (std::size_t k = 0; k < pairs.size(); ++k) {
+      auto one = spar_sink_uot(grid, grid, cs, frames[pairs[k].first], frames[pairs[k].second], cfg, s, seeds[k], o);
+      CHECK(!batch[k].failed);
+      CHECK(batch[k].result.report.sketch_nnz == one.report.sketch_nnz);
+      CHECK(std::abs(static_cast<long>(batch[k].result.report.iterations) - static_cast<long>(one.report.iterations)) <= 1);
+      CHECK_CLOSE(batch[k].result.report.objective, one.report.objective, 1e-6);
+      CHECK(batch[k].result.plan.log_domain && batch[k].result.plan.u.size() == n);
+    }
+    CHECK_THROWS_AS(spar_sink_uot_pairs(grid, cs, frames, pairs, cfg, s, {1, 2}, o), LengthMismatch);
+  });
   std::printf("%d checks passed, %d failed\n", g_pass, g_fail);
   return g_fail;
 }
