@@ -54,10 +54,31 @@ __device__ __forceinline__ double cost_from_d2_rt(int kind, double d2, double et
   return cost_from_d2<2>(d2, eta);
 }
 
+// exp(x) with the reference's (glibc's) underflow boundary. K != 0 decides
+// the sketch support and therefore every later draw counter of the row
+// (sparsify.cpp:184-198), so the boundary must be bit-exact: glibc's exp is
+// correctly rounded there -- exp(x) != 0 exactly for x >= -0x1.74910d52d3051p+9,
+// the double just above -1075 ln 2 (tests/test_exp_boundary.py re-derives it
+// from the host libm) -- while CUDA's exp flushes part of the deepest subnormal
+// range to 0 (config 4: 142 of 10^12 pairs). Subnormal results are formed as
+// rint(e^(x + 1074 ln 2)) quanta of 2^-1074 (Cody-Waite split of 1074 ln 2; the
+// first sum is exact by Sterbenz), within a few quanta of glibc's value.
+constexpr double kExpLastNonzero = -0x1.74910d52d3051p+9;  // glibc: exp(x) == 2^-1074 here, 0 below
+constexpr double kExpSubnormal = -708.39641853226408;      // ln(2^-1022): below, results are subnormal
+__device__ __forceinline__ double exp_ref(double x) {
+  if (!(x < kExpSubnormal)) return exp(x);  // normal results (and NaN, +-inf handled by exp)
+  if (x < kExpLastNonzero) return 0.0;
+  constexpr double kHi = 1074.0 * 0x1.62e42feep-1;  // ln2_hi (21 trailing zero bits): exact product
+  constexpr double kLo = 1074.0 * 0x1.a39ef35793c76p-33;  // 1074 * ln2_lo
+  const double y = __dadd_rn(__dadd_rn(x, kHi), kLo);
+  const double q = fmax(rint(exp(y)), 1.0);  // quanta of 2^-1074; >= 1 on the support
+  return __longlong_as_double((long long)q);
+}
+
 // K = isinf(C) ? 0 : exp(-C/eps) with C = cost(d2)/scale (geometry.cpp:83-102)
 __device__ __forceinline__ double kernel_from_d2(int kind, double d2, double eta, double scale, double eps) {
   const double c = cost_from_d2_rt(kind, d2, eta) / scale;
-  return isinf(c) ? 0.0 : exp(-c / eps);
+  return isinf(c) ? 0.0 : exp_ref(-c / eps);
 }
 
 template <int KIND>

@@ -22,7 +22,7 @@ struct KCoords {
   double eta, scale, eps;
   __device__ __forceinline__ double operator()(int64_t i, int64_t j) const {
     const double c = coord_cost(x + i * dim, y + j * dim, dim, kind, eta) / scale;
-    return isinf(c) ? 0.0 : exp(-c / eps);
+    return isinf(c) ? 0.0 : exp_ref(-c / eps);
   }
 };
 

@@ -50,7 +50,7 @@ __device__ __forceinline__ double kernel_entry(const KSrc& S, int64_t i, int64_t
   else if (S.kind == SPK_COST_EUCLID) c = cost_entry<1>(p, q, S.dim, S.eta);
   else c = cost_entry<2>(p, q, S.dim, S.eta);
   c = c / S.scale;
-  return isinf(c) ? 0.0 : exp(-c / S.eps);
+  return isinf(c) ? 0.0 : exp_ref(-c / S.eps);
 }
 
 // ---- plan ---------------------------------------------------------------------
@@ -224,7 +224,7 @@ __global__ void cost_query_kernel(KSrc S, int64_t m, const int64_t* qi, const in
     else c = cost_entry<2>(p, r, S.dim, S.eta);
     c = c / S.scale;
     cost[q] = c;
-    kern[q] = isinf(c) ? 0.0 : exp(-c / S.eps);
+    kern[q] = isinf(c) ? 0.0 : exp_ref(-c / S.eps);
   }
 }
 
@@ -1207,7 +1207,7 @@ __global__ void kernel_from_cost_kernel(const double* C, int64_t m, double eps, 
   unsigned long long local = 0;
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < m; q += (int64_t)gridDim.x * blockDim.x) {
     const double c = C[q];
-    const double v = isinf(c) ? 0.0 : exp(-c / eps);  // geometry.cpp:95
+    const double v = isinf(c) ? 0.0 : exp_ref(-c / eps);  // geometry.cpp:95
     K[q] = v;
     local += v > 0.0 ? 1 : 0;
   }

@@ -84,37 +84,54 @@ __device__ __forceinline__ T* peer(T* p, unsigned rank) {
   return q;
 }
 
-// Warp-per-row dot with generic (shared or global) sketch pointers and a
-// shared x: linear sum of v * x (FMA), or the two-pass log-sum-exp
-// (solvers.cpp:99-111; fp32 sketches take the fp32-accurate exp).
+constexpr int kSG = 8;          // lanes per row (config-1 rows: ~55 entries)
+constexpr int kSR = 32 / kSG;   // rows per warp at once
+
+template <class T>
+__device__ __forceinline__ T group_sum(T v) {
+#pragma unroll
+  for (int o = kSG / 2; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double group_max(double v) {
+#pragma unroll
+  for (int o = kSG / 2; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// One row's dot over [b, e) by the kSG lanes of a group (generic pointers:
+// the sketch share is staged in shared memory), x shared: linear sum of
+// v * x (FMA), or the two-pass log-sum-exp (solvers.cpp:99-111; fp32 sketches
+// take the fp32-accurate exp). Every lane of the warp must call it.
 template <bool LOG, class VT>
-__device__ __forceinline__ double row_dot(const VT* val, const uint32_t* idx, long long b, long long e,
-                                          const double* x, int lane) {
+__device__ __forceinline__ double group_dot(const VT* val, const uint32_t* idx, long long b, long long e,
+                                            const double* x, int gl) {
   if constexpr (!LOG) {
     double a0 = 0.0, a1 = 0.0;
-    long long p = b + lane;
-    for (; p + 32 < e; p += 64) {
+    long long p = b + gl;
+    for (; p + kSG < e; p += 2 * kSG) {
       a0 = fma((double)val[p], x[idx[p]], a0);
-      a1 = fma((double)val[p + 32], x[idx[p + 32]], a1);
+      a1 = fma((double)val[p + kSG], x[idx[p + kSG]], a1);
     }
     if (p < e) a0 = fma((double)val[p], x[idx[p]], a0);
-    return warp_sum(a0 + a1);
+    return group_sum(a0 + a1);
   } else {
     double m = -CUDART_INF;
-    for (long long p = b + lane; p < e; p += 32) {
+    for (long long p = b + gl; p < e; p += kSG) {
       const double xv = x[idx[p]];
       if (xv == -CUDART_INF) continue;
       m = fmax(m, log_of(val[p]) + xv);
     }
-    m = warp_max(m);
-    if (m == -CUDART_INF) return -CUDART_INF;
+    m = group_max(m);
     double s = 0.0;
-    for (long long p = b + lane; p < e; p += 32) {
-      const double xv = x[idx[p]];
-      if (xv == -CUDART_INF) continue;
-      s += exp_term<VT>(log_of(val[p]) + xv - m);
-    }
-    return m + log(warp_sum(s));
+    if (m != -CUDART_INF)
+      for (long long p = b + gl; p < e; p += kSG) {
+        const double xv = x[idx[p]];
+        if (xv == -CUDART_INF) continue;
+        s += exp_term<VT>(log_of(val[p]) + xv - m);
+      }
+    s = group_sum(s);
+    return m == -CUDART_INF ? -CUDART_INF : m + log(s);
   }
 }
 
@@ -142,12 +159,20 @@ __global__ void __launch_bounds__(kThreads, 1) cluster_loop_kernel(ClusterArgs<V
     ne_own[h] = reinterpret_cast<unsigned char*>(tail);
     tail += (own + 15) & ~int64_t(15);
   }
+  double* w_own[2];
+  for (int h = 0; h < 2; ++h) {
+    const int64_t own = h ? own1 : own0;
+    w_own[h] = reinterpret_cast<double*>(tail);
+    tail += sizeof(double) * ((own + 1) & ~int64_t(1));
+  }
+  const double* w_s[2] = {w_own[0] - A.lo[0][rank], w_own[1] - A.lo[1][rank]};
   unsigned char* ne_s[2] = {ne_own[0] - A.lo[0][rank], ne_own[1] - A.lo[1][rank]};
   int* dyn_s[2] = {dyn_own[0] - A.lo[0][rank], dyn_own[1] - A.lo[1][rank]};
   for (int h = 0; h < 2; ++h)
     for (int64_t i = A.lo[h][rank] + threadIdx.x; i < A.lo[h][rank + 1]; i += blockDim.x) {
       ne_s[h][i] = A.ne[h][i];
       dyn_s[h][i] = 0;
+      w_own[h][i - A.lo[h][rank]] = A.w[h][i];
     }
   // staged sketch share: per half rows+1 offsets (int64), entries' values then indices
   const long long* ptr[2] = {A.ptr[0], A.ptr[1]};
@@ -193,7 +218,7 @@ __global__ void __launch_bounds__(kThreads, 1) cluster_loop_kernel(ClusterArgs<V
   if (CS > 1) cluster_barrier();
   else __syncthreads();
 
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5, gl = lane & (kSG - 1);
   long long mr = A.masked0[0], mc = A.masked0[1];
   long long t = 0;
   int converged = 0, diverged = 0, ekind = 0, ehalf = 0, dhalf = 0;
@@ -206,17 +231,27 @@ __global__ void __launch_bounds__(kThreads, 1) cluster_loop_kernel(ClusterArgs<V
     double* out = X[h];
     double err = 0.0;
     long long masks = 0;
-    for (int64_t i = r0 + warp; i < r1; i += nw) {
-      const double old = out[i];
-      if (lane == 0) prev[h][i - r0] = old;
-      if (!ne_s[h][i]) continue;  // structurally empty / masked: keeps its value
-      const int64_t li = i - rbase[h];
-      const double tmp = row_dot<LOG, VT>(val[h], idx[h], ptr[h][li] - base[h], ptr[h][li + 1] - base[h], x, lane);
-      if (lane == 0)
-        err += finalize_atom<LOG>(i, tmp, old, __ldg(A.w[h] + i), A.exponent, A.policy, (int)t, ne_s[h], dyn_s[h],
-                                  out, &flag_sh[h], masks);
+    // kSG lanes per row, kSR rows per warp at once: every row of a config-1
+    // slab is in flight in one pass
+    for (int64_t i0 = r0 + (int64_t)warp * kSR; i0 < r1; i0 += (int64_t)nw * kSR) {
+      const int64_t i = i0 + lane / kSG;
+      const bool in = i < r1;
+      const double old = in ? out[i] : 0.0;
+      if (in && gl == 0) prev[h][i - r0] = old;
+      const bool live = in && ne_s[h][i];  // structurally empty / masked: keeps its value
+      long long b = 0, e = 0;
+      if (live) {
+        const int64_t li = i - rbase[h];
+        b = ptr[h][li] - base[h];
+        e = ptr[h][li + 1] - base[h];
+      }
+      const double tmp = group_dot<LOG, VT>(val[h], idx[h], b, e, x, gl);
+      if (live && gl == 0)
+        err += finalize_atom<LOG>(i, tmp, old, w_s[h][i], A.exponent, A.policy, (int)t, ne_s[h], dyn_s[h], out,
+                                  &flag_sh[h], masks);
       __syncwarp();
-      if (CS > 1 && lane >= 1 && lane < CS) *peer(out + i, (rank + lane) % CS) = out[i];  // DSMEM broadcast
+      if (CS > 1 && live)  // DSMEM broadcast of the new value, the group's lanes sharing the peers
+        for (int r = gl + 1; r < CS; r += kSG) *peer(out + i, (rank + r) % CS) = out[i];
     }
     // CTA partials in a fixed order
     err = warp_sum(err);
@@ -418,7 +453,8 @@ bool run_cluster_t(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, doub
       }
     }
     size_t base = sizeof(double) * (2 * (size_t)npad + ((own[0] + 1) & ~1) + ((own[1] + 1) & ~1));
-    for (int h = 0; h < 2; ++h) base += sizeof(int) * ((own[h] + 3) & ~3) + ((own[h] + 15) & ~15);
+    for (int h = 0; h < 2; ++h)
+      base += sizeof(int) * ((own[h] + 3) & ~3) + ((own[h] + 15) & ~15) + sizeof(double) * ((own[h] + 1) & ~1);
     size_t staged = 0;
     for (int h = 0; h < 2; ++h)
       staged += sizeof(long long) * ((own[h] + 2) & ~1) + (sizeof(VT) + 4) * ((ent[h] + 3) & ~3);
