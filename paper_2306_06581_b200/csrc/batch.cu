@@ -85,12 +85,6 @@ struct BatchArgs {
   int npad;  // shared doubles per vector
 };
 
-// Per-CTA values every CTA of the cluster reads after the half's barrier.
-struct Xch {
-  double err[2];
-  long long masks[2];
-  unsigned long long bad[2];
-};
 
 // Entry stream of one half: packed u64 (PACKED) or u32 index + fp64 log K~.
 template <bool PACKED>
@@ -140,11 +134,6 @@ __device__ __forceinline__ typename std::conditional<FAST, float, double>::type 
 
 __device__ __forceinline__ double* peer_ptr(double* p, unsigned rank) {
   double* q;
-  asm volatile("mapa.u64 %0, %1, %2;" : "=l"(q) : "l"(p), "r"(rank));
-  return q;
-}
-__device__ __forceinline__ const Xch* peer_xch(const Xch* p, unsigned rank) {
-  const Xch* q;
   asm volatile("mapa.u64 %0, %1, %2;" : "=l"(q) : "l"(p), "r"(rank));
   return q;
 }
@@ -300,8 +289,9 @@ __global__ void __launch_bounds__(kBatchThreads, 1) batch_log_kernel(BatchArgs A
   __shared__ double scratch[32];
   __shared__ long long masks_sh[2];
   __shared__ unsigned long long bad_sh[2];
-  __shared__ Xch xch;
-  __shared__ Xch comb;  // the cluster-wide combination, read by every thread
+  __shared__ double xe[2][CS];  // per half: every CTA's partials, slot = its rank
+  __shared__ long long xm[2][CS];
+  __shared__ unsigned long long xb[2][CS];
   // u = v = 1 (log 0) on covered atoms, masked atoms -inf (:424-428)
   for (int64_t w = threadIdx.x; w < (A.npad >> 5); w += blockDim.x) {
     unsigned int bu = 0u, bv = 0u;
@@ -331,33 +321,33 @@ __global__ void __launch_bounds__(kBatchThreads, 1) batch_log_kernel(BatchArgs A
   if (CS > 1) cluster_barrier();  // peers' shared memory initialised before any DSMEM write
   else __syncthreads();
   // the half's cluster-wide outcome: residual, new masks, first failing atom
+  // (cta_sum has synchronised the CTA: masks_sh / bad_sh are final.) Lanes
+  // r < CS of warp 0 push this CTA's partials into slot [rank] of CTA r's
+  // exchange arrays before the barrier; after it, every CTA sums its local
+  // slots in rank order (the same values everywhere).
   auto exchange = [&](int h, double e_cta, double& e_all, long long& m_all, unsigned long long& b_all) {
-    if (threadIdx.x == 0) {
-      xch.err[h] = e_cta;
-      xch.masks[h] = masks_sh[h];
-      xch.bad[h] = bad_sh[h];
+    if (threadIdx.x < CS) {
+      const unsigned r = threadIdx.x;
+      double* pe = (CS == 1 || r == rank) ? &xe[h][rank] : peer_ptr(&xe[h][rank], r);
+      long long* pm = reinterpret_cast<long long*>(
+          (CS == 1 || r == rank) ? (double*)&xm[h][rank] : peer_ptr((double*)&xm[h][rank], r));
+      unsigned long long* pb = reinterpret_cast<unsigned long long*>(
+          (CS == 1 || r == rank) ? (double*)&xb[h][rank] : peer_ptr((double*)&xb[h][rank], r));
+      *pe = e_cta;
+      *pm = masks_sh[h];
+      *pb = bad_sh[h];
     }
     if (CS > 1) cluster_barrier();  // new values + partials visible cluster-wide
     else __syncthreads();
-    if (threadIdx.x == 0) {  // one thread reads the peers; rank order: the same sum on every CTA
-      double e = 0.0;
-      long long mk = 0;
-      unsigned long long bb = ~0ull;
+    e_all = 0.0;
+    m_all = 0;
+    b_all = ~0ull;
 #pragma unroll
-      for (int r = 0; r < CS; ++r) {
-        const Xch* px = (r == (int)rank || CS == 1) ? &xch : peer_xch(&xch, (unsigned)r);
-        e += px->err[h];
-        mk += px->masks[h];
-        bb = min(bb, px->bad[h]);
-      }
-      comb.err[h] = e;
-      comb.masks[h] = mk;
-      comb.bad[h] = bb;
+    for (int r = 0; r < CS; ++r) {
+      e_all += xe[h][r];
+      m_all += xm[h][r];
+      b_all = min(b_all, xb[h][r]);
     }
-    __syncthreads();
-    e_all = comb.err[h];
-    m_all = comb.masks[h];
-    b_all = comb.bad[h];
   };
   while (t < A.max_iter) {
     ++t;
@@ -405,7 +395,7 @@ __global__ void __launch_bounds__(kBatchThreads, 1) batch_log_kernel(BatchArgs A
       break;
     }
   }
-  if (CS > 1) cluster_barrier();  // no CTA leaves while a peer may still read its Xch
+  if (CS > 1) cluster_barrier();  // every DSMEM access of the solve is complete before any CTA leaves
   // every CTA holds the full vectors: each stores its own share
   for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) I.lu[i] = lu[i];
   for (int64_t i = c0 + threadIdx.x; i < c1; i += blockDim.x) I.lv[i] = lv[i];

@@ -22,6 +22,7 @@
 #include <cstring>
 
 #include "common.cuh"
+#include "seqsum.h"
 #include "internal.h"
 
 namespace spk {
@@ -1129,6 +1130,17 @@ void plan_finish(spk_ctx* ctx, DevKernel& dk, bool need_pass, double theta, Plan
     SPK_CUDA(cudaMemcpyAsync(&total, tot.p, sizeof total, cudaMemcpyDeviceToHost, ctx->stream));
     SPK_CUDA(cudaMemcpyAsync(&support, tn.p, sizeof support, cudaMemcpyDeviceToHost, ctx->stream));
     SPK_CUDA(cudaStreamSynchronize(ctx->stream));
+    // Equal grid terms (uniform marginals: config 4): the reference's
+    // row-major sequential sum of the masked grid is a function of the support
+    // count alone -- reproduce it bit for bit (seqsum.h). A tree sum differs
+    // by 1.6e-5 relative at 10^12 terms (each sequential add drops the same
+    // ulp fraction), which would move p* and flip sampled entries. Unequal
+    // terms keep the tree (their sequential rounding errors are random, ~1e-12
+    // relative at 10^8 terms: configs 2 and 3 show no index differences).
+    if (plan_kind != SPK_PLAN_UOT && plan_kind != SPK_PLAN_UNIFORM && support > 0 &&
+        std::all_of(plan.row_w.begin(), plan.row_w.end(), [&](double w) { return w == plan.row_w[0]; }) &&
+        std::all_of(plan.col_w.begin(), plan.col_w.end(), [&](double w) { return w == plan.col_w[0]; }))
+      total = seq_sum_const(plan.row_w[0] * plan.col_w[0], static_cast<uint64_t>(support));
   }
   const bool zero_mass = plan.zero_mass;
   if (!dk.dense) {

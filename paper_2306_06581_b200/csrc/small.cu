@@ -63,12 +63,6 @@ struct ClusterArgs {
   int64_t stage_rows[2];
 };
 
-struct Xch {
-  double err[2];
-  long long masks[2];
-  unsigned long long flag[2];
-};
-
 __device__ __forceinline__ unsigned cluster_rank() {
   unsigned r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
@@ -205,10 +199,9 @@ __global__ void __launch_bounds__(kThreads, 1) cluster_loop_kernel(ClusterArgs<V
   __shared__ long long mscratch[32];
   __shared__ unsigned long long flag_sh[2];
   __shared__ long long masks_sh;
-  __shared__ Xch xch;
-  __shared__ double comb_err;
-  __shared__ long long comb_masks;
-  __shared__ unsigned long long comb_flag;
+  __shared__ double xe[2][CS];  // per half: every CTA's partials, slot = its rank
+  __shared__ long long xm[2][CS];
+  __shared__ unsigned long long xf[2][CS];
   const double on = LOG ? 0.0 : 1.0, off = LOG ? -CUDART_INF : 0.0;
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {  // u = v = 1 on covered atoms (:277-281, :424-428)
     X[0][i] = A.ne[0][i] ? on : off;
@@ -253,7 +246,10 @@ __global__ void __launch_bounds__(kThreads, 1) cluster_loop_kernel(ClusterArgs<V
       if (CS > 1 && live)  // DSMEM broadcast of the new value, the group's lanes sharing the peers
         for (int r = gl + 1; r < CS; r += kSG) *peer(out + i, (rank + r) % CS) = out[i];
     }
-    // CTA partials in a fixed order
+    // CTA partials: warp sums, then warp 0 sums the warps (fixed shuffle
+    // tree) and PUSHES the CTA's (residual, masks, first failing atom) into
+    // slot [rank] of every CTA's exchange arrays (DSMEM stores) before the
+    // cluster barrier; after it, every CTA sums its local slots in rank order.
     err = warp_sum(err);
     masks = warp_sum_ll(masks);
     if (lane == 0) {
@@ -261,50 +257,34 @@ __global__ void __launch_bounds__(kThreads, 1) cluster_loop_kernel(ClusterArgs<V
       mscratch[warp] = masks;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-      double e = 0.0;
-      long long m = 0;
-      for (int k = 0; k < nw; ++k) {
-        e += scratch[k];
-        m += mscratch[k];
+    if (warp == 0) {
+      double e = lane < nw ? scratch[lane] : 0.0;
+      long long m = lane < nw ? mscratch[lane] : 0;
+      e = warp_sum(e);
+      m = warp_sum_ll(m);
+      const unsigned long long f = flag_sh[h];
+      __syncwarp();
+      if (lane < CS) {
+        double* pe = (CS == 1 || lane == (int)rank) ? &xe[h][rank] : peer(&xe[h][rank], (unsigned)lane);
+        long long* pm = (CS == 1 || lane == (int)rank) ? &xm[h][rank] : peer(&xm[h][rank], (unsigned)lane);
+        unsigned long long* pf = (CS == 1 || lane == (int)rank) ? &xf[h][rank] : peer(&xf[h][rank], (unsigned)lane);
+        *pe = e;
+        *pm = m;
+        *pf = f;
       }
-      xch.err[h] = e;
-      xch.masks[h] = m;
-      xch.flag[h] = flag_sh[h];
-      flag_sh[h] = kNone;  // recycled: read back only through xch
+      if (lane == 0) flag_sh[h] = kNone;  // recycled for this half's next iteration
     }
     if (CS > 1) cluster_barrier();  // new values and partials visible cluster-wide
     else __syncthreads();
-    // warp 0 gathers the CS partials (lane r reads CTA r) and combines them in
-    // rank order; the CTA reads the result from shared memory
-    if (warp == 0) {
-      double e = 0.0;
-      long long mk = 0;
-      unsigned long long f = kNone;
-      if (lane < CS) {
-        const Xch* px = (CS == 1 || lane == (int)rank) ? &xch : peer(&xch, (unsigned)lane);
-        e = px->err[h];
-        mk = px->masks[h];
-        f = px->flag[h];
-      }
-      double et = 0.0;
-      long long mt = 0;
-      unsigned long long ft = kNone;
-      for (int r = 0; r < CS; ++r) {  // fixed order: the same sums on every CTA
-        et += __shfl_sync(0xffffffffu, e, r);
-        mt += __shfl_sync(0xffffffffu, mk, r);
-        ft = min(ft, __shfl_sync(0xffffffffu, f, r));
-      }
-      if (lane == 0) {
-        comb_err = et;
-        comb_masks = mt;
-        comb_flag = ft;
-      }
+    err_all = 0.0;
+    masks_all = 0;
+    flag_all = kNone;
+#pragma unroll
+    for (int r = 0; r < CS; ++r) {  // rank order: the same sums on every CTA
+      err_all += xe[h][r];
+      masks_all += xm[h][r];
+      flag_all = min(flag_all, xf[h][r]);
     }
-    __syncthreads();
-    err_all = comb_err;
-    masks_all = comb_masks;
-    flag_all = comb_flag;
   };
   auto restore = [&](int h) {  // previous iterate of this CTA's atoms (every CTA restores its own)
     const int64_t r0 = A.lo[h][rank], r1 = A.lo[h][rank + 1];

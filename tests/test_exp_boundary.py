@@ -64,3 +64,21 @@ def test_device_kernel_from_cost_matches_glibc_at_underflow(ctx):
     assert nnz.value == int(np.count_nonzero(ref))
     quanta = np.abs(K.view(np.int64) - ref.view(np.int64))
     assert quanta.max() <= 64, quanta.max()  # subnormal values: a few 2^-1074 quanta (relative ~1e-14 at the top)
+
+
+def test_sequential_sum_emulation(tmp_path):
+    """csrc/seqsum.h: the reference's sequential sum of N equal grid terms,
+    emulated in O(binades): equal to the plain loop on random cases and to
+    the committed 10^12-term config-4 normaliser (17 CPU-minutes to sum)."""
+    import json
+    import subprocess
+
+    exe = tmp_path / "seqsum"
+    subprocess.run(["g++", "-std=c++17", "-O2", "-ffp-contract=off", "-I",
+                    str(ROOT / "paper_2306_06581_b200" / "csrc"), str(ROOT / "tests" / "cpp" / "test_seqsum.cpp"),
+                    "-o", str(exe)], check=True)
+    fx = json.loads((ROOT / "tests" / "golden" / "c4_normaliser.json").read_text())
+    ra = math.sqrt(1.0 / 1_000_000) / float.fromhex(fx["sa"])
+    res = subprocess.run([str(exe), (ra * ra).hex(), str(fx["kernel_nnz"])], capture_output=True, text=True)
+    assert res.returncode == 0, res.stdout
+    assert float.fromhex(res.stdout.split()[-1]) == float.fromhex(fx["total"])

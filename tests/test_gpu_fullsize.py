@@ -54,10 +54,13 @@ def c4_sketch(c4):
 
 
 def test_config4_normaliser_pinned(c4, c4_sketch, oracle):
-    """The device's fixed-order tree over the 10^12 masked-grid terms against
-    the reference's sequential row-major sum (oracle/masked_normaliser.c,
-    committed): within a few ULP; kernel support count exact; sampled rows
-    re-drawn with the REFERENCE-order normaliser are the device's rows."""
+    """The masked-grid normaliser over config 4's 10^12 terms against the
+    reference's sequential row-major sum (oracle/masked_normaliser.c, 17 CPU
+    minutes, committed): bit-equal (the device emulates the sequential sum of
+    equal terms exactly, csrc/seqsum.h); the kernel support count exact (the
+    glibc exp underflow boundary, csrc/common.cuh exp_ref); 200 random rows
+    re-drawn by the oracle with the reference's normaliser are the device's
+    rows bit for bit."""
     fx = json.loads((GOLD / "c4_normaliser.json").read_text())
     h = hashlib.sha256()
     for arr in (c4.x, c4.y):
@@ -67,9 +70,9 @@ def test_config4_normaliser_pinned(c4, c4_sketch, oracle):
     ctx, kern, sk = c4_sketch
     plan = sk.plan()
     inv_ref = float.fromhex(fx["inv"])
-    ulps = abs(plan["inv"] - inv_ref) / math.ulp(inv_ref)
-    print(f"C4 normaliser: device inv {plan['inv']!r} reference-order {inv_ref!r} ({ulps:.0f} ulp)")
-    assert ulps <= 8
+    print(f"C4 normaliser: device inv {plan['inv']!r} reference-order {inv_ref!r}; support {sk.kernel_nnz} vs "
+          f"{fx['kernel_nnz']}")
+    assert plan["inv"] == inv_ref
     assert sk.kernel_nnz == fx["kernel_nnz"]
     rp, ci, vv = sk.csr()
     ra = np.sqrt(c4.a)
@@ -77,7 +80,9 @@ def test_config4_normaliser_pinned(c4, c4_sketch, oracle):
     for t in ra.tolist():
         sa += t
     row_w = ra / sa
-    for i in [0, 3, 77, 123_456, 654_321, 999_998]:
+    rows = [0, 3, 77, 123_456, 654_321, 999_998] + sorted(np.random.default_rng(44).choice(sk.n, 200, replace=False))
+    for i in rows:
+        i = int(i)
         orp, oci, ovv = oracle.sample_rows_coords(c4.x, c4.y, "sqeuclid", 0.0, c4.scale, c4.eps, "ot", False,
                                                   row_w, row_w, 0.0, inv_ref, c4.s, 7, i, i + 1)
         assert np.array_equal(ci[rp[i]:rp[i + 1]], oci), f"row {i}"
