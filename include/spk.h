@@ -181,7 +181,8 @@ enum spk_option {
 int spk_ctx_set_option(spk_ctx* ctx, int key, int64_t value);
 /* Current value of an option key (SPK_STATUS_INPUT for an unknown key). */
 int spk_ctx_get_option(const spk_ctx* ctx, int key, int64_t* value);
-/* Status of the last failed call on ctx: category (spk_status), class
+/* Status of the last failed call on ctx (ctx = NULL: of the last failed
+ * spk_spar_sink_multi, which owns its contexts): category (spk_status), class
  * (spk_error_kind) and message. Returns the category. */
 int spk_last_error(const spk_ctx* ctx, int* category, int* kind, char* msg, size_t len);
 /* Number of kernels this context has launched so far. */
@@ -357,6 +358,64 @@ int spk_shard_status(spk_shard* sh, spk_report* rep, int32_t* stopped, int32_t* 
  * infinite cost + 1 (0 = none), first atom with KL mass off support + 1. */
 int spk_shard_readout(spk_shard* sh, const double* u_dev, const double* v_dev, int log_domain, int uot,
                       int want_objective, double* out);
+
+/* ---- multi-GPU through the library: communicators + the sharded driver ------
+ *
+ * The collectives of the sharded solve above, owned by the library so a C /
+ * C++ caller reaches config 4 on several GPUs (SURVEY §8(b) C-ABI row,
+ * §8(e)). NCCL is loaded at run time (the copy already in the process, else
+ * $SPK_NCCL_LIB, else libnccl.so.2). One rank per process (spk_comm_init with
+ * an id made by spk_comm_unique_id on one rank and shared out of band), or
+ * one process driving several GPUs (spk_comm_init_all / spk_spar_sink_multi).
+ * An emulated communicator (threads of one process sharing one GPU,
+ * host-synchronised copies) exercises the same driver in tests. */
+typedef struct spk_comm spk_comm;
+typedef struct spk_comm_group spk_comm_group;
+int spk_comm_unique_id(unsigned char id[128]);
+/* Rank `rank` of `world` on ctx's device (ncclCommInitRank). */
+int spk_comm_init(spk_ctx* ctx, const unsigned char id[128], int world, int rank, spk_comm** out);
+/* One process, ndev devices: ctxs[r] must be a context on devices[r]; comms[r] receives rank r. */
+int spk_comm_init_all(const int* devices, int ndev, spk_ctx** ctxs, spk_comm** comms);
+/* Emulated ranks: a host group of `world` threads; rank r's communicator on ctx. */
+int spk_comm_group_create(int world, spk_comm_group** out);
+void spk_comm_group_destroy(spk_comm_group* group);
+int spk_comm_init_emulated(spk_ctx* ctx, spk_comm_group* group, int rank, spk_comm** out);
+void spk_comm_destroy(spk_comm* comm);
+int spk_comm_info(const spk_comm* comm, int* world, int* rank, int* nccl_backed);
+
+/* This rank's share of a row/column-sharded sketch (build_sketch,
+ * solvers.cpp:314-335, over the communicator's ranks: plan row sums
+ * gathered in rank order, local sampling, the column all-to-all, coverage
+ * totals). Every rank passes the same inputs. kd: coordinate form. */
+typedef struct spk_sharded spk_sharded;
+int spk_sharded_build(spk_comm* comm, const spk_kernel_desc* kd, const double* a, const double* b, int plan_kind,
+                      double lambda, double epsilon, double s, uint64_t seed, const spk_sketch_opts* opts,
+                      spk_sharded** out);
+/* sinkhorn_ot / sinkhorn_uot<SparseKernel> (solvers.hpp:209-232) on the
+ * sharded sketch, then the objective (rank-order sums). Every rank gets the
+ * full u, v (and log_u, log_v after a log-domain solve; any may be NULL) and
+ * the same report. With NCCL the iteration loop (per iteration: 2 half
+ * kernels + 2 all-gathers) runs as one captured CUDA graph, replayed by later
+ * solves with the same configuration: no host work per half-step. */
+int spk_sharded_solve(spk_sharded* sh, const spk_solver_cfg* cfg, int uot, double* u, double* v, double* log_u,
+                      double* log_v, spk_report* rep);
+/* n, total sketch entries, kernel support, this rank's slab [lo, hi), and
+ * the kernel launches inside the captured loop graph (0 if none). */
+int spk_sharded_info(const spk_sharded* sh, int64_t* n, int64_t* nnz, int64_t* kernel_nnz, int64_t* lo, int64_t* hi,
+                     int64_t* captured_launches);
+void spk_sharded_free(spk_sharded* sh);
+/* spar_sink_ot / spar_sink_uot (solvers.cpp:339-378) over the
+ * communicator's ranks: build + solve + free. */
+int spk_spar_sink_sharded(spk_comm* comm, const spk_kernel_desc* kd, const double* a, const double* b,
+                          const spk_solver_cfg* cfg, double s, uint64_t seed, const spk_sketch_opts* opts, int uot,
+                          double* u, double* v, double* log_u, double* log_v, spk_report* rep);
+/* The same from ONE host thread over `ndev` GPUs of this process: contexts,
+ * NCCL communicators (ncclCommInitAll) and one driver thread per GPU are
+ * created and torn down inside. On failure spk_last_error(NULL, ...) reports
+ * the failing rank's error. */
+int spk_spar_sink_multi(const int* devices, int ndev, const spk_kernel_desc* kd, const double* a, const double* b,
+                        const spk_solver_cfg* cfg, double s, uint64_t seed, const spk_sketch_opts* opts, int uot,
+                        double* u, double* v, double* log_u, double* log_v, spk_report* rep);
 
 /* ---- barycenters --------------------------------------------
  * BarycenterResult (barycenter.hpp:20-26) without the weights (written to q). */

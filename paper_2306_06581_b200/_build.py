@@ -17,7 +17,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-CUDA_SOURCES = ["spk_api.cu", "sampler.cu", "loop.cu", "blocked.cu", "dense.cu", "readout.cu", "shard.cu", "ibp.cu", "batch.cu", "small.cu"]
+CUDA_SOURCES = ["spk_api.cu", "sampler.cu", "loop.cu", "blocked.cu", "dense.cu", "readout.cu", "shard.cu", "ibp.cu", "batch.cu", "small.cu", "comm.cu", "sharded.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr",
               "-Xptxas", "-v", "-I", str(ROOT / "include")]
@@ -66,6 +66,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
 
         with ThreadPoolExecutor(max_workers=min(len(todo), os.cpu_count() or 4) or 1) as ex:
             list(ex.map(compile_one, todo))
+        # no link-time NCCL: comm.cu dlopens libnccl.so.2 when a communicator is made
         _run([NVCC, *ARCH, "-shared", "-o", str(LIB), *objs, "-lcudart_static", "-lrt", "-ldl", "-lpthread"])
     shim_src = CSRC / "host" / "sparsink_b200.cpp"
     if shim_src.exists():

@@ -125,6 +125,26 @@ SIGNATURES = {
     "spk_shard_export": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, I64P]),
     "spk_shard_import": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64]),
     "spk_shard_coverage": (C.c_int, [C.c_void_p, I64P, I64P]),
+    # communicators + the library's sharded driver
+    "spk_comm_unique_id": (C.c_int, [C.c_char_p]),
+    "spk_comm_init": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
+    "spk_comm_init_all": (C.c_int, [C.POINTER(C.c_int), C.c_int, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)]),
+    "spk_comm_group_create": (C.c_int, [C.c_int, C.POINTER(C.c_void_p)]),
+    "spk_comm_group_destroy": (None, [C.c_void_p]),
+    "spk_comm_init_emulated": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.POINTER(C.c_void_p)]),
+    "spk_comm_destroy": (None, [C.c_void_p]),
+    "spk_comm_info": (C.c_int, [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "spk_sharded_build": (C.c_int, [C.c_void_p, C.POINTER(KernelDesc), DP, DP, C.c_int, C.c_double, C.c_double,
+                                    C.c_double, C.c_uint64, C.POINTER(SketchOpts), C.POINTER(C.c_void_p)]),
+    "spk_sharded_solve": (C.c_int, [C.c_void_p, C.POINTER(SolverCfg), C.c_int, DP, DP, DP, DP, C.POINTER(Report)]),
+    "spk_sharded_info": (C.c_int, [C.c_void_p, I64P, I64P, I64P, I64P, I64P, I64P]),
+    "spk_sharded_free": (None, [C.c_void_p]),
+    "spk_spar_sink_sharded": (C.c_int, [C.c_void_p, C.POINTER(KernelDesc), DP, DP, C.POINTER(SolverCfg), C.c_double,
+                                        C.c_uint64, C.POINTER(SketchOpts), C.c_int, DP, DP, DP, DP,
+                                        C.POINTER(Report)]),
+    "spk_spar_sink_multi": (C.c_int, [C.POINTER(C.c_int), C.c_int, C.POINTER(KernelDesc), DP, DP,
+                                      C.POINTER(SolverCfg), C.c_double, C.c_uint64, C.POINTER(SketchOpts), C.c_int,
+                                      DP, DP, DP, DP, C.POINTER(Report)]),
     "spk_shard_begin": (C.c_int, [C.c_void_p, C.POINTER(SolverCfg), C.c_int, C.c_int, C.c_int64, C.c_int64, C.c_void_p,
                                   C.c_void_p]),
     "spk_shard_half": (C.c_int, [C.c_void_p, C.c_int, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]),

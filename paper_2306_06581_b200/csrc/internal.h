@@ -22,6 +22,8 @@ struct Failure : std::runtime_error {
 };
 
 [[noreturn]] void fail(int kind, const std::string& text);  // maps kind -> category, prefixes class
+// error record of calls that own their contexts (spk_last_error(NULL, ...))
+void set_process_error(int category, int kind, const std::string& msg);
 [[noreturn]] void fail_device(const char* what, cudaError_t e);
 
 #define SPK_CUDA(x)                                  \
@@ -321,6 +323,9 @@ void run_sparse_loop(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, do
                      int policy, LoopState& st, LoopOut& out);
 void ensure_coverage(spk_ctx* ctx, spk_sketch* sk);
 void ensure_log_values(spk_ctx* ctx, spk_sketch* sk);
+// shard.cu: half/finish launches since spk_shard_begin (selects the loop-state
+// buffer); a replayed CUDA graph of the loop sets it as if issued
+void shard_set_calls(spk_shard* sh, long long calls);
 // small.cu: the loop on one cluster (scalings in shared memory); false = not applicable
 bool run_cluster_loop(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, double exponent, int policy,
                       LoopState& st, LoopOut& out);

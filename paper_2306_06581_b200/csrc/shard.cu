@@ -349,6 +349,10 @@ void launch_half(spk_shard* sh, shard::HalfArgs& A, int grid) {
 
 }  // namespace
 
+namespace spk {
+void shard_set_calls(spk_shard* sh, long long calls) { sh->calls = calls; }
+}  // namespace spk
+
 extern "C" {
 
 int spk_shard_plan_rows(spk_ctx* ctx, const spk_kernel_desc* kd, const double* a, const double* b, int plan_kind,

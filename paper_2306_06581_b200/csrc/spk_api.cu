@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <chrono>
+#include <mutex>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -59,6 +60,10 @@ int category_of(int kind) {
 double now_s() {
   return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
+
+std::mutex g_proc_err_mu;
+int g_proc_err_cat = 0, g_proc_err_kind = 0;
+std::string g_proc_err_msg;
 
 void init_report(spk_report* rep) {
   if (!rep) return;
@@ -172,6 +177,13 @@ double solver_exponent(const spk_solver_cfg& cfg, int uot, double a_total, doubl
   }
   if (!(cfg.lambda > 0) || !std::isfinite(cfg.lambda)) fail(SPK_E_ERROR, "sinkhorn_uot needs finite lambda > 0");
   return cfg.lambda / (cfg.lambda + cfg.epsilon);
+}
+
+void set_process_error(int category, int kind, const std::string& msg) {
+  std::lock_guard<std::mutex> lk(g_proc_err_mu);
+  g_proc_err_cat = category;
+  g_proc_err_kind = kind;
+  g_proc_err_msg = msg;
 }
 
 [[noreturn]] void fail(int kind, const std::string& text) {
@@ -314,7 +326,13 @@ int spk_ctx_get_option(const spk_ctx* ctx, int key, int64_t* value) {
 }
 
 int spk_last_error(const spk_ctx* ctx, int* category, int* kind, char* msg, size_t len) {
-  if (!ctx) return SPK_STATUS_INPUT;
+  if (!ctx) {  // the last failure of a call that owns its contexts (spk_spar_sink_multi)
+    std::lock_guard<std::mutex> lk(g_proc_err_mu);
+    if (category) *category = g_proc_err_cat;
+    if (kind) *kind = g_proc_err_kind;
+    if (msg && len) std::snprintf(msg, len, "%s", g_proc_err_msg.c_str());
+    return g_proc_err_cat;
+  }
   if (category) *category = ctx->err_category;
   if (kind) *kind = ctx->err_kind;
   if (msg && len) std::snprintf(msg, len, "%s", ctx->err_msg.c_str());

@@ -457,3 +457,121 @@ def run_emulated(world: int, fn, device: int = 0, options: dict | None = None):
         if e is not None:
             raise e
     return out
+
+
+# ---- the library's own driver (include/spk.h spk_comm_* / spk_sharded_*) -----------
+# The same sharded solve run entirely inside libspk_b200.so: NCCL loaded by the
+# library (the CUDA-graph-captured loop) or the emulated communicator (threads
+# sharing one GPU). A C / C++ caller uses exactly these entry points.
+class LibComm:
+    """A communicator owned by the library for `ctx` (an api.Context)."""
+
+    def __init__(self, ctx, ptr):
+        self.ctx, self.ptr, self.lib = ctx, ptr, ctx.lib
+
+    @staticmethod
+    def unique_id(lib=None) -> bytes:
+        lib = lib or L.load()
+        buf = C.create_string_buffer(128)
+        rc = lib.spk_comm_unique_id(buf)
+        if rc:
+            raise RuntimeError("spk_comm_unique_id failed (NCCL unavailable?)")
+        return buf.raw
+
+    @classmethod
+    def nccl(cls, ctx, uid: bytes, world: int, rank: int) -> "LibComm":
+        p = C.c_void_p()
+        _raise(ctx.ptr, ctx.lib.spk_comm_init(ctx.ptr, C.c_char_p(uid), world, rank, C.byref(p)))
+        return cls(ctx, p)
+
+    @classmethod
+    def emulated(cls, ctx, group, rank: int) -> "LibComm":
+        p = C.c_void_p()
+        _raise(ctx.ptr, ctx.lib.spk_comm_init_emulated(ctx.ptr, group, rank, C.byref(p)))
+        return cls(ctx, p)
+
+    def info(self) -> dict:
+        w, r, nc = C.c_int(), C.c_int(), C.c_int()
+        self.lib.spk_comm_info(self.ptr, C.byref(w), C.byref(r), C.byref(nc))
+        return {"world": w.value, "rank": r.value, "nccl": bool(nc.value)}
+
+    def close(self):
+        if self.ptr:
+            self.lib.spk_comm_destroy(self.ptr)
+            self.ptr = None
+
+
+class EmulatedGroup:
+    def __init__(self, world: int, lib=None):
+        self.lib = lib or L.load()
+        self.ptr = C.c_void_p()
+        if self.lib.spk_comm_group_create(world, C.byref(self.ptr)):
+            raise RuntimeError("spk_comm_group_create failed")
+
+    def close(self):
+        if self.ptr:
+            self.lib.spk_comm_group_destroy(self.ptr)
+            self.ptr = None
+
+
+class LibShardedSketch:
+    """spk_sharded_build / spk_sharded_solve: this rank's share of the sharded
+    sketch, built and solved by the library's driver."""
+
+    def __init__(self, comm: LibComm, kernel: Coords, a, b, plan: str, lambda_: float, epsilon: float, s: float,
+                 seed: int, opts: SparSinkOptions | None = None):
+        self.comm, self.lib = comm, comm.lib
+        self.a = np.ascontiguousarray(a, dtype=np.float64)
+        self.b = np.ascontiguousarray(b, dtype=np.float64)
+        kd, self._keep = kernel.desc()
+        o = (opts or SparSinkOptions()).c()
+        kind = L.PLAN_UNIFORM if (opts and opts.probs == "uniform") else (L.PLAN_UOT if plan == "uot" else L.PLAN_OT)
+        self.ptr = C.c_void_p()
+        _raise(comm.ctx.ptr, self.lib.spk_sharded_build(comm.ptr, C.byref(kd), L.dptr(self.a), L.dptr(self.b), kind,
+                                                        float(lambda_), float(epsilon), float(s),
+                                                        C.c_uint64(seed & 0xFFFFFFFFFFFFFFFF), C.byref(o),
+                                                        C.byref(self.ptr)))
+        self.info = self._info()
+
+    def _info(self) -> dict:
+        v = [C.c_int64() for _ in range(6)]
+        self.lib.spk_sharded_info(self.ptr, *[C.byref(x) for x in v])
+        return dict(zip(("n", "nnz", "kernel_nnz", "lo", "hi", "captured_launches"), (x.value for x in v)))
+
+    def solve(self, cfg: SolverConfig, uot: bool = False, want_scalings: bool = True) -> ShardedResult:
+        n = self.info["n"]
+        u, v, lu, lv = ((np.empty(n) for _ in range(4)) if want_scalings else (None,) * 4)
+        rep = L.Report()
+        c = cfg.c(L.POLICY_MASK)
+        _raise(self.comm.ctx.ptr, self.lib.spk_sharded_solve(self.ptr, C.byref(c), int(uot), L.dptr(u), L.dptr(v),
+                                                             L.dptr(lu), L.dptr(lv), C.byref(rep)))
+        self.info = self._info()
+        log = bool(rep.log_domain)
+        return ShardedResult(u, v, lu if log else None, lv if log else None, rep.as_dict())
+
+    def free(self):
+        if self.ptr:
+            self.lib.spk_sharded_free(self.ptr)
+            self.ptr = None
+
+
+def spar_sink_multi(devices, kernel: Coords, a, b, cfg: SolverConfig, s: float, seed: int,
+                    opts: SparSinkOptions | None = None, uot: bool = False) -> ShardedResult:
+    """spk_spar_sink_multi: one call from one host thread over several GPUs of
+    this process (NCCL communicators and a driver thread per GPU inside)."""
+    lib = L.load()
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    kd, keep = kernel.desc()
+    n = int(kd.n)
+    u, v, lu, lv = (np.empty(n) for _ in range(4))
+    rep = L.Report()
+    devs = (C.c_int * len(devices))(*devices)
+    o = (opts or SparSinkOptions()).c()
+    c = cfg.c(L.POLICY_MASK)
+    rc = lib.spk_spar_sink_multi(devs, len(devices), C.byref(kd), L.dptr(a), L.dptr(b), C.byref(c), float(s),
+                                 C.c_uint64(seed & 0xFFFFFFFFFFFFFFFF), C.byref(o), int(uot), L.dptr(u), L.dptr(v),
+                                 L.dptr(lu), L.dptr(lv), C.byref(rep))
+    _raise(None, rc)
+    log = bool(rep.log_domain)
+    return ShardedResult(u, v, lu if log else None, lv if log else None, rep.as_dict())
