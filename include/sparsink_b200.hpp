@@ -261,6 +261,11 @@ struct SparSinkOptions {
   SketchProbs probs = SketchProbs::Importance;
   bool strict = false;
   ValuePrecision values = ValuePrecision::F64;  // B200 extension
+  // B200 extension: GPUs of this process for the coordinate overloads of
+  // spar_sink_*. Empty = the thread's device (set_device). Listed: the sketch's
+  // rows and columns are sharded over them (NCCL inside the library, one
+  // driver thread per GPU, spk_spar_sink_multi).
+  std::vector<int> devices;
 };
 
 SolveResult spar_sink_ot(const KernelMatrix& K, const CostMatrix& C, const DiscreteMeasure& a,

@@ -17,6 +17,7 @@
 //               folded into fp64. SFU/FMA-bound, no n^2 memory.
 #include <algorithm>
 #include <cmath>
+#include <type_traits>
 #include <vector>
 
 #include "common.cuh"
@@ -176,6 +177,7 @@ __device__ __forceinline__ float ex2_ftz(float e) {
   return r;
 }
 
+template <int D>
 struct OtfFastOp {
   static constexpr int kThreads = loopcore::kBlock;
   static constexpr int kMinBlocks = 1;  // 128 registers (at 64 the point records spilled)
@@ -183,6 +185,25 @@ struct OtfFastOp {
   int dim;
   const float4* out_rec[2];  // [role] output-side records (2 float4 per atom)
   const float4* in_rec[2];   // [role] input-side records
+
+  // exponent of K_ij in log2 units: bias_i + bias_j + <p_i, y_j>, D + 1 FMA-pipe ops
+  __device__ __forceinline__ static float expo(const float (&p)[D + 1], const float (&q)[8]) {
+    float e = p[D] + q[7];
+#pragma unroll
+    for (int k = 0; k < D; ++k) e = fmaf(p[k], q[k], e);
+    return e;
+  }
+  __device__ __forceinline__ static void load_rec(const float4* rp, float (&q)[8]) {
+    const float4 a = __ldg(rp);
+    q[0] = a.x; q[1] = a.y; q[2] = a.z; q[3] = a.w;
+    if (D > 3) {  // d <= 3: coordinates + bias fit the first float4... the bias lives in slot 7
+      const float4 b = __ldg(rp + 1);
+      q[4] = b.x; q[5] = b.y; q[6] = b.z; q[7] = b.w;
+    } else {
+      const float4 b = __ldg(rp + 1);
+      q[7] = b.w;
+    }
+  }
 
   template <int ROLE, bool LOG, bool DET>
   __device__ void half(const double* x, const double* wgt, const double* old, double* out, unsigned char* ne,
@@ -198,7 +219,7 @@ struct OtfFastOp {
     const int64_t ntiles = (n + tile_rows - 1) / tile_rows;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
       const int64_t r0 = tile * tile_rows;
-      float p[kOtfRows][kOtfDim];
+      float p[kOtfRows][D + 1];
       double acc[kOtfRows];
 #pragma unroll
       for (int r = 0; r < kOtfRows; ++r) {
@@ -208,8 +229,10 @@ struct OtfFastOp {
           a = orec[2 * i];
           b = orec[2 * i + 1];
         }
-        p[r][0] = a.x; p[r][1] = a.y; p[r][2] = a.z; p[r][3] = a.w;
-        p[r][4] = b.x; p[r][5] = b.y; p[r][6] = b.z; p[r][7] = b.w;
+        const float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+        for (int k = 0; k < D; ++k) p[r][k] = v[k];
+        p[r][D] = v[7];  // bias_i
         acc[r] = 0.0;
       }
       // warp w handles column chunks w, w + nwarps, ...
@@ -223,23 +246,25 @@ struct OtfFastOp {
         const float4* qp = irec + 2 * c0;
         const double* xp = x + c0;
         const int len = (int)(c1 - c0);
-        for (int jj = 0; jj < len; ++jj) {  // 32-bit induction: no 64-bit counter arithmetic per column
-          const float4 qa = __ldg(qp + 2 * jj);
-          const float4 qb = __ldg(qp + 2 * jj + 1);
-          const float xj = (float)__ldcg(xp + jj);
+        int jj = 0;
+        for (; jj + 1 < len; jj += 2) {  // two columns per step: independent exp chains
+          float q0[8], q1[8];
+          load_rec(qp + 2 * jj, q0);
+          load_rec(qp + 2 * jj + 2, q1);
+          const float x0 = (float)__ldcg(xp + jj), x1 = (float)__ldcg(xp + jj + 1);
 #pragma unroll
           for (int r = 0; r < kOtfRows; ++r) {
-            // bias_i (p[r][dim] slot) + bias_j (qb.w) + <p_i, y_j>
-            float e = p[r][7] + qb.w;
-            e = fmaf(p[r][0], qa.x, e);
-            e = fmaf(p[r][1], qa.y, e);
-            e = fmaf(p[r][2], qa.z, e);
-            e = fmaf(p[r][3], qa.w, e);
-            e = fmaf(p[r][4], qb.x, e);
-            e = fmaf(p[r][5], qb.y, e);
-            e = fmaf(p[r][6], qb.z, e);
-            part[r] = fmaf(ex2_ftz(e), xj, part[r]);
+            const float e0 = expo(p[r], q0), e1 = expo(p[r], q1);
+            part[r] = fmaf(ex2_ftz(e0), x0, part[r]);
+            part[r] = fmaf(ex2_ftz(e1), x1, part[r]);
           }
+        }
+        if (jj < len) {
+          float q0[8];
+          load_rec(qp + 2 * jj, q0);
+          const float x0 = (float)__ldcg(xp + jj);
+#pragma unroll
+          for (int r = 0; r < kOtfRows; ++r) part[r] = fmaf(ex2_ftz(expo(p[r], q0)), x0, part[r]);
         }
 #pragma unroll
         for (int r = 0; r < kOtfRows; ++r) acc[r] += (double)part[r];
@@ -355,13 +380,7 @@ void run_dense_loop(spk_ctx* ctx, DevKernel& dk, const spk_solver_cfg& cfg, doub
   otf_records_kernel<<<g, 256, 0, ctx->stream>>>(dk.x.as<double>(), n, dk.dim, alpha, xo.as<float4>(), xi.as<float4>());
   otf_records_kernel<<<g, 256, 0, ctx->stream>>>(dk.y.as<double>(), n, dk.dim, alpha, yo.as<float4>(), yi.as<float4>());
   ctx->launches += 2;
-  OtfFastOp op;
-  op.n = n;
-  op.dim = dk.dim;
-  op.out_rec[0] = xo.as<float4>();  // rows: x_i against y_j
-  op.in_rec[0] = yi.as<float4>();
-  op.out_rec[1] = yo.as<float4>();  // columns: y_j against x_i
-  op.in_rec[1] = xi.as<float4>();
+  const float4* recs[4] = {xo.as<float4>(), yi.as<float4>(), yo.as<float4>(), xi.as<float4>()};
   // coverage: exp2 of finite exponents never reaches 0 for max-normalised
   // costs with 1/eps < 700; otherwise use the exact coverage pass.
   LoopWs W;
@@ -377,8 +396,27 @@ void run_dense_loop(spk_ctx* ctx, DevKernel& dk, const spk_solver_cfg& cfg, doub
   unsigned long long emp[2];
   download(ctx, emp, empty, sizeof emp);
   const int64_t useful = (n + 32 * kOtfRows - 1) / (32 * kOtfRows);
-  loopcore::run_core<false>(ctx, op, n, W, (long long)emp[0], (long long)emp[1], cfg, exponent, policy, st, useful,
-                            out);
+  // the point-record width is a compile-time constant: D + 1 FMA-pipe ops per evaluation
+  auto go = [&](auto dtag) {
+    constexpr int D = decltype(dtag)::value;
+    OtfFastOp<D> op;
+    op.n = n;
+    op.dim = dk.dim;
+    op.out_rec[0] = recs[0];  // rows: x_i against y_j
+    op.in_rec[0] = recs[1];
+    op.out_rec[1] = recs[2];  // columns: y_j against x_i
+    op.in_rec[1] = recs[3];
+    loopcore::run_core<false>(ctx, op, n, W, (long long)emp[0], (long long)emp[1], cfg, exponent, policy, st,
+                              useful, out);
+  };
+  switch (dk.dim) {
+    case 1: go(std::integral_constant<int, 1>{}); break;
+    case 2: go(std::integral_constant<int, 2>{}); break;
+    case 3: go(std::integral_constant<int, 3>{}); break;
+    case 4: go(std::integral_constant<int, 4>{}); break;
+    case 5: go(std::integral_constant<int, 5>{}); break;
+    default: go(std::integral_constant<int, 6>{}); break;
+  }
 }
 
 }  // namespace spk

@@ -234,8 +234,15 @@ SolveResult spar_sink(const spk_kernel_desc& d, const DiscreteMeasure& a, const 
   spk_sketch_opts o = c_opts(opts);
   std::vector<double> u(n), v(n), lu(n), lv(n);
   spk_report r;
-  check(spk_spar_sink(ctx(), &d, a.weights.data(), b.weights.data(), &c, s, seed, &o, uot ? 1 : 0, u.data(),
-                      v.data(), lu.data(), lv.data(), &r));
+  if (!opts.devices.empty() && d.x) {  // rows / columns sharded over the listed GPUs of this process
+    const int rc = spk_spar_sink_multi(opts.devices.data(), static_cast<int>(opts.devices.size()), &d,
+                                       a.weights.data(), b.weights.data(), &c, s, seed, &o, uot ? 1 : 0, u.data(),
+                                       v.data(), lu.data(), lv.data(), &r);
+    if (rc != SPK_OK) rethrow(nullptr);
+  } else {
+    check(spk_spar_sink(ctx(), &d, a.weights.data(), b.weights.data(), &c, s, seed, &o, uot ? 1 : 0, u.data(),
+                        v.data(), lu.data(), lv.data(), &r));
+  }
   SolveResult res = make_result(n, r, std::move(u), std::move(v), std::move(lu), std::move(lv));
   res.report.objective = r.objective;
   res.report.sketch_nnz = static_cast<std::size_t>(r.sketch_nnz);

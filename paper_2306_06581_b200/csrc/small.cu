@@ -37,7 +37,7 @@ namespace {
 using loopcore::finalize_atom;
 using loopcore::kNone;
 
-constexpr int kThreads = 1024;
+constexpr int kThreads = 512;  // 16 warps x 4 row groups = 64 rows in flight; 128 registers
 constexpr int kMaxCS = 16;
 
 template <class VT>
@@ -202,6 +202,9 @@ __global__ void __launch_bounds__(kThreads, 1) cluster_loop_kernel(ClusterArgs<V
   __shared__ double xe[2][CS];  // per half: every CTA's partials, slot = its rank
   __shared__ long long xm[2][CS];
   __shared__ unsigned long long xf[2][CS];
+  __shared__ double comb_e;
+  __shared__ long long comb_m;
+  __shared__ unsigned long long comb_f;
   const double on = LOG ? 0.0 : 1.0, off = LOG ? -CUDART_INF : 0.0;
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {  // u = v = 1 on covered atoms (:277-281, :424-428)
     X[0][i] = A.ne[0][i] ? on : off;
@@ -273,18 +276,33 @@ __global__ void __launch_bounds__(kThreads, 1) cluster_loop_kernel(ClusterArgs<V
         *pf = f;
       }
       if (lane == 0) flag_sh[h] = kNone;  // recycled for this half's next iteration
+      __syncwarp();
+      // one release for the whole CTA: every thread's DSMEM stores were
+      // ordered before warp 0 by the __syncthreads above (cumulativity)
+      if (CS > 1 && lane == 0) asm volatile("fence.acq_rel.cluster;" ::: "memory");
     }
-    if (CS > 1) cluster_barrier();  // new values and partials visible cluster-wide
+    if (CS > 1)  // new values and partials visible cluster-wide
+      asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
     else __syncthreads();
-    err_all = 0.0;
-    masks_all = 0;
-    flag_all = kNone;
-#pragma unroll
-    for (int r = 0; r < CS; ++r) {  // rank order: the same sums on every CTA
-      err_all += xe[h][r];
-      masks_all += xm[h][r];
-      flag_all = min(flag_all, xf[h][r]);
+    if (warp == 0) {  // rank order: the same sums on every CTA
+      double e = 0.0;
+      long long mk = 0;
+      unsigned long long f = kNone;
+      for (int r = 0; r < CS; ++r) {
+        e += xe[h][r];
+        mk += xm[h][r];
+        f = min(f, xf[h][r]);
+      }
+      if (lane == 0) {
+        comb_e = e;
+        comb_m = mk;
+        comb_f = f;
+      }
     }
+    __syncthreads();
+    err_all = comb_e;
+    masks_all = comb_m;
+    flag_all = comb_f;
   };
   auto restore = [&](int h) {  // previous iterate of this CTA's atoms (every CTA restores its own)
     const int64_t r0 = A.lo[h][rank], r1 = A.lo[h][rank + 1];

@@ -374,6 +374,27 @@ int main() {
     }
     CHECK_THROWS_AS(spar_sink_uot_pairs(grid, cs, frames, pairs, cfg, s, {1, 2}, o), LengthMismatch);
   });
+  run("sharded over the listed GPUs (SparSinkOptions::devices) == one-GPU solve", [] {
+    auto inst = random_instance(400, 0.05, 91);
+    SolverConfig cfg = tight(0.05);
+    cfg.delta = -1.0;
+    cfg.max_iter = 80;
+    CostSpec cs;
+    cs.scale = 1.0;
+    auto one = spar_sink_ot(inst.a.support, inst.b.support, cs, inst.a, inst.b, cfg, 6000.0, 23);
+    SparSinkOptions o;
+    o.devices = {0};
+    auto sh = spar_sink_ot(inst.a.support, inst.b.support, cs, inst.a, inst.b, cfg, 6000.0, 23, o);
+    CHECK(one.report.sketch_nnz == sh.report.sketch_nnz);
+    CHECK(one.report.iterations == sh.report.iterations);
+    CHECK_CLOSE(sh.report.objective, one.report.objective, 1e-10);
+    for (std::size_t i = 0; i < 400; ++i) CHECK_CLOSE(sh.plan.u[i], one.plan.u[i], 1e-10);
+    // the failing rank's exception class crosses the multi-GPU driver
+    DiscreteMeasure bad = inst.b;
+    for (auto& w : bad.weights) w *= 2.0;
+    bad.total_mass *= 2.0;
+    CHECK_THROWS_AS(spar_sink_ot(inst.a.support, inst.b.support, cs, inst.a, bad, cfg, 6000.0, 23, o), NotNormalized);
+  });
   std::printf("%d checks passed, %d failed\n", g_pass, g_fail);
   return g_fail;
 }

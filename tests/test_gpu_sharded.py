@@ -151,7 +151,11 @@ def test_sharded_uot_converges_like_single_gpu(ctx, stabilize):
                                                                        check_every=8))
     for r in outs:
         assert r.report["converged"] == ref.report["converged"] == 1
-        assert abs(r.report["iterations"] - ref.report["iterations"]) <= 1  # residual within rounding of delta
+        # the delta stop: near convergence the residual sum_i |du_i| (~1e-9)
+        # carries rounding noise of ~1e-16 u per atom, so another summation
+        # order (3 ranks vs the one-cluster loop) may cross delta a few
+        # iterations apart; the scalings below pin the result
+        assert abs(r.report["iterations"] - ref.report["iterations"]) <= 3
         np.testing.assert_allclose(r.u, ref.u, rtol=1e-6)
         np.testing.assert_allclose(r.v, ref.v, rtol=1e-6)
         assert r.report["objective"] == pytest.approx(ref.report["objective"], rel=1e-7)
