@@ -373,12 +373,16 @@ def run_ours(args, ws, rank, local):
     per_launch_iters = iters_done / args.steps
     mean_loop = sum(loop_s) / len(loop_s)
     achieved = b_iter * per_launch_iters / mean_loop / 1e9
-    traffic = None  # DRAM bytes per launch from the committed ncu --set full capture of this kernel
+    # DRAM bytes per launch: NOT measured in this run (no profiler in a timed
+    # run) -- the per-iteration DRAM bytes of the committed ncu --set full
+    # capture of this loop, times this launch's iterations; labelled as such
+    traffic, traffic_src = None, None
     prof = ROOT / "profiles" / f"ncu_{w.name.lower()}_loop.json"
     if prof.exists():
         k0 = json.loads(prof.read_text())["kernels"][0]
         if "dram_bytes_per_iteration" in k0:
             traffic = k0["dram_bytes_per_iteration"] * per_launch_iters
+            traffic_src = f"copied from {prof.relative_to(ROOT)} ({k0.get('variant', 'ncu capture')}), not measured in this run"
 
     # ---- end to end through the C ABI with host buffers ----
     e2e = None
@@ -400,17 +404,30 @@ def run_ours(args, ws, rank, local):
 
     # ---- CPU baseline: the reference loop on this very sketch (rank 0, N=1) ----
     cpu = None
+    parity = None
     if rank == 0 and ws == 1 and not args.no_cpu:
         from oracle import Oracle, Reference
 
         rp, ci, vv = sk.csr()
         k_cpu = args.cpu_iters
         if Reference.available():
-            secs, _ = Reference().sparse_loop_seconds((rp, ci, vv), w.a, w.b, w.eps, k_cpu, w.lam, w.uot)
+            # the reference's sinkhorn_<plan><SparseKernel> on this very sketch for k_cpu
+            # fixed iterations: its wall time is the CPU baseline, its scalings
+            # the parity check of the production loop on the same iterations
+            t0 = time.perf_counter()
+            ru, rv, _, _, rrep = Reference().sinkhorn(w.a, w.b, w.eps, w.lam, -1.0, k_cpu, stabilize=w.stabilize,
+                                                      policy="mask", uot=w.uot, csr=(rp, ci, vv))
+            secs = rrep["wall_time_s"] if rrep.get("wall_time_s") else time.perf_counter() - t0
             kind = "reference"
+            g = sk.solve(spk.SolverConfig(w.eps, w.lam, -1.0, k_cpu, w.stabilize), w.uot)
+            rel = lambda a, b: float(np.max(np.abs(a - b) / np.maximum(np.abs(b), 1e-300)))  # noqa: E731
+            parity = {"iterations": k_cpu, "max_rel_diff_u": rel(g.u, ru), "max_rel_diff_v": rel(g.v, rv),
+                      "masked_rows_equal": g.report["masked_rows"] == rrep["masked_rows"],
+                      "against": "reference sinkhorn on the same GPU-built sketch (oracle/_ref)"}
         else:
             t, _, _ = Oracle().time_scaling_iters((rp, ci, vv), w.a, w.b, k_cpu)
             secs, kind = t * k_cpu, "port"
+            parity = None
         cpu = {"value": k_cpu / secs, "unit": "iters/s", "cores": 1, "host_cores": os.cpu_count(), "kind": kind,
                "sample": f"{k_cpu} of {iters} iterations of sinkhorn_{plan}<SparseKernel> on the GPU-built "
                          f"{w.name} sketch ({sk.nnz} nnz) copied to host, 1 of {os.cpu_count()} host cores "
@@ -445,12 +462,13 @@ def run_ours(args, ws, rank, local):
                    "l2": f"inputs larger than L2: sketch {(sk.nnz * 2 * (vb + 4)) / 1e9:.2f} GB"
                          if args.config == "c4" else "sketch L2-resident (config smaller than L2)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "kernel": "loop_kernel (persistent, both halves)",
+                     "traffic": traffic, "traffic_source": traffic_src, "kernel": "loop_kernel (persistent, both halves)",
                      "bytes_per_iter": b_iter, "peak_source": peak_src},
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": launches,
         "clocks": clk.summary(),
+        "parity": parity,
         "extra": {"setup_s": setup_s, "loop_ms_per_iter": 1e3 * mean_loop / per_launch_iters,
                   "kernel_nnz": sk.kernel_nnz, "factorized_plan": sk.factorized_plan},
     }

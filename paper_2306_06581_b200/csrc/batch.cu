@@ -498,6 +498,7 @@ void run_batch_log(spk_ctx* ctx, spk_sketch* const* sks, int count, const spk_so
                    const std::vector<double>& exponents, int policy, std::vector<LoopOut>& outs,
                    std::vector<std::string>& errors, std::vector<int>& error_kinds) {
   cudaStream_t s = ctx->stream;
+  NvtxRange nr("spk:batch_loop");
   int64_t nmax = 0;
   for (int k = 0; k < count; ++k) nmax = std::max(nmax, sks[k]->n);
   const int npad = (int)((nmax + 31) / 32 * 32);

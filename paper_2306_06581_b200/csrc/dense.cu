@@ -25,6 +25,8 @@
 #include "ksrc.cuh"
 #include "loop_core.cuh"
 
+#include <cooperative_groups.h>
+
 namespace spk {
 
 namespace {
@@ -185,6 +187,8 @@ struct OtfFastOp {
   int dim;
   const float4* out_rec[2];  // [role] output-side records (2 float4 per atom)
   const float4* in_rec[2];   // [role] input-side records
+  int parts;                 // column ranges per row block (work items ~ warps of the grid)
+  double* partial;           // [parts][n] partial row sums
 
   // exponent of K_ij in log2 units: bias_i + bias_j + <p_i, y_j>, D + 1 FMA-pipe ops
   __device__ __forceinline__ static float expo(const float (&p)[D + 1], const float (&q)[8]) {
@@ -205,20 +209,31 @@ struct OtfFastOp {
     }
   }
 
+  // Work item = (block of 32 x kOtfRows rows) x (one of `parts` column
+  // ranges), one WARP each, no CTA barrier: items ~ warps of the grid, so
+  // every warp streams the same number of evaluations. Each item leaves fp64
+  // partial row sums in part[cp * n + i]; after one grid barrier the rows are
+  // finalised from their `parts` partials summed in column-range order.
   template <int ROLE, bool LOG, bool DET>
   __device__ void half(const double* x, const double* wgt, const double* old, double* out, unsigned char* ne,
                        int* dyn, double exponent, int policy, int t, unsigned long long* flag, double* absdiff,
                        double& err, long long& masks) const {
-    __shared__ double red[loopcore::kBlock / 32][32 * kOtfRows];
     const int lane = threadIdx.x & 31;
-    const int w = threadIdx.x >> 5;
     const int nwarps = blockDim.x >> 5;
     const float4* orec = out_rec[ROLE];
     const float4* irec = in_rec[ROLE];
     const int64_t tile_rows = 32 * kOtfRows;
-    const int64_t ntiles = (n + tile_rows - 1) / tile_rows;
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-      const int64_t r0 = tile * tile_rows;
+    const int64_t nrb = (n + tile_rows - 1) / tile_rows;
+    const int64_t items = nrb * parts;
+    const int64_t gw = (int64_t)blockIdx.x * nwarps + (threadIdx.x >> 5);
+    const int64_t tw = (int64_t)gridDim.x * nwarps;
+    for (int64_t item = gw; item < items; item += tw) {
+      const int64_t rbk = item / parts;
+      const int cp = (int)(item - rbk * parts);
+      const int64_t r0 = rbk * tile_rows;
+      // column range of this part (even boundaries: two columns per step)
+      const int64_t per = ((n + parts - 1) / parts + 1) & ~int64_t(1);
+      const int64_t c_lo = min(n, cp * per), c_hi = min(n, c_lo + per);
       float p[kOtfRows][D + 1];
       double acc[kOtfRows];
 #pragma unroll
@@ -235,17 +250,13 @@ struct OtfFastOp {
         p[r][D] = v[7];  // bias_i
         acc[r] = 0.0;
       }
-      // warp w handles column chunks w, w + nwarps, ...
-      const int64_t nchunks = (n + kOtfChunk - 1) / kOtfChunk;
-      for (int64_t ch = w; ch < nchunks; ch += nwarps) {
-        const int64_t c0 = ch * kOtfChunk;
-        const int64_t c1 = min(c0 + kOtfChunk, n);
+      for (int64_t c0 = c_lo; c0 < c_hi; c0 += kOtfChunk) {  // fp32 partials per chunk, folded into fp64
+        const int len = (int)min((int64_t)kOtfChunk, c_hi - c0);
         float part[kOtfRows];
 #pragma unroll
         for (int r = 0; r < kOtfRows; ++r) part[r] = 0.f;
         const float4* qp = irec + 2 * c0;
         const double* xp = x + c0;
-        const int len = (int)(c1 - c0);
         int jj = 0;
         for (; jj + 1 < len; jj += 2) {  // two columns per step: independent exp chains
           float q0[8], q1[8];
@@ -270,22 +281,21 @@ struct OtfFastOp {
         for (int r = 0; r < kOtfRows; ++r) acc[r] += (double)part[r];
       }
 #pragma unroll
-      for (int r = 0; r < kOtfRows; ++r) red[w][lane + 32 * r] = acc[r];
-      __syncthreads();
-      // warp 0..: combine warps in fixed order, finalize atoms
-      for (int q = threadIdx.x; q < tile_rows; q += blockDim.x) {
-        const int64_t i = r0 + q;
-        if (i >= n) continue;
-        double tmp = 0.0;
-        for (int k = 0; k < nwarps; ++k) tmp += red[k][q];
-        const double o = __ldcg(old + i);
-        if (!ne[i]) {
-          out[i] = o;
-          continue;
-        }
-        err += finalize_atom<false>(i, tmp, o, wgt[i], exponent, policy, t, ne, dyn, out, flag, masks);
+      for (int r = 0; r < kOtfRows; ++r) {
+        const int64_t i = r0 + lane + 32 * r;
+        if (i < n) partial[(int64_t)cp * n + i] = acc[r];
       }
-      __syncthreads();
+    }
+    cooperative_groups::this_grid().sync();  // every partial row sum written
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+      double tmp = 0.0;
+      for (int c = 0; c < parts; ++c) tmp += __ldcg(partial + (int64_t)c * n + i);  // column-range order
+      const double o = __ldcg(old + i);
+      if (!ne[i]) {
+        out[i] = o;
+        continue;
+      }
+      err += finalize_atom<false>(i, tmp, o, wgt[i], exponent, policy, t, ne, dyn, out, flag, masks);
     }
   }
 };
@@ -395,7 +405,19 @@ void run_dense_loop(spk_ctx* ctx, DevKernel& dk, const spk_solver_cfg& cfg, doub
   ++ctx->launches;
   unsigned long long emp[2];
   download(ctx, emp, empty, sizeof emp);
-  const int64_t useful = (n + 32 * kOtfRows - 1) / (32 * kOtfRows);
+  // grid = co-resident CTAs (run_core: occupancy x SMs); pick the column
+  // ranges so that (row blocks x ranges) matches the grid's warps
+  int per_sm = 1;
+  {
+    auto k5 = loopcore::loop_kernel<false, false, OtfFastOp<5>>;
+    SPK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k5, loopcore::kBlock, 0));
+    per_sm = std::max(per_sm, 1);
+  }
+  const int64_t nrb = (n + 32 * kOtfRows - 1) / (32 * kOtfRows);
+  const int64_t warps = (int64_t)ctx->num_sms * per_sm * (loopcore::kBlock / 32);
+  const int parts = (int)std::max<int64_t>(1, std::min<int64_t>(64, (warps + nrb / 2) / std::max<int64_t>(nrb, 1)));
+  DBuf partial(sizeof(double) * (size_t)parts * n);
+  const int64_t useful = (int64_t)ctx->num_sms * per_sm;
   // the point-record width is a compile-time constant: D + 1 FMA-pipe ops per evaluation
   auto go = [&](auto dtag) {
     constexpr int D = decltype(dtag)::value;
@@ -406,6 +428,8 @@ void run_dense_loop(spk_ctx* ctx, DevKernel& dk, const spk_solver_cfg& cfg, doub
     op.in_rec[0] = recs[1];
     op.out_rec[1] = recs[2];  // columns: y_j against x_i
     op.in_rec[1] = recs[3];
+    op.parts = parts;
+    op.partial = partial.as<double>();
     loopcore::run_core<false>(ctx, op, n, W, (long long)emp[0], (long long)emp[1], cfg, exponent, policy, st,
                               useful, out);
   };

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <cstdint>
 #include <memory>
@@ -177,6 +178,15 @@ namespace spk {
 
 void upload(spk_ctx* ctx, DBuf& dst, const void* src, size_t bytes);
 void download(spk_ctx* ctx, void* dst, const DBuf& src, size_t bytes);
+
+// NVTX range over a phase (plan / sample / loop / readout / ...): visible in
+// nsys / ncu timelines; free when no tool is attached (NVTX v3, header-only).
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 struct Timer {
   cudaEvent_t a = nullptr, b = nullptr;

@@ -208,6 +208,7 @@ void ensure_log_values(spk_ctx* ctx, spk_sketch* sk) {
 void run_sparse_loop(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, double exponent, int policy,
                      LoopState& st, LoopOut& out) {
   const bool log_domain = cfg.stabilize != 0;
+  NvtxRange nr(log_domain ? "spk:loop(log)" : "spk:loop");
   ensure_coverage(ctx, sk);
   // small sketches: one cluster, scalings in shared memory, no grid barriers
   if (run_cluster_loop(ctx, sk, cfg, exponent, policy, st, out)) return;

@@ -87,6 +87,7 @@ void build(spk_sharded* S, const spk_kernel_desc* kd, const double* a, const dou
   spk_ctx* ctx = S->ctx;
   const int W = comm->world, r = comm->rank;
   cudaStream_t st = ctx->stream;
+  NvtxRange nr("spk:sharded_build");
   const int64_t n = kd->n;
   int64_t m, lo, hi;
   slab(n, W, r, m, lo, hi);
@@ -217,6 +218,7 @@ void solve(spk_sharded* S, const spk_solver_cfg& cfg, int uot, double* u, double
   cudaStream_t st = ctx->stream;
   const int W = comm->world, r = comm->rank;
   const int policy = S->strict ? SPK_POLICY_ERROR : SPK_POLICY_MASK;
+  NvtxRange nr("spk:sharded_solve");
   const double t0 = now_s();
   Timer tm(st);
   check_rc(ctx, spk_shard_begin(S->sh, &cfg, uot, policy, S->empty_rows, S->empty_cols, S->U[0].as<double>(),

@@ -145,9 +145,13 @@ void build_sketch(spk_ctx* ctx, DevKernel& dk, const double* a, const double* b,
                   double eps, double theta, double s, uint64_t seed, int value_type, spk_sketch* sk, double* t_plan,
                   double* t_sample) {
   PlanInfo plan;
-  Timer tp(ctx->stream);
-  build_plan(ctx, dk, a, b, plan_kind, lambda, eps, theta > 0.0 ? theta : 0.0, plan);
-  *t_plan = tp.stop();
+  {
+    NvtxRange r("spk:plan");
+    Timer tp(ctx->stream);
+    build_plan(ctx, dk, a, b, plan_kind, lambda, eps, theta > 0.0 ? theta : 0.0, plan);
+    *t_plan = tp.stop();
+  }
+  NvtxRange r("spk:sample");
   Timer ts(ctx->stream);
   sample_sketch(ctx, dk, plan, s, seed, value_type, sk);
   *t_sample = ts.stop();
@@ -363,6 +367,7 @@ int spk_spar_sink(spk_ctx* ctx, const spk_kernel_desc* kd, const double* a, cons
     if (o.strict) strict_coverage(ctx, &sk);
     solve_on_sketch(ctx, &sk, *cfg, uot, o.strict ? SPK_POLICY_ERROR : SPK_POLICY_MASK, rep);
     ReadoutOut ro;
+    NvtxRange nr("spk:readout");
     Timer tr(ctx->stream);
     sparse_readout(ctx, &sk, &dk, sk.last_log_domain, sk.a.as<double>(), sk.b.as<double>(), true, uot, cfg->lambda,
                    cfg->epsilon, nullptr, nullptr, ro);
