@@ -19,6 +19,7 @@
 // and sinkhorn_ot/uot (K recomputed on the fly), plus batched frame pairs.
 #pragma once
 
+#include <algorithm>
 #include <cmath>
 #include <cstddef>
 #include <cstdint>
@@ -76,6 +77,46 @@ class DeviceError : public std::runtime_error {
   using std::runtime_error::runtime_error;
 };
 
+// ---- counter-based RNG (rng.hpp:10-50) ----------------------------------------------
+// Draw t (t = 1, 2, ...) of stream (seed, stream) is the splitmix64 finalizer
+// of mix_seed(seed, stream) + t * golden: any draw of any stream is addressable
+// directly (the GPU sampler evaluates draw t of row i in closed form).
+constexpr std::uint64_t kGoldenGamma = 0x9e3779b97f4a7c15ULL;
+inline std::uint64_t splitmix64_finalize(std::uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+inline std::uint64_t splitmix64(std::uint64_t x) { return splitmix64_finalize(x + kGoldenGamma); }
+inline std::uint64_t mix_seed(std::uint64_t seed, std::uint64_t stream) {
+  return splitmix64(seed ^ splitmix64(stream + 0x632be59bd9b4e019ULL));
+}
+
+class CounterRng {
+ public:
+  explicit CounterRng(std::uint64_t seed, std::uint64_t stream = 0) : base_(mix_seed(seed, stream)) {}
+  std::uint64_t next_u64() { return splitmix64_finalize(base_ + (++t_) * kGoldenGamma); }
+  double next_double() { return static_cast<double>(next_u64() >> 11) * 0x1.0p-53; }  // 53 bits in [0, 1)
+  // Box-Muller, two draws per pair, the sine half kept for the next call (rng.cpp:7-21)
+  double next_normal() {
+    if (spare_ok_) {
+      spare_ok_ = false;
+      return spare_;
+    }
+    const double u1 = std::max(next_double(), 1e-300), u2 = next_double();
+    const double r = std::sqrt(-2.0 * std::log(u1)), th = 2.0 * 3.14159265358979323846 * u2;
+    spare_ = r * std::sin(th);
+    spare_ok_ = true;
+    return r * std::cos(th);
+  }
+
+ private:
+  std::uint64_t base_;
+  std::uint64_t t_ = 0;
+  bool spare_ok_ = false;
+  double spare_ = 0.0;
+};
+
 // ---- containers ---------------------------------------------------------------------
 class Matrix {
  public:
@@ -131,6 +172,9 @@ CostMatrix sq_euclidean_cost(const PointList& x, const PointList& y);
 CostMatrix euclidean_cost(const PointList& x, const PointList& y);
 CostMatrix wfr_cost(const PointList& x, const PointList& y, double eta);
 KernelMatrix kernel_from_cost(const CostMatrix& cost, double epsilon);
+// WFR eta whose cut pi * eta keeps the target fraction of the n^2 pairwise
+// distances (geometry.cpp:104-135).
+double eta_for_sparsity(const PointList& x, double target_nnz_ratio);
 
 // ---- sketches ---------------------------------------------------------------------------
 enum class PlanKind { OT, UOT, Barycenter, Uniform };
@@ -149,6 +193,7 @@ class SamplingPlan {
   friend SamplingPlan uot_probabilities(const DiscreteMeasure&, const DiscreteMeasure&, const KernelMatrix&, double,
                                         double);
   friend SamplingPlan uniform_probabilities(const KernelMatrix&);
+  friend SamplingPlan barycenter_probabilities(const DiscreteMeasure&, const KernelMatrix&);
   friend SamplingPlan shrink_with_uniform(const SamplingPlan&, double);
   friend struct PlanAccess;
 
@@ -175,6 +220,9 @@ SamplingPlan ot_probabilities(const DiscreteMeasure& a, const DiscreteMeasure& b
 SamplingPlan uot_probabilities(const DiscreteMeasure& a, const DiscreteMeasure& b, const KernelMatrix& K,
                                double lambda, double epsilon);
 SamplingPlan uniform_probabilities(const KernelMatrix& K);
+// Spar-IBP's column plan for kernel k: rows 1/n, columns sqrt(b_k) normalised,
+// masked to the support (sparsify.cpp:117-135).
+SamplingPlan barycenter_probabilities(const DiscreteMeasure& b_k, const KernelMatrix& K_k);
 SamplingPlan shrink_with_uniform(const SamplingPlan& plan, double theta);
 SparseKernel poisson_sparsify(const KernelMatrix& K, const SamplingPlan& plan, double s, std::uint64_t seed);
 std::vector<double> spmv(const SparseKernel& M, const std::vector<double>& v);

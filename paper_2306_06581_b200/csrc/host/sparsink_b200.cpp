@@ -446,6 +446,42 @@ SamplingPlan uniform_probabilities(const KernelMatrix& K) {
   return p;
 }
 
+SamplingPlan barycenter_probabilities(const DiscreteMeasure& b_k, const KernelMatrix& K_k) {
+  check_plan_sizes(b_k, b_k, K_k);
+  SamplingPlan p;
+  p.kind_ = PlanKind::Barycenter;
+  p.kernel_ = &K_k;
+  p.a_.assign(K_k.size(), 1.0);  // unused by the column-constant plan
+  p.b_ = b_k.weights;
+  p.epsilon_ = K_k.epsilon > 0 ? K_k.epsilon : 1.0;
+  p.factorized_storage();  // surfaces AllZeroKernel("zero-mass measure") eagerly
+  return p;
+}
+
+double eta_for_sparsity(const PointList& x, double target_nnz_ratio) {
+  if (!(target_nnz_ratio > 0.0 && target_nnz_ratio <= 1.0))
+    throw ThetaOutOfRange("target nnz ratio must lie in (0,1]");
+  const std::size_t n = x.size();
+  if (n < 2) throw DegenerateSupport("need at least two points");
+  // all n^2 distances (the pairwise cost on the device, Euclidean form)
+  CostMatrix d = euclidean_cost(x, x);
+  std::vector<double>& v = d.entries.data();
+  const double dmax = *std::max_element(v.begin(), v.end());
+  if (dmax == 0.0) {
+    if (target_nnz_ratio < 1.0) throw DegenerateSupport("all points identical");
+    return 1.0;
+  }
+  constexpr double kPi = 3.14159265358979323846;
+  if (target_nnz_ratio >= 1.0) return dmax / kPi * 1.0001 + 1e-12;
+  const std::size_t keep = std::max<std::size_t>(
+      1, static_cast<std::size_t>(std::llround(target_nnz_ratio * static_cast<double>(n) * static_cast<double>(n))));
+  // the kept quantile and the next one: two order statistics, no full sort
+  std::nth_element(v.begin(), v.begin() + (keep - 1), v.end());
+  const double q_in = v[keep - 1];
+  const double q_out = keep < v.size() ? *std::min_element(v.begin() + keep, v.end()) : q_in * 1.0001;
+  return (q_in == q_out ? q_in * (1.0 + 1e-9) : 0.5 * (q_in + q_out)) / kPi;
+}
+
 SamplingPlan shrink_with_uniform(const SamplingPlan& plan, double theta) {
   if (!(theta >= 0.0 && theta < 1.0)) throw ThetaOutOfRange("theta = " + std::to_string(theta));
   SamplingPlan out = plan;

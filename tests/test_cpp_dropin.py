@@ -31,3 +31,33 @@ def test_dropin_reference_scenarios(tmp_path):
     print(res.stdout)
     assert res.returncode == 0, res.stdout + res.stderr
     assert "0 failed" in res.stdout
+
+
+REF_TESTS = ROOT / "tests" / "cpp" / "_ref_tests"
+
+
+def test_reference_unit_tests_compile_unmodified():
+    """CPU: the reference's test_solvers.cpp / test_sparsify.cpp /
+    test_geometry.cpp compile UNMODIFIED against include/sparsink_b200.hpp
+    (own doctest-compatible runner + reference header names as shims)."""
+    import sys
+
+    sys.path.insert(0, str(ROOT / "tests" / "cpp"))
+    import build_reftests
+
+    if not build_reftests.REF_TESTS.exists():
+        pytest.skip("reference sources absent here (the GPU box): nothing to compile")
+    exes = build_reftests.build()
+    assert [e.name for e in exes] == build_reftests.NAMES
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["test_solvers", "test_sparsify", "test_geometry"])
+def test_reference_unit_tests_pass_on_the_b200(name):
+    exe = REF_TESTS / name
+    if not exe.exists():
+        pytest.skip("reference unit tests were not built (no /root/reference at build time)")
+    res = subprocess.run([str(exe)], capture_output=True, text=True, timeout=900)
+    print(res.stdout[-3000:])
+    assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-2000:]
+    assert "0 failed" in res.stdout
