@@ -182,7 +182,7 @@ __device__ __forceinline__ float ex2_ftz(float e) {
 template <int D>
 struct OtfFastOp {
   static constexpr int kThreads = loopcore::kBlock;
-  static constexpr int kMinBlocks = 1;  // 128 registers (at 64 the point records spilled)
+  static constexpr int kMinBlocks = 1;  // 128 registers (at 64 the point records spill)
   int64_t n;
   int dim;
   const float4* out_rec[2];  // [role] output-side records (2 float4 per atom)
@@ -409,7 +409,7 @@ void run_dense_loop(spk_ctx* ctx, DevKernel& dk, const spk_solver_cfg& cfg, doub
   // ranges so that (row blocks x ranges) matches the grid's warps
   int per_sm = 1;
   {
-    auto k5 = loopcore::loop_kernel<false, false, OtfFastOp<5>>;
+    auto k5 = loopcore::loop_kernel<false, false, OtfFastOp<5>>;  // (D <= 5 share the occupancy)
     SPK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k5, loopcore::kBlock, 0));
     per_sm = std::max(per_sm, 1);
   }

@@ -183,9 +183,9 @@ void build(spk_sharded* S, const spk_kernel_desc* kd, const double* a, const dou
     fail(SPK_E_DEGENERATE_SKETCH_ERROR, "sketch orphaned " + std::to_string(S->empty_rows) + " rows and " +
                                             std::to_string(S->empty_cols) +
                                             " columns; raise s or theta, or use a different seed");
-  for (int k = 0; k < 2; ++k) {
-    S->U[k].alloc(sizeof(double) * W * stride);
-    S->V[k].alloc(sizeof(double) * W * stride);
+  for (int k = 0; k < 2; ++k) {  // + 2 doubles: the last x tile's 16-byte-rounded TMA copy may read 8 bytes past
+    S->U[k].alloc(sizeof(double) * (W * stride + 2));
+    S->V[k].alloc(sizeof(double) * (W * stride + 2));
     SPK_CUDA(cudaMemsetAsync(S->U[k].p, 0, sizeof(double) * W * stride, st));
     SPK_CUDA(cudaMemsetAsync(S->V[k].p, 0, sizeof(double) * W * stride, st));
   }

@@ -352,8 +352,10 @@ class ShardedSketch:
                 f"DegenerateSketchError: sketch orphaned {self.empty_rows} rows and {self.empty_cols} columns; "
                 "raise s or theta, or use a different seed")
         S = self.stride * W
-        self.U = [shard.zeros(S), shard.zeros(S)]
-        self.V = [shard.zeros(S), shard.zeros(S)]
+        # + 2 doubles: the slab x block loop's last x tile is a 16-byte-rounded
+        # TMA copy, which may read 8 bytes past the gathered vector
+        self.U = [shard.zeros(S + 2)[:S], shard.zeros(S + 2)[:S]]
+        self.V = [shard.zeros(S + 2)[:S], shard.zeros(S + 2)[:S]]
 
     def solve(self, cfg: SolverConfig, uot: bool = False, check_every: int = 0, on_loop=None,
               want_scalings: bool = True) -> ShardedResult:
