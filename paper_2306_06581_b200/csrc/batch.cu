@@ -102,6 +102,33 @@ struct Stream {
       l = __ldg(lv + p);
     }
   }
+  // running position in the stream (pointers, so loads take immediate offsets)
+  struct Cursor {
+    const unsigned long long* pk;
+    const uint32_t* idx;
+    const double* lv;
+    __device__ __forceinline__ void load(int off, uint32_t& j, double& l) const {
+      if constexpr (PACKED) {
+        const unsigned long long w = __ldg(pk + off);
+        j = (uint32_t)(w & 0xffffull);
+        l = __longlong_as_double((long long)(w & ~0xffffull));
+      } else {
+        j = __ldg(idx + off);
+        l = __ldg(lv + off);
+      }
+    }
+    __device__ __forceinline__ void advance(int d) {
+      if constexpr (PACKED) pk += d;
+      else {
+        idx += d;
+        lv += d;
+      }
+    }
+  };
+  __device__ __forceinline__ Cursor cursor(long long p) const {
+    if constexpr (PACKED) return Cursor{pk + p, nullptr, nullptr};
+    else return Cursor{nullptr, idx + p, lv + p};
+  }
   __device__ __forceinline__ void prefetch_l2(long long b, long long e, int gl) const {
     const long long nb = (e - b) * (PACKED ? 8 : 12);
     const long long lines = (nb + 127) >> 7;
@@ -203,26 +230,37 @@ __device__ __forceinline__ double batch_half(int64_t i_lo, int64_t i_hi, const l
     using Acc = typename std::conditional<FAST, float, double>::type;
     double m = -CUDART_INF;
     Acc s = 0;
-    for (long long p = b + gl; p < e; p += U * kG) {
+    // this lane's entries: b + gl, b + gl + kG, ... (nk of them); full blocks
+    // of U loads at immediate offsets from a running cursor, then one partial
+    // block (32-bit counts: no 64-bit index arithmetic per load)
+    const int cnt = (int)(e - b);
+    int left = cnt > gl ? (cnt - gl + kG - 1) / kG : 0;
+    typename Stream<PACKED>::Cursor cur = st.cursor(b + gl);
+    auto block = [&](int nload) {
       double t[U];
 #pragma unroll
       for (int k = 0; k < U; ++k) {
         uint32_t j = 0;
         double l = -CUDART_INF;
-        if (p + k * kG < e) st.load(p + k * kG, j, l);
-        t[k] = l + x[j];
+        if (k < nload) cur.load(k * kG, j, l);
+        t[k] = l + x[j];  // l = -inf (K~ = 0, or padding) or x = -inf (masked column): exp -> 0
       }
       double M = t[0];
 #pragma unroll
       for (int k = 1; k < U; ++k) M = fmax(M, t[k]);
-      if (M == -CUDART_INF) continue;  // every term of the block is -inf
+      if (M == -CUDART_INF) return;  // every term of the block is -inf
       if (M > m) {
         s = (m == -CUDART_INF) ? Acc(0) : s * lse_term<FAST>(m - M);
         m = M;
       }
 #pragma unroll
       for (int k = 0; k < U; ++k) s += lse_term<FAST>(t[k] - m);
+    };
+    for (; left >= U; left -= U) {
+      block(U);
+      cur.advance(U * kG);
     }
+    if (left > 0) block(left);
 #pragma unroll
     for (int o = kG / 2; o; o >>= 1) {
       const double m2 = __shfl_xor_sync(0xffffffffu, m, o);
