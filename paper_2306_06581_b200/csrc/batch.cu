@@ -16,9 +16,10 @@
 // one CTA per pair (4 waves run), 6.7 waves as CTA pairs (7 run).
 //
 // Entry stream: fp32 sketches (config 3) stream ONE u64 per entry -- log K~
-// as an fp64 rounded to a 37-bit mantissa (relative error 2^-37, far below
-// the fp32 rounding of K~ itself) with the 16-bit column (row) index in the
-// low mantissa bits (n <= 65,536: the batch limit is ~14k). 8 bytes per entry,
+// as an fp64 rounded to a 35-bit mantissa (relative error 2^-35, far below
+// the fp32 rounding of K~ itself) with the byte offset of the gathered x
+// (column / row index << 3) in the low 17 bits (n <= 16,384: the batch limit
+// is ~14k). 8 bytes per entry,
 // SURVEY 8(d)'s V + I. fp64 sketches stream u32 indices + fp64 log K~ (12 B).
 //
 // Semantics: detail::log_scaling_loop (include/sparsink/solvers.hpp:397-513):
@@ -86,34 +87,32 @@ struct BatchArgs {
 };
 
 
+// Packed entry: log K~ as fp64 with its low 17 bits replaced by the byte
+// offset of the gathered x (index << 3, index < 2^14): a 35-bit mantissa
+// (relative 3e-11, far below the fp32 rounding of K~ itself).
+constexpr unsigned long long kPackLowMask = 0x1ffffull;
+constexpr uint32_t kPackOffMask = 0x1fff8u;
+constexpr int64_t kPackMaxN = 1 << 14;
+
 // Entry stream of one half: packed u64 (PACKED) or u32 index + fp64 log K~.
 template <bool PACKED>
 struct Stream {
   const unsigned long long* pk;
   const uint32_t* idx;
   const double* lv;
-  __device__ __forceinline__ void load(long long p, uint32_t& j, double& l) const {
-    if constexpr (PACKED) {
-      const unsigned long long w = __ldg(pk + p);
-      j = (uint32_t)(w & 0xffffull);
-      l = __longlong_as_double((long long)(w & ~0xffffull));
-    } else {
-      j = __ldg(idx + p);
-      l = __ldg(lv + p);
-    }
-  }
   // running position in the stream (pointers, so loads take immediate offsets)
   struct Cursor {
     const unsigned long long* pk;
     const uint32_t* idx;
     const double* lv;
-    __device__ __forceinline__ void load(int off, uint32_t& j, double& l) const {
+    // jo: byte offset of the gathered x (index * 8), l: log K~
+    __device__ __forceinline__ void load(int off, uint32_t& jo, double& l) const {
       if constexpr (PACKED) {
         const unsigned long long w = __ldg(pk + off);
-        j = (uint32_t)(w & 0xffffull);
-        l = __longlong_as_double((long long)(w & ~0xffffull));
+        jo = (uint32_t)w & kPackOffMask;
+        l = __longlong_as_double((long long)(w & ~kPackLowMask));
       } else {
-        j = __ldg(idx + off);
+        jo = __ldg(idx + off) << 3;
         l = __ldg(lv + off);
       }
     }
@@ -240,14 +239,26 @@ __device__ __forceinline__ double batch_half(int64_t i_lo, int64_t i_hi, const l
       double t[U];
 #pragma unroll
       for (int k = 0; k < U; ++k) {
-        uint32_t j = 0;
+        uint32_t jo = 0;
         double l = -CUDART_INF;
-        if (k < nload) cur.load(k * kG, j, l);
-        t[k] = l + x[j];  // l = -inf (K~ = 0, or padding) or x = -inf (masked column): exp -> 0
+        if (k < nload) cur.load(k * kG, jo, l);
+        // l = -inf (K~ = 0, or padding) or x = -inf (masked column): exp -> 0
+        t[k] = l + *reinterpret_cast<const double*>(reinterpret_cast<const char*>(x) + jo);
       }
-      double M = t[0];
+      // block maximum: any M near the true one gives the same log-sum-exp
+      // (t - M stays far inside the exp range), so FAST takes it in fp32
+      // (FMNMX) instead of fp64 fmax (NaN-aware DSETP sequences)
+      double M;
+      if constexpr (FAST) {
+        float mf = __double2float_rn(t[0]);
 #pragma unroll
-      for (int k = 1; k < U; ++k) M = fmax(M, t[k]);
+        for (int k = 1; k < U; ++k) mf = fmaxf(mf, __double2float_rn(t[k]));
+        M = (double)mf;
+      } else {
+        M = t[0];
+#pragma unroll
+        for (int k = 1; k < U; ++k) M = fmax(M, t[k]);
+      }
       if (M == -CUDART_INF) return;  // every term of the block is -inf
       if (M > m) {
         s = (m == -CUDART_INF) ? Acc(0) : s * lse_term<FAST>(m - M);
@@ -276,7 +287,11 @@ __device__ __forceinline__ double batch_half(int64_t i_lo, int64_t i_hi, const l
       if (inext < i_hi && en > bn) st.prefetch_l2(bn, en, gl);
     }
     if (live && gl == 0) {
-      const double lse = m == -CUDART_INF ? -CUDART_INF : m + log((double)s);
+      // FAST: the sum is fp32-accurate, so is its log (MUFU.LG2, ~2^-22 absolute
+      // for s in [1, 256]) -- 2 instructions instead of the ~40 of an fp64 log
+      const double lse = m == -CUDART_INF ? -CUDART_INF
+                                          : m + (FAST ? (double)(__log2f((float)s) * 0.693147180559945f)
+                                                      : log((double)s));
       double nv;
       bool write = true;
       if (lse == -CUDART_INF) {
@@ -450,14 +465,14 @@ __global__ void __launch_bounds__(kBatchThreads, 1) batch_log_kernel(BatchArgs A
 }
 
 // Packed entry stream of an fp32 sketch: log K~ (fp64 log of the stored fp32
-// value, rounded to a 37-bit mantissa; -inf stays -inf) | 16-bit index.
+// value, rounded to a 35-bit mantissa; -inf stays -inf) | index << 3.
 __global__ void pack_log_kernel(const float* __restrict__ v, const uint32_t* __restrict__ idx, int64_t m,
                                 unsigned long long* __restrict__ out) {
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < m; k += (int64_t)gridDim.x * blockDim.x) {
     const double l = log((double)v[k]);
     unsigned long long b = (unsigned long long)__double_as_longlong(l);
-    if (isfinite(l)) b += 0x8000ull;  // round to nearest on the kept bits
-    out[k] = (b & ~0xffffull) | (unsigned long long)(idx[k] & 0xffffu);
+    if (isfinite(l)) b += (kPackLowMask + 1) >> 1;  // round to nearest on the kept bits
+    out[k] = (b & ~kPackLowMask) | ((unsigned long long)idx[k] << 3);
   }
 }
 
@@ -544,8 +559,8 @@ void run_batch_log(spk_ctx* ctx, spk_sketch* const* sks, int count, const spk_so
   for (int k = 0; k < count; ++k) {
     spk_sketch* sk = sks[k];
     const int64_t n = sk->n;
-    if (n > 65536) fail(SPK_E_LENGTH_MISMATCH, "batched loop: dimension above 65536");
     const bool packed = sk->value_type == SPK_VALUES_F32;
+    if (packed && n > kPackMaxN) fail(SPK_E_LENGTH_MISMATCH, "batched loop: dimension above 16384");
     ensure_coverage(ctx, sk);
     if (packed) ensure_log_packed(ctx, sk);
     else ensure_log_values(ctx, sk);

@@ -258,39 +258,16 @@ struct OtfFastOp {
         const float4* qp = irec + 2 * c0;
         const double* xp = x + c0;
         int jj = 0;
-        if (len >= 2) {
-          // two columns per step (independent exp chains); the next pair's
-          // records and scalings are loaded while this pair computes
+        for (; jj + 1 < len; jj += 2) {  // two columns per step: independent exp chains
           float q0[8], q1[8];
-          load_rec(qp, q0);
-          load_rec(qp + 2, q1);
-          double xd0 = __ldcg(xp), xd1 = __ldcg(xp + 1);
-          for (; jj + 1 < len; jj += 2) {
-            float n0[8], n1[8];
-            double nd0 = 0.0, nd1 = 0.0;
-            const bool more = jj + 3 < len;
-            if (more) {
-              load_rec(qp + 2 * jj + 4, n0);
-              load_rec(qp + 2 * jj + 6, n1);
-              nd0 = __ldcg(xp + jj + 2);
-              nd1 = __ldcg(xp + jj + 3);
-            }
-            const float x0 = (float)xd0, x1 = (float)xd1;
+          load_rec(qp + 2 * jj, q0);
+          load_rec(qp + 2 * jj + 2, q1);
+          const float x0 = (float)__ldcg(xp + jj), x1 = (float)__ldcg(xp + jj + 1);
 #pragma unroll
-            for (int r = 0; r < kOtfRows; ++r) {
-              const float e0 = expo(p[r], q0), e1 = expo(p[r], q1);
-              part[r] = fmaf(ex2_ftz(e0), x0, part[r]);
-              part[r] = fmaf(ex2_ftz(e1), x1, part[r]);
-            }
-            if (more) {
-#pragma unroll
-              for (int k = 0; k < 8; ++k) {
-                q0[k] = n0[k];
-                q1[k] = n1[k];
-              }
-              xd0 = nd0;
-              xd1 = nd1;
-            }
+          for (int r = 0; r < kOtfRows; ++r) {
+            const float e0 = expo(p[r], q0), e1 = expo(p[r], q1);
+            part[r] = fmaf(ex2_ftz(e0), x0, part[r]);
+            part[r] = fmaf(ex2_ftz(e1), x1, part[r]);
           }
         }
         if (jj < len) {

@@ -22,6 +22,8 @@
 // iterate of its own atoms and puts it back.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <type_traits>
 #include <vector>
 
@@ -59,6 +61,7 @@ struct ClusterArgs {
   long long masked0[2];
   int npad;   // doubles per shared vector
   int stage;  // 1: the CTA's sketch share lives in shared memory
+  unsigned long long* trace;  // SPK_TRACE_SMALL: globaltimer stamps [iter<8][half][rank][5]
   int64_t stage_ent[2];  // max entries of one CTA's share per half (staged layout)
   int64_t stage_rows[2];
 };
@@ -71,6 +74,41 @@ __device__ __forceinline__ unsigned cluster_rank() {
 __device__ __forceinline__ void cluster_barrier() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+// shared::cluster address of the same shared location in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t map_cluster(uint32_t a, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+// 8-byte remote shared store that completes 8 bytes of the receiver's mbarrier transaction count
+__device__ __forceinline__ void st_async_b64(uint32_t remote, unsigned long long v, uint32_t remote_bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(remote), "l"(v),
+               "r"(remote_bar)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_init_s(uint64_t* b) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+// bounded wait (a lost transaction must not hang the GPU: the host raises a device error)
+__device__ __forceinline__ bool mbar_wait_s(uint64_t* b, uint32_t parity) {
+  for (long long spin = 0; spin < (1ll << 26); ++spin) {
+    uint32_t done;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+    if (done) return true;
+  }
+  return false;
+}
+
 template <class T>
 __device__ __forceinline__ T* peer(T* p, unsigned rank) {
   T* q;
@@ -168,32 +206,31 @@ __global__ void __launch_bounds__(kThreads, 1) cluster_loop_kernel(ClusterArgs<V
       dyn_s[h][i] = 0;
       w_own[h][i - A.lo[h][rank]] = A.w[h][i];
     }
-  // staged sketch share: per half rows+1 offsets (int64), entries' values then indices
-  const long long* ptr[2] = {A.ptr[0], A.ptr[1]};
-  const uint32_t* idx[2] = {A.idx[0], A.idx[1]};
-  const VT* val[2] = {A.val[0], A.val[1]};
-  long long base[2] = {0, 0};  // entry offset subtracted from ptr (staged: share-relative)
-  int64_t rbase[2] = {0, 0};   // atom offset subtracted from the row index into ptr
-  if (A.stage) {
-    for (int h = 0; h < 2; ++h) {
-      const int64_t r0 = A.lo[h][rank], r1 = A.lo[h][rank + 1];
-      const long long e0 = A.ptr[h][r0], e1 = A.ptr[h][r1];
-      long long* sp = reinterpret_cast<long long*>(tail);
-      tail += sizeof(long long) * ((A.stage_rows[h] + 2) & ~int64_t(1));
-      VT* sv = reinterpret_cast<VT*>(tail);
-      tail += sizeof(VT) * ((A.stage_ent[h] + 3) & ~int64_t(3));
-      uint32_t* si = reinterpret_cast<uint32_t*>(tail);
-      tail += sizeof(uint32_t) * ((A.stage_ent[h] + 3) & ~int64_t(3));
-      for (int64_t k = threadIdx.x; k <= r1 - r0; k += blockDim.x) sp[k] = A.ptr[h][r0 + k] - e0;
-      for (long long k = threadIdx.x; k < e1 - e0; k += blockDim.x) {
-        sv[k] = A.val[h][e0 + k];
-        si[k] = A.idx[h][e0 + k];
-      }
-      ptr[h] = sp;
-      idx[h] = si;
-      val[h] = sv;
-      rbase[h] = r0;
+  // the CTA's share of the sketch, staged in shared memory once (per half:
+  // rows+1 offsets relative to the share, values, indices); pointers derived
+  // from the shared array, so every access is an LDS
+  const long long* ptr[2];
+  const uint32_t* idx[2];
+  const VT* val[2];
+  int64_t rbase[2];  // atom offset subtracted from the row index into ptr
+  for (int h = 0; h < 2; ++h) {
+    const int64_t r0 = A.lo[h][rank], r1 = A.lo[h][rank + 1];
+    const long long e0 = A.ptr[h][r0], e1 = A.ptr[h][r1];
+    long long* sp = reinterpret_cast<long long*>(tail);
+    tail += sizeof(long long) * ((A.stage_rows[h] + 2) & ~int64_t(1));
+    VT* sv = reinterpret_cast<VT*>(tail);
+    tail += sizeof(VT) * ((A.stage_ent[h] + 3) & ~int64_t(3));
+    uint32_t* si = reinterpret_cast<uint32_t*>(tail);
+    tail += sizeof(uint32_t) * ((A.stage_ent[h] + 3) & ~int64_t(3));
+    for (int64_t k = threadIdx.x; k <= r1 - r0; k += blockDim.x) sp[k] = A.ptr[h][r0 + k] - e0;
+    for (long long k = threadIdx.x; k < e1 - e0; k += blockDim.x) {
+      sv[k] = A.val[h][e0 + k];
+      si[k] = A.idx[h][e0 + k];
     }
+    ptr[h] = sp;
+    idx[h] = si;
+    val[h] = sv;
+    rbase[h] = r0;
   }
   __shared__ double scratch[32];
   __shared__ long long mscratch[32];
@@ -202,16 +239,25 @@ __global__ void __launch_bounds__(kThreads, 1) cluster_loop_kernel(ClusterArgs<V
   __shared__ double xe[2][CS];  // per half: every CTA's partials, slot = its rank
   __shared__ long long xm[2][CS];
   __shared__ unsigned long long xf[2][CS];
-  __shared__ double comb_e;
-  __shared__ long long comb_m;
-  __shared__ unsigned long long comb_f;
+  __shared__ __align__(8) uint64_t mbar[2];  // per half: the peers' st.async bytes
   const double on = LOG ? 0.0 : 1.0, off = LOG ? -CUDART_INF : 0.0;
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {  // u = v = 1 on covered atoms (:277-281, :424-428)
     X[0][i] = A.ne[0][i] ? on : off;
     X[1][i] = A.ne[1][i] ? on : off;
   }
-  if (threadIdx.x == 0) flag_sh[0] = flag_sh[1] = kNone;
-  if (CS > 1) cluster_barrier();
+  if (threadIdx.x == 0) {
+    flag_sh[0] = flag_sh[1] = kNone;
+    mbar_init_s(&mbar[0]);
+    mbar_init_s(&mbar[1]);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  // bytes each half receives from the peers: their atoms' new values + their
+  // partials (residual, masks, first failing atom)
+  uint32_t rx_bytes[2] = {0u, 0u};
+  for (int h = 0; h < 2; ++h)
+    for (int r = 0; r < CS; ++r)
+      if (r != (int)rank) rx_bytes[h] += (uint32_t)(8 * (A.lo[h][r + 1] - A.lo[h][r]) + 24);
+  if (CS > 1) cluster_barrier();  // peers' vectors and barriers initialised before any remote store
   else __syncthreads();
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5, gl = lane & (kSG - 1);
@@ -219,12 +265,31 @@ __global__ void __launch_bounds__(kThreads, 1) cluster_loop_kernel(ClusterArgs<V
   long long t = 0;
   int converged = 0, diverged = 0, ekind = 0, ehalf = 0, dhalf = 0;
   long long eidx = 0, didx = 0, mr_before = mr, mc_before = mc, mu_last = 0;
+  uint32_t parity = 0u;  // bit h: phase parity of mbar[h] to wait for next
+  bool faulted = false;  // a peer transfer never completed (reported, never hangs)
 
-  // one half: h = 0 rows against v (u-half), h = 1 columns against the new u
+  // one half: h = 0 rows against v (u-half), h = 1 columns against the new u.
+  // Every new value goes to the peers as st.async (remote shared store that
+  // completes a transaction count on the RECEIVER's mbarrier), and so do the
+  // CTA's partials: a CTA proceeds once its mbarrier has seen every byte of
+  // the half from every peer -- no cluster barrier, no release fence. Reuse is
+  // safe: a peer can only start writing this half's vector again after it has
+  // received all of this CTA's values of the following half, i.e. after this
+  // CTA stopped reading it.
+  auto stamp = [&](int h, int k) {
+    if (A.trace && t <= 8 && threadIdx.x == 0) {
+      unsigned long long g;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+      A.trace[(((t - 1) * 2 + h) * CS + rank) * 5 + k] = g;
+    }
+  };
   auto half = [&](int h, double& err_all, long long& masks_all, unsigned long long& flag_all) {
+    stamp(h, 0);
+    if (CS > 1 && threadIdx.x == 0) mbar_expect_tx(&mbar[h], rx_bytes[h]);
     const int64_t r0 = A.lo[h][rank], r1 = A.lo[h][rank + 1];
     const double* x = X[h ^ 1];
     double* out = X[h];
+    const uint32_t bar_h = smem_u32(&mbar[h]);
     double err = 0.0;
     long long masks = 0;
     // kSG lanes per row, kSR rows per warp at once: every row of a config-1
@@ -238,21 +303,23 @@ __global__ void __launch_bounds__(kThreads, 1) cluster_loop_kernel(ClusterArgs<V
       long long b = 0, e = 0;
       if (live) {
         const int64_t li = i - rbase[h];
-        b = ptr[h][li] - base[h];
-        e = ptr[h][li + 1] - base[h];
+        b = ptr[h][li];
+        e = ptr[h][li + 1];
       }
       const double tmp = group_dot<LOG, VT>(val[h], idx[h], b, e, x, gl);
       if (live && gl == 0)
         err += finalize_atom<LOG>(i, tmp, old, w_s[h][i], A.exponent, A.policy, (int)t, ne_s[h], dyn_s[h], out,
                                   &flag_sh[h], masks);
       __syncwarp();
-      if (CS > 1 && live)  // DSMEM broadcast of the new value, the group's lanes sharing the peers
-        for (int r = gl + 1; r < CS; r += kSG) *peer(out + i, (rank + r) % CS) = out[i];
+      if (CS > 1 && in) {  // every atom's value (masked ones too: the peers count bytes), lanes sharing the peers
+        const double nv = out[i];
+        const uint32_t a = smem_u32(out + i);
+        for (int r = gl + 1; r < CS; r += kSG) {
+          const uint32_t pr = (rank + (uint32_t)r) % CS;
+          st_async_b64(map_cluster(a, pr), (unsigned long long)__double_as_longlong(nv), map_cluster(bar_h, pr));
+        }
+      }
     }
-    // CTA partials: warp sums, then warp 0 sums the warps (fixed shuffle
-    // tree) and PUSHES the CTA's (residual, masks, first failing atom) into
-    // slot [rank] of every CTA's exchange arrays (DSMEM stores) before the
-    // cluster barrier; after it, every CTA sums its local slots in rank order.
     err = warp_sum(err);
     masks = warp_sum_ll(masks);
     if (lane == 0) {
@@ -260,49 +327,42 @@ __global__ void __launch_bounds__(kThreads, 1) cluster_loop_kernel(ClusterArgs<V
       mscratch[warp] = masks;
     }
     __syncthreads();
-    if (warp == 0) {
+    stamp(h, 1);
+    if (warp == 0) {  // CTA partials (fixed shuffle tree) into slot [rank] of every CTA
       double e = lane < nw ? scratch[lane] : 0.0;
       long long m = lane < nw ? mscratch[lane] : 0;
       e = warp_sum(e);
       m = warp_sum_ll(m);
       const unsigned long long f = flag_sh[h];
       __syncwarp();
-      if (lane < CS) {
-        double* pe = (CS == 1 || lane == (int)rank) ? &xe[h][rank] : peer(&xe[h][rank], (unsigned)lane);
-        long long* pm = (CS == 1 || lane == (int)rank) ? &xm[h][rank] : peer(&xm[h][rank], (unsigned)lane);
-        unsigned long long* pf = (CS == 1 || lane == (int)rank) ? &xf[h][rank] : peer(&xf[h][rank], (unsigned)lane);
-        *pe = e;
-        *pm = m;
-        *pf = f;
+      if (lane == (int)rank) {
+        xe[h][rank] = e;
+        xm[h][rank] = m;
+        xf[h][rank] = f;
+      } else if (CS > 1 && lane < CS) {
+        const uint32_t pr = (uint32_t)lane, rb = map_cluster(bar_h, pr);
+        st_async_b64(map_cluster(smem_u32(&xe[h][rank]), pr), (unsigned long long)__double_as_longlong(e), rb);
+        st_async_b64(map_cluster(smem_u32(&xm[h][rank]), pr), (unsigned long long)m, rb);
+        st_async_b64(map_cluster(smem_u32(&xf[h][rank]), pr), f, rb);
       }
       if (lane == 0) flag_sh[h] = kNone;  // recycled for this half's next iteration
-      __syncwarp();
-      // one release for the whole CTA: every thread's DSMEM stores were
-      // ordered before warp 0 by the __syncthreads above (cumulativity)
-      if (CS > 1 && lane == 0) asm volatile("fence.acq_rel.cluster;" ::: "memory");
     }
-    if (CS > 1)  // new values and partials visible cluster-wide
-      asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-    else __syncthreads();
-    if (warp == 0) {  // rank order: the same sums on every CTA
-      double e = 0.0;
-      long long mk = 0;
-      unsigned long long f = kNone;
-      for (int r = 0; r < CS; ++r) {
-        e += xe[h][r];
-        mk += xm[h][r];
-        f = min(f, xf[h][r]);
-      }
-      if (lane == 0) {
-        comb_e = e;
-        comb_m = mk;
-        comb_f = f;
-      }
+    stamp(h, 2);
+    if (CS > 1) {  // every peer's values and partials of this half have landed
+      if (!mbar_wait_s(&mbar[h], (parity >> h) & 1u)) faulted = true;
+      parity ^= 1u << h;
     }
-    __syncthreads();
-    err_all = comb_e;
-    masks_all = comb_m;
-    flag_all = comb_f;
+    __syncthreads();  // this CTA's own slot and values (generic stores) too
+    stamp(h, 3);
+    err_all = 0.0;
+    masks_all = 0;
+    flag_all = kNone;
+    for (int r = 0; r < CS; ++r) {  // rank order: the same sums on every CTA
+      err_all += xe[h][r];
+      masks_all += xm[h][r];
+      flag_all = min(flag_all, xf[h][r]);
+    }
+    stamp(h, 4);
   };
   auto restore = [&](int h) {  // previous iterate of this CTA's atoms (every CTA restores its own)
     const int64_t r0 = A.lo[h][rank], r1 = A.lo[h][rank + 1];
@@ -317,6 +377,7 @@ __global__ void __launch_bounds__(kThreads, 1) cluster_loop_kernel(ClusterArgs<V
     long long mu, mv;
     unsigned long long fu, fv;
     half(0, eu, mu, fu);
+    if (__syncthreads_or(faulted)) break;
     if (fu != kNone) {
       if (A.policy == SPK_POLICY_MASK && !LOG) {
         diverged = 1;
@@ -332,6 +393,7 @@ __global__ void __launch_bounds__(kThreads, 1) cluster_loop_kernel(ClusterArgs<V
       break;
     }
     half(1, ev, mv, fv);
+    if (__syncthreads_or(faulted)) break;
     if (fv != kNone) {
       if (A.policy == SPK_POLICY_MASK && !LOG) {
         diverged = 1;
@@ -370,7 +432,7 @@ __global__ void __launch_bounds__(kThreads, 1) cluster_loop_kernel(ClusterArgs<V
     s->iterations = t;
     s->converged = converged;
     s->diverged = diverged;
-    s->error_kind = ekind;
+    s->error_kind = faulted ? SPK_E_DEVICE : ekind;
     s->error_half = ehalf;
     s->error_index = eidx;
     s->cur = 0;
@@ -523,6 +585,13 @@ bool run_cluster_t(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, doub
   A.masked0[0] = sk->cov_empty_rows;
   A.masked0[1] = sk->cov_empty_cols;
   A.npad = npad;
+  DBuf trace;
+  const bool tracing = std::getenv("SPK_TRACE_SMALL") != nullptr;
+  if (tracing) {
+    trace.alloc(sizeof(unsigned long long) * 8 * 2 * kMaxCS * 5);
+    SPK_CUDA(cudaMemsetAsync(trace.p, 0, trace.bytes, s));
+    A.trace = trace.as<unsigned long long>();
+  }
   Timer tm(s);
   bool ok = false;
   switch (CS) {
@@ -538,6 +607,25 @@ bool run_cluster_t(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, doub
   SPK_CUDA(cudaGetLastError());
   loopcore::Status S;
   download(ctx, &S, W.status, sizeof S);
+  if (S.error_kind == SPK_E_DEVICE) fail_device("small loop: a peer's st.async transfer timed out", cudaErrorLaunchTimeout);
+  if (tracing) {  // per-phase means over iterations 2..8 (ns): rows, partials, barrier, combine; half length
+    std::vector<unsigned long long> tr(8 * 2 * kMaxCS * 5);
+    download(ctx, tr.data(), trace, sizeof(unsigned long long) * tr.size());
+    double ph[5] = {0, 0, 0, 0, 0};
+    int cnt = 0;
+    for (int it = 1; it < 8 && it < S.iterations; ++it)
+      for (int h = 0; h < 2; ++h)
+        for (int r = 0; r < CS; ++r) {
+          const unsigned long long* q = &tr[(((size_t)it * 2 + h) * CS + r) * 5];
+          for (int k = 0; k < 4; ++k) ph[k] += (double)(q[k + 1] - q[k]);
+          const unsigned long long* nx = &tr[(((size_t)it * 2 + h) * CS + 0) * 5];
+          ph[4] += (double)(q[4] - nx[0]);
+          ++cnt;
+        }
+    if (cnt)
+      std::fprintf(stderr, "SPK_TRACE_SMALL CS=%d: rows %.0f ns, partials %.0f ns, peer wait %.0f ns, combine %.0f ns\n",
+                   CS, ph[0] / cnt, ph[1] / cnt, ph[2] / cnt, ph[3] / cnt);
+  }
   loopcore::loop_epilogue<LOG>(ctx, S, n, W, A.out[0], A.out[1], st, out);
   return true;
 }
