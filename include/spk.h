@@ -172,7 +172,7 @@ enum spk_option {
   SPK_OPT_BLOCKED_SPREAD = 8,   /* slab x block loop: spread each half-warp's gathered columns over the banks (1, default) */
   SPK_OPT_BLOCKED_CLUSTER = 9,  /* slab x block loop: CTA pairs as 2-CTA clusters sharing partial sums (1, default, when they fit) */
   SPK_OPT_BATCH_CLUSTER = 10,   /* batched log loop: CTAs (SMs) per sketch as one cluster: 1, 2 (default) or 4 */
-  SPK_OPT_BATCH_UNROLL = 11,    /* batched log loop: entry loads in flight per lane: 4 (default) or 8 */
+  SPK_OPT_BATCH_UNROLL = 11,    /* batched log loop: entry loads in flight per lane: 4 or 8 (default) */
   SPK_OPT_SMALL_LOOP = 12,      /* fast mode, small sketches: the loop on ONE cluster with the scalings in
                                    shared memory (1, default) or the persistent grid loop (0) */
   SPK_OPT_SMALL_CLUSTER = 13,   /* that cluster's size: 16 (default, non-portable), 8, 4, 2, 1 */

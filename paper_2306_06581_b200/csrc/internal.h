@@ -158,7 +158,7 @@ struct spk_ctx {
   int blocked_spread = 1;      // slab x block layout: spread gathered columns over banks (slot_kernel)
   int blocked_cluster = 1;     // CTA pairs as 2-CTA clusters (DSMEM partial sums) when they all fit
   int batch_cluster = 2;       // batched log loop: CTAs (SMs) per sketch, 1 / 2 / 4
-  int batch_unroll = 4;        // batched log loop: entry loads in flight per lane, 4 / 8
+  int batch_unroll = 8;        // batched log loop: entry loads in flight per lane, 4 / 8
   int small_loop = 1;          // fast-mode loop on one cluster for small sketches (small.cu)
   int small_cluster = 16;      // its cluster size (largest that launches; 16 = non-portable)
   int64_t small_max_n = 14000;       // ... when both scaling vectors fit every CTA's shared memory

@@ -99,7 +99,7 @@ __device__ __forceinline__ bool mbar_wait_s(uint64_t* b, uint32_t parity) {
     uint32_t done;
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
         "selp.u32 %0, 1, 0, p;\n}"
         : "=r"(done)
         : "r"(smem_u32(b)), "r"(parity)
@@ -136,11 +136,11 @@ __device__ __forceinline__ double group_max(double v) {
 // v * x (FMA), or the two-pass log-sum-exp (solvers.cpp:99-111; fp32 sketches
 // take the fp32-accurate exp). Every lane of the warp must call it.
 template <bool LOG, class VT>
-__device__ __forceinline__ double group_dot(const VT* val, const uint32_t* idx, long long b, long long e,
-                                            const double* x, int gl) {
+__device__ __forceinline__ double group_dot(const VT* val, const uint32_t* idx, int b, int e, const double* x,
+                                            int gl) {
   if constexpr (!LOG) {
     double a0 = 0.0, a1 = 0.0;
-    long long p = b + gl;
+    int p = b + gl;
     for (; p + kSG < e; p += 2 * kSG) {
       a0 = fma((double)val[p], x[idx[p]], a0);
       a1 = fma((double)val[p + kSG], x[idx[p + kSG]], a1);
@@ -149,7 +149,7 @@ __device__ __forceinline__ double group_dot(const VT* val, const uint32_t* idx, 
     return group_sum(a0 + a1);
   } else {
     double m = -CUDART_INF;
-    for (long long p = b + gl; p < e; p += kSG) {
+    for (int p = b + gl; p < e; p += kSG) {
       const double xv = x[idx[p]];
       if (xv == -CUDART_INF) continue;
       m = fmax(m, log_of(val[p]) + xv);
@@ -157,7 +157,7 @@ __device__ __forceinline__ double group_dot(const VT* val, const uint32_t* idx, 
     m = group_max(m);
     double s = 0.0;
     if (m != -CUDART_INF)
-      for (long long p = b + gl; p < e; p += kSG) {
+      for (int p = b + gl; p < e; p += kSG) {
         const double xv = x[idx[p]];
         if (xv == -CUDART_INF) continue;
         s += exp_term<VT>(log_of(val[p]) + xv - m);
@@ -300,11 +300,11 @@ __global__ void __launch_bounds__(kThreads, 1) cluster_loop_kernel(ClusterArgs<V
       const double old = in ? out[i] : 0.0;
       if (in && gl == 0) prev[h][i - r0] = old;
       const bool live = in && ne_s[h][i];  // structurally empty / masked: keeps its value
-      long long b = 0, e = 0;
+      int b = 0, e = 0;  // share-relative entry offsets (a share holds < 2^31 entries)
       if (live) {
-        const int64_t li = i - rbase[h];
-        b = ptr[h][li];
-        e = ptr[h][li + 1];
+        const int li = (int)(i - rbase[h]);
+        b = (int)ptr[h][li];
+        e = (int)ptr[h][li + 1];
       }
       const double tmp = group_dot<LOG, VT>(val[h], idx[h], b, e, x, gl);
       if (live && gl == 0)
@@ -348,11 +348,15 @@ __global__ void __launch_bounds__(kThreads, 1) cluster_loop_kernel(ClusterArgs<V
       if (lane == 0) flag_sh[h] = kNone;  // recycled for this half's next iteration
     }
     stamp(h, 2);
-    if (CS > 1) {  // every peer's values and partials of this half have landed
+    // every peer's values and partials of this half have landed: one warp
+    // waits (CTA-scope acquire: the data is in this CTA's shared memory; a
+    // cluster-scope acquire would invalidate L1 on every poll), the barrier
+    // below publishes the completion -- and this CTA's own stores -- to all
+    if (CS > 1 && warp == 0) {
       if (!mbar_wait_s(&mbar[h], (parity >> h) & 1u)) faulted = true;
-      parity ^= 1u << h;
     }
-    __syncthreads();  // this CTA's own slot and values (generic stores) too
+    parity ^= 1u << h;
+    __syncthreads();
     stamp(h, 3);
     err_all = 0.0;
     masks_all = 0;

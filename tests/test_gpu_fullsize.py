@@ -224,7 +224,7 @@ def test_config3_batch_vs_reference(reference):
               f"batch vs single |dlog u| {du1:.2e}, objective rel {abs(objs[q] - obj1) / abs(obj1):.2e}")
         assert objs[q] == pytest.approx(oobj, rel=1e-6)  # measured ~6e-9
         assert objs[q] == pytest.approx(obj1, rel=1e-5)
-        assert du <= 2e-5 and dv <= 2e-5  # measured ~2.3e-6 (fp32 K~ values, fp32-accurate exp)
+        assert du <= 5e-5 and dv <= 5e-5  # fp32 bar 1e-4 on u, v; measured 1.5e-5 (fp32 K~, MUFU exp2 / lg2)
 
 
 def oracle_readout(csr, lu, lv, a, b, coords):
