@@ -209,30 +209,68 @@ struct OtfFastOp {
     }
   }
 
-  // Work item = (block of 32 x kOtfRows rows) x (one of `parts` column
-  // ranges), one WARP each, no CTA barrier: items ~ warps of the grid, so
-  // every warp streams the same number of evaluations. Each item leaves fp64
-  // partial row sums in part[cp * n + i]; after one grid barrier the rows are
-  // finalised from their `parts` partials summed in column-range order.
+  // Work item = (a group of 16 row blocks of 32 x kOtfRows rows, one per
+  // warp) x (one of `parts` column ranges), one CTA each. The CTA streams the
+  // range's column records and scalings through shared memory in chunks of
+  // kOtfChunk columns (cp.async, double-buffered): every warp reads them as
+  // broadcast LDS instead of each warp fetching them from L2. Items go to
+  // CTAs round-robin (items ~ a multiple of the grid). Each warp leaves fp64
+  // partial row sums in partial[cp * n + i]; after one grid barrier the rows
+  // are finalised from their `parts` partials summed in column-range order.
+  static constexpr int kWarps = loopcore::kBlock / 32;
+  static constexpr int kChunkRecBytes = kOtfChunk * 32;  // 2 float4 per column
+  static constexpr int kChunkXBytes = kOtfChunk * 8;
+  static constexpr int kStageBytes = kChunkRecBytes + kChunkXBytes;
+
+  __device__ static void stage_chunk(char* dst, const float4* irec, const double* x, int64_t c0, int len) {
+    // records: len * 32 bytes, x: len * 8 bytes (16-byte cp.async pieces; tails zero-filled)
+    const char* rs = reinterpret_cast<const char*>(irec + 2 * c0);
+    for (int k = threadIdx.x; k < kChunkRecBytes / 16; k += blockDim.x) {
+      const int col = k >> 1;
+      void* d = dst + 16 * k;
+      if (col < len) {
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(d)),
+                     "l"(rs + 16 * k)
+                     : "memory");
+      } else {
+        *reinterpret_cast<float4*>(d) = make_float4(0.f, 0.f, 0.f, 0.f);  // finite exp2, times x = 0 below
+      }
+    }
+    const char* xs = reinterpret_cast<const char*>(x + c0);
+    for (int k = threadIdx.x; k < kChunkXBytes / 16; k += blockDim.x) {
+      void* d = dst + kChunkRecBytes + 16 * k;
+      if (2 * k + 1 < len) {
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(d)),
+                     "l"(xs + 16 * k)
+                     : "memory");
+      } else {
+        double2 v = make_double2(0.0, 0.0);
+        if (2 * k < len) v.x = __ldcg(x + c0 + 2 * k);
+        *reinterpret_cast<double2*>(d) = v;
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+
   template <int ROLE, bool LOG, bool DET>
   __device__ void half(const double* x, const double* wgt, const double* old, double* out, unsigned char* ne,
                        int* dyn, double exponent, int policy, int t, unsigned long long* flag, double* absdiff,
                        double& err, long long& masks) const {
+    __shared__ __align__(16) char stage[2][kStageBytes];
     const int lane = threadIdx.x & 31;
-    const int nwarps = blockDim.x >> 5;
+    const int w = threadIdx.x >> 5;
     const float4* orec = out_rec[ROLE];
     const float4* irec = in_rec[ROLE];
     const int64_t tile_rows = 32 * kOtfRows;
     const int64_t nrb = (n + tile_rows - 1) / tile_rows;
-    const int64_t items = nrb * parts;
-    const int64_t gw = (int64_t)blockIdx.x * nwarps + (threadIdx.x >> 5);
-    const int64_t tw = (int64_t)gridDim.x * nwarps;
-    for (int64_t item = gw; item < items; item += tw) {
-      const int64_t rbk = item / parts;
-      const int cp = (int)(item - rbk * parts);
+    const int64_t ngroups = (nrb + kWarps - 1) / kWarps;
+    const int64_t items = ngroups * parts;
+    const int64_t per = ((n + parts - 1) / parts + 1) & ~int64_t(1);  // columns per range (even)
+    for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
+      const int64_t grp = item / parts;
+      const int cp = (int)(item - grp * parts);
+      const int64_t rbk = grp * kWarps + w;  // this warp's row block
       const int64_t r0 = rbk * tile_rows;
-      // column range of this part (even boundaries: two columns per step)
-      const int64_t per = ((n + parts - 1) / parts + 1) & ~int64_t(1);
       const int64_t c_lo = min(n, cp * per), c_hi = min(n, c_lo + per);
       float p[kOtfRows][D + 1];
       double acc[kOtfRows];
@@ -250,35 +288,48 @@ struct OtfFastOp {
         p[r][D] = v[7];  // bias_i
         acc[r] = 0.0;
       }
-      for (int64_t c0 = c_lo; c0 < c_hi; c0 += kOtfChunk) {  // fp32 partials per chunk, folded into fp64
+      const int nch = (int)((c_hi - c_lo + kOtfChunk - 1) / kOtfChunk);
+      __syncthreads();  // the previous item's readers of the stage buffers are done
+      if (nch > 0) stage_chunk(stage[0], irec, x, c_lo, (int)min((int64_t)kOtfChunk, c_hi - c_lo));
+      for (int ch = 0; ch < nch; ++ch) {
+        const int64_t c0 = c_lo + (int64_t)ch * kOtfChunk;
         const int len = (int)min((int64_t)kOtfChunk, c_hi - c0);
+        if (ch + 1 < nch) {  // next chunk in flight while this one computes
+          const int64_t c1 = c0 + kOtfChunk;
+          stage_chunk(stage[(ch + 1) & 1], irec, x, c1, (int)min((int64_t)kOtfChunk, c_hi - c1));
+          asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+          asm volatile("cp.async.wait_group 0;" ::: "memory");
+        }
+        __syncthreads();  // chunk ch staged by every thread
+        const float4* qs = reinterpret_cast<const float4*>(stage[ch & 1]);
+        const double* xs = reinterpret_cast<const double*>(stage[ch & 1] + kChunkRecBytes);
         float part[kOtfRows];
 #pragma unroll
         for (int r = 0; r < kOtfRows; ++r) part[r] = 0.f;
-        const float4* qp = irec + 2 * c0;
-        const double* xp = x + c0;
-        int jj = 0;
-        for (; jj + 1 < len; jj += 2) {  // two columns per step: independent exp chains
-          float q0[8], q1[8];
-          load_rec(qp + 2 * jj, q0);
-          load_rec(qp + 2 * jj + 2, q1);
-          const float x0 = (float)__ldcg(xp + jj), x1 = (float)__ldcg(xp + jj + 1);
+        if (r0 < n) {
+          for (int jj = 0; jj < len; jj += 2) {  // two columns per step (a zero-filled odd tail adds 0)
+            float q0[8], q1[8];
+            {
+              const float4 a0 = qs[2 * jj], b0 = qs[2 * jj + 1], a1 = qs[2 * jj + 2], b1 = qs[2 * jj + 3];
+              q0[0] = a0.x; q0[1] = a0.y; q0[2] = a0.z; q0[3] = a0.w;
+              q0[4] = b0.x; q0[5] = b0.y; q0[6] = b0.z; q0[7] = b0.w;
+              q1[0] = a1.x; q1[1] = a1.y; q1[2] = a1.z; q1[3] = a1.w;
+              q1[4] = b1.x; q1[5] = b1.y; q1[6] = b1.z; q1[7] = b1.w;
+            }
+            const double2 xd = *reinterpret_cast<const double2*>(xs + jj);
+            const float x0 = (float)xd.x, x1 = (float)xd.y;
 #pragma unroll
-          for (int r = 0; r < kOtfRows; ++r) {
-            const float e0 = expo(p[r], q0), e1 = expo(p[r], q1);
-            part[r] = fmaf(ex2_ftz(e0), x0, part[r]);
-            part[r] = fmaf(ex2_ftz(e1), x1, part[r]);
+            for (int r = 0; r < kOtfRows; ++r) {
+              const float e0 = expo(p[r], q0), e1 = expo(p[r], q1);
+              part[r] = fmaf(ex2_ftz(e0), x0, part[r]);
+              part[r] = fmaf(ex2_ftz(e1), x1, part[r]);
+            }
           }
-        }
-        if (jj < len) {
-          float q0[8];
-          load_rec(qp + 2 * jj, q0);
-          const float x0 = (float)__ldcg(xp + jj);
-#pragma unroll
-          for (int r = 0; r < kOtfRows; ++r) part[r] = fmaf(ex2_ftz(expo(p[r], q0)), x0, part[r]);
         }
 #pragma unroll
         for (int r = 0; r < kOtfRows; ++r) acc[r] += (double)part[r];
+        __syncthreads();  // every warp is done with chunk ch before its buffer is refilled
       }
 #pragma unroll
       for (int r = 0; r < kOtfRows; ++r) {
@@ -413,9 +464,27 @@ void run_dense_loop(spk_ctx* ctx, DevKernel& dk, const spk_solver_cfg& cfg, doub
     SPK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k5, loopcore::kBlock, 0));
     per_sm = std::max(per_sm, 1);
   }
+  // CTA items = (groups of 16 row blocks) x parts: a whole number of rounds
+  // over the co-resident CTAs, >= 4 rounds so a short last group costs little
   const int64_t nrb = (n + 32 * kOtfRows - 1) / (32 * kOtfRows);
-  const int64_t warps = (int64_t)ctx->num_sms * per_sm * (loopcore::kBlock / 32);
-  const int parts = (int)std::max<int64_t>(1, std::min<int64_t>(64, (warps + nrb / 2) / std::max<int64_t>(nrb, 1)));
+  const int64_t ngroups = (nrb + loopcore::kBlock / 32 - 1) / (loopcore::kBlock / 32);
+  const int64_t ctas = (int64_t)ctx->num_sms * per_sm;
+  int parts = 1;
+  {
+    double best = 0.0;
+    for (int pp = 1; pp <= 128; ++pp) {
+      const int64_t items = ngroups * pp;
+      const int64_t rounds = (items + ctas - 1) / ctas;
+      const int64_t cols = (n + pp - 1) / pp;
+      if (cols < 2 * kOtfChunk && pp > 1) break;  // ranges shorter than two chunks: staging overhead
+      const double eff = (double)items / (double)(rounds * ctas);
+      if (eff > best + 1e-9) {
+        best = eff;
+        parts = pp;
+      }
+      if (eff > 0.97 && rounds >= 2) break;
+    }
+  }
   DBuf partial(sizeof(double) * (size_t)parts * n);
   const int64_t useful = (int64_t)ctx->num_sms * per_sm;
   // the point-record width is a compile-time constant: D + 1 FMA-pipe ops per evaluation

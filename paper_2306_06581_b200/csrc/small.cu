@@ -87,6 +87,12 @@ __device__ __forceinline__ void st_async_b64(uint32_t remote, unsigned long long
                "r"(remote_bar)
                : "memory");
 }
+// bytes of the slab [lo, hi) a CTA sends: lo is even (split_by_entries), the
+// end rounded up to even (16-byte bulk copies; the round-up only reaches the
+// vector's padding, never another CTA's atoms)
+__host__ __device__ __forceinline__ int64_t slab_bytes(int64_t lo, int64_t hi) {
+  return hi > lo ? 8 * (((hi + 1) & ~int64_t(1)) - lo) : 0;
+}
 __device__ __forceinline__ void mbar_init_s(uint64_t* b) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(b)) : "memory");
 }
@@ -256,7 +262,7 @@ __global__ void __launch_bounds__(kThreads, 1) cluster_loop_kernel(ClusterArgs<V
   uint32_t rx_bytes[2] = {0u, 0u};
   for (int h = 0; h < 2; ++h)
     for (int r = 0; r < CS; ++r)
-      if (r != (int)rank) rx_bytes[h] += (uint32_t)(8 * (A.lo[h][r + 1] - A.lo[h][r]) + 24);
+      if (r != (int)rank) rx_bytes[h] += (uint32_t)(slab_bytes(A.lo[h][r], A.lo[h][r + 1]) + 24);
   if (CS > 1) cluster_barrier();  // peers' vectors and barriers initialised before any remote store
   else __syncthreads();
 
@@ -310,15 +316,6 @@ __global__ void __launch_bounds__(kThreads, 1) cluster_loop_kernel(ClusterArgs<V
       if (live && gl == 0)
         err += finalize_atom<LOG>(i, tmp, old, w_s[h][i], A.exponent, A.policy, (int)t, ne_s[h], dyn_s[h], out,
                                   &flag_sh[h], masks);
-      __syncwarp();
-      if (CS > 1 && in) {  // every atom's value (masked ones too: the peers count bytes), lanes sharing the peers
-        const double nv = out[i];
-        const uint32_t a = smem_u32(out + i);
-        for (int r = gl + 1; r < CS; r += kSG) {
-          const uint32_t pr = (rank + (uint32_t)r) % CS;
-          st_async_b64(map_cluster(a, pr), (unsigned long long)__double_as_longlong(nv), map_cluster(bar_h, pr));
-        }
-      }
     }
     err = warp_sum(err);
     masks = warp_sum_ll(masks);
@@ -340,7 +337,21 @@ __global__ void __launch_bounds__(kThreads, 1) cluster_loop_kernel(ClusterArgs<V
         xm[h][rank] = m;
         xf[h][rank] = f;
       } else if (CS > 1 && lane < CS) {
+        // this CTA's slab of the new vector to peer `lane` as ONE bulk copy
+        // (shared -> peer shared, completing bytes on the peer's mbarrier;
+        // the fence makes the CTA's generic stores visible to the async proxy),
+        // then the partials as three 8-byte st.async on the same mbarrier
         const uint32_t pr = (uint32_t)lane, rb = map_cluster(bar_h, pr);
+        const uint32_t bytes = (uint32_t)slab_bytes(r0, r1);
+        if (bytes) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          const uint32_t src = smem_u32(out + r0);
+          asm volatile(
+              "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                  map_cluster(src, pr)),
+              "r"(src), "r"(bytes), "r"(rb)
+              : "memory");
+        }
         st_async_b64(map_cluster(smem_u32(&xe[h][rank]), pr), (unsigned long long)__double_as_longlong(e), rb);
         st_async_b64(map_cluster(smem_u32(&xm[h][rank]), pr), (unsigned long long)m, rb);
         st_async_b64(map_cluster(smem_u32(&xf[h][rank]), pr), f, rb);
@@ -457,6 +468,7 @@ void split_by_entries(const std::vector<long long>& ptr, int64_t n, int CS, int6
   for (int r = 1; r < CS; ++r) {
     const long long target = (long long)((double)total * r / CS);
     lo[r] = std::lower_bound(ptr.begin(), ptr.begin() + n + 1, target) - ptr.begin();
+    lo[r] = std::min<int64_t>(n, (lo[r] + 1) & ~int64_t(1));  // even: 16-byte aligned slabs (bulk copies)
     lo[r] = std::max(lo[r], lo[r - 1]);
   }
   lo[CS] = n;
