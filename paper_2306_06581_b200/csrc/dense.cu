@@ -189,6 +189,7 @@ struct OtfFastOp {
   const float4* in_rec[2];   // [role] input-side records
   int parts;                 // column ranges per row block (work items ~ warps of the grid)
   double* partial;           // [parts][n] partial row sums
+  float* xf;                 // [n + 4] fp32 copy of the gathered scalings of the half
 
   // exponent of K_ij in log2 units: bias_i + bias_j + <p_i, y_j>, D + 1 FMA-pipe ops
   __device__ __forceinline__ static float expo(const float (&p)[D + 1], const float (&q)[8]) {
@@ -219,11 +220,11 @@ struct OtfFastOp {
   // are finalised from their `parts` partials summed in column-range order.
   static constexpr int kWarps = loopcore::kBlock / 32;
   static constexpr int kChunkRecBytes = kOtfChunk * 32;  // 2 float4 per column
-  static constexpr int kChunkXBytes = kOtfChunk * 8;
+  static constexpr int kChunkXBytes = kOtfChunk * 4;  // fp32 copy of the scalings
   static constexpr int kStageBytes = kChunkRecBytes + kChunkXBytes;
 
-  __device__ static void stage_chunk(char* dst, const float4* irec, const double* x, int64_t c0, int len) {
-    // records: len * 32 bytes, x: len * 8 bytes (16-byte cp.async pieces; tails zero-filled)
+  __device__ static void stage_chunk(char* dst, const float4* irec, const float* x, int64_t c0, int len) {
+    // records: len * 32 bytes, x: len * 4 bytes (16-byte cp.async pieces; tails zero-filled)
     const char* rs = reinterpret_cast<const char*>(irec + 2 * c0);
     for (int k = threadIdx.x; k < kChunkRecBytes / 16; k += blockDim.x) {
       const int col = k >> 1;
@@ -239,14 +240,16 @@ struct OtfFastOp {
     const char* xs = reinterpret_cast<const char*>(x + c0);
     for (int k = threadIdx.x; k < kChunkXBytes / 16; k += blockDim.x) {
       void* d = dst + kChunkRecBytes + 16 * k;
-      if (2 * k + 1 < len) {
+      if (4 * k + 3 < len) {
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(d)),
                      "l"(xs + 16 * k)
                      : "memory");
       } else {
-        double2 v = make_double2(0.0, 0.0);
-        if (2 * k < len) v.x = __ldcg(x + c0 + 2 * k);
-        *reinterpret_cast<double2*>(d) = v;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (4 * k < len) v.x = __ldcg(x + c0 + 4 * k);
+        if (4 * k + 1 < len) v.y = __ldcg(x + c0 + 4 * k + 1);
+        if (4 * k + 2 < len) v.z = __ldcg(x + c0 + 4 * k + 2);
+        *reinterpret_cast<float4*>(d) = v;
       }
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
@@ -261,11 +264,17 @@ struct OtfFastOp {
     const int w = threadIdx.x >> 5;
     const float4* orec = out_rec[ROLE];
     const float4* irec = in_rec[ROLE];
+    // fp32 copy of the gathered scalings, once per half (one conversion per
+    // column instead of one per column per warp: the conversions share the
+    // MUFU pipe with the exp2s)
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
+      xf[j] = (float)__ldcg(x + j);
+    cooperative_groups::this_grid().sync();
     const int64_t tile_rows = 32 * kOtfRows;
     const int64_t nrb = (n + tile_rows - 1) / tile_rows;
     const int64_t ngroups = (nrb + kWarps - 1) / kWarps;
     const int64_t items = ngroups * parts;
-    const int64_t per = ((n + parts - 1) / parts + 1) & ~int64_t(1);  // columns per range (even)
+    const int64_t per = ((n + parts - 1) / parts + 3) & ~int64_t(3);  // columns per range (multiple of 4: 16-byte fp32 x pieces)
     for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
       const int64_t grp = item / parts;
       const int cp = (int)(item - grp * parts);
@@ -290,20 +299,20 @@ struct OtfFastOp {
       }
       const int nch = (int)((c_hi - c_lo + kOtfChunk - 1) / kOtfChunk);
       __syncthreads();  // the previous item's readers of the stage buffers are done
-      if (nch > 0) stage_chunk(stage[0], irec, x, c_lo, (int)min((int64_t)kOtfChunk, c_hi - c_lo));
+      if (nch > 0) stage_chunk(stage[0], irec, xf, c_lo, (int)min((int64_t)kOtfChunk, c_hi - c_lo));
       for (int ch = 0; ch < nch; ++ch) {
         const int64_t c0 = c_lo + (int64_t)ch * kOtfChunk;
         const int len = (int)min((int64_t)kOtfChunk, c_hi - c0);
         if (ch + 1 < nch) {  // next chunk in flight while this one computes
           const int64_t c1 = c0 + kOtfChunk;
-          stage_chunk(stage[(ch + 1) & 1], irec, x, c1, (int)min((int64_t)kOtfChunk, c_hi - c1));
+          stage_chunk(stage[(ch + 1) & 1], irec, xf, c1, (int)min((int64_t)kOtfChunk, c_hi - c1));
           asm volatile("cp.async.wait_group 1;" ::: "memory");
         } else {
           asm volatile("cp.async.wait_group 0;" ::: "memory");
         }
         __syncthreads();  // chunk ch staged by every thread
         const float4* qs = reinterpret_cast<const float4*>(stage[ch & 1]);
-        const double* xs = reinterpret_cast<const double*>(stage[ch & 1] + kChunkRecBytes);
+        const float* xs = reinterpret_cast<const float*>(stage[ch & 1] + kChunkRecBytes);
         float part[kOtfRows];
 #pragma unroll
         for (int r = 0; r < kOtfRows; ++r) part[r] = 0.f;
@@ -317,8 +326,8 @@ struct OtfFastOp {
               q1[0] = a1.x; q1[1] = a1.y; q1[2] = a1.z; q1[3] = a1.w;
               q1[4] = b1.x; q1[5] = b1.y; q1[6] = b1.z; q1[7] = b1.w;
             }
-            const double2 xd = *reinterpret_cast<const double2*>(xs + jj);
-            const float x0 = (float)xd.x, x1 = (float)xd.y;
+            const float2 xd = *reinterpret_cast<const float2*>(xs + jj);
+            const float x0 = xd.x, x1 = xd.y;
 #pragma unroll
             for (int r = 0; r < kOtfRows; ++r) {
               const float e0 = expo(p[r], q0), e1 = expo(p[r], q1);
@@ -486,6 +495,7 @@ void run_dense_loop(spk_ctx* ctx, DevKernel& dk, const spk_solver_cfg& cfg, doub
     }
   }
   DBuf partial(sizeof(double) * (size_t)parts * n);
+  DBuf xf(sizeof(float) * ((size_t)n + 4));
   const int64_t useful = (int64_t)ctx->num_sms * per_sm;
   // the point-record width is a compile-time constant: D + 1 FMA-pipe ops per evaluation
   auto go = [&](auto dtag) {
@@ -499,6 +509,7 @@ void run_dense_loop(spk_ctx* ctx, DevKernel& dk, const spk_solver_cfg& cfg, doub
     op.in_rec[1] = recs[3];
     op.parts = parts;
     op.partial = partial.as<double>();
+    op.xf = xf.as<float>();
     loopcore::run_core<false>(ctx, op, n, W, (long long)emp[0], (long long)emp[1], cfg, exponent, policy, st,
                               useful, out);
   };
