@@ -245,20 +245,12 @@ __device__ __forceinline__ double batch_half(int64_t i_lo, int64_t i_hi, const l
         // l = -inf (K~ = 0, or padding) or x = -inf (masked column): exp -> 0
         t[k] = l + *reinterpret_cast<const double*>(reinterpret_cast<const char*>(x) + jo);
       }
-      // block maximum: any M near the true one gives the same log-sum-exp
-      // (t - M stays far inside the exp range), so FAST takes it in fp32
-      // (FMNMX) instead of fp64 fmax (NaN-aware DSETP sequences)
-      double M;
-      if constexpr (FAST) {
-        float mf = __double2float_rn(t[0]);
+      // block maximum by compare-and-select (terms are finite or -inf, never
+      // NaN: no NaN-aware fmax sequence, and no conversions on the MUFU/XU
+      // pipe, which the exp2s already load)
+      double M = t[0];
 #pragma unroll
-        for (int k = 1; k < U; ++k) mf = fmaxf(mf, __double2float_rn(t[k]));
-        M = (double)mf;
-      } else {
-        M = t[0];
-#pragma unroll
-        for (int k = 1; k < U; ++k) M = fmax(M, t[k]);
-      }
+      for (int k = 1; k < U; ++k) M = t[k] > M ? t[k] : M;
       if (M == -CUDART_INF) return;  // every term of the block is -inf
       if (M > m) {
         s = (m == -CUDART_INF) ? Acc(0) : s * lse_term<FAST>(m - M);
