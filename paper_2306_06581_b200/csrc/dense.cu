@@ -179,7 +179,12 @@ __device__ __forceinline__ float ex2_ftz(float e) {
   return r;
 }
 
-template <int D>
+// FOLD: the input side's bias_j = alpha |y_j|^2 is folded into its scaling
+// (x'_j = x_j exp2(bias_j), once per half) so an evaluation is exp2(bias_i +
+// <p_i, y_j>) * x'_j: D FMA-pipe ops for the exponent instead of D + 1. Used
+// only when |alpha| max |pt|^2 <= 60, so neither exp2(bias_i + <p_i, y_j>) =
+// exp2(e_ij - bias_j) can overflow nor exp2(bias_j) underflow.
+template <int D, bool FOLD>
 struct OtfFastOp {
   static constexpr int kThreads = loopcore::kBlock;
   static constexpr int kMinBlocks = 1;  // 128 registers (at 64 the point records spill)
@@ -190,10 +195,11 @@ struct OtfFastOp {
   int parts;                 // column ranges per row block (work items ~ warps of the grid)
   double* partial;           // [parts][n] partial row sums
   float* xf;                 // [n + 4] fp32 copy of the gathered scalings of the half
+  const float* colscale[2];  // [role] FOLD: exp2(bias_j) of the input side
 
   // exponent of K_ij in log2 units: bias_i + bias_j + <p_i, y_j>, D + 1 FMA-pipe ops
   __device__ __forceinline__ static float expo(const float (&p)[D + 1], const float (&q)[8]) {
-    float e = p[D] + q[7];
+    float e = FOLD ? p[D] : p[D] + q[7];
 #pragma unroll
     for (int k = 0; k < D; ++k) e = fmaf(p[k], q[k], e);
     return e;
@@ -268,7 +274,7 @@ struct OtfFastOp {
     // column instead of one per column per warp: the conversions share the
     // MUFU pipe with the exp2s)
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
-      xf[j] = (float)__ldcg(x + j);
+      xf[j] = FOLD ? (float)__ldcg(x + j) * __ldg(colscale[ROLE] + j) : (float)__ldcg(x + j);
     cooperative_groups::this_grid().sync();
     const int64_t tile_rows = 32 * kOtfRows;
     const int64_t nrb = (n + tile_rows - 1) / tile_rows;
@@ -404,7 +410,7 @@ void run_exact(spk_ctx* ctx, KF kf, int64_t n, const spk_solver_cfg& cfg, double
 }
 
 __global__ void otf_records_kernel(const double* pts, int64_t n, int dim, double alpha, float4* out_rec,
-                                   float4* in_rec) {
+                                   float4* in_rec, float* in_scale) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     float o[kOtfDim] = {0, 0, 0, 0, 0, 0, 0, 0};
     float q[kOtfDim] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -421,6 +427,7 @@ __global__ void otf_records_kernel(const double* pts, int64_t n, int dim, double
     out_rec[2 * i + 1] = make_float4(o[4], o[5], o[6], o[7]);
     in_rec[2 * i] = make_float4(q[0], q[1], q[2], q[3]);
     in_rec[2 * i + 1] = make_float4(q[4], q[5], q[6], q[7]);
+    in_scale[i] = exp2f((float)(alpha * nrm));  // FOLD: exp2(bias) of this point as an input
   }
 }
 
@@ -447,8 +454,13 @@ void run_dense_loop(spk_ctx* ctx, DevKernel& dk, const spk_solver_cfg& cfg, doub
   DBuf xo(sizeof(float4) * 2 * n), xi(sizeof(float4) * 2 * n), yo(sizeof(float4) * 2 * n), yi(sizeof(float4) * 2 * n);
   const double alpha = -1.4426950408889634 / (dk.scale * dk.eps);
   const int g = loopcore::simple_grid(ctx, n);
-  otf_records_kernel<<<g, 256, 0, ctx->stream>>>(dk.x.as<double>(), n, dk.dim, alpha, xo.as<float4>(), xi.as<float4>());
-  otf_records_kernel<<<g, 256, 0, ctx->stream>>>(dk.y.as<double>(), n, dk.dim, alpha, yo.as<float4>(), yi.as<float4>());
+  DBuf xs(sizeof(float) * n), ys(sizeof(float) * n);
+  otf_records_kernel<<<g, 256, 0, ctx->stream>>>(dk.x.as<double>(), n, dk.dim, alpha, xo.as<float4>(), xi.as<float4>(),
+                                                 xs.as<float>());
+  otf_records_kernel<<<g, 256, 0, ctx->stream>>>(dk.y.as<double>(), n, dk.dim, alpha, yo.as<float4>(), yi.as<float4>(),
+                                                 ys.as<float>());
+  // fold the input bias into the scalings when no exp2 can leave the fp32 range
+  const bool fold = std::fabs(alpha) * dk.dim * dk.max_abs * dk.max_abs <= 60.0;
   ctx->launches += 2;
   const float4* recs[4] = {xo.as<float4>(), yi.as<float4>(), yo.as<float4>(), xi.as<float4>()};
   // coverage: exp2 of finite exponents never reaches 0 for max-normalised
@@ -469,7 +481,7 @@ void run_dense_loop(spk_ctx* ctx, DevKernel& dk, const spk_solver_cfg& cfg, doub
   // ranges so that (row blocks x ranges) matches the grid's warps
   int per_sm = 1;
   {
-    auto k5 = loopcore::loop_kernel<false, false, OtfFastOp<5>>;  // (D <= 5 share the occupancy)
+    auto k5 = loopcore::loop_kernel<false, false, OtfFastOp<5, true>>;  // (all variants share the occupancy)
     SPK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k5, loopcore::kBlock, 0));
     per_sm = std::max(per_sm, 1);
   }
@@ -498,9 +510,12 @@ void run_dense_loop(spk_ctx* ctx, DevKernel& dk, const spk_solver_cfg& cfg, doub
   DBuf xf(sizeof(float) * ((size_t)n + 4));
   const int64_t useful = (int64_t)ctx->num_sms * per_sm;
   // the point-record width is a compile-time constant: D + 1 FMA-pipe ops per evaluation
-  auto go = [&](auto dtag) {
+  auto go2 = [&](auto dtag, auto ftag) {
     constexpr int D = decltype(dtag)::value;
-    OtfFastOp<D> op;
+    constexpr bool FOLD = decltype(ftag)::value;
+    OtfFastOp<D, FOLD> op;
+    op.colscale[0] = ys.as<float>();  // rows: inputs are the y points
+    op.colscale[1] = xs.as<float>();
     op.n = n;
     op.dim = dk.dim;
     op.out_rec[0] = recs[0];  // rows: x_i against y_j
@@ -512,6 +527,10 @@ void run_dense_loop(spk_ctx* ctx, DevKernel& dk, const spk_solver_cfg& cfg, doub
     op.xf = xf.as<float>();
     loopcore::run_core<false>(ctx, op, n, W, (long long)emp[0], (long long)emp[1], cfg, exponent, policy, st,
                               useful, out);
+  };
+  auto go = [&](auto dtag) {
+    if (fold) go2(dtag, std::true_type{});
+    else go2(dtag, std::false_type{});
   };
   switch (dk.dim) {
     case 1: go(std::integral_constant<int, 1>{}); break;
