@@ -450,6 +450,10 @@ def run_ours(args, ws, rank, local):
                               "kind": "port (oracle restatement of poisson_sparsify on coordinates), 1 core",
                               "gpu_sample_s": e2e["phases_s"]["sample"] if e2e else None}
 
+    dense = None
+    if args.config == "c5" and rank == 0:
+        dense = c5_dense_comparison(ctx, w, kernel, iters, args.no_cpu)
+
     line = {
         "metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * elapsed / args.steps, "higher_is_better": True,
@@ -469,6 +473,7 @@ def run_ours(args, ws, rank, local):
         "gpu_launches": launches,
         "clocks": clk.summary(),
         "parity": parity,
+        "dense_comparison": dense,
         "extra": {"setup_s": setup_s, "loop_ms_per_iter": 1e3 * mean_loop / per_launch_iters,
                   "kernel_nnz": sk.kernel_nnz, "factorized_plan": sk.factorized_plan},
     }
@@ -476,6 +481,53 @@ def run_ours(args, ws, rank, local):
         print(json.dumps(line), flush=True)
     sk.free()
     ctx.close()
+
+
+def c5_dense_comparison(ctx, w, kernel, iters, no_cpu):
+    """Config 5 as BASELINE.json states it: the classical Sinkhorn with K
+    recomputed on the fly every iteration (the dense comparator, fp32 K) for
+    `iters` iterations, and Spar-Sink at s = 4, 8, 16 n ln n with the
+    objective error against it. The comparator's roofline is the measured
+    MUFU.EX2 peak (2 n^2 exp2 per iteration). CPU: the reference's dense
+    sinkhorn_ot<KernelMatrix> at n = 8000 (2 iterations, its K built by the
+    reference) scaled by n^2 to config 5's n (labelled)."""
+    import paper_2306_06581_b200 as spk
+
+    MUFU_PEAK = 4.619e12  # profiles/microbench/r1_sfu_fma_peak_b200.txt (measured MUFU.EX2 / s)
+    cfg = spk.SolverConfig(w.eps, w.lam, -1.0, iters)
+    ctx.sinkhorn(kernel, w.a, w.b, spk.SolverConfig(w.eps, w.lam, -1.0, 5))  # warm-up
+    d = ctx.sinkhorn(kernel, w.a, w.b, cfg)
+    evals = 2.0 * w.n * w.n * d.report["iterations"] / d.report["t_loop_s"]
+    out = {"n": w.n, "iterations": d.report["iterations"], "loop_s": d.report["t_loop_s"],
+           "ms_per_iteration": 1e3 * d.report["t_loop_s"] / d.report["iterations"],
+           "kernel_evals_per_s": evals, "mufu_ex2_peak_per_s": MUFU_PEAK, "frac_of_mufu_peak": evals / MUFU_PEAK,
+           "objective": d.report["objective"], "spar_sink": []}
+    for mult in (4, 8, 16):
+        sp = ctx.spar_sink(kernel, w.a, w.b, cfg, mult * w.n * math.log(w.n), 7)
+        out["spar_sink"].append({"s_over_nlogn": mult, "sketch_nnz": sp.report["sketch_nnz"],
+                                 "objective": sp.report["objective"],
+                                 "rel_error_vs_dense": abs(sp.report["objective"] - d.report["objective"]) /
+                                 abs(d.report["objective"])})
+    if not no_cpu:
+        from oracle import Reference
+        from paper_2306_06581_b200 import workloads as W
+
+        if Reference.available():
+            m = 8000
+            ws = W.c5(n=m)
+            R = Reference()
+            Cm, c0 = R.pairwise_cost(ws.x, ws.y)
+            Cm /= c0
+            K, r = R.kernel_from_cost(Cm, ws.eps)
+            del Cm
+            _, _, _, _, rep = R.sinkhorn(ws.a, ws.b, ws.eps, ws.lam, -1.0, 2, K=K, nnz_ratio=r)
+            per_it = rep["wall_time_s"] / 2
+            out["cpu_reference_dense"] = {
+                "n_timed": m, "s_per_iteration": per_it, "kind": "reference", "cores": 1,
+                "extrapolated_s_per_iteration_at_n": per_it * (w.n / m) ** 2,
+                "sample": f"2 iterations of the reference's dense sinkhorn_ot<KernelMatrix> at n = {m} "
+                          f"(K built by the reference), scaled by n^2 to n = {w.n} (labelled extrapolation)"}
+    return out
 
 
 def run_sharded(args, ws, rank, local):
