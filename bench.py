@@ -323,6 +323,10 @@ def run_ours(args, ws, rank, local):
         from paper_2306_06581_b200 import _lib as L
 
         ctx.set_option(L.OPT_SMALL_LOOP, int(os.environ["SPK_SMALL"]))
+    if os.environ.get("SPK_ROW_LANES") is not None:  # grid loop: lanes per row (profiling)
+        from paper_2306_06581_b200 import _lib as L
+
+        ctx.set_option(L.OPT_ROW_LANES, int(os.environ["SPK_ROW_LANES"]))
     if os.environ.get("SPK_SMALL_CS") is not None:
         from paper_2306_06581_b200 import _lib as L
 

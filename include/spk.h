@@ -176,7 +176,9 @@ enum spk_option {
   SPK_OPT_SMALL_LOOP = 12,      /* fast mode, small sketches: the loop on ONE cluster with the scalings in
                                    shared memory (1, default) or the persistent grid loop (0) */
   SPK_OPT_SMALL_CLUSTER = 13,   /* that cluster's size: 16 (default, non-portable), 8, 4, 2, 1 */
-  SPK_OPT_SMALL_MAX_NNZ = 14    /* largest sketch (entries) it takes (default 4e6) */
+  SPK_OPT_SMALL_MAX_NNZ = 14,   /* largest sketch (entries) it takes (default 4e6) */
+  SPK_OPT_ROW_LANES = 15        /* grid loop, fast mode: lanes per sketch row: 0 auto (8 when rows average <= 256
+                                   entries: 4 rows in flight per warp), 8, 32 */
 };
 int spk_ctx_set_option(spk_ctx* ctx, int key, int64_t value);
 /* Current value of an option key (SPK_STATUS_INPUT for an unknown key). */

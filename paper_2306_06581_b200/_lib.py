@@ -31,6 +31,7 @@ OPT_BATCH_UNROLL = 11
 OPT_SMALL_LOOP = 12
 OPT_SMALL_CLUSTER = 13
 OPT_SMALL_MAX_NNZ = 14
+OPT_ROW_LANES = 15
 
 ERROR_CLASSES = {
     1: "Error", 2: "NegativeWeight", 3: "LengthMismatch", 4: "NotNormalized", 5: "AllBlack",

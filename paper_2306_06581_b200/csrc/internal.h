@@ -165,6 +165,7 @@ struct spk_ctx {
   int64_t small_max_nnz = 4000000;   // ... and the sketch is small enough that 16 SMs stream it faster
                                      //     than a grid barrier pair costs
   int force_two_pass = 0;      // sampler: skip the single-pass tiled path (testing)
+  int row_lanes = 0;           // grid loop, fast mode: lanes per row, 0 auto (8 for short rows), 8, 32
   int64_t launches = 0;
   // last error
   int err_category = 0;

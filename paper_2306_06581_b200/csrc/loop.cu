@@ -27,7 +27,56 @@ namespace {
 
 using loopcore::finalize_atom;
 
-template <class VT>
+// One row's value by the G lanes of a group (fast mode): FMA sum of v * x,
+// or the two-pass log-sum-exp; x read through L2 (rewritten in the launch).
+// Every lane of the warp calls it (the group reductions are warp shuffles).
+template <int G, bool LOG, class VT>
+__device__ __forceinline__ double group_row(const VT* __restrict__ val, const uint32_t* __restrict__ idx, int b, int e,
+                                            const double* x, int gl) {
+  if constexpr (!LOG) {
+    // four independent index -> x chains in flight per lane
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int p = b + gl;
+    for (; p + 3 * G < e; p += 4 * G) {
+      const uint32_t c0 = __ldg(idx + p), c1 = __ldg(idx + p + G), c2 = __ldg(idx + p + 2 * G),
+                     c3 = __ldg(idx + p + 3 * G);
+      const double w0 = (double)__ldg(val + p), w1 = (double)__ldg(val + p + G), w2 = (double)__ldg(val + p + 2 * G),
+                   w3 = (double)__ldg(val + p + 3 * G);
+      a0 = fma(w0, __ldcg(x + c0), a0);
+      a1 = fma(w1, __ldcg(x + c1), a1);
+      a2 = fma(w2, __ldcg(x + c2), a2);
+      a3 = fma(w3, __ldcg(x + c3), a3);
+    }
+    for (; p < e; p += G) a0 = fma((double)__ldg(val + p), __ldcg(x + __ldg(idx + p)), a0);
+    double s = (a0 + a1) + (a2 + a3);
+#pragma unroll
+    for (int o = G / 2; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    return s;
+  } else {
+    double m = -CUDART_INF;
+    for (int p = b + gl; p < e; p += G) {
+      const double xv = __ldcg(x + __ldg(idx + p));
+      if (xv == -CUDART_INF) continue;
+      m = fmax(m, log_of(ldg_val(val + p)) + xv);
+    }
+#pragma unroll
+    for (int o = G / 2; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    double s = 0.0;
+    if (m != -CUDART_INF)
+      for (int p = b + gl; p < e; p += G) {
+        const double xv = __ldcg(x + __ldg(idx + p));
+        if (xv == -CUDART_INF) continue;
+        s += exp_term<VT>(log_of(ldg_val(val + p)) + xv - m);
+      }
+#pragma unroll
+    for (int o = G / 2; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    return m == -CUDART_INF ? -CUDART_INF : m + log(s);
+  }
+}
+
+// G: lanes per row in fast mode (8 for short rows: 4 rows in flight per warp,
+// the next rows' bounds loaded one step ahead; 32 for long rows).
+template <class VT, int G = 32>
 struct SparseOp {
   static constexpr int kThreads = loopcore::kBlock;
   static constexpr int kMinBlocks = 2;
@@ -61,7 +110,7 @@ struct SparseOp {
         }
         absdiff[i] = d;
       }
-    } else {
+    } else if constexpr (G == 32) {
       const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
       const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
       for (int64_t i = warp; i < n; i += nw) {
@@ -73,6 +122,39 @@ struct SparseOp {
         if (lane == 0)
           err += finalize_atom<LOG>(i, tmp, __ldcg(old + i), __ldg(wgt + i), exponent, policy, t, ne, dyn, out, flag,
                                     masks);
+      }
+    } else {
+      // 32 / G rows per warp at once (rows of ~50-200 entries: a warp per row
+      // would leave its loads one L2 round trip at a time)
+      constexpr int R = 32 / G;
+      const int gl = lane & (G - 1);
+      const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+      const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+      int64_t i = warp * R + lane / G;
+      long long bn = 0, en = 0;
+      if (i < n) {
+        bn = __ldg(ptr + i);
+        en = __ldg(ptr + i + 1);
+      }
+      for (int64_t i0 = warp * R; i0 < n; i0 += nw * R) {
+        i = i0 + lane / G;
+        const bool in = i < n;
+        const bool live = in && ne[i];
+        const long long b = live ? bn : 0, e = live ? en : 0;
+        const int64_t inext = i + nw * R;
+        if (inext < n) {  // the next rows' bounds in flight while this row runs
+          bn = __ldg(ptr + inext);
+          en = __ldg(ptr + inext + 1);
+        }
+        const VT* vr = vv + b;
+        const uint32_t* ir = idx + b;
+        const double tmp = group_row<G, LOG, VT>(vr, ir, 0, (int)(e - b), x, gl);
+        if (in && gl == 0) {
+          if (!live) out[i] = __ldcg(old + i);
+          else
+            err += finalize_atom<LOG>(i, tmp, __ldcg(old + i), __ldg(wgt + i), exponent, policy, t, ne, dyn, out,
+                                      flag, masks);
+        }
       }
     }
   }
@@ -91,8 +173,21 @@ __global__ void coverage_kernel(const long long* row_ptr, const long long* col_p
   }
 }
 
+template <bool LOG, class VT, int G>
+void run_g(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, double exponent, int policy, LoopState& st,
+           LoopOut& out);
+
+// fast mode on short rows (<= 256 entries on average): 8 lanes per row
 template <bool LOG, class VT>
 void run_t(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, double exponent, int policy, LoopState& st,
+           LoopOut& out) {
+  const bool short_rows = ctx->row_lanes == 8 || (ctx->row_lanes == 0 && sk->nnz <= 256 * sk->n);
+  if (!ctx->deterministic && short_rows) run_g<LOG, VT, 8>(ctx, sk, cfg, exponent, policy, st, out);
+  else run_g<LOG, VT, 32>(ctx, sk, cfg, exponent, policy, st, out);
+}
+
+template <bool LOG, class VT, int G>
+void run_g(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, double exponent, int policy, LoopState& st,
            LoopOut& out) {
   const int64_t n = sk->n;
   LoopWs& W = sk->ws;
@@ -100,7 +195,7 @@ void run_t(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, double expon
   W.col_ne.ensure(n);
   SPK_CUDA(cudaMemcpyAsync(W.row_ne.p, sk->cov_row.p, n, cudaMemcpyDeviceToDevice, ctx->stream));
   SPK_CUDA(cudaMemcpyAsync(W.col_ne.p, sk->cov_col.p, n, cudaMemcpyDeviceToDevice, ctx->stream));
-  SparseOp<VT> op;
+  SparseOp<VT, G> op;
   op.n = n;
   op.row_ptr = sk->row_ptr.as<long long>();
   op.col_idx = sk->col_idx.as<uint32_t>();
@@ -113,8 +208,10 @@ void run_t(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, double expon
     op.val = sk->values.as<VT>();
     op.val_t = sk->values_t.as<VT>();
   }
-  const int64_t per_block = ctx->deterministic ? loopcore::kBlock : loopcore::kBlock / 32;
-  const int64_t useful = (n + per_block - 1) / per_block;
+  const int64_t per_block = ctx->deterministic ? loopcore::kBlock : loopcore::kBlock / G;
+  // G = 8: every co-resident CTA (a grid just above the SM count would give
+  // a few SMs two CTAs' rows and make every half wait for them)
+  const int64_t useful = (!ctx->deterministic && G < 32) ? (int64_t)1 << 30 : (n + per_block - 1) / per_block;
   loopcore::run_core<LOG>(ctx, op, n, W, sk->cov_empty_rows, sk->cov_empty_cols, cfg, exponent, policy, st, useful,
                           out);
 }

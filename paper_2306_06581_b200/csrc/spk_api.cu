@@ -302,6 +302,10 @@ int spk_ctx_set_option(spk_ctx* ctx, int key, int64_t value) {
       ctx->small_cluster = (int)value;
       return SPK_OK;
     case 14: ctx->small_max_nnz = std::max<int64_t>(0, value); return SPK_OK;
+    case 15:
+      if (value != 0 && value != 8 && value != 32) return SPK_STATUS_INPUT;
+      ctx->row_lanes = (int)value;
+      return SPK_OK;
     case 8: ctx->blocked_spread = value ? 1 : 0; return SPK_OK;
     case 7: ctx->blocked_split = (int)std::max<int64_t>(0, std::min<int64_t>(value, 2)); return SPK_OK;
     default: return SPK_STATUS_INPUT;
@@ -325,6 +329,7 @@ int spk_ctx_get_option(const spk_ctx* ctx, int key, int64_t* value) {
     case 12: *value = ctx->small_loop; return SPK_OK;
     case 13: *value = ctx->small_cluster; return SPK_OK;
     case 14: *value = ctx->small_max_nnz; return SPK_OK;
+    case 15: *value = ctx->row_lanes; return SPK_OK;
     default: return SPK_STATUS_INPUT;
   }
 }
