@@ -181,7 +181,12 @@ void run_g(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, double expon
 template <bool LOG, class VT>
 void run_t(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, double exponent, int policy, LoopState& st,
            LoopOut& out) {
-  const bool short_rows = ctx->row_lanes == 8 || (ctx->row_lanes == 0 && sk->nnz <= 256 * sk->n);
+  // auto: 8 lanes per row when rows are short AND a warp per row would leave
+  // each warp several rows in sequence (measured: C5-sparse 13.5k -> 16.4k
+  // iterations/s; C2, 10k rows = ~2 per warp, keeps a warp per row)
+  const int64_t warps = (int64_t)ctx->num_sms * 2 * (loopcore::kBlock / 32);
+  const bool short_rows = ctx->row_lanes == 8 ||
+                          (ctx->row_lanes == 0 && sk->nnz <= 256 * sk->n && sk->n > 4 * warps);
   if (!ctx->deterministic && short_rows) run_g<LOG, VT, 8>(ctx, sk, cfg, exponent, policy, st, out);
   else run_g<LOG, VT, 32>(ctx, sk, cfg, exponent, policy, st, out);
 }
