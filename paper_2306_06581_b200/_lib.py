@@ -7,12 +7,13 @@ import fails loudly; there is no CPU fallback anywhere in this package.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 import numpy as np
 
 PKG = Path(__file__).resolve().parent
-LIB_PATH = PKG / "libspk_b200.so"
+LIB_PATH = Path(os.environ.get("SPK_LIB_PATH", str(PKG / "libspk_b200.so")))  # override: variant builds (profiling)
 
 # ---- enums (spk.h) ------------------------------------------------------------
 SPK_OK = 0

@@ -76,7 +76,7 @@ struct DBuf {
 // Reusable device scratch of one Sinkhorn loop / readout (kept per sketch so
 // repeated solves allocate nothing).
 struct LoopWs {
-  DBuf row_ne, col_ne, dyn_row, dyn_col, u2, v2, la, lb, absdiff, part, flag, status, scalar, xchg, pair;
+  DBuf row_ne, col_ne, dyn_row, dyn_col, u2, v2, la, lb, absdiff, part, flag, status, scalar, xchg, pair, slices;
 };
 struct ReadWs {
   DBuf row_m, col_m, row_c, row_h, terms, flag, tmp, sums, bad;

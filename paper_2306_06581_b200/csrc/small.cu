@@ -32,6 +32,10 @@
 #include "loop_core.cuh"
 #include "rowdot.cuh"
 
+#ifndef SPK_SMALL_WAIT
+#define SPK_SMALL_WAIT 0  // 1: test_wait polling, 2: try_wait with a 20 ns suspend hint
+#endif
+
 namespace spk {
 
 namespace {
@@ -61,9 +65,15 @@ struct ClusterArgs {
   long long masked0[2];
   int npad;   // doubles per shared vector
   int stage;  // 1: the CTA's sketch share lives in shared memory
-  unsigned long long* trace;  // SPK_TRACE_SMALL: globaltimer stamps [iter<8][half][rank][5]
-  int64_t stage_ent[2];  // max entries of one CTA's share per half (staged layout)
+  unsigned long long* trace;  // SPK_TRACE_SMALL=t0: SM clock stamps of iterations t0+1..t0+8 [8][half][rank][kTraceSlots]
+  long long trace_t0;
+  int64_t stage_ent[2];  // max entries of one CTA's share per half (sliced layout, with padding)
   int64_t stage_rows[2];
+  int64_t stage_slices[2];
+  // sliced layout of each CTA's share (see group_dot): entry offset of every
+  // kSR-row slice, per half, CTAs back to back (CTA r's first slice: soff[h][r])
+  const int* sbase[2];
+  int64_t soff[2][kMaxCS + 1];
 };
 
 __device__ __forceinline__ unsigned cluster_rank() {
@@ -80,12 +90,6 @@ __device__ __forceinline__ uint32_t map_cluster(uint32_t a, uint32_t rank) {
   uint32_t r;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
   return r;
-}
-// 8-byte remote shared store that completes 8 bytes of the receiver's mbarrier transaction count
-__device__ __forceinline__ void st_async_b64(uint32_t remote, unsigned long long v, uint32_t remote_bar) {
-  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(remote), "l"(v),
-               "r"(remote_bar)
-               : "memory");
 }
 // bytes of the slab [lo, hi) a CTA sends: lo is even (split_by_entries), the
 // end rounded up to even (16-byte bulk copies; the round-up only reaches the
@@ -105,7 +109,13 @@ __device__ __forceinline__ bool mbar_wait_s(uint64_t* b, uint32_t parity) {
     uint32_t done;
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
+#if SPK_SMALL_WAIT == 1
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+#elif SPK_SMALL_WAIT == 2
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, 20;\n\t"
+#else
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+#endif
         "selp.u32 %0, 1, 0, p;\n}"
         : "=r"(done)
         : "r"(smem_u32(b)), "r"(parity)
@@ -122,7 +132,13 @@ __device__ __forceinline__ T* peer(T* p, unsigned rank) {
   return q;
 }
 
-constexpr int kSG = 8;          // lanes per row (config-1 rows: ~55 entries)
+#ifndef SPK_SMALL_BULK
+#define SPK_SMALL_BULK 1  // 0: slabs as 16-byte st.async per lane (measured slower)
+#endif
+#ifndef SPK_SMALL_SG
+#define SPK_SMALL_SG 4
+#endif
+constexpr int kSG = SPK_SMALL_SG;  // lanes per row (config-1 rows: ~55 entries)
 constexpr int kSR = 32 / kSG;   // rows per warp at once
 
 template <class T>
@@ -137,25 +153,29 @@ __device__ __forceinline__ double group_max(double v) {
   return v;
 }
 
-// One row's dot over [b, e) by the kSG lanes of a group (generic pointers:
-// the sketch share is staged in shared memory), x shared: linear sum of
-// v * x (FMA), or the two-pass log-sum-exp (solvers.cpp:99-111; fp32 sketches
-// take the fp32-accurate exp). Every lane of the warp must call it.
+// One row's dot by the kSG lanes of a group over the sliced share: the
+// kSR rows a warp handles at once are stored step-major -- step k of lane l
+// at b + 32 k with b = slice base + l -- so every step reads 32 consecutive
+// values and indices (no bank conflicts; only the x gather is random).
+// `cnt` = this lane's entries of its row. x shared: linear sum of v * x (FMA),
+// or the two-pass log-sum-exp (solvers.cpp:99-111; fp32 sketches take the
+// fp32-accurate exp). Every lane of the warp must call it.
 template <bool LOG, class VT>
-__device__ __forceinline__ double group_dot(const VT* val, const uint32_t* idx, int b, int e, const double* x,
-                                            int gl) {
+__device__ __forceinline__ double group_dot(const VT* val, const uint32_t* idx, int b, int cnt, const double* x) {
   if constexpr (!LOG) {
     double a0 = 0.0, a1 = 0.0;
-    int p = b + gl;
-    for (; p + kSG < e; p += 2 * kSG) {
+    int k = 0;
+    for (; k + 1 < cnt; k += 2) {
+      const int p = b + 32 * k;
       a0 = fma((double)val[p], x[idx[p]], a0);
-      a1 = fma((double)val[p + kSG], x[idx[p + kSG]], a1);
+      a1 = fma((double)val[p + 32], x[idx[p + 32]], a1);
     }
-    if (p < e) a0 = fma((double)val[p], x[idx[p]], a0);
+    if (k < cnt) a0 = fma((double)val[b + 32 * k], x[idx[b + 32 * k]], a0);
     return group_sum(a0 + a1);
   } else {
     double m = -CUDART_INF;
-    for (int p = b + gl; p < e; p += kSG) {
+    for (int k = 0; k < cnt; ++k) {
+      const int p = b + 32 * k;
       const double xv = x[idx[p]];
       if (xv == -CUDART_INF) continue;
       m = fmax(m, log_of(val[p]) + xv);
@@ -163,7 +183,8 @@ __device__ __forceinline__ double group_dot(const VT* val, const uint32_t* idx, 
     m = group_max(m);
     double s = 0.0;
     if (m != -CUDART_INF)
-      for (int p = b + gl; p < e; p += kSG) {
+      for (int k = 0; k < cnt; ++k) {
+        const int p = b + 32 * k;
         const double xv = x[idx[p]];
         if (xv == -CUDART_INF) continue;
         s += exp_term<VT>(log_of(val[p]) + xv - m);
@@ -172,6 +193,8 @@ __device__ __forceinline__ double group_dot(const VT* val, const uint32_t* idx, 
     return m == -CUDART_INF ? -CUDART_INF : m + log(s);
   }
 }
+
+constexpr int kTraceSlots = 10;
 
 template <bool LOG, class VT, int CS>
 __global__ void __launch_bounds__(kThreads, 1) cluster_loop_kernel(ClusterArgs<VT> A) {
@@ -212,40 +235,57 @@ __global__ void __launch_bounds__(kThreads, 1) cluster_loop_kernel(ClusterArgs<V
       dyn_s[h][i] = 0;
       w_own[h][i - A.lo[h][rank]] = A.w[h][i];
     }
-  // the CTA's share of the sketch, staged in shared memory once (per half:
-  // rows+1 offsets relative to the share, values, indices); pointers derived
-  // from the shared array, so every access is an LDS
-  const long long* ptr[2];
+  // the CTA's share of the sketch, staged in shared memory once in the
+  // sliced layout (per half: slice bases, row lengths, values, indices);
+  // pointers derived from the shared array, so every access is an LDS
+  const int* sl[2];
+  const int* ln[2];
   const uint32_t* idx[2];
   const VT* val[2];
-  int64_t rbase[2];  // atom offset subtracted from the row index into ptr
   for (int h = 0; h < 2; ++h) {
-    const int64_t r0 = A.lo[h][rank], r1 = A.lo[h][rank + 1];
-    const long long e0 = A.ptr[h][r0], e1 = A.ptr[h][r1];
-    long long* sp = reinterpret_cast<long long*>(tail);
-    tail += sizeof(long long) * ((A.stage_rows[h] + 2) & ~int64_t(1));
+    const int64_t r0 = A.lo[h][rank], r1 = A.lo[h][rank + 1], rows = r1 - r0;
+    const int64_t ns = (rows + kSR - 1) / kSR;
+    int* ssl = reinterpret_cast<int*>(tail);
+    tail += sizeof(int) * ((A.stage_slices[h] + 3) & ~int64_t(3));
+    int* sln = reinterpret_cast<int*>(tail);
+    tail += sizeof(int) * ((A.stage_rows[h] + 3) & ~int64_t(3));
     VT* sv = reinterpret_cast<VT*>(tail);
     tail += sizeof(VT) * ((A.stage_ent[h] + 3) & ~int64_t(3));
     uint32_t* si = reinterpret_cast<uint32_t*>(tail);
     tail += sizeof(uint32_t) * ((A.stage_ent[h] + 3) & ~int64_t(3));
-    for (int64_t k = threadIdx.x; k <= r1 - r0; k += blockDim.x) sp[k] = A.ptr[h][r0 + k] - e0;
-    for (long long k = threadIdx.x; k < e1 - e0; k += blockDim.x) {
-      sv[k] = A.val[h][e0 + k];
-      si[k] = A.idx[h][e0 + k];
+    const long long* gp = A.ptr[h];
+    for (int64_t k = threadIdx.x; k < ns; k += blockDim.x) ssl[k] = A.sbase[h][A.soff[h][rank] + k];
+    for (int64_t k = threadIdx.x; k < rows; k += blockDim.x) sln[k] = (int)(gp[r0 + k + 1] - gp[r0 + k]);
+    __syncthreads();
+    // scatter: row li's entry e goes to step e / kSG of lane (li % kSR) kSG + e % kSG
+    for (int64_t li = threadIdx.x >> 5; li < rows; li += blockDim.x >> 5) {
+      const int bse = ssl[li / kSR] + (int)(li % kSR) * kSG;
+      const long long e0 = gp[r0 + li];
+      for (int e = (int)(threadIdx.x & 31); e < sln[li]; e += 32) {
+        const int dst = bse + (e / kSG) * 32 + (e % kSG);
+        sv[dst] = A.val[h][e0 + e];
+        si[dst] = A.idx[h][e0 + e];
+      }
     }
-    ptr[h] = sp;
+    sl[h] = ssl;
+    ln[h] = sln;
     idx[h] = si;
     val[h] = sv;
-    rbase[h] = r0;
   }
   __shared__ double scratch[32];
-  __shared__ long long mscratch[32];
+  __shared__ int mscratch[32];
+  __shared__ double comb_e[2];  // per half: the cluster's combined partials
+  __shared__ long long comb_m[2];
+  __shared__ unsigned long long comb_f[2];
   __shared__ unsigned long long flag_sh[2];
-  __shared__ long long masks_sh;
-  __shared__ double xe[2][CS];  // per half: every CTA's partials, slot = its rank
-  __shared__ long long xm[2][CS];
-  __shared__ unsigned long long xf[2][CS];
+  // per half: every peer's partials {residual (lo, hi), masks, first failing
+  // atom or ~0}, slot = its rank (the own slot stays in registers)
+  static_assert(CS <= kThreads / 32, "one sending warp per peer");
+  __shared__ uint4 xs[2][CS];
   __shared__ __align__(8) uint64_t mbar[2];  // per half: the peers' st.async bytes
+  __shared__ unsigned long long trace_sh[8 * 2 * kTraceSlots];  // SPK_TRACE_SMALL stamps, copied out at the end
+  if (A.trace)
+    for (int k = threadIdx.x; k < 8 * 2 * kTraceSlots; k += blockDim.x) trace_sh[k] = 0ull;
   const double on = LOG ? 0.0 : 1.0, off = LOG ? -CUDART_INF : 0.0;
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {  // u = v = 1 on covered atoms (:277-281, :424-428)
     X[0][i] = A.ne[0][i] ? on : off;
@@ -262,11 +302,14 @@ __global__ void __launch_bounds__(kThreads, 1) cluster_loop_kernel(ClusterArgs<V
   uint32_t rx_bytes[2] = {0u, 0u};
   for (int h = 0; h < 2; ++h)
     for (int r = 0; r < CS; ++r)
-      if (r != (int)rank) rx_bytes[h] += (uint32_t)(slab_bytes(A.lo[h][r], A.lo[h][r + 1]) + 24);
+      if (r != (int)rank) rx_bytes[h] += (uint32_t)(slab_bytes(A.lo[h][r], A.lo[h][r + 1]) + 16);
   if (CS > 1) cluster_barrier();  // peers' vectors and barriers initialised before any remote store
   else __syncthreads();
+  unsigned long long clock0 = 0;  // SPK_TRACE_SMALL: common origin of the CTAs' clocks
+  if (A.trace) asm volatile("mov.u64 %0, %%clock64;" : "=l"(clock0));
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5, gl = lane & (kSG - 1);
+  const bool need_err = A.delta >= 0.0;  // eu + ev <= delta can only hold for delta >= 0
   long long mr = A.masked0[0], mc = A.masked0[1];
   long long t = 0;
   int converged = 0, diverged = 0, ekind = 0, ehalf = 0, dhalf = 0;
@@ -283,10 +326,12 @@ __global__ void __launch_bounds__(kThreads, 1) cluster_loop_kernel(ClusterArgs<V
   // received all of this CTA's values of the following half, i.e. after this
   // CTA stopped reading it.
   auto stamp = [&](int h, int k) {
-    if (A.trace && t <= 8 && threadIdx.x == 0) {
+    if (A.trace && t > A.trace_t0 && t <= A.trace_t0 + 8 && threadIdx.x == 0) {
       unsigned long long g;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
-      A.trace[(((t - 1) * 2 + h) * CS + rank) * 5 + k] = g;
+      asm volatile("mov.u64 %0, %%clock64;" : "=l"(g));
+      trace_sh[((t - 1 - A.trace_t0) * 2 + h) * kTraceSlots + k] = g - clock0;  // shared: no global store in flight
+      // (%globaltimer reads cost ~0.5 us each here: SM clocks only, aligned
+      // across the cluster by the clock each CTA read leaving the first cluster barrier)
     }
   };
   auto half = [&](int h, double& err_all, long long& masks_all, unsigned long long& flag_all) {
@@ -306,45 +351,53 @@ __global__ void __launch_bounds__(kThreads, 1) cluster_loop_kernel(ClusterArgs<V
       const double old = in ? out[i] : 0.0;
       if (in && gl == 0) prev[h][i - r0] = old;
       const bool live = in && ne_s[h][i];  // structurally empty / masked: keeps its value
-      int b = 0, e = 0;  // share-relative entry offsets (a share holds < 2^31 entries)
+      int b = 0, cnt = 0;  // lane's first staged entry (a share holds < 2^31), its entry count
       if (live) {
-        const int li = (int)(i - rbase[h]);
-        b = (int)ptr[h][li];
-        e = (int)ptr[h][li + 1];
+        const int li = (int)(i - r0), len = ln[h][li];
+        b = sl[h][li / kSR] + lane;
+        cnt = len > gl ? (len - gl + kSG - 1) / kSG : 0;
       }
-      const double tmp = group_dot<LOG, VT>(val[h], idx[h], b, e, x, gl);
+      const double tmp = group_dot<LOG, VT>(val[h], idx[h], b, cnt, x);
       if (live && gl == 0)
         err += finalize_atom<LOG>(i, tmp, old, w_s[h][i], A.exponent, A.policy, (int)t, ne_s[h], dyn_s[h], out,
                                   &flag_sh[h], masks);
     }
-    err = warp_sum(err);
-    masks = warp_sum_ll(masks);
+    // the residual only feeds the delta stop: no reductions when it is off
+    if (need_err) err = warp_sum(err);
+    const int wm = (int)__reduce_add_sync(0xffffffffu, (unsigned)masks);
     if (lane == 0) {
       scratch[warp] = err;
-      mscratch[warp] = masks;
+      mscratch[warp] = wm;
     }
     __syncthreads();
     stamp(h, 1);
-    if (warp == 0) {  // CTA partials (fixed shuffle tree) into slot [rank] of every CTA
-      double e = lane < nw ? scratch[lane] : 0.0;
-      long long m = lane < nw ? mscratch[lane] : 0;
-      e = warp_sum(e);
-      m = warp_sum_ll(m);
-      const unsigned long long f = flag_sh[h];
-      __syncwarp();
-      if (lane == (int)rank) {
-        xe[h][rank] = e;
-        xm[h][rank] = m;
-        xf[h][rank] = f;
-      } else if (CS > 1 && lane < CS) {
-        // this CTA's slab of the new vector to peer `lane` as ONE bulk copy
-        // (shared -> peer shared, completing bytes on the peer's mbarrier;
-        // the fence makes the CTA's generic stores visible to the async proxy),
-        // then the partials as three 8-byte st.async on the same mbarrier
-        const uint32_t pr = (uint32_t)lane, rb = map_cluster(bar_h, pr);
+    // CTA partials (fixed shuffle tree: every warp gets the same values) and
+    // the transfers: warp w serves peer w -- ONE bulk copy of this CTA's slab
+    // of the new vector (shared -> peer shared, completing bytes on the peer's
+    // mbarrier; the fence makes the CTA's generic stores visible to the async
+    // proxy) and ONE 16-byte st.async of the partials on the same mbarrier.
+    double own_e = 0.0;
+    int own_m = 0;
+    unsigned own_f = 0xffffffffu;
+    if (warp < CS) {
+      double e = (need_err && lane < nw) ? scratch[lane] : 0.0;
+      if (need_err) e = warp_sum(e);
+      const int m = (int)__reduce_add_sync(0xffffffffu, lane < nw ? (unsigned)mscratch[lane] : 0u);
+      const unsigned long long f64 = flag_sh[h];
+      const unsigned f = f64 == kNone ? 0xffffffffu : (unsigned)f64;  // atom index < 2^31
+      stamp(h, 8);
+      if (warp == 0) {  // the combining warp keeps the CTA's own slot in registers
+        own_e = e;
+        own_m = m;
+        own_f = f;
+      }
+      if (warp != (int)rank) {
+        const uint32_t pr = (uint32_t)warp, rb = map_cluster(bar_h, pr);
         const uint32_t bytes = (uint32_t)slab_bytes(r0, r1);
-        if (bytes) {
+#if SPK_SMALL_BULK
+        if (lane == 0 && bytes) {
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          stamp(h, 9);
           const uint32_t src = smem_u32(out + r0);
           asm volatile(
               "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -352,31 +405,60 @@ __global__ void __launch_bounds__(kThreads, 1) cluster_loop_kernel(ClusterArgs<V
               "r"(src), "r"(bytes), "r"(rb)
               : "memory");
         }
-        st_async_b64(map_cluster(smem_u32(&xe[h][rank]), pr), (unsigned long long)__double_as_longlong(e), rb);
-        st_async_b64(map_cluster(smem_u32(&xm[h][rank]), pr), (unsigned long long)m, rb);
-        st_async_b64(map_cluster(smem_u32(&xf[h][rank]), pr), f, rb);
+#else
+        // the slab as 16-byte remote stores, one per lane and step (the TMA
+        // path serialises the CTA's CS - 1 small bulk copies: ~1.7 us a half)
+        const uint32_t dst = map_cluster(smem_u32(out + r0), pr);
+        const uint4* src = reinterpret_cast<const uint4*>(out + r0);
+        for (uint32_t c = (uint32_t)lane; c < bytes / 16u; c += 32u) {
+          const uint4 v = src[c];
+          asm volatile(
+              "st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
+                  dst + 16u * c),
+              "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "r"(rb)
+              : "memory");
+        }
+#endif
+        if (lane == 0)
+          asm volatile(
+              "st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
+                  map_cluster(smem_u32(&xs[h][rank]), pr)),
+              "r"((unsigned)__double2loint(e)), "r"((unsigned)__double2hiint(e)), "r"((unsigned)m), "r"(f), "r"(rb)
+              : "memory");
       }
-      if (lane == 0) flag_sh[h] = kNone;  // recycled for this half's next iteration
     }
     stamp(h, 2);
     // every peer's values and partials of this half have landed: one warp
     // waits (CTA-scope acquire: the data is in this CTA's shared memory; a
     // cluster-scope acquire would invalidate L1 on every poll), the barrier
     // below publishes the completion -- and this CTA's own stores -- to all
-    if (CS > 1 && warp == 0) {
-      if (!mbar_wait_s(&mbar[h], (parity >> h) & 1u)) faulted = true;
+    // The same warp then combines the CS slots (a fixed butterfly over lanes
+    // 0..CS-1: identical sums on every CTA) and publishes them with the barrier.
+    if (warp == 0) {
+      if (CS > 1 && !mbar_wait_s(&mbar[h], (parity >> h) & 1u)) faulted = true;
+      const uint4 sl = (lane < CS && lane != (int)rank) ? xs[h][lane] : make_uint4(0u, 0u, 0u, 0xffffffffu);
+      double e = lane == (int)rank ? own_e : need_err ? __hiloint2double((int)sl.y, (int)sl.x) : 0.0;
+      int m = lane == (int)rank ? own_m : (int)sl.z;
+      unsigned f = lane == (int)rank ? own_f : sl.w;
+#pragma unroll
+      for (int o = 1; o < CS; o <<= 1) {
+        if (need_err) e += __shfl_xor_sync(0xffffffffu, e, o);
+        m += __shfl_xor_sync(0xffffffffu, m, o);
+        f = min(f, __shfl_xor_sync(0xffffffffu, f, o));
+      }
+      if (lane == 0) {
+        comb_e[h] = e;
+        comb_m[h] = m;
+        comb_f[h] = f == 0xffffffffu ? kNone : (unsigned long long)f;
+      }
     }
     parity ^= 1u << h;
     __syncthreads();
     stamp(h, 3);
-    err_all = 0.0;
-    masks_all = 0;
-    flag_all = kNone;
-    for (int r = 0; r < CS; ++r) {  // rank order: the same sums on every CTA
-      err_all += xe[h][r];
-      masks_all += xm[h][r];
-      flag_all = min(flag_all, xf[h][r]);
-    }
+    if (threadIdx.x == 0) flag_sh[h] = kNone;  // every warp has read it: recycled for the next pass of this half
+    err_all = comb_e[h];
+    masks_all = comb_m[h];
+    flag_all = comb_f[h];
     stamp(h, 4);
   };
   auto restore = [&](int h) {  // previous iterate of this CTA's atoms (every CTA restores its own)
@@ -441,6 +523,9 @@ __global__ void __launch_bounds__(kThreads, 1) cluster_loop_kernel(ClusterArgs<V
       A.out[h][i] = X[h][i];
       A.dyn[h][i] = dyn_s[h][i];
     }
+  if (A.trace)
+    for (int k = threadIdx.x; k < 8 * 2 * kTraceSlots; k += blockDim.x)
+      A.trace[((k / kTraceSlots) * CS + rank) * kTraceSlots + k % kTraceSlots] = trace_sh[k];
   if (CS > 1) cluster_barrier();  // no CTA leaves while a peer may still read its Xch
   if (threadIdx.x == 0 && rank == 0) {
     loopcore::Status* s = A.status;
@@ -507,7 +592,7 @@ bool run_cluster_t(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, doub
   const int64_t n = sk->n;
   int optin = 0;
   SPK_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
-  const size_t budget = (size_t)optin - 2048;  // static shared use
+  const size_t budget = (size_t)optin - 4096;  // static shared use
   const int npad = (int)((n + 31) & ~int64_t(31));
   std::vector<long long> rp(n + 1), cp(n + 1);
   download(ctx, rp.data(), sk->row_ptr, sizeof(long long) * (n + 1));
@@ -515,34 +600,49 @@ bool run_cluster_t(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, doub
   ClusterArgs<VT> A{};
   int CS = 0;
   size_t smem = 0;
+  std::vector<int> sb[2];  // slice bases of the chosen split
   for (int cs : {ctx->small_cluster, 8, 4, 2, 1}) {  // largest cluster first; stage the sketch when it fits
     if (cs < 1 || cs > kMaxCS || (cs & (cs - 1))) continue;
     ClusterArgs<VT> B{};
     split_by_entries(rp, n, cs, B.lo[0]);
     split_by_entries(cp, n, cs, B.lo[1]);
-    int64_t own[2] = {0, 0}, ent[2] = {0, 0};
+    int64_t own[2] = {0, 0}, ent[2] = {0, 0}, nsl[2] = {0, 0};
+    std::vector<int> bases[2];
     for (int h = 0; h < 2; ++h) {
       const std::vector<long long>& p = h ? cp : rp;
       for (int r = 0; r < cs; ++r) {
-        own[h] = std::max(own[h], B.lo[h][r + 1] - B.lo[h][r]);
-        ent[h] = std::max<int64_t>(ent[h], p[B.lo[h][r + 1]] - p[B.lo[h][r]]);
+        const int64_t r0 = B.lo[h][r], r1 = B.lo[h][r + 1];
+        own[h] = std::max(own[h], r1 - r0);
+        B.soff[h][r] = (int64_t)bases[h].size();
+        int64_t acc = 0;  // padded entries of the share: every slice takes its longest row's steps x 32
+        for (int64_t s0 = r0; s0 < r1; s0 += kSR) {
+          long long steps = 0;
+          for (int64_t i = s0; i < std::min(r1, s0 + kSR); ++i) steps = std::max(steps, (p[i + 1] - p[i] + kSG - 1) / kSG);
+          bases[h].push_back((int)acc);
+          acc += 32 * steps;
+        }
+        ent[h] = std::max(ent[h], acc);
+        nsl[h] = std::max<int64_t>(nsl[h], (int64_t)bases[h].size() - B.soff[h][r]);
       }
+      B.soff[h][cs] = (int64_t)bases[h].size();
     }
     size_t base = sizeof(double) * (2 * (size_t)npad + ((own[0] + 1) & ~1) + ((own[1] + 1) & ~1));
     for (int h = 0; h < 2; ++h)
       base += sizeof(int) * ((own[h] + 3) & ~3) + ((own[h] + 15) & ~15) + sizeof(double) * ((own[h] + 1) & ~1);
     size_t staged = 0;
     for (int h = 0; h < 2; ++h)
-      staged += sizeof(long long) * ((own[h] + 2) & ~1) + (sizeof(VT) + 4) * ((ent[h] + 3) & ~3);
+      staged += sizeof(int) * (((nsl[h] + 3) & ~3) + ((own[h] + 3) & ~3)) + (sizeof(VT) + 4) * ((ent[h] + 3) & ~3);
     // the cluster's SMs win only while the sketch lives in their shared memory:
     // streamed from L2 by <= 16 SMs it loses to the whole-GPU grid loop
-    if (base + staged > budget) continue;
+    if (ent[0] >= (1ll << 31) || ent[1] >= (1ll << 31) || base + staged > budget) continue;
     B.stage = 1;
-    B.stage_ent[0] = ent[0];
-    B.stage_ent[1] = ent[1];
-    B.stage_rows[0] = own[0];
-    B.stage_rows[1] = own[1];
-    smem = base + (B.stage ? staged : 0);
+    for (int h = 0; h < 2; ++h) {
+      B.stage_ent[h] = ent[h];
+      B.stage_rows[h] = own[h];
+      B.stage_slices[h] = nsl[h];
+      sb[h] = std::move(bases[h]);
+    }
+    smem = base + staged;
     A = B;
     CS = cs;
     break;
@@ -601,10 +701,18 @@ bool run_cluster_t(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, doub
   A.masked0[0] = sk->cov_empty_rows;
   A.masked0[1] = sk->cov_empty_cols;
   A.npad = npad;
+  {  // slice bases of both halves in one buffer
+    std::vector<int> all(sb[0]);
+    all.insert(all.end(), sb[1].begin(), sb[1].end());
+    upload(ctx, W.slices, all.data(), sizeof(int) * all.size());
+    A.sbase[0] = W.slices.as<int>();
+    A.sbase[1] = W.slices.as<int>() + sb[0].size();
+  }
   DBuf trace;
   const bool tracing = std::getenv("SPK_TRACE_SMALL") != nullptr;
+  if (tracing) A.trace_t0 = std::max(0ll, std::atoll(std::getenv("SPK_TRACE_SMALL")));
   if (tracing) {
-    trace.alloc(sizeof(unsigned long long) * 8 * 2 * kMaxCS * 5);
+    trace.alloc(sizeof(unsigned long long) * 8 * 2 * kMaxCS * kTraceSlots);
     SPK_CUDA(cudaMemsetAsync(trace.p, 0, trace.bytes, s));
     A.trace = trace.as<unsigned long long>();
   }
@@ -624,23 +732,58 @@ bool run_cluster_t(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, doub
   loopcore::Status S;
   download(ctx, &S, W.status, sizeof S);
   if (S.error_kind == SPK_E_DEVICE) fail_device("small loop: a peer's st.async transfer timed out", cudaErrorLaunchTimeout);
-  if (tracing) {  // per-phase means over iterations 2..8 (ns): rows, partials, barrier, combine; half length
-    std::vector<unsigned long long> tr(8 * 2 * kMaxCS * 5);
+  if (tracing) {  // per-phase mean SM cycles over iterations 2..8 (thread 0 of every CTA)
+    std::vector<unsigned long long> tr(8 * 2 * kMaxCS * kTraceSlots);
     download(ctx, tr.data(), trace, sizeof(unsigned long long) * tr.size());
-    double ph[5] = {0, 0, 0, 0, 0};
+    double ph[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    int cnt9 = 0;
     int cnt = 0;
-    for (int it = 1; it < 8 && it < S.iterations; ++it)
+    for (int it = 1; it < 8 && it + A.trace_t0 < S.iterations; ++it)
       for (int h = 0; h < 2; ++h)
         for (int r = 0; r < CS; ++r) {
-          const unsigned long long* q = &tr[(((size_t)it * 2 + h) * CS + r) * 5];
+          const unsigned long long* q = &tr[(((size_t)it * 2 + h) * CS + r) * kTraceSlots];
           for (int k = 0; k < 4; ++k) ph[k] += (double)(q[k + 1] - q[k]);
-          const unsigned long long* nx = &tr[(((size_t)it * 2 + h) * CS + 0) * 5];
-          ph[4] += (double)(q[4] - nx[0]);
+          ph[8] += (double)(q[8] - q[1]);  // CTA partial reductions
+          if (q[9]) {
+            ph[9] += (double)(q[9] - q[8]);  // proxy fence
+            ++cnt9;
+          }
           ++cnt;
         }
+    for (int h = 0; h < 2; ++h) {  // per-rank row pass and stamp-0 skew (iterations 2..8)
+      std::fprintf(stderr, "SPK_TRACE_SMALL half %d rows/start-skew per rank:", h);
+      for (int r = 0; r < CS; ++r) {
+        double rows = 0, skew = 0;
+        int c = 0;
+        for (int it = 1; it < 8 && it + A.trace_t0 < S.iterations; ++it, ++c) {
+          const unsigned long long* q = &tr[(((size_t)it * 2 + h) * CS + r) * kTraceSlots];
+          rows += (double)(q[1] - q[0]);
+          skew += (double)(q[3] - q[2]);
+        }
+        if (c) std::fprintf(stderr, " %.0f/%.0f", rows / c, skew / c);
+      }
+      std::fprintf(stderr, "\n");
+    }
+    for (int h = 0; h < 2; ++h) {  // cluster timeline of one half (cycles after the earliest start), iterations 2..8
+      std::fprintf(stderr, "SPK_TRACE_SMALL half %d timeline per rank [start rows-done sent peers-in combined]:", h);
+      for (int r = 0; r < CS; ++r) {
+        double ph2[5] = {0, 0, 0, 0, 0};
+        int c = 0;
+        for (int it = 1; it < 8 && it + A.trace_t0 < S.iterations; ++it, ++c) {
+          unsigned long long t0 = ~0ull;
+          for (int r2 = 0; r2 < CS; ++r2) t0 = std::min(t0, tr[(((size_t)it * 2 + h) * CS + r2) * kTraceSlots]);
+          const unsigned long long* q = &tr[(((size_t)it * 2 + h) * CS + r) * kTraceSlots];
+          for (int k = 0; k < 5; ++k) ph2[k] += (double)(q[k] - t0);
+        }
+        if (c) std::fprintf(stderr, " r%d[%.0f %.0f %.0f %.0f %.0f]", r, ph2[0] / c, ph2[1] / c, ph2[2] / c, ph2[3] / c, ph2[4] / c);
+      }
+      std::fprintf(stderr, "\n");
+    }
     if (cnt)
-      std::fprintf(stderr, "SPK_TRACE_SMALL CS=%d: rows %.0f ns, partials %.0f ns, peer wait %.0f ns, combine %.0f ns\n",
-                   CS, ph[0] / cnt, ph[1] / cnt, ph[2] / cnt, ph[3] / cnt);
+      std::fprintf(stderr,
+                   "SPK_TRACE_SMALL CS=%d (cycles): rows %.0f, partials %.0f [reduce %.0f fence %.0f], peer wait %.0f, "
+                   "combine %.0f\n",
+                   CS, ph[0] / cnt, ph[1] / cnt, ph[8] / cnt, cnt9 ? ph[9] / cnt9 : 0.0, ph[2] / cnt, ph[3] / cnt);
   }
   loopcore::loop_epilogue<LOG>(ctx, S, n, W, A.out[0], A.out[1], st, out);
   return true;
