@@ -55,7 +55,13 @@ constexpr int kNW = 15;                 // consumer warps per CTA (+1 producer =
 constexpr int kThreadsBlocked = 32 * (kNW + 1);
 constexpr int kTileW = 4096;            // x tile: 32 KB of fp64
 constexpr int kGE = 128;                // entries per group (4 chunks; one 16-byte load per lane)
-constexpr uint32_t kPad = 0xffffffffu;  // padding entry (never a valid packed value)
+// Packed key of an entry: row_local << 16 | kNewBlock? | col_local, bits 13-15
+// zero (so key >> 13 is the byte offset of the row's fp64 accumulator).
+constexpr uint32_t kNewBlock = 0x1000u;  // this chunk is the first of the next column block
+constexpr uint32_t kColMask = 0x0fffu;
+// Padding entries (value 0) add into sink rows max_rows .. max_rows + 15 of the half: one per bank pair, so a
+// pad can take a bank class its half-chunk does not use.
+constexpr int kSinkRows = 16;
 
 // ---- PTX helpers: mbarrier + 1-D bulk copy (TMA) ------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -114,6 +120,18 @@ __device__ __forceinline__ void cp_async_wait_group() {
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async;" ::: "memory"); }
 __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+
+// Shared-memory fp64 accesses by 32-bit shared address: the accumulator and
+// tile bases stay in registers (the generic-pointer form re-derived the
+// shared window base, an S2UR and its wait, for every chunk).
+__device__ __forceinline__ double lds_f64(uint32_t a) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts_f64(uint32_t a, double v) {
+  asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
+}
 
 __device__ __forceinline__ void record_fault(unsigned int* fault, unsigned int code) {
   if (atomicCAS(fault, 0u, code) == 0u) fault[1] = blockIdx.x;
@@ -185,7 +203,7 @@ struct BlockedOp {
   unsigned long long* trace;  // SPK_TRACE_BLOCKED: globaltimer stamps of the first 4 iterations
   bool fresh;                 // one launch per half (sharded): initialise the barriers on every call
 
-  __host__ __device__ size_t head_bytes() const { return align16((size_t)(acc_rows + 1) * 8) + 128; }
+  __host__ __device__ size_t head_bytes() const { return align16((size_t)(acc_rows + kSinkRows) * 8) + 128; }
   size_t smem_bytes() const { return head_bytes() + (size_t)STG * kTileW * 8; }
 
   __device__ __forceinline__ static double value(const Group<VT>& g, int k) {
@@ -204,12 +222,28 @@ struct BlockedOp {
   // lane adds its product straight into its row's accumulator. A row's
   // entries arrive in column order (earlier chunks, earlier blocks), so each
   // row is summed like the reference's spmv / spmv_t loop
-  // (sparsify.cpp:203-226): acc += v * x, no FMA.
-  __device__ __forceinline__ static void fold(uint32_t u, double v, const double* xs, double* acc, uint32_t arows) {
-    // padding (u = kPad, v = 0) lands in the sink row acc[acc_rows], never read
-    const uint32_t rl = min(u >> 16, arows);
-    acc[rl] = __dadd_rn(acc[rl], __dmul_rn(v, xs[u & (kTileW - 1)]));
+  // (sparsify.cpp:203-226): acc += v * x, no FMA. Padding (v = 0) carries
+  // the half's sink row (its max_rows), never read.
+  __device__ __forceinline__ static void fold(uint32_t u, double v, uint32_t xs_s, uint32_t acc_s) {
+    const double p = __dmul_rn(v, lds_f64(xs_s + ((u & kColMask) << 3)));
+    const uint32_t a = acc_s + (u >> 13);
+    sts_f64(a, __dadd_rn(lds_f64(a), p));
     __syncwarp();  // the next chunk may revisit a row through another lane
+  }
+  // Four chunks inside one column block: the x gathers do not depend on the
+  // accumulators, so all four are issued before the read-modify-write chain.
+  __device__ __forceinline__ static void fold4(const Group<VT>& g, uint32_t xs_s, uint32_t acc_s) {
+    double p[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) p[k] = lds_f64(xs_s + ((key(g, k) & kColMask) << 3));
+#pragma unroll
+    for (int k = 0; k < 4; ++k) p[k] = __dmul_rn(value(g, k), p[k]);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t a = acc_s + (key(g, k) >> 13);
+      sts_f64(a, __dadd_rn(lds_f64(a), p[k]));
+      __syncwarp();
+    }
   }
 
   __device__ __forceinline__ void load_group(const uint32_t* gk, const VT* gv, int g, int lane, uint64_t pol,
@@ -230,7 +264,7 @@ struct BlockedOp {
                        double& err, long long& masks) const {
     extern __shared__ __align__(128) unsigned char dsm[];
     double* acc = reinterpret_cast<double*>(dsm);
-    uint64_t* full = reinterpret_cast<uint64_t*>(dsm + align16((size_t)(acc_rows + 1) * 8));
+    uint64_t* full = reinterpret_cast<uint64_t*>(dsm + align16((size_t)(acc_rows + kSinkRows) * 8));
     uint64_t* empty = full + STG;
     uint32_t* ph = reinterpret_cast<uint32_t*>(empty + STG);  // phases completed per stage
     double* tiles = reinterpret_cast<double*>(dsm + head_bytes());
@@ -258,8 +292,13 @@ struct BlockedOp {
       }
       fence_mbar_init();
     }
-    unsigned long long* tr = (trace && t <= 4) ? trace + (((size_t)(t - 1) * 2 + ROLE) * gridDim.x + cta) * 20 : nullptr;
-    if (tr && threadIdx.x == 0) tr[0] = globaltimer();
+    unsigned long long* tr = (trace && t <= 4) ? trace + (((size_t)(t - 1) * 2 + ROLE) * gridDim.x + cta) * 24 : nullptr;
+    if (tr && threadIdx.x == 0) {
+      tr[0] = globaltimer();
+      unsigned smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      tr[20] = smid;
+    }
     for (int r = threadIdx.x; r < nrows; r += blockDim.x) acc[r] = 0.0;
     __syncthreads();
     // bit s: parity of the next phase of stage s; flipped after every wait on it
@@ -295,65 +334,77 @@ struct BlockedOp {
       // 4 chunks in flight in registers ahead of the group being folded ----
       const long long* ofs = H.off + ((int64_t)cta * kNW + w) * (H.Bh + 1);  // block starts; [nb] = stream end
       const long long sbeg = ofs[0];
-      const int nch = (int)((ofs[nb] - sbeg) >> 5);  // chunks in the stream
-      const int ngroups = (nch + 3) >> 2;
+      // every block holds at least one chunk and streams are padded to whole
+      // groups, so the stream is a whole number of groups
+      const int ngroups = (int)((ofs[nb] - sbeg + kGE - 1) / kGE);
       const uint32_t* gk = H.packed + sbeg;
       const VT* gv = gval + sbeg;
       const uint64_t pol = evict_first_policy();
-      // Loads are unconditional (clamped to the last group: streams are padded
-      // to whole groups) so no predicated register merge forces a wait.
+      // Loads are unconditional (clamped to the last group) so no predicated
+      // register merge forces a wait.
       const int glast = max(ngroups - 1, 0);
-      Group<VT> R[kDepth];
+      // Two register sets of kDepth groups. ptxas tracks every streaming load
+      // on one scoreboard, so any wait is a wait for ALL loads in flight: the
+      // loads of set B are therefore issued only once set A has landed (their
+      // addresses carry a zero derived from A's keys) and stay in flight
+      // while A is folded -- one exposed wait per 4 * kDepth chunks.
+      Group<VT> A[kDepth], Bq[kDepth];
 #pragma unroll
-      for (int d = 0; d < kDepth; ++d) load_group(gk, gv, min(d, glast), lane, pol, R[d]);
-      int cb = 0, cs = 0;  // current block and its stage
-      int cb_end = (int)((ofs[1] - sbeg) >> 5);
-      int cb_next = (int)((ofs[nb > 1 ? 2 : 1] - sbeg) >> 5);  // next boundary, loaded one transition early
-      const double* xs = tiles;  // tile of the current block
-      if (!mbar_wait(&full[0], pmask & 1u, fault)) record_fault(fault, 0x20000000u | ((unsigned)ROLE << 24));
-      pmask ^= 1u;
-      const uint32_t arows = (uint32_t)acc_rows;
-      for (int g0 = 0; g0 < ngroups; g0 += kDepth) {
-#pragma unroll
-        for (int d = 0; d < kDepth; ++d) {
-          const int g = g0 + d;
-          const Group<VT> cur = R[d];
-          load_group(gk, gv, min(g + kDepth, glast), lane, pol, R[d]);
-          if (g < ngroups) {  // warp-uniform
-            const int c0 = 4 * g;
-            if (c0 + 4 <= cb_end && c0 + 4 <= nch) {
-              // the whole group lies inside the current block: no boundary checks
-#pragma unroll
-              for (int k = 0; k < 4; ++k) fold(key(cur, k), value(cur, k), xs, acc, arows);
-            } else {
-#pragma unroll
-              for (int k = 0; k < 4; ++k) {
-                const int c = c0 + k;
-                if (c < nch) {  // warp-uniform
-                  while (c >= cb_end && cb + 1 < nb) {  // release tile cb, enter the next
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&empty[cs]);
-                    ++cb;
-                    cs = cs + 1 == STG ? 0 : cs + 1;
-                    cb_end = cb_next;
-                    cb_next = (int)((ofs[min(cb + 2, nb)] - sbeg) >> 5);
-                    xs = tiles + (size_t)cs * kTileW;
-                    if (!mbar_wait(&full[cs], (pmask >> cs) & 1u, fault))
-                      record_fault(fault, 0x30000000u | ((unsigned)ROLE << 24) | (unsigned)cb);
-                    pmask ^= 1u << cs;
-                  }
-                  fold(key(cur, k), value(cur, k), xs, acc, arows);
-                }
-              }
-            }
-          }
+      for (int d = 0; d < kDepth; ++d) load_group(gk, gv, min(d, glast), lane, pol, A[d]);
+      // Block boundaries travel in the stream itself: every entry (and pad) of a
+      // block's first chunk carries kNewBlock, so entering the next x tile
+      // costs no dependent global load.
+      int cb = -1, cs = STG - 1;  // current block and its stage
+      const uint32_t acc_s = smem_u32(acc);
+      const uint32_t tiles_s = smem_u32(tiles);
+      uint32_t xs_s = tiles_s;  // tile of the current block
+      auto run_group = [&](const Group<VT>& cur) {
+        if (((cur.k.x | cur.k.y | cur.k.z | cur.k.w) & kNewBlock) == 0) {  // warp-uniform
+          fold4(cur, xs_s, acc_s);
+          return;
         }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint32_t u = key(cur, k);
+          if (u & kNewBlock) {  // warp-uniform: release tile cb, enter the next
+            __syncwarp();
+            if (cb >= 0 && lane == 0) mbar_arrive(&empty[cs]);
+            ++cb;
+            cs = cs + 1 == STG ? 0 : cs + 1;
+            xs_s = tiles_s + (uint32_t)cs * (kTileW * 8);
+            if (!mbar_wait(&full[cs], (pmask >> cs) & 1u, fault))
+              record_fault(fault, 0x30000000u | ((unsigned)ROLE << 24) | (unsigned)cb);
+            pmask ^= 1u << cs;
+          }
+          fold(u, value(cur, k), xs_s, acc_s);
+        }
+      };
+      auto landed = [&](const Group<VT>* G) -> int {  // 0 once the set's keys are in registers
+        uint32_t o = 0;
+#pragma unroll
+        for (int d = 0; d < kDepth; ++d) o |= G[d].k.x;
+        return (int)((o >> 13) & 7u);  // bits 13-15 of a key are zero
+      };
+      for (int g0 = 0; g0 < ngroups; g0 += 2 * kDepth) {
+        const int za = landed(A);
+#pragma unroll
+        for (int d = 0; d < kDepth; ++d) load_group(gk, gv, min(g0 + kDepth + d + za, glast), lane, pol, Bq[d]);
+#pragma unroll
+        for (int d = 0; d < kDepth; ++d)
+          if (g0 + d < ngroups) run_group(A[d]);  // warp-uniform
+        const int zb = landed(Bq);
+#pragma unroll
+        for (int d = 0; d < kDepth; ++d) load_group(gk, gv, min(g0 + 2 * kDepth + d + zb, glast), lane, pol, A[d]);
+#pragma unroll
+        for (int d = 0; d < kDepth; ++d)
+          if (g0 + kDepth + d < ngroups) run_group(Bq[d]);
       }
       if (tr && lane == 0) tr[1 + w] = globaltimer();
-      // release the remaining blocks in order (tile present before release)
+      // release the last block; a stream that (against the layout's promise)
+      // ended early still passes through every remaining tile in order
       for (;;) {
         __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[cs]);
+        if (cb >= 0 && lane == 0) mbar_arrive(&empty[cs]);
         if (++cb >= nb) break;
         cs = cs + 1 == STG ? 0 : cs + 1;
         if (!mbar_wait(&full[cs], (pmask >> cs) & 1u, fault))
@@ -618,11 +669,247 @@ __global__ void __launch_bounds__(32 * kSlotWarps) slot_warp_kernel(
     for (int e = lane; e < E; e += 32) newpos[u0 + e] = -1;
 }
 
+
+// ---- chunk placement by edge colouring (option blocked_spread = 1, the default) ----
+// A segment's entries are the edges of a bipartite multigraph: 16 row bank
+// classes (the fp64 accumulator's bank pair, row_local & 15) against 16
+// column bank classes (the x tile's bank pair, col_local & 15). A 64-bit
+// shared access is served per half-warp, one wavefront per distinct address
+// in the busiest bank pair (profiles/microbench/lds64_conflicts.cu), so a
+// half-chunk whose 16 entries form a MATCHING -- distinct row classes and
+// distinct column classes -- costs the ideal 1 + 1 + 1 wavefronts for the x
+// gather, the accumulator load and its store. The H = 2C half-chunks are the
+// colours of an edge colouring: an edge takes a colour free at both its
+// classes; when the two have no common free colour, the a/b alternating path
+// from the column class is flipped (Kempe chain; bipartite, so it cannot end
+// at the row class) and the edge takes a. Only edges of a class with more
+// than H entries stay uncoloured; they (and the few whose flip broke the
+// one-row-once-per-chunk rule) are then dealt to the half-chunk with room
+// where they add the fewest wavefronts. Measured at config 4: 3.8 / 4.05
+// wavefronts per accumulator / gather access with the run-length placement
+// plus greedy column dealing (slot_warp_kernel), ~2.8 / 2.8 with this.
+// One warp per segment; all state in shared memory. newpos[q] = chunk * 32 +
+// lane, or -1 (whole segment) when the segment does not fit this scheme.
+constexpr int kColorWarps = 4;
+constexpr int kColorMaxE = 1024;  // 32 chunks of 32
+struct ColorWs {
+  unsigned short at[32][64];   // edge holding colour h at class x (0-15 rows, 16-31 columns)
+  unsigned short erow[kColorMaxE];
+  unsigned char evert[kColorMaxE];  // row class | column class << 4
+  unsigned char ecol[kColorMaxE];   // colour (half-chunk) or 0xff
+  unsigned char cnt[64][32];        // entries of class x in half-chunk h
+  unsigned char fill[64], rmax[64], cmax[64];
+  unsigned int slot[64];
+};
+__global__ void __launch_bounds__(32 * kColorWarps) color_warp_kernel(
+    int64_t nkeys, const long long* useg, const unsigned long long* cnt, const long long* nchunk, const uint32_t* rl,
+    const unsigned char* colc, const long long* seg_base, uint32_t padrow, int* newpos, uint32_t* packed,
+    unsigned long long* stats) {
+  __shared__ ColorWs ws_all[kColorWarps];
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  const int64_t k = (int64_t)blockIdx.x * kColorWarps + wl;
+  if (k >= nkeys) return;
+  const int E = (int)cnt[k];
+  const int C = (int)nchunk[k];
+  if (E == 0 || C > 32 || E > kColorMaxE) return;
+  const int H = 2 * C;
+  const long long u0 = useg[k];
+  ColorWs& ws = ws_all[wl];
+  const unsigned FULL = 0xffffffffu;
+  for (int i = lane; i < 32 * 64; i += 32) (&ws.at[0][0])[i] = 0xffffu;
+  for (int e = lane; e < E; e += 32) {
+    const uint32_t r = rl[u0 + e];
+    ws.erow[e] = (unsigned short)r;
+    ws.evert[e] = (unsigned char)((r & 15u) | ((uint32_t)colc[u0 + e] << 4));
+    ws.ecol[e] = 0xff;
+  }
+  __syncwarp();
+  // lane x keeps the free colours of class x
+  unsigned long long freec = H == 64 ? ~0ull : ((1ull << H) - 1ull);
+  int st = 37;
+  {
+    const int primes[6] = {37, 41, 43, 47, 53, 59};
+    for (int j = 0; j < 6; ++j)
+      if (E % primes[j]) {
+        st = primes[j];
+        break;
+      }
+  }
+  // colours of the other entries of e's row (a run of the sorted list): their chunks are closed to e
+  auto run_forbidden = [&](int e) -> unsigned long long {
+    unsigned long long forb = 0;
+    const unsigned short r = ws.erow[e];
+    for (int j = e - 1; j >= 0 && ws.erow[j] == r; --j)
+      if (ws.ecol[j] != 0xff) forb |= 3ull << (ws.ecol[j] & 0xfe);
+    for (int j = e + 1; j < E && ws.erow[j] == r; ++j)
+      if (ws.ecol[j] != 0xff) forb |= 3ull << (ws.ecol[j] & 0xfe);
+    return forb;
+  };
+  bool ok = true;
+  int pos = 0;
+  for (int i = 0; i < E && ok; ++i) {
+    const int e = pos;
+    pos += st;
+    while (pos >= E) pos -= E;
+    const int vb = ws.evert[e];
+    const int u = vb & 15, v = 16 + (vb >> 4);
+    const unsigned long long forb = run_forbidden(e);
+    const unsigned long long fu = __shfl_sync(FULL, freec, u) & ~forb;
+    const unsigned long long fv = __shfl_sync(FULL, freec, v) & ~forb;
+    int a;
+    if (fu & fv) {
+      a = __ffsll((long long)(fu & fv)) - 1;
+    } else if (fu && fv) {
+      a = __ffsll((long long)fu) - 1;            // free at u, used at v
+      const int b = __ffsll((long long)fv) - 1;  // free at v, used at u
+      int x = v, c = a, len = 0;
+      unsigned short mine = 0xffffu;
+      for (;;) {
+        const unsigned short f = ws.at[x][c];
+        if (f == 0xffffu) break;
+        if (len >= 32) {
+          ok = false;
+          if (stats && lane == 0) atomicAdd(&stats[2], 1ull);
+          break;
+        }
+        if (lane == len) mine = f;
+        ++len;
+        const int fb = ws.evert[f];
+        const int fu2 = fb & 15, fv2 = 16 + (fb >> 4);
+        x = x == fu2 ? fv2 : fu2;
+        c ^= a ^ b;
+      }
+      if (!ok) break;
+      int oldc = 0, y0 = 0, y1 = 0;
+      if (lane < len) {
+        oldc = ws.ecol[mine];
+        const int fb = ws.evert[mine];
+        y0 = fb & 15;
+        y1 = 16 + (fb >> 4);
+        ws.at[y0][oldc] = 0xffffu;
+        ws.at[y1][oldc] = 0xffffu;
+      }
+      __syncwarp();
+      if (lane < len) {
+        const int newc = oldc ^ a ^ b;
+        ws.at[y0][newc] = mine;
+        ws.at[y1][newc] = mine;
+        ws.ecol[mine] = (unsigned char)newc;
+      }
+      __syncwarp();
+      // v: a freed by the flip (and taken again below), b now used; the path's
+      // far end swaps which of a, b it holds; interior classes hold both
+      if (lane == v) freec &= ~(1ull << b);
+      if (lane == x) freec ^= (1ull << a) | (1ull << b);
+    } else {
+      if (stats && lane == 0) atomicAdd(&stats[4], 1ull);
+      continue;  // a class with more entries than colours: dealt below
+    }
+    if (lane == 0) {
+      ws.ecol[e] = (unsigned char)a;
+      ws.at[u][a] = (unsigned short)e;
+      ws.at[v][a] = (unsigned short)e;
+    }
+    if (lane == u || lane == v) freec &= ~(1ull << a);
+    __syncwarp();
+  }
+  if (ok) {
+    // a flip may have moved an entry into a chunk that already holds its row: evict the later one
+    for (int e = lane; e < E; e += 32) {
+      if (e > 0 && ws.erow[e - 1] == ws.erow[e]) continue;  // run heads only
+      unsigned int chunks = 0;
+      for (int j = e; j < E && ws.erow[j] == ws.erow[e]; ++j) {
+        const int c = ws.ecol[j];
+        if (c == 0xff) continue;
+        if ((chunks >> (c >> 1)) & 1u) {
+          const int vb = ws.evert[j];
+          ws.at[vb & 15][c] = 0xffffu;
+          ws.at[16 + (vb >> 4)][c] = 0xffffu;
+          ws.ecol[j] = 0xff;
+          if (stats) atomicAdd(&stats[5], 1ull);
+        } else {
+          chunks |= 1u << (c >> 1);
+        }
+      }
+    }
+    __syncwarp();
+    for (int i = lane; i < 64 * 32; i += 32) {
+      const int h = i >> 5, x = i & 31;
+      ws.cnt[h][x] = (h < H && ws.at[x][h] != 0xffffu) ? 1 : 0;
+    }
+    __syncwarp();
+    for (int h = lane; h < 64; h += 32) {
+      int f = 0;
+      for (int x = 0; x < 16; ++x) f += ws.cnt[h][x];
+      ws.fill[h] = (unsigned char)f;
+      ws.rmax[h] = ws.cmax[h] = f > 0 ? 1 : 0;
+      ws.slot[h] = 0u;
+    }
+    __syncwarp();
+    for (int e = 0; e < E && ok; ++e) {
+      if (ws.ecol[e] != 0xff) continue;  // warp-uniform
+      const int vb = ws.evert[e];
+      const int u = vb & 15, v = 16 + (vb >> 4);
+      const unsigned long long forb = run_forbidden(e);
+      unsigned int key = 0xffffffffu;
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        const int h = lane + 32 * hh;
+        if (h < H && ws.fill[h] < 16 && !((forb >> h) & 1ull)) {
+          const int d = 2 * (ws.cnt[h][u] + 1 > max(1, (int)ws.rmax[h])) + (ws.cnt[h][v] + 1 > max(1, (int)ws.cmax[h]));
+          key = min(key, ((unsigned)d << 16) | ((unsigned)ws.fill[h] << 8) | (unsigned)h);
+        }
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) key = min(key, __shfl_xor_sync(FULL, key, o));
+      if (key == 0xffffffffu) {
+        ok = false;
+        if (stats && lane == 0) atomicAdd(&stats[3], 1ull);
+        break;
+      }
+      const int h = (int)(key & 255u);
+      if (lane == 0) {
+        ws.ecol[e] = (unsigned char)h;
+        ws.rmax[h] = (unsigned char)max((int)ws.rmax[h], ++ws.cnt[h][u]);
+        ws.cmax[h] = (unsigned char)max((int)ws.cmax[h], ++ws.cnt[h][v]);
+        ++ws.fill[h];
+      }
+      __syncwarp();
+    }
+  }
+  if (stats && lane == 0) atomicAdd(&stats[ok ? 0 : 1], 1ull);
+  if (!ok) {
+    for (int e = lane; e < E; e += 32) newpos[u0 + e] = -1;
+    return;
+  }
+  for (int e = lane; e < E; e += 32) {
+    const int h = ws.ecol[e];
+    const unsigned int sl = atomicAdd(&ws.slot[h], 1u);
+    newpos[u0 + e] = (h >> 1) * 32 + (h & 1) * 16 + (int)sl;
+  }
+  // the free lanes of every half-chunk: padding in row and column classes the half-chunk does not use
+  const int64_t Cg0 = seg_base[k] >> 5;
+  for (int h = lane; h < H; h += 32) {
+    unsigned int usedr = 0, usedc = 0;
+    for (int x = 0; x < 16; ++x) {
+      if (ws.cnt[h][x]) usedr |= 1u << x;
+      if (ws.cnt[h][16 + x]) usedc |= 1u << x;
+    }
+    for (int sl = ws.fill[h]; sl < 16; ++sl) {
+      const int jr = __ffs((int)(~usedr & 0xffffu)) - 1, jc = __ffs((int)(~usedc & 0xffffu)) - 1;
+      usedr |= 1u << jr;
+      usedc |= 1u << jc;
+      const uint32_t row = padrow + (((uint32_t)jr - padrow) & 15u);
+      packed[pos_packed(Cg0 + (h >> 1), (h & 1) * 16 + sl)] = (row << 16) | (uint32_t)jc | (h < 2 ? kNewBlock : 0u);
+    }
+  }
+}
+
 template <class VT>
 __global__ void place_kernel(const uint32_t* keys_s, const uint32_t* perm, const uint32_t* rl, const uint32_t* start,
                              const uint32_t* runlen, const long long* useg, const long long* seg_base,
                              const long long* nchunk, const uint32_t* idx, const VT* val, int W, int64_t m,
-                             const int* newpos, uint32_t* packed, VT* vout) {
+                             const int* newpos, bool direct, uint32_t* packed, VT* vout) {
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < m; q += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t key = keys_s[q];
     const long long C = nchunk[key];
@@ -631,7 +918,12 @@ __global__ void place_kernel(const uint32_t* keys_s, const uint32_t* perm, const
     const long long mr = runlen[start[q]];
     const long long a = ps % C, wrap = a + mr - C;
     long long c, pp;
-    if (newpos[q] >= 0) {  // column-spread position (slot_kernel)
+    int lane;
+    if (direct && newpos[q] >= 0) {  // chunk * 32 + lane (color_warp_kernel)
+      c = newpos[q] >> 5;
+      lane = newpos[q] & 31;
+      pp = -1;
+    } else if (newpos[q] >= 0) {  // column-spread position (slot_warp_kernel)
       pp = newpos[q];
       c = pp % C;
     } else if (wrap > 0 && kk < wrap) {
@@ -641,12 +933,30 @@ __global__ void place_kernel(const uint32_t* keys_s, const uint32_t* perm, const
       c = wrap > 0 ? a + (kk - wrap) : a + kk;
       pp = ps + (c - a);
     }
-    const long long slot = pp / C;  // even slots -> lanes 0-15, odd -> 16-31: each half-warp spans the classes
-    const int lane = (int)(((slot & 1) << 4) + (slot >> 1));
+    if (pp >= 0) {
+      const long long slot = pp / C;  // even slots -> lanes 0-15, odd -> 16-31: each half-warp spans the classes
+      lane = (int)(((slot & 1) << 4) + (slot >> 1));
+    }
     const int64_t Cg = (seg_base[key] >> 5) + c;  // global chunk index
     const uint32_t src = perm[q];
-    packed[pos_packed(Cg, lane)] = (rl[q] << 16) | (idx[src] % (uint32_t)W);
+    packed[pos_packed(Cg, lane)] = (rl[q] << 16) | (idx[src] % (uint32_t)W) | (c == 0 ? kNewBlock : 0u);
     vout[sizeof(VT) == 4 ? pos_packed(Cg, lane) : pos_f64(Cg, lane)] = val[src];
+  }
+}
+
+__global__ void fill_u32(uint32_t* v, int64_t m, uint32_t x) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < m; q += (int64_t)gridDim.x * blockDim.x)
+    v[q] = x;
+}
+
+// The first chunk of every segment announces its column block: all 32 slots
+// (padding included; real entries are re-written by place_kernel) carry kNewBlock.
+__global__ void first_chunk_kernel(int64_t nkeys, const long long* seg_base, const long long* nchunk,
+                                   uint32_t pad, uint32_t* packed) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nkeys * 32;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = q >> 5;
+    if (nchunk[k] > 0) packed[pos_packed(seg_base[k] >> 5, (int)(q & 31))] = pad | kNewBlock;
   }
 }
 
@@ -690,7 +1000,7 @@ bool build_blocked(spk_ctx* ctx, int P, int S, int W, int64_t n_out, int64_t n_i
   slab_row0[Q] = (int)n_out;
   int max_rows = 0;
   for (int k = 0; k < Q; ++k) max_rows = std::max(max_rows, slab_row0[k + 1] - slab_row0[k]);
-  if (max_rows >= 65535) return false;
+  if (max_rows + kSinkRows >= 65535) return false;
   const int B = (int)((n_in + W - 1) / W);
   const int Bh = (B + S - 1) / S;
   cudaStream_t s = ctx->stream;
@@ -795,7 +1105,11 @@ bool build_blocked(spk_ctx* ctx, int P, int S, int W, int64_t n_out, int64_t n_i
       const int64_t k = sw * Bh + b;
       useg[k] = u_acc;
       u_acc += (long long)h[k];
-      nch[k] = std::max<long long>(((long long)h[k] + 31) / 32, (long long)mx[k]);
+      // every block of the CTA's column part holds at least one chunk (all
+      // padding if need be): its first chunk carries the block-boundary flag
+      const int part = (int)((sw / kNW) % S);
+      const bool exists = part * Bh + b < B;
+      nch[k] = exists ? std::max<long long>({1LL, ((long long)h[k] + 31) / 32, (long long)mx[k]}) : 0;
       seg_base[k] = p_acc;
       off[(size_t)sw * (Bh + 1) + b] = p_acc;
       p_acc += 32 * nch[k];
@@ -816,36 +1130,68 @@ bool build_blocked(spk_ctx* ctx, int P, int S, int W, int64_t n_out, int64_t n_i
   upload(ctx, out.slab_row0, slab_row0.data(), sizeof(int) * (Q + 1));
   out.packed.alloc(sizeof(uint32_t) * total);
   out.val.alloc((size_t)vbytes * total);
-  SPK_CUDA(cudaMemsetAsync(out.packed.p, 0xff, out.packed.bytes, s));  // padding = kPad
+  const uint32_t pad = (uint32_t)max_rows << 16;  // padding entry: the half's sink row, column 0, value 0
+  fill_u32<<<grid_cap(ctx, total), 256, 0, s>>>(out.packed.as<uint32_t>(), total, pad);
+  first_chunk_kernel<<<grid_cap(ctx, nkeys * 32), 256, 0, s>>>(nkeys, d_seg.as<long long>(), d_nch.as<long long>(), pad,
+                                                                out.packed.as<uint32_t>());
+  ctx->launches += 2;
   SPK_CUDA(cudaMemsetAsync(out.val.p, 0, out.val.bytes, s));
   if (m > 0) {
     DBuf newpos(sizeof(int) * mm);
     SPK_CUDA(cudaMemsetAsync(newpos.p, 0xff, newpos.bytes, s));
     phase("runs + host offsets");
+    const bool direct = ctx->blocked_spread == 1;
     if (ctx->blocked_spread) {
       DBuf colc(mm);
       colclass_kernel<<<grid_cap(ctx, m), 256, 0, s>>>(perm.as<uint32_t>(), idx_d.as<uint32_t>(), W, m,
                                                        colc.as<unsigned char>());
-      slot_warp_kernel<<<(int)((nkeys + kSlotWarps - 1) / kSlotWarps), 32 * kSlotWarps, 0, s>>>(
-          nkeys, d_useg.as<long long>(), hist.as<unsigned long long>(), d_nch.as<long long>(), rl.as<uint32_t>(),
-          colc.as<unsigned char>(), start.as<uint32_t>(), runlen.as<uint32_t>(), newpos.as<int>());
+      if (direct) {
+        DBuf stats;
+        const bool want = std::getenv("SPK_DEBUG_BLOCKED") != nullptr;
+        if (want) {
+          stats.alloc(sizeof(unsigned long long) * 8);
+          SPK_CUDA(cudaMemsetAsync(stats.p, 0, stats.bytes, s));
+        }
+        color_warp_kernel<<<(int)((nkeys + kColorWarps - 1) / kColorWarps), 32 * kColorWarps, 0, s>>>(
+            nkeys, d_useg.as<long long>(), hist.as<unsigned long long>(), d_nch.as<long long>(), rl.as<uint32_t>(),
+            colc.as<unsigned char>(), d_seg.as<long long>(), pad >> 16, newpos.as<int>(), out.packed.as<uint32_t>(),
+            want ? stats.as<unsigned long long>() : nullptr);
+        if (want) {
+          unsigned long long hs[8];
+          download(ctx, hs, stats, sizeof hs);
+          std::fprintf(stderr, "[blocked] colouring: %llu segments placed, %llu fell back (path %llu, no room %llu); "
+                       "%llu entries beyond their class's colours, %llu evicted after a flip\n",
+                       hs[0], hs[1], hs[2], hs[3], hs[4], hs[5]);
+        }
+      } else
+        slot_warp_kernel<<<(int)((nkeys + kSlotWarps - 1) / kSlotWarps), 32 * kSlotWarps, 0, s>>>(
+            nkeys, d_useg.as<long long>(), hist.as<unsigned long long>(), d_nch.as<long long>(), rl.as<uint32_t>(),
+            colc.as<unsigned char>(), start.as<uint32_t>(), runlen.as<uint32_t>(), newpos.as<int>());
       ++ctx->launches;
     }
     if (vbytes == 4)
       place_kernel<float><<<grid_cap(ctx, m), 256, 0, s>>>(
           keys_s.as<uint32_t>(), perm.as<uint32_t>(), rl.as<uint32_t>(), start.as<uint32_t>(), runlen.as<uint32_t>(),
           d_useg.as<long long>(), d_seg.as<long long>(), d_nch.as<long long>(), idx_d.as<uint32_t>(),
-          val_d.as<float>(), W, m, newpos.as<int>(), out.packed.as<uint32_t>(), out.val.as<float>());
+          val_d.as<float>(), W, m, newpos.as<int>(), direct, out.packed.as<uint32_t>(), out.val.as<float>());
     else
       place_kernel<double><<<grid_cap(ctx, m), 256, 0, s>>>(
           keys_s.as<uint32_t>(), perm.as<uint32_t>(), rl.as<uint32_t>(), start.as<uint32_t>(), runlen.as<uint32_t>(),
           d_useg.as<long long>(), d_seg.as<long long>(), d_nch.as<long long>(), idx_d.as<uint32_t>(),
-          val_d.as<double>(), W, m, newpos.as<int>(), out.packed.as<uint32_t>(), out.val.as<double>());
+          val_d.as<double>(), W, m, newpos.as<int>(), direct, out.packed.as<uint32_t>(), out.val.as<double>());
     ctx->launches += ctx->blocked_spread ? 2 : 1;
   }
   SPK_CUDA(cudaGetLastError());
   SPK_CUDA(cudaStreamSynchronize(s));
   phase("spread + place");
+  if (const char* dump = std::getenv("SPK_DUMP_BLOCKED")) {  // layout diagnostics: the head of the key stream
+    std::vector<uint32_t> hk((size_t)std::min<int64_t>(total, 1 << 21));
+    download(ctx, hk.data(), out.packed, hk.size() * 4);
+    if (FILE* f = std::fopen(dump, "wb")) {
+      std::fwrite(hk.data(), 4, hk.size(), f);
+      std::fclose(f);
+    }
+  }
   out.max_rows = max_rows;
   out.padded = p_acc;
   out.cta_entries.assign(P, 0);
@@ -889,7 +1235,7 @@ void launch_blocked(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, dou
   static const bool trace = std::getenv("SPK_TRACE_BLOCKED") != nullptr;
   DBuf tbuf;
   if (trace) {
-    tbuf.alloc(sizeof(unsigned long long) * 4 * 2 * op.L[0].P * 20);
+    tbuf.alloc(sizeof(unsigned long long) * 4 * 2 * op.L[0].P * 24);
     SPK_CUDA(cudaMemsetAsync(tbuf.p, 0, tbuf.bytes, ctx->stream));
     op.trace = tbuf.as<unsigned long long>();
   }
@@ -917,7 +1263,7 @@ void launch_blocked(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, dou
         long double smean = 0;
         int cntw = 0;
         for (int c = 0; c < P; ++c) {
-          const unsigned long long* e = h.data() + (((size_t)it * 2 + role) * P + c) * 20;
+          const unsigned long long* e = h.data() + (((size_t)it * 2 + role) * P + c) * 24;
           if (!e[0]) continue;
           t0 = std::min(t0, e[0]);
           t1 = std::max(t1, e[0]);
@@ -940,7 +1286,7 @@ void launch_blocked(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, dou
         double d1 = 0, d2 = 0, d3 = 0, d4 = 0;
         int nc = 0;
         for (int c = 0; c < P; ++c) {
-          const unsigned long long* e = h.data() + (((size_t)it * 2 + role) * P + c) * 20;
+          const unsigned long long* e = h.data() + (((size_t)it * 2 + role) * P + c) * 24;
           if (!e[0] || !e[16]) continue;
           unsigned long long se = 0;
           for (int w = 0; w < kNW; ++w) se = std::max(se, e[1 + w]);
@@ -955,7 +1301,7 @@ void launch_blocked(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, dou
           double sx = 0, sy = 0, sxx = 0, syy = 0, sxy = 0, wspread = 0;
           int cnt = 0;
           for (int c = 0; c < P && c < (int)ce.size(); ++c) {
-            const unsigned long long* e = h.data() + (((size_t)it * 2 + role) * P + c) * 20;
+            const unsigned long long* e = h.data() + (((size_t)it * 2 + role) * P + c) * 24;
             if (!e[0]) continue;
             unsigned long long se = 0, smn = ~0ull;
             for (int w = 0; w < kNW; ++w)
@@ -973,6 +1319,36 @@ void launch_blocked(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, dou
           std::fprintf(stderr, "[trace]   CTA stream time vs padded entries: corr %.3f, entries cv %.4f, time cv %.4f; "
                        "warp spread in a CTA %.1f us\n", cov / std::sqrt(vx * vy + 1e-30), std::sqrt(vx) / (sx / cnt),
                        std::sqrt(vy) / (sy / cnt), wspread / cnt * 1e-3);
+        }
+        if (it == 3) {  // are the slow CTAs the same from iteration to iteration? (SM position vs data)
+          std::vector<std::pair<double, int>> tm;
+          double sa = 0, sb = 0, saa = 0, sbb = 0, sab = 0;
+          for (int c = 0; c < P; ++c) {
+            const unsigned long long* e3 = h.data() + (((size_t)3 * 2 + role) * P + c) * 24;
+            const unsigned long long* e2 = h.data() + (((size_t)2 * 2 + role) * P + c) * 24;
+            unsigned long long s3 = 0, s2 = 0;
+            for (int w = 0; w < kNW; ++w) {
+              s3 = std::max(s3, e3[1 + w]);
+              s2 = std::max(s2, e2[1 + w]);
+            }
+            const double a = (double)(s3 - e3[0]), b = (double)(s2 - e2[0]);
+            tm.push_back({a, c});
+            sa += a; sb += b; saa += a * a; sbb += b * b; sab += a * b;
+          }
+          const double ca = sab / P - sa / P * sb / P, va = saa / P - sa / P * sa / P, vb = sbb / P - sb / P * sb / P;
+          std::sort(tm.begin(), tm.end());
+          std::fprintf(stderr, "[trace]   per-CTA stream time, iteration 4 vs 3: corr %.3f; slowest CTAs (cta:smid:us):",
+                       ca / std::sqrt(va * vb + 1e-30));
+          for (int k = 0; k < 12; ++k) {
+            const int c = tm[P - 1 - k].second;
+            std::fprintf(stderr, " %d:%llu:%.1f", c, h[(((size_t)3 * 2 + role) * P + c) * 24 + 20], tm[P - 1 - k].first * 1e-3);
+          }
+          std::fprintf(stderr, "; fastest:");
+          for (int k = 0; k < 12; ++k) {
+            const int c = tm[k].second;
+            std::fprintf(stderr, " %d:%llu:%.1f", c, h[(((size_t)3 * 2 + role) * P + c) * 24 + 20], tm[k].first * 1e-3);
+          }
+          std::fprintf(stderr, "\n");
         }
         std::fprintf(stderr, "[trace]   per CTA: release %.2f us, xchg %.2f us, pair wait %.2f us, finalize %.2f us\n",
                      d1 / nc * 1e-3, d2 / nc * 1e-3, d3 / nc * 1e-3, d4 / nc * 1e-3);

@@ -155,7 +155,7 @@ struct spk_ctx {
   int use_blocked = 2;         // fast sparse loop layout: 0 CSR/CSC, 1 slab x block, 2 auto (large n)
   int blocked_max_w = 16384;   // cap on the shared tile width (tests force many blocks)
   int blocked_split = 0;       // column parts per row slab: 0 auto, 1, 2
-  int blocked_spread = 1;      // slab x block layout: spread gathered columns over banks (slot_kernel)
+  int blocked_spread = 1;      // slab x block layout: 1 = chunks by edge colouring (row and column bank classes), 2 = greedy column dealing, 0 = plain
   int blocked_cluster = 1;     // CTA pairs as 2-CTA clusters (DSMEM partial sums) when they all fit
   int batch_cluster = 2;       // batched log loop: CTAs (SMs) per sketch, 1 / 2 / 4
   int batch_unroll = 8;        // batched log loop: entry loads in flight per lane, 4 / 8

@@ -306,7 +306,7 @@ int spk_ctx_set_option(spk_ctx* ctx, int key, int64_t value) {
       if (value != 0 && value != 8 && value != 32) return SPK_STATUS_INPUT;
       ctx->row_lanes = (int)value;
       return SPK_OK;
-    case 8: ctx->blocked_spread = value ? 1 : 0; return SPK_OK;
+    case 8: ctx->blocked_spread = value < 0 || value > 2 ? 1 : (int)value; return SPK_OK;
     case 7: ctx->blocked_split = (int)std::max<int64_t>(0, std::min<int64_t>(value, 2)); return SPK_OK;
     default: return SPK_STATUS_INPUT;
   }
