@@ -51,7 +51,10 @@ namespace spk {
 
 namespace {
 
-constexpr int kNW = 15;                 // consumer warps per CTA (+1 producer = 16 warps: 4 per SMSP, 128 registers)
+#ifndef SPK_NW
+#define SPK_NW 15  // variant builds (profiling): 7 and 11 consumer warps measured slower, DESIGN.md section 6
+#endif
+constexpr int kNW = SPK_NW;             // consumer warps per CTA (+1 producer = 16 warps: 4 per SMSP, 128 registers)
 constexpr int kThreadsBlocked = 32 * (kNW + 1);
 constexpr int kTileW = 4096;            // x tile: 32 KB of fp64
 constexpr int kGE = 128;                // entries per group (4 chunks; one 16-byte load per lane)
@@ -193,7 +196,11 @@ struct BlockedOp {
   static constexpr int kThreads = kThreadsBlocked;
   static constexpr int kCluster = CL ? 2 : 1;
   static constexpr int kMinBlocks = 1;  // one CTA per SM: full register file, up to 227 KB shared
-  static constexpr int kDepth = sizeof(VT) == 4 ? 3 : 2;  // groups in flight per consumer warp (registers)
+#ifdef SPK_DEPTH
+  static constexpr int kDepth = SPK_DEPTH;
+#else
+  static constexpr int kDepth = sizeof(VT) == 4 ? 3 : 2;  // groups per register set (two sets per consumer warp)
+#endif
   BlockedHalf L[2];
   int64_t n;
   int acc_rows;         // shared accumulator capacity (max rows of a slab over both halves)

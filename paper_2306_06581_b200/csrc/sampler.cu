@@ -341,7 +341,11 @@ int grid_for(spk_ctx* ctx, int64_t items, int threads) {
 // support), so supported pairs cost only the screen; UOT needs K^g_k on
 // every supported pair and takes the exact path there.
 
+#ifndef SPK_TILED_MINB
+#define SPK_TILED_MINB 3  // resident CTAs per SM the tiled kernels are compiled for (80 registers)
+#endif
 constexpr int kTileJ = 1024;
+constexpr int kSuper = 8;  // column tiles tested at once for "every pair supported" (one scan over 8192 columns)
 constexpr int kRPW = 4;  // rows per warp
 constexpr int kTileRows = 8 * kRPW;
 
@@ -361,6 +365,7 @@ struct TiledArgs {
   float lof, hif;    // the same bounds in fp32 (rounded outwards)
   float mg;          // screen margin factor; +inf disables the screen
   const double* ytile_r;  // per column tile: max |y_j| (rounded up)
+  const double* ysuper_r;  // per run of kSuper column tiles
   DPlan P;
   double s;
   uint64_t seed;
@@ -517,7 +522,7 @@ __device__ __forceinline__ uint32_t entry_threshold(const TiledArgs& A, double r
 }
 
 template <int DIM, bool SAMPLE, bool NEEDK, class VT>
-__global__ void __launch_bounds__(256, 3) tiled_kernel(TiledArgs A) {
+__global__ void __launch_bounds__(256, SPK_TILED_MINB) tiled_kernel(TiledArgs A) {
   __shared__ float yfs[DIM][kTileJ];  // the screen's fp32 columns (exact paths read y from L2)
   __shared__ float yns[kTileJ];
   __shared__ double xmx[8];
@@ -580,14 +585,27 @@ __global__ void __launch_bounds__(256, 3) tiled_kernel(TiledArgs A) {
 #pragma unroll
       for (int k = 1; k < 8; ++k) xmax_cta = fmax(xmax_cta, xmx[k]);
     }
-    for (int64_t j0 = 0; j0 < A.n; j0 += kTileJ) {
+    int span = kTileJ;
+    for (int64_t j0 = 0; j0 < A.n; j0 += span) {
       // |x_i - y_j| <= |x_i| + max_tile |y_j|: when that bound is inside the
       // support, every pair of the tile is supported. When it holds for all
       // 32 rows of the CTA no path reads the staged fp32 tile (the screen is
       // skipped; exact paths read y from L2), so the staging and both CTA
       // barriers are skipped too (every thread takes the same decision).
-      const double R = A.ytile_r[j0 / kTileJ];
-      const bool cta_all = (xmax_cta + R) * (xmax_cta + R) * (1.0 + 1e-12) < A.lo;
+      // The same test on a run of kSuper tiles lets one scan cover all of
+      // them (config 4: 99.9993% of the pairs are supported).
+      span = kTileJ;
+      double R;
+      bool cta_all = false;
+      if (j0 % ((int64_t)kTileJ * kSuper) == 0) {
+        R = A.ysuper_r[j0 / ((int64_t)kTileJ * kSuper)];
+        cta_all = (xmax_cta + R) * (xmax_cta + R) * (1.0 + 1e-12) < A.lo;
+        if (cta_all) span = kTileJ * kSuper;
+      }
+      if (!cta_all) {
+        R = A.ytile_r[j0 / kTileJ];
+        cta_all = (xmax_cta + R) * (xmax_cta + R) * (1.0 + 1e-12) < A.lo;
+      }
       if (!cta_all) {
         __syncthreads();
         for (int e = threadIdx.x; e < kTileJ * DIM; e += blockDim.x) {
@@ -598,7 +616,7 @@ __global__ void __launch_bounds__(256, 3) tiled_kernel(TiledArgs A) {
         for (int jj = threadIdx.x; jj < kTileJ; jj += blockDim.x) yns[jj] = j0 + jj < A.n ? A.yn[j0 + jj] : 0.f;
         __syncthreads();
       }
-      const int jend = (int)min((int64_t)kTileJ, A.n - j0);
+      const int jend = (int)min((int64_t)span, A.n - j0);
       bool tile_all = true;
 #pragma unroll
       for (int q = 0; q < kRPW; ++q) {
@@ -615,6 +633,7 @@ __global__ void __launch_bounds__(256, 3) tiled_kernel(TiledArgs A) {
           uint64_t xq[kRPW];  // draw input of the lane at tcnt (advanced by 64 golden per pass)
 #pragma unroll
           for (int q = 0; q < kRPW; ++q) xq[q] = lb[q] + (uint64_t)tcnt[q] * kGolden;
+          const int c_in = c;  // all four rows advance together: their draw counters follow c
           for (; c + 64 <= jend; c += 64) {  // two steps per pass: 8 independent chains
             bool c0 = false, c1 = false;
 #pragma unroll
@@ -624,19 +643,14 @@ __global__ void __launch_bounds__(256, 3) tiled_kernel(TiledArgs A) {
             }
             const bool a0 = __any_sync(0xffffffffu, c0), a1 = __any_sync(0xffffffffu, c1);
             if (a0 || a1) {
-              if (!a0) {  // the first step keeps nothing: stop at the second
-#pragma unroll
-                for (int q = 0; q < kRPW; ++q) tcnt[q] += 32u;
-                c += 32;
-              }
+              if (!a0) c += 32;  // the first step keeps nothing: stop at the second
               break;
             }
 #pragma unroll
-            for (int q = 0; q < kRPW; ++q) {
-              tcnt[q] += 64u;
-              xq[q] += 64ull * kGolden;
-            }
+            for (int q = 0; q < kRPW; ++q) xq[q] += 64ull * kGolden;
           }
+#pragma unroll
+          for (int q = 0; q < kRPW; ++q) tcnt[q] += (uint32_t)(c - c_in);
           for (; c + 32 <= jend; c += 32) {
             bool cand = false;
 #pragma unroll
@@ -818,6 +832,14 @@ __global__ void tile_radius_kernel(const double* y, int64_t n, int dim, double* 
   }
 }
 
+__global__ void super_radius_kernel(const double* r, int64_t tiles, int64_t supers, double* rs) {
+  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s >= supers) return;
+  double m = 0.0;
+  for (int64_t t = s * kSuper; t < min(tiles, (s + 1) * kSuper); ++t) m = fmax(m, r[t]);
+  rs[s] = m;
+}
+
 // fp32 copies of the points and their squared norms (screen inputs).
 __global__ void to_f32_kernel(const double* x, int64_t n, int dim, float* xf, float* xn) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -927,9 +949,12 @@ TiledArgs tiled_args(spk_ctx* ctx, DevKernel& dk) {
     to_f32_kernel<<<grid_for(ctx, n, 256), 256, 0, ctx->stream>>>(dk.y.as<double>(), n, dk.dim, dk.yf.as<float>(),
                                                                    dk.yn.as<float>());
     const int64_t tiles = (n + kTileJ - 1) / kTileJ;
-    dk.ytr.alloc(sizeof(double) * tiles);
+    const int64_t supers = (tiles + kSuper - 1) / kSuper;
+    dk.ytr.alloc(sizeof(double) * (tiles + supers));  // tile radii, then the radii of runs of kSuper tiles
     tile_radius_kernel<<<(int)tiles, 256, 0, ctx->stream>>>(dk.y.as<double>(), n, dk.dim, dk.ytr.as<double>());
-    ctx->launches += 3;
+    super_radius_kernel<<<(int)((supers + 255) / 256), 256, 0, ctx->stream>>>(dk.ytr.as<double>(), tiles, supers,
+                                                                               dk.ytr.as<double>() + tiles);
+    ctx->launches += 4;
   }
   A.x = dk.x.as<double>();
   A.y = dk.y.as<double>();
@@ -938,6 +963,7 @@ TiledArgs tiled_args(spk_ctx* ctx, DevKernel& dk) {
   A.xn = dk.xn.as<float>();
   A.yn = dk.yn.as<float>();
   A.ytile_r = dk.ytr.as<double>();
+  A.ysuper_r = dk.ytr.as<double>() + (n + kTileJ - 1) / kTileJ;
   A.n = n;
   A.n_rows = n;
   A.row_base = 0;
