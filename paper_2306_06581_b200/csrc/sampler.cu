@@ -345,6 +345,7 @@ int grid_for(spk_ctx* ctx, int64_t items, int threads) {
 #define SPK_TILED_MINB 3  // resident CTAs per SM the tiled kernels are compiled for (80 registers)
 #endif
 constexpr int kTileJ = 1024;
+constexpr int kQueue = 160;  // candidate queue slots per warp: 31 left over + one step's 4 x 32
 constexpr int kSuper = 8;  // column tiles tested at once for "every pair supported" (one scan over 8192 columns)
 constexpr int kRPW = 4;  // rows per warp
 constexpr int kTileRows = 8 * kRPW;
@@ -526,6 +527,19 @@ __global__ void __launch_bounds__(256, SPK_TILED_MINB) tiled_kernel(TiledArgs A)
   __shared__ float yfs[DIM][kTileJ];  // the screen's fp32 columns (exact paths read y from L2)
   __shared__ float yns[kTileJ];
   __shared__ double xmx[8];
+  // Candidate queue (sample pass, all-supported tiles): a screened entry's
+  // exact decision -- fp64 distance, two divisions, exp, the full draw -- runs
+  // on ONE lane when taken where it is found (1.4% of the 128-pair steps at
+  // config 4 hold a candidate), so candidates wait here, in row order, until
+  // 32 of them fill a warp.
+  // (static shared memory: the staged tile of DIM > 6 leaves no room for it)
+  constexpr bool kUseQueue = SAMPLE && !NEEDK && DIM <= 6;
+  constexpr int kQ = kUseQueue ? kQueue : 1;
+  __shared__ uint32_t qj[8][kQ];   // column
+  __shared__ uint32_t qt[8][kQ];   // draw index
+  __shared__ unsigned char qr[8][kQ];  // row of the warp (0..3)
+  __shared__ double q_rw[8][kRPW];
+  __shared__ uint64_t q_st0[8][kRPW];
   const int lane = threadIdx.x & 31;
   const int w = threadIdx.x >> 5;
   const unsigned lt_mask = (1u << lane) - 1u;
@@ -572,6 +586,67 @@ __global__ void __launch_bounds__(256, SPK_TILED_MINB) tiled_kernel(TiledArgs A)
       base[q] = (SAMPLE && valid) ? A.slot_off[row[q]] : 0;
       cap[q] = (SAMPLE && valid) ? A.slot_cap[row[q]] : 0;
     }
+    int qn = 0;  // queued candidates (warp-uniform)
+    if (kUseQueue) {
+      __syncwarp();
+      if (lane < kRPW) {
+#pragma unroll
+        for (int q = 0; q < kRPW; ++q)
+          if (lane == q) {
+            q_rw[w][q] = rw[q];
+            q_st0[w][q] = st0[q];
+          }
+      }
+      __syncwarp();
+    }
+    // Exact decisions of the first min(32, qn) queued candidates, one per lane
+    // (same arithmetic and the same per-row output order as taking them in place).
+    auto flush = [&]() {
+      const int np = min(qn, 32);
+      bool keep = false;
+      double kv = -1.0, ps = 0.0;
+      int myq = -1;
+      uint32_t j = 0;
+      if (lane < np) {
+        myq = qr[w][lane];
+        j = qj[w][lane];
+        const uint64_t x0 = q_st0[w][myq] + (uint64_t)qt[w][lane] * kGolden;
+        const double* xp = A.x + (A.row_base + g * kTileRows + w * kRPW + myq) * DIM;
+        keep = exact_keep<DIM>(A, xp, (int64_t)j, q_rw[w][myq], A.P.col_w[j], x0, kv, ps);
+      }
+#pragma unroll
+      for (int q = 0; q < kRPW; ++q) {
+        const unsigned km = __ballot_sync(0xffffffffu, keep && myq == q);
+        if (keep && myq == q) {
+          const uint32_t pos = cnt[q] + (uint32_t)__popc(km & lt_mask);
+          if (pos < (uint32_t)cap[q]) {
+            A.pool_col[base[q] + pos] = j;
+            static_cast<VT*>(A.pool_val)[base[q] + pos] = (VT)(ps >= 1.0 ? kv : kv / ps);
+          }
+        }
+        cnt[q] += (uint32_t)__popc(km);
+      }
+      // the rest moves to the front
+      __syncwarp();
+      for (int b = 32; b < qn; b += 32) {
+        const int e = b + lane;
+        uint32_t tj = 0, tt = 0;
+        unsigned char tr = 0;
+        if (e < qn) {
+          tj = qj[w][e];
+          tt = qt[w][e];
+          tr = qr[w][e];
+        }
+        __syncwarp();
+        if (e < qn) {
+          qj[w][e - 32] = tj;
+          qt[w][e - 32] = tt;
+          qr[w][e - 32] = tr;
+        }
+        __syncwarp();
+      }
+      qn -= np;
+    };
     // largest |x_i| of the CTA's 32 rows (inf if any row is padding)
     double xmax_cta;
     {
@@ -660,6 +735,31 @@ __global__ void __launch_bounds__(256, SPK_TILED_MINB) tiled_kernel(TiledArgs A)
             for (int q = 0; q < kRPW; ++q) tcnt[q] += 32u;
           }
           if (c >= jend) break;
+          if (kUseQueue && c + 32 <= jend) {
+            // a step that may keep something: queue the lanes whose exact
+            // out_hi passes the row bound (draw t = tcnt + lane + 1: every
+            // pair of the tile is supported)
+#pragma unroll
+            for (int q = 0; q < kRPW; ++q) {
+              const uint32_t t = tcnt[q] + (uint32_t)lane + 1u;
+              const bool cand = rvalid[q] && sm_finalize_hi(st0[q] + (uint64_t)t * kGolden) <= th[q];
+              const unsigned m = __ballot_sync(0xffffffffu, cand);
+              if (cand) {
+                const int e = qn + __popc(m & lt_mask);
+                qj[w][e] = (uint32_t)(j0 + c + lane);
+                qt[w][e] = t;
+                qr[w][e] = (unsigned char)q;
+              }
+              qn += __popc(m);
+              tcnt[q] += 32u;
+            }
+            __syncwarp();
+            while (qn >= 32) flush();
+            continue;
+          }
+        }
+        if (kUseQueue) {  // in-place decisions below write the same rows: queued ones go first
+          while (qn > 0) flush();
         }
         const int jj = c + lane;
         const bool jvalid = jj < jend;
@@ -770,6 +870,9 @@ __global__ void __launch_bounds__(256, SPK_TILED_MINB) tiled_kernel(TiledArgs A)
           cnt[q] += (uint32_t)__popc(km);
         }
       }
+    }
+    if (kUseQueue) {
+      while (qn > 0) flush();
     }
 #pragma unroll
     for (int q = 0; q < kRPW; ++q) {
