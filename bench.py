@@ -381,7 +381,9 @@ def run_ours(args, ws, rank, local):
     # run) -- the per-iteration DRAM bytes of the committed ncu --set full
     # capture of this loop, times this launch's iterations; labelled as such
     traffic, traffic_src = None, None
-    prof = ROOT / "profiles" / f"ncu_{w.name.lower()}_loop.json"
+    prof = ROOT / "profiles" / f"r2_ncu_{w.name.lower()}_loop.json"  # latest committed capture of this loop
+    if not prof.exists():
+        prof = ROOT / "profiles" / f"ncu_{w.name.lower()}_loop.json"
     if prof.exists():
         k0 = json.loads(prof.read_text())["kernels"][0]
         if "dram_bytes_per_iteration" in k0:
