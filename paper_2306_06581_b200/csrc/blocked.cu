@@ -149,9 +149,17 @@ __device__ __forceinline__ uint64_t evict_first_policy() {
 }
 __device__ __forceinline__ uint4 ldg_stream(const void* p, uint64_t pol) {
   uint4 r;
+#if defined(SPK_LDPOL) && SPK_LDPOL == 1  // variant builds (profiling): no L2 policy
+  asm("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+#elif defined(SPK_LDPOL) && SPK_LDPOL == 2  // L1 allocating, evict-first
+  asm("ld.global.nc.L1::evict_first.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+      : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+      : "l"(p), "l"(pol));
+#else
   asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
       : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
       : "l"(p), "l"(pol));
+#endif
   return r;
 }
 
@@ -289,8 +297,10 @@ struct BlockedOp {
     const VT* gval = static_cast<const VT*>(H.val);
     const int r0 = H.slab_row0[q];
     const int nrows = H.slab_row0[q + 1] - r0;
-    const int bb0 = part * H.Bh;
-    const int nb = max(0, min(H.B, bb0 + H.Bh) - bb0);  // blocks of this CTA
+    // the CTA's column part [pstart, pend) in blocks of W
+    const int64_t pstart = part == 0 ? 0 : H.split;
+    const int64_t pend = (S == 1 || part == S - 1) ? H.n_in : H.split;
+    const int nb = (int)((pend - pstart + H.W - 1) / H.W);
 
     // Barriers are initialised once per launch (first half of iteration 1)
     // and never re-initialised; each stage's phase count carries over from
@@ -331,8 +341,8 @@ struct BlockedOp {
               record_fault(fault, 0x10000000u | ((unsigned)ROLE << 24) | (unsigned)b);
             pmask ^= 1u << s;
           }
-          const int64_t c0 = (int64_t)(bb0 + b) * H.W;
-          const int64_t cnt = min((int64_t)H.W, H.n_in - c0);
+          const int64_t c0 = pstart + (int64_t)b * H.W;
+          const int64_t cnt = min((int64_t)H.W, pend - c0);
           const uint32_t bytes = (uint32_t)align16((size_t)cnt * 8);
           mbar_arrive_expect_tx(&full[s], bytes);
           bulk_copy_g2s(tiles + (size_t)s * kTileW, x + c0, bytes, &full[s]);
@@ -530,17 +540,17 @@ __global__ void split_count_kernel(const long long* ptr, const uint32_t* idx, in
 // positions c, c+C, ... and so spreads its rows over all banks.
 __global__ void key_kernel(const long long* ptr, const uint32_t* idx, int64_t n_out, const int* slab_of,
                            const unsigned char* warp_of, const int* slab_row0_of_row, int W, int S, int Bh,
-                           uint32_t* seg, unsigned long long* key) {
+                           uint32_t split, uint32_t* seg, unsigned long long* key) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t i = warp; i < n_out; i += nw) {
     const uint32_t rl = (uint32_t)(i - slab_row0_of_row[i]);
     for (long long q = ptr[i] + lane; q < ptr[i + 1]; q += 32) {
-      const uint32_t blk = idx[q] / (uint32_t)W;
-      const uint32_t part = blk / (uint32_t)Bh;
+      const uint32_t part = idx[q] >= split ? 1u : 0u;  // split = n_in when S = 1
+      const uint32_t blk = (idx[q] - (part ? split : 0u)) / (uint32_t)W;  // block inside the part
       const uint32_t cta = (uint32_t)slab_of[i] * (uint32_t)S + part;
-      const uint32_t sg = (cta * kNW + warp_of[part * n_out + i]) * (uint32_t)Bh + (blk - part * Bh);
+      const uint32_t sg = (cta * kNW + warp_of[part * n_out + i]) * (uint32_t)Bh + blk;
       seg[q] = sg;
       key[q] = ((unsigned long long)sg << 20) | ((unsigned long long)(rl & 15u) << 16) | rl;
     }
@@ -595,9 +605,12 @@ __global__ void runlen_kernel(const uint32_t* keys_s, const uint32_t* rl, const 
 // per chunk, no extra padding. newpos[q] = chosen list position, or -1 where
 // a segment keeps the plain placement.
 // Column bank class of each sorted entry (coalesced; read by slot_warp_kernel).
-__global__ void colclass_kernel(const uint32_t* perm, const uint32_t* idx, int W, int64_t m, unsigned char* cc) {
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < m; q += (int64_t)gridDim.x * blockDim.x)
-    cc[q] = (unsigned char)((idx[perm[q]] % (uint32_t)W) & 15u);
+__global__ void colclass_kernel(const uint32_t* perm, const uint32_t* idx, int W, uint32_t split, int64_t m,
+                                unsigned char* cc) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < m; q += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t j = idx[perm[q]];
+    cc[q] = (unsigned char)(((j >= split ? j - split : j) % (uint32_t)W) & 15u);
+  }
 }
 
 // The free positions of a class are scored by the lanes in parallel (cost =
@@ -920,7 +933,8 @@ __global__ void __launch_bounds__(32 * kColorWarps) color_warp_kernel(
 template <class VT>
 __global__ void place_kernel(const uint32_t* keys_s, const uint32_t* perm, const uint32_t* rl, const uint32_t* start,
                              const uint32_t* runlen, const long long* useg, const long long* seg_base,
-                             const long long* nchunk, const uint32_t* idx, const VT* val, int W, int64_t m,
+                             const long long* nchunk, const uint32_t* idx, const VT* val, int W, uint32_t split,
+                             int64_t m,
                              const int* newpos, bool direct, uint32_t* packed, VT* vout) {
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < m; q += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t key = keys_s[q];
@@ -951,7 +965,9 @@ __global__ void place_kernel(const uint32_t* keys_s, const uint32_t* perm, const
     }
     const int64_t Cg = (seg_base[key] >> 5) + c;  // global chunk index
     const uint32_t src = perm[q];
-    packed[pos_packed(Cg, lane)] = (rl[q] << 16) | (idx[src] % (uint32_t)W) | (c == 0 ? kNewBlock : 0u);
+    const uint32_t j = idx[src];
+    packed[pos_packed(Cg, lane)] =
+        (rl[q] << 16) | ((j >= split ? j - split : j) % (uint32_t)W) | (c == 0 ? kNewBlock : 0u);
     vout[sizeof(VT) == 4 ? pos_packed(Cg, lane) : pos_f64(Cg, lane)] = val[src];
   }
 }
@@ -1013,15 +1029,21 @@ bool build_blocked(spk_ctx* ctx, int P, int S, int W, int64_t n_out, int64_t n_i
   int max_rows = 0;
   for (int k = 0; k < Q; ++k) max_rows = std::max(max_rows, slab_row0[k + 1] - slab_row0[k]);
   if (max_rows + kSinkRows >= 65535) return false;
-  const int B = (int)((n_in + W - 1) / W);
-  const int Bh = (B + S - 1) / S;
+  // S = 2: the column parts hold the same number of input atoms (a split on a
+  // block boundary left part 0 one block -- 1.5% of the entries at config 4 --
+  // heavier, and every half waits for its slowest CTA); multiple of 16 atoms
+  // so that part 1's tiles stay 16-byte aligned TMA sources
+  const int64_t split = S == 1 ? n_in : std::min<int64_t>(n_in, ((n_in / 2 + 15) / 16) * 16);
+  const int nb0 = (int)((split + W - 1) / W), nb1 = (int)((n_in - split + W - 1) / W);
+  const int B = nb0 + nb1;
+  const int Bh = std::max(nb0, nb1);
   cudaStream_t s = ctx->stream;
   // entries of each row inside each column part
   std::vector<int> cnt0(n_out);
   if (S == 2) {
     DBuf d_cnt0(sizeof(int) * std::max<int64_t>(n_out, 1));
     split_count_kernel<<<grid_cap(ctx, n_out), 256, 0, s>>>(ptr_d.as<long long>(), idx_d.as<uint32_t>(), n_out,
-                                                             (uint32_t)std::min<int64_t>((int64_t)Bh * W, n_in),
+                                                             (uint32_t)split,
                                                              d_cnt0.as<int>());
     ++ctx->launches;
     download(ctx, cnt0.data(), d_cnt0, sizeof(int) * n_out);
@@ -1070,7 +1092,7 @@ bool build_blocked(spk_ctx* ctx, int P, int S, int W, int64_t n_out, int64_t n_i
   phase("host cuts");
   key_kernel<<<grid_cap(ctx, n_out * 32), 256, 0, s>>>(ptr_d.as<long long>(), idx_d.as<uint32_t>(), n_out,
                                                         d_slab_of.as<int>(), d_warp_of.as<unsigned char>(),
-                                                        d_s0r.as<int>(), W, S, Bh, keys.as<uint32_t>(),
+                                                        d_s0r.as<int>(), W, S, Bh, (uint32_t)split, keys.as<uint32_t>(),
                                                         key64.as<unsigned long long>());
   iota_u32<<<grid_cap(ctx, m), 256, 0, s>>>(iota.as<uint32_t>(), m);
   key_hist_kernel<<<grid_cap(ctx, m), 256, 0, s>>>(keys.as<uint32_t>(), m, hist.as<unsigned long long>());
@@ -1120,7 +1142,7 @@ bool build_blocked(spk_ctx* ctx, int P, int S, int W, int64_t n_out, int64_t n_i
       // every block of the CTA's column part holds at least one chunk (all
       // padding if need be): its first chunk carries the block-boundary flag
       const int part = (int)((sw / kNW) % S);
-      const bool exists = part * Bh + b < B;
+      const bool exists = b < (part == 0 ? nb0 : nb1);
       nch[k] = exists ? std::max<long long>({1LL, ((long long)h[k] + 31) / 32, (long long)mx[k]}) : 0;
       seg_base[k] = p_acc;
       off[(size_t)sw * (Bh + 1) + b] = p_acc;
@@ -1155,7 +1177,7 @@ bool build_blocked(spk_ctx* ctx, int P, int S, int W, int64_t n_out, int64_t n_i
     const bool direct = ctx->blocked_spread == 1;
     if (ctx->blocked_spread) {
       DBuf colc(mm);
-      colclass_kernel<<<grid_cap(ctx, m), 256, 0, s>>>(perm.as<uint32_t>(), idx_d.as<uint32_t>(), W, m,
+      colclass_kernel<<<grid_cap(ctx, m), 256, 0, s>>>(perm.as<uint32_t>(), idx_d.as<uint32_t>(), W, (uint32_t)split, m,
                                                        colc.as<unsigned char>());
       if (direct) {
         DBuf stats;
@@ -1185,12 +1207,12 @@ bool build_blocked(spk_ctx* ctx, int P, int S, int W, int64_t n_out, int64_t n_i
       place_kernel<float><<<grid_cap(ctx, m), 256, 0, s>>>(
           keys_s.as<uint32_t>(), perm.as<uint32_t>(), rl.as<uint32_t>(), start.as<uint32_t>(), runlen.as<uint32_t>(),
           d_useg.as<long long>(), d_seg.as<long long>(), d_nch.as<long long>(), idx_d.as<uint32_t>(),
-          val_d.as<float>(), W, m, newpos.as<int>(), direct, out.packed.as<uint32_t>(), out.val.as<float>());
+          val_d.as<float>(), W, (uint32_t)split, m, newpos.as<int>(), direct, out.packed.as<uint32_t>(), out.val.as<float>());
     else
       place_kernel<double><<<grid_cap(ctx, m), 256, 0, s>>>(
           keys_s.as<uint32_t>(), perm.as<uint32_t>(), rl.as<uint32_t>(), start.as<uint32_t>(), runlen.as<uint32_t>(),
           d_useg.as<long long>(), d_seg.as<long long>(), d_nch.as<long long>(), idx_d.as<uint32_t>(),
-          val_d.as<double>(), W, m, newpos.as<int>(), direct, out.packed.as<uint32_t>(), out.val.as<double>());
+          val_d.as<double>(), W, (uint32_t)split, m, newpos.as<int>(), direct, out.packed.as<uint32_t>(), out.val.as<double>());
     ctx->launches += ctx->blocked_spread ? 2 : 1;
   }
   SPK_CUDA(cudaGetLastError());
@@ -1215,6 +1237,7 @@ bool build_blocked(spk_ctx* ctx, int P, int S, int W, int64_t n_out, int64_t n_i
   out.h.P = P;
   out.h.S = S;
   out.h.B = B;
+  out.h.split = split;
   out.h.Bh = Bh;
   out.h.W = W;
   out.h.n_out = n_out;

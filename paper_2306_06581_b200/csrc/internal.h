@@ -89,6 +89,7 @@ struct BlockedHalf {
   int B, Bh;    // column blocks in all, per part
   int W;        // columns per block (one staged x tile)
   int64_t n_out, n_in;
+  int64_t split;  // S = 2: input atoms [0, split) go to column part 0, the rest to part 1 (S = 1: n_in)
   const int* slab_row0;    // [Q+1] global row starts
   const long long* off;    // [P*NW*(Bh+1)] entry offsets of (CTA, warp, block); [Bh] = stream end
   const uint32_t* packed;  // row_local << 16 | col_local, 4-chunk groups interleaved per lane
