@@ -402,6 +402,40 @@ def test_blocked_loop_matches_csr(oracle, max_w):
             assert res.report["masked_rows"] == ores["masked_rows"]
 
 
+def test_blocked_layout_placements_agree():
+    """The three chunk placements of the slab x block layout -- plain run
+    placement (0), edge colouring of the row / column bank classes (1, the
+    default: Kempe-chain flips, leftovers of over-full classes, per-class
+    padding) and greedy column dealing (2) -- on a config-4-law sketch large
+    enough for realistic segments (n = 1.5e5: ~180 rows per warp, several
+    entries per row and block, both cluster and L2-swap pair exchange). Each
+    must give the CSR loop's scalings: the same fp32 entries summed in fp64,
+    only the order differs."""
+    from paper_2306_06581_b200 import _lib as L
+    from paper_2306_06581_b200 import workloads as W
+
+    w = W.c4(n=150_000, pairs=1_000_000)
+    cfg = spk.SolverConfig(w.eps, w.lam, -1.0, 12)
+    with spk.Context(0) as c:
+        kern = spk.Coords(w.x, w.y, w.cost, w.eta, scale=w.scale, eps=w.eps)
+        c.set_option(L.OPT_BLOCKED_LOOP, 0)
+        sk = c.sketch(kern, w.a, w.b, "ot", w.lam, w.eps, w.s, 7, spk.SparSinkOptions(values=w.values))
+        ref = sk.solve(cfg)
+        sk.free()
+        for spread, cluster in ((0, 1), (1, 1), (1, 0), (2, 1)):
+            c.set_option(L.OPT_BLOCKED_LOOP, 1)
+            c.set_option(L.OPT_BLOCKED_SPREAD, spread)
+            c.set_option(L.OPT_BLOCKED_CLUSTER, cluster)
+            assert c.get_option(L.OPT_BLOCKED_SPREAD) == spread
+            sk = c.sketch(kern, w.a, w.b, "ot", w.lam, w.eps, w.s, 7, spk.SparSinkOptions(values=w.values))
+            res = sk.solve(cfg)
+            sk.free()
+            assert res.report["iterations"] == ref.report["iterations"] == 12
+            assert res.report["masked_rows"] == ref.report["masked_rows"]
+            np.testing.assert_allclose(res.u, ref.u, rtol=1e-11)
+            np.testing.assert_allclose(res.v, ref.v, rtol=1e-11)
+
+
 # ---- BASELINE configs at full size -------------------------------------------------------------
 
 
