@@ -1458,7 +1458,9 @@ bool run_blocked_t(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, doub
                                  : BlockedOp<VT, 1, kStg1>{{}, 0, acc_rows}.smem_bytes();
       // auto mode keeps the CSR loop when rows are too few per warp to fill
       // conflict-free chunks (padding would outweigh the staged gathers)
-      const bool dense_pad = ctx->use_blocked == 2 && (double)(R->padded + C->padded) > 1.35 * 2.0 * (double)sk->nnz;
+      // (config 5, n = 5e4: 41% padding and still 27.0k against the CSR loop's 16.5k iterations/s;
+      // the stream time grows with the padded entries, so ~2.3x would break even)
+      const bool dense_pad = ctx->use_blocked == 2 && (double)(R->padded + C->padded) > 1.8 * 2.0 * (double)sk->nnz;
       if (smem <= kSmemBudget && !dense_pad) {
         sk->blk_rows = std::move(R);
         sk->blk_cols = std::move(C);

@@ -83,6 +83,11 @@ struct ReadWs {
 };
 
 // Slab x block layout of one half of a sketch (blocked.cu).
+// Auto mode of the slab x block loop: from this n on the layout is tried (and kept unless its chunk padding
+// exceeds 80%). Config 5's sketch (n = 5e4, 87 entries per row): 27.0k against 16.5k iterations/s for the CSR
+// loop; config 2 (n = 1e4, 4.8x padding): 24.3k against 28.3k.
+constexpr int64_t kBlockedAutoMinN = int64_t(1) << 15;
+
 struct BlockedHalf {
   int P;        // CTAs (= Q row slabs x S column parts)
   int S;        // column parts per row slab (1, or 2 = pairs of CTAs split x)
@@ -141,6 +146,7 @@ struct spk_sketch {
   spk::ReadWs rws;
   // fast-path layouts (built lazily by the first fast-mode solve)
   bool blocked_tried = false;
+  int loop_solves = 0;  // sparse-loop runs on this sketch (a mid-size sketch earns its slab x block layout on reuse)
   int blocked_stages = 0;
   std::unique_ptr<spk::BlockedHost> blk_rows, blk_cols;
 };
@@ -153,7 +159,7 @@ struct spk_ctx {
   int deterministic = 0;
   int loop_blocks_per_sm = 0;  // 0 = occupancy-derived
   int otf_fp32 = 1;            // dense on-the-fly comparator computes K in fp32
-  int use_blocked = 2;         // fast sparse loop layout: 0 CSR/CSC, 1 slab x block, 2 auto (large n)
+  int use_blocked = 2;         // fast sparse loop layout: 0 CSR/CSC, 1 slab x block, 2 auto (n >= kBlockedAutoMinN and chunk padding <= 80%)
   int blocked_max_w = 16384;   // cap on the shared tile width (tests force many blocks)
   int blocked_split = 0;       // column parts per row slab: 0 auto, 1, 2
   int blocked_spread = 1;      // slab x block layout: 1 = chunks by edge colouring (row and column bank classes), 2 = greedy column dealing, 0 = plain

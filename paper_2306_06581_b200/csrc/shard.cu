@@ -626,7 +626,7 @@ int spk_shard_begin(spk_shard* sh, const spk_solver_cfg* cfg, int uot, int polic
     // fast path: slab x block layouts of the row and column slabs, indices
     // already in the gathered layout (x of a half = W blocks of stride doubles)
     const bool want_blk = !sh->log_domain && !ctx->deterministic && sh->m_own > 0 &&
-                          (ctx->use_blocked == 1 || (ctx->use_blocked == 2 && n >= (int64_t(1) << 17)));
+                          (ctx->use_blocked == 1 || (ctx->use_blocked == 2 && n >= kBlockedAutoMinN));
     if (want_blk && !sh->blk_tried) {
       sh->blk_tried = true;
       if (!shard::blocked_shard_build(ctx, sh->m_own, (int64_t)sh->world * sh->stride, sh->rows.nnz, sh->rows.row_ptr,
@@ -689,7 +689,7 @@ static int shard_step(spk_shard* sh, int half, int compute, int64_t t, const dou
     const int grid = A.compute ? shard::grid_rows(ctx, sh->m_own) : 1;
     const bool f32 = sh->value_type == SPK_VALUES_F32;
     const bool blk = A.compute && !sh->log_domain && sh->blk.R && !ctx->deterministic &&
-                     (ctx->use_blocked == 1 || (ctx->use_blocked == 2 && sh->n >= (int64_t(1) << 17)));
+                     (ctx->use_blocked == 1 || (ctx->use_blocked == 2 && sh->n >= kBlockedAutoMinN));
     if (blk) {
       shard::blocked_shard_half(ctx, A, sh->blk);
       ++sh->calls;
