@@ -165,11 +165,13 @@ enum spk_option {
   SPK_OPT_DETERMINISTIC = 1,
   SPK_OPT_LOOP_BLOCKS_PER_SM = 2,
   SPK_OPT_OTF_FP32 = 3,      /* dense on-the-fly comparator: K in fp32 (1) or fp64 (0) */
-  SPK_OPT_BLOCKED_LOOP = 4,  /* fast sparse loop: slab x block layout (1), CSR/CSC (0), auto (2, default: n >= 2^17) */
+  SPK_OPT_BLOCKED_LOOP = 4,  /* fast sparse loop: slab x block layout (1), CSR/CSC (0), auto (2, default: n >= 2^17 always;
+                                2^15 <= n < 2^17 once a sketch is solved again or max_iter >= 400; chunk padding <= 80%) */
   SPK_OPT_BLOCKED_MAX_W = 5, /* cap on the staged tile width (testing) */
   SPK_OPT_TWO_PASS_SAMPLER = 6, /* sampler: always the exact two-pass kernels (testing) */
   SPK_OPT_BLOCKED_SPLIT = 7,    /* slab x block loop: column parts per row slab (0 auto, 1, 2 = CTA pairs) */
-  SPK_OPT_BLOCKED_SPREAD = 8,   /* slab x block loop: spread each half-warp's gathered columns over the banks (1, default) */
+  SPK_OPT_BLOCKED_SPREAD = 8,   /* slab x block layout, chunk placement: 1 (default) edge colouring of the accumulator / x bank
+                                   classes, 2 greedy column dealing, 0 plain run placement */
   SPK_OPT_BLOCKED_CLUSTER = 9,  /* slab x block loop: CTA pairs as 2-CTA clusters sharing partial sums (1, default, when they fit) */
   SPK_OPT_BATCH_CLUSTER = 10,   /* batched log loop: CTAs (SMs) per sketch as one cluster: 1, 2 (default) or 4 */
   SPK_OPT_BATCH_UNROLL = 11,    /* batched log loop: entry loads in flight per lane: 4 or 8 (default) */
