@@ -278,7 +278,16 @@ struct DevKernel {
   DBuf ytr;                     // per sampler column tile: max |y_j|
   double d0 = 0.0;              // support threshold on d^2 (threshold_kernel), once per kernel
   bool have_d0 = false;
+  // Batched UOT sketches on one coordinate kernel (config 3: 496 frame pairs on
+  // one pixel grid): K and K^g_k are the same n x n matrices for every pair, so
+  // they are evaluated once (exp, pow per entry) and every pair's plan and
+  // sampling passes stream them instead (sampler.cu: *_cached_kernel).
+  DBuf cK, cKg;
+  double cache_g = -1.0;  // the exponent cKg was built for
 };
+
+// Fill dk.cK / dk.cKg for UOT plans with exponent g_k when n^2 entries fit the budget; false otherwise.
+bool cache_uot_kernel(spk_ctx* ctx, DevKernel& dk, double g_k);
 
 void make_dev_kernel(spk_ctx* ctx, const spk_kernel_desc* kd, double default_eps, DevKernel& dk,
                      bool need_cost);

@@ -202,6 +202,98 @@ __global__ void sample_rows_kernel(KSrc S, DPlan P, double s, uint64_t seed, int
   }
 }
 
+// ---- cached UOT kernel: K and K^g_k evaluated once for many (a, b) pairs ---------
+// Same arithmetic and the same summation / draw order as plan_rows_kernel and
+// sample_rows_kernel on the coordinate form (which the tiled kernels reproduce
+// bit for bit), with the per-entry exp and pow replaced by two loads.
+
+__global__ void cache_fill_kernel(KSrc S, double g_k, double* K, double* Kg) {
+  const int64_t total = S.n * S.n;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / S.n, j = e - i * S.n;
+    const double k = kernel_entry(S, i, j);
+    K[e] = k;
+    Kg[e] = k != 0.0 ? pow(k, g_k) : 0.0;  // 0 < g_k < 1 and K <= 1: K^g_k >= K, so 0 marks the support exactly
+  }
+}
+
+__global__ void plan_rows_cached_kernel(const double* Kg, int64_t n, DPlan P, long long* row_nnz, double* row_sum) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = warp; i < n; i += nwarps) {
+    long long cnt = 0;
+    double acc = 0.0;
+    const double rw = P.row_w[i];
+    const double* row = Kg + i * n;
+    for (int64_t j = lane; j < n; j += 32) {
+      const double kg = __ldcs(row + j);
+      if (kg != 0.0) {
+        ++cnt;
+        acc += dmul(dmul(rw, P.col_w[j]), kg);  // grid_raw (UOT)
+      }
+    }
+    cnt = warp_sum_ll(cnt);
+    acc = warp_sum(acc);
+    if (lane == 0) {
+      row_nnz[i] = cnt;
+      row_sum[i] = acc;
+    }
+  }
+}
+
+template <bool EMIT, class VT>
+__global__ void sample_rows_cached_kernel(const double* K, const double* Kg, int64_t n, DPlan P, double s,
+                                          uint64_t seed, long long* row_cnt, const long long* row_ptr,
+                                          uint32_t* col_out, VT* val_out) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = warp; i < n; i += nwarps) {
+    const uint64_t state0 = mix_seed(seed, (uint64_t)i);
+    const double rw = P.row_w[i];
+    const double* row = Kg + i * n;
+    uint64_t base_t = 0;
+    long long cnt = 0;
+    const long long out0 = EMIT ? row_ptr[i] : 0;
+    for (int64_t j0 = 0; j0 < n; j0 += 32) {
+      const int64_t j = j0 + lane;
+      const double kg = (j < n) ? __ldcs(row + j) : 0.0;
+      const bool nz = (kg != 0.0);
+      const unsigned m = __ballot_sync(0xffffffffu, nz);
+      const uint64_t t = base_t + (uint64_t)__popc(m & lt_mask) + 1u;
+      base_t += (uint64_t)__popc(m);
+      bool keep = false;
+      double ps = 0.0;
+      if (nz) {
+        // plan_prob of a UOT grid entry: ((pa_i pb_j) K^g_k) inv, theta folded into the grid
+        double base = dmul(dmul(dmul(rw, P.col_w[j]), kg), P.inv);
+        if (P.theta_mode == 2) base = base > 0.0 ? dadd(dmul(P.omt, base), P.unif) : base;
+        ps = min1(dmul(s, base));
+        if (ps > 0.0) {
+          if (ps >= 1.0) {
+            keep = true;
+          } else {
+            const double draw = u64_to_unit(sm_finalize(state0 + t * kGolden));
+            keep = draw < ps;
+          }
+        }
+      }
+      const unsigned km = __ballot_sync(0xffffffffu, keep);
+      if (EMIT && keep) {
+        const long long pos = out0 + cnt + __popc(km & lt_mask);
+        const double k = K[i * n + j];
+        col_out[pos] = (uint32_t)j;
+        val_out[pos] = (VT)(ps >= 1.0 ? k : k / ps);
+      }
+      cnt += __popc(km);
+    }
+    if (!EMIT && lane == 0) row_cnt[i] = cnt;
+  }
+}
+
 // ---- query helpers ------------------------------------------------------------
 
 __global__ void plan_query_kernel(KSrc S, DPlan P, int64_t m, const int64_t* qi, const int64_t* qj,
@@ -1154,6 +1246,25 @@ void make_dev_kernel(spk_ctx* ctx, const spk_kernel_desc* kd, double default_eps
   }
 }
 
+bool cache_uot_kernel(spk_ctx* ctx, DevKernel& dk, double g_k) {
+  if (dk.dense || !(g_k > 0.0 && g_k < 1.0)) return false;
+  if (dk.cKg.p && dk.cache_g == g_k) return true;
+  const int64_t n = dk.n;
+  const double bytes = 16.0 * (double)n * (double)n;
+  size_t free_b = 0, total_b = 0;
+  if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) return false;
+  if (bytes > 8e9 || bytes > 0.4 * (double)free_b) return false;  // n <= ~22k, and never most of the free memory
+  dk.cK.alloc(sizeof(double) * n * n);
+  dk.cKg.alloc(sizeof(double) * n * n);
+  KSrc S = make_src(dk);
+  cache_fill_kernel<<<grid_for(ctx, n * n, 256), 256, 0, ctx->stream>>>(S, g_k, dk.cK.as<double>(),
+                                                                         dk.cKg.as<double>());
+  ++ctx->launches;
+  SPK_CUDA(cudaGetLastError());
+  dk.cache_g = g_k;
+  return true;
+}
+
 bool plan_weights(spk_ctx* ctx, DevKernel& dk, const double* a, const double* b, int plan_kind, double lambda,
                   double eps, PlanInfo& plan) {
   (void)ctx;
@@ -1220,7 +1331,11 @@ void plan_pass_rows(spk_ctx* ctx, DevKernel& dk, const PlanInfo& plan, int64_t r
   P.col_w = cw.as<double>();
   P.kind = plan.kind;
   P.g_k = plan.g_k;
-  if (!dk.dense && tiled_dim_ok(dk.dim)) {
+  if (!dk.dense && plan.kind == SPK_PLAN_UOT && dk.cKg.p && dk.cache_g == plan.g_k && row0 == 0 && row1 == n) {
+    plan_rows_cached_kernel<<<grid_for_rows(ctx, n, 8), 256, 0, ctx->stream>>>(dk.cKg.as<double>(), n, P, row_nnz,
+                                                                                row_sum);
+    ++ctx->launches;
+  } else if (!dk.dense && tiled_dim_ok(dk.dim)) {
     TiledArgs A = tiled_args(ctx, dk);
     A.n_rows = rows;
     A.row_base = row0;
@@ -1413,6 +1528,45 @@ void sample_sketch(spk_ctx* ctx, DevKernel& dk, const PlanInfo& plan, double s, 
   sk->row_ptr.alloc(sizeof(long long) * (n + 1));
   const size_t vbytes = value_type == SPK_VALUES_F32 ? 4 : 8;
 
+  const bool cached = !dk.dense && plan.kind == SPK_PLAN_UOT && !plan.factorized && dk.cKg.p &&
+                      dk.cache_g == plan.g_k && row0 == 0 && n == ncols;
+  if (cached) {
+    // ---- K and K^g_k of this kernel are resident (batched UOT sketches): count, scan, emit ----
+    DBuf cnt(sizeof(long long) * n);
+    const int grid = grid_for_rows(ctx, n, 8);
+    sample_rows_cached_kernel<false, double><<<grid, 256, 0, ctx->stream>>>(
+        dk.cK.as<double>(), dk.cKg.as<double>(), n, P, s, seed, cnt.as<long long>(), nullptr, nullptr, nullptr);
+    ++ctx->launches;
+    SPK_CUDA(cudaMemsetAsync(sk->row_ptr.p, 0, sizeof(long long), ctx->stream));
+    size_t tmp_bytes = 0;
+    SPK_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tmp_bytes, cnt.as<long long>(), sk->row_ptr.as<long long>() + 1,
+                                           (int)n, ctx->stream));
+    ctx->scratch.ensure(tmp_bytes);
+    SPK_CUDA(cub::DeviceScan::InclusiveSum(ctx->scratch.p, tmp_bytes, cnt.as<long long>(),
+                                           sk->row_ptr.as<long long>() + 1, (int)n, ctx->stream));
+    ++ctx->launches;
+    long long nnz = 0;
+    SPK_CUDA(cudaMemcpyAsync(&nnz, sk->row_ptr.as<long long>() + n, sizeof nnz, cudaMemcpyDeviceToHost,
+                             ctx->stream));
+    SPK_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (nnz > 0xffffffffLL) fail(SPK_E_BUDGET_TOO_LARGE, "sketch exceeds 2^32 entries");
+    sk->nnz = nnz;
+    sk->col_idx.alloc(sizeof(uint32_t) * std::max<long long>(nnz, 1));
+    sk->values.alloc(vbytes * std::max<long long>(nnz, 1));
+    if (value_type == SPK_VALUES_F32)
+      sample_rows_cached_kernel<true, float><<<grid, 256, 0, ctx->stream>>>(
+          dk.cK.as<double>(), dk.cKg.as<double>(), n, P, s, seed, nullptr, sk->row_ptr.as<long long>(),
+          sk->col_idx.as<uint32_t>(), sk->values.as<float>());
+    else
+      sample_rows_cached_kernel<true, double><<<grid, 256, 0, ctx->stream>>>(
+          dk.cK.as<double>(), dk.cKg.as<double>(), n, P, s, seed, nullptr, sk->row_ptr.as<long long>(),
+          sk->col_idx.as<uint32_t>(), sk->values.as<double>());
+    ++ctx->launches;
+    SPK_CUDA(cudaGetLastError());
+    build_csc(ctx, sk);
+    sk->kernel_mean = sketch_kernel_mean(ctx, sk);
+    return;
+  }
   if (!dk.dense && tiled_dim_ok(dk.dim) && (plan.factorized || plan.have_rows) && !ctx->force_two_pass) {
     // ---- single pass: row slots sized from the plan's row masses ----
     DBuf cap(sizeof(int) * n), capll(sizeof(long long) * n), off(sizeof(long long) * (n + 1));

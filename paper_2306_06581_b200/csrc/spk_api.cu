@@ -479,6 +479,10 @@ int spk_sketch_build_batch(spk_ctx* ctx, const spk_kernel_desc* kd, int count, c
     DevKernel dk;  // coordinates, fp32 screen copies and the support threshold: once for the batch
     make_dev_kernel(ctx, kd, epsilon, dk, /*need_cost=*/false);
     const int64_t n = dk.n;
+    // UOT plans: K^g_k (and K) are the same n x n matrices for every pair of the
+    // batch -- evaluated once when they fit, streamed by every pair's passes
+    if (plan_kind == SPK_PLAN_UOT && count >= 2 && lambda > 0.0 && epsilon > 0.0 && !ctx->force_two_pass)
+      cache_uot_kernel(ctx, dk, epsilon / (2.0 * lambda + epsilon));
     std::vector<std::unique_ptr<spk_sketch>> made;
     for (int k = 0; k < count; ++k) {
       auto sk = std::make_unique<spk_sketch>();
