@@ -47,7 +47,10 @@ namespace spk {
 namespace {
 
 constexpr int kBatchThreads = 1024;
-constexpr int kG = 8;      // lanes per row (config 3 rows: ~94 entries)
+#ifndef SPK_BATCH_G
+#define SPK_BATCH_G 8
+#endif
+constexpr int kG = SPK_BATCH_G;  // lanes per row (config 3 rows: ~94 entries)
 constexpr int kRows = 32 / kG;
 
 struct BatchItem {
