@@ -715,33 +715,38 @@ __global__ void __launch_bounds__(32 * kSlotWarps) slot_warp_kernel(
 // plus greedy column dealing (slot_warp_kernel), ~2.8 / 2.8 with this.
 // One warp per segment; all state in shared memory. newpos[q] = chunk * 32 +
 // lane, or -1 (whole segment) when the segment does not fit this scheme.
-constexpr int kColorWarps = 4;
-constexpr int kColorMaxE = 1024;  // 32 chunks of 32
+// Two instances: segments of up to 512 entries in up to 16 chunks (all of config
+// 4's) run with 5.2 KB of state per warp, 8 warps per CTA -- the kernel is a
+// latency-bound sequential walk, so resident warps are its throughput --
+// and the rest with the full-size state.
+template <int MAXE, int MAXH>
 struct ColorWs {
-  unsigned short at[32][64];   // edge holding colour h at class x (0-15 rows, 16-31 columns)
-  unsigned short erow[kColorMaxE];
-  unsigned char evert[kColorMaxE];  // row class | column class << 4
-  unsigned char ecol[kColorMaxE];   // colour (half-chunk) or 0xff
-  unsigned char cnt[64][32];        // entries of class x in half-chunk h
-  unsigned char fill[64], rmax[64], cmax[64];
-  unsigned int slot[64];
+  unsigned short at[32][MAXH];   // edge holding colour h at class x (0-15 rows, 16-31 columns)
+  unsigned short erow[MAXE];
+  unsigned char evert[MAXE];  // row class | column class << 4
+  unsigned char ecol[MAXE];   // colour (half-chunk) or 0xff
+  unsigned char cnt[MAXH][32];        // entries of class x in half-chunk h
+  unsigned char fill[MAXH], rmax[MAXH], cmax[MAXH];
+  unsigned int slot[MAXH];
 };
-__global__ void __launch_bounds__(32 * kColorWarps) color_warp_kernel(
+template <int MAXE, int MAXH, int WARPS, bool REST>
+__global__ void __launch_bounds__(32 * WARPS) color_warp_kernel(
     int64_t nkeys, const long long* useg, const unsigned long long* cnt, const long long* nchunk, const uint32_t* rl,
     const unsigned char* colc, const long long* seg_base, uint32_t padrow, int* newpos, uint32_t* packed,
     unsigned long long* stats) {
-  __shared__ ColorWs ws_all[kColorWarps];
+  __shared__ ColorWs<MAXE, MAXH> ws_all[WARPS];
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
-  const int64_t k = (int64_t)blockIdx.x * kColorWarps + wl;
+  const int64_t k = (int64_t)blockIdx.x * WARPS + wl;
   if (k >= nkeys) return;
   const int E = (int)cnt[k];
   const int C = (int)nchunk[k];
-  if (E == 0 || C > 32 || E > kColorMaxE) return;
+  if (E == 0 || 2 * C > MAXH || E > MAXE) return;
+  if (REST && 2 * C <= 32 && E <= 512) return;  // placed by the small instance
   const int H = 2 * C;
   const long long u0 = useg[k];
-  ColorWs& ws = ws_all[wl];
+  ColorWs<MAXE, MAXH>& ws = ws_all[wl];
   const unsigned FULL = 0xffffffffu;
-  for (int i = lane; i < 32 * 64; i += 32) (&ws.at[0][0])[i] = 0xffffu;
+  for (int i = lane; i < 32 * MAXH; i += 32) (&ws.at[0][0])[i] = 0xffffu;
   for (int e = lane; e < E; e += 32) {
     const uint32_t r = rl[u0 + e];
     ws.erow[e] = (unsigned short)r;
@@ -858,12 +863,12 @@ __global__ void __launch_bounds__(32 * kColorWarps) color_warp_kernel(
       }
     }
     __syncwarp();
-    for (int i = lane; i < 64 * 32; i += 32) {
+    for (int i = lane; i < MAXH * 32; i += 32) {
       const int h = i >> 5, x = i & 31;
       ws.cnt[h][x] = (h < H && ws.at[x][h] != 0xffffu) ? 1 : 0;
     }
     __syncwarp();
-    for (int h = lane; h < 64; h += 32) {
+    for (int h = lane; h < MAXH; h += 32) {
       int f = 0;
       for (int x = 0; x < 16; ++x) f += ws.cnt[h][x];
       ws.fill[h] = (unsigned char)f;
@@ -878,7 +883,7 @@ __global__ void __launch_bounds__(32 * kColorWarps) color_warp_kernel(
       const unsigned long long forb = run_forbidden(e);
       unsigned int key = 0xffffffffu;
 #pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {
+      for (int hh = 0; hh < (MAXH + 31) / 32; ++hh) {
         const int h = lane + 32 * hh;
         if (h < H && ws.fill[h] < 16 && !((forb >> h) & 1ull)) {
           const int d = 2 * (ws.cnt[h][u] + 1 > max(1, (int)ws.rmax[h])) + (ws.cnt[h][v] + 1 > max(1, (int)ws.cmax[h]));
@@ -1186,10 +1191,15 @@ bool build_blocked(spk_ctx* ctx, int P, int S, int W, int64_t n_out, int64_t n_i
           stats.alloc(sizeof(unsigned long long) * 8);
           SPK_CUDA(cudaMemsetAsync(stats.p, 0, stats.bytes, s));
         }
-        color_warp_kernel<<<(int)((nkeys + kColorWarps - 1) / kColorWarps), 32 * kColorWarps, 0, s>>>(
+        color_warp_kernel<512, 32, 8, false><<<(int)((nkeys + 7) / 8), 32 * 8, 0, s>>>(
             nkeys, d_useg.as<long long>(), hist.as<unsigned long long>(), d_nch.as<long long>(), rl.as<uint32_t>(),
             colc.as<unsigned char>(), d_seg.as<long long>(), pad >> 16, newpos.as<int>(), out.packed.as<uint32_t>(),
             want ? stats.as<unsigned long long>() : nullptr);
+        color_warp_kernel<1024, 64, 4, true><<<(int)((nkeys + 3) / 4), 32 * 4, 0, s>>>(
+            nkeys, d_useg.as<long long>(), hist.as<unsigned long long>(), d_nch.as<long long>(), rl.as<uint32_t>(),
+            colc.as<unsigned char>(), d_seg.as<long long>(), pad >> 16, newpos.as<int>(), out.packed.as<uint32_t>(),
+            want ? stats.as<unsigned long long>() : nullptr);
+        ++ctx->launches;
         if (want) {
           unsigned long long hs[8];
           download(ctx, hs, stats, sizeof hs);

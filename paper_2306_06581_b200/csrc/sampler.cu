@@ -1630,13 +1630,24 @@ void sample_sketch(spk_ctx* ctx, DevKernel& dk, const PlanInfo& plan, double s, 
       sk->nnz = nnz;
       sk->col_idx.alloc(sizeof(uint32_t) * std::max<long long>(nnz, 1));
       sk->values.alloc(vbytes * std::max<long long>(nnz, 1));
+      static const bool dbg = std::getenv("SPK_DEBUG_TIMING") != nullptr;
+      std::unique_ptr<Timer> tq(dbg ? new Timer(ctx->stream) : nullptr);
       compact_kernel<<<grid_for_rows(ctx, n, 8), 256, 0, ctx->stream>>>(
           n, off.as<long long>(), sk->row_ptr.as<long long>(), pcol.as<uint32_t>(), pval.as<unsigned char>(),
           (int)vbytes, sk->col_idx.as<uint32_t>(), sk->values.as<unsigned char>());
       ++ctx->launches;
       SPK_CUDA(cudaGetLastError());
+      if (tq) {
+        std::fprintf(stderr, "[timing]   compact %.4f s\n", tq->stop());
+        tq.reset(new Timer(ctx->stream));
+      }
       build_csc(ctx, sk);
+      if (tq) {
+        std::fprintf(stderr, "[timing]   build_csc %.4f s\n", tq->stop());
+        tq.reset(new Timer(ctx->stream));
+      }
       sk->kernel_mean = sketch_kernel_mean(ctx, sk);
+      if (tq) std::fprintf(stderr, "[timing]   kernel_mean %.4f s\n", tq->stop());
       return;
     }
     // a row outgrew its slot: redo exactly with the two-pass kernels below
