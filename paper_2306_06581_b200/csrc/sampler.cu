@@ -436,6 +436,11 @@ int grid_for(spk_ctx* ctx, int64_t items, int threads) {
 #ifndef SPK_TILED_MINB
 #define SPK_TILED_MINB 3  // resident CTAs per SM the tiled kernels are compiled for (80 registers)
 #endif
+#ifndef SPK_TILED_MINB_SCAN
+// the OT-like sample pass is bound by the integer pipes, not by latency: 2 CTAs with 128 registers (no
+// spills) measured 0.886 s against 0.898 s (3 CTAs) and 0.975 s (4) at config 4
+#define SPK_TILED_MINB_SCAN 2
+#endif
 constexpr int kTileJ = 1024;
 constexpr int kQueue = 160;  // candidate queue slots per warp: 31 left over + one step's 4 x 32
 constexpr int kSuper = 8;  // column tiles tested at once for "every pair supported" (one scan over 8192 columns)
@@ -615,7 +620,7 @@ __device__ __forceinline__ uint32_t entry_threshold(const TiledArgs& A, double r
 }
 
 template <int DIM, bool SAMPLE, bool NEEDK, class VT>
-__global__ void __launch_bounds__(256, SPK_TILED_MINB) tiled_kernel(TiledArgs A) {
+__global__ void __launch_bounds__(256, (SAMPLE && !NEEDK) ? SPK_TILED_MINB_SCAN : SPK_TILED_MINB) tiled_kernel(TiledArgs A) {
   __shared__ float yfs[DIM][kTileJ];  // the screen's fp32 columns (exact paths read y from L2)
   __shared__ float yns[kTileJ];
   __shared__ double xmx[8];
