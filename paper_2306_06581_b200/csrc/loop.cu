@@ -30,7 +30,7 @@ using loopcore::finalize_atom;
 // One row's value by the G lanes of a group (fast mode): FMA sum of v * x,
 // or the two-pass log-sum-exp; x read through L2 (rewritten in the launch).
 // Every lane of the warp calls it (the group reductions are warp shuffles).
-template <int G, bool LOG, class VT>
+template <int G, bool LOG, class VT, bool XS = false>
 __device__ __forceinline__ double group_row(const VT* __restrict__ val, const uint32_t* __restrict__ idx, int b, int e,
                                             const double* x, int gl) {
   if constexpr (!LOG) {
@@ -42,12 +42,12 @@ __device__ __forceinline__ double group_row(const VT* __restrict__ val, const ui
                      c3 = __ldg(idx + p + 3 * G);
       const double w0 = (double)__ldg(val + p), w1 = (double)__ldg(val + p + G), w2 = (double)__ldg(val + p + 2 * G),
                    w3 = (double)__ldg(val + p + 3 * G);
-      a0 = fma(w0, __ldcg(x + c0), a0);
-      a1 = fma(w1, __ldcg(x + c1), a1);
-      a2 = fma(w2, __ldcg(x + c2), a2);
-      a3 = fma(w3, __ldcg(x + c3), a3);
+      a0 = fma(w0, ld_x<XS>(x, c0), a0);
+      a1 = fma(w1, ld_x<XS>(x, c1), a1);
+      a2 = fma(w2, ld_x<XS>(x, c2), a2);
+      a3 = fma(w3, ld_x<XS>(x, c3), a3);
     }
-    for (; p < e; p += G) a0 = fma((double)__ldg(val + p), __ldcg(x + __ldg(idx + p)), a0);
+    for (; p < e; p += G) a0 = fma((double)__ldg(val + p), ld_x<XS>(x, __ldg(idx + p)), a0);
     double s = (a0 + a1) + (a2 + a3);
 #pragma unroll
     for (int o = G / 2; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
@@ -55,7 +55,7 @@ __device__ __forceinline__ double group_row(const VT* __restrict__ val, const ui
   } else {
     double m = -CUDART_INF;
     for (int p = b + gl; p < e; p += G) {
-      const double xv = __ldcg(x + __ldg(idx + p));
+      const double xv = ld_x<XS>(x, __ldg(idx + p));
       if (xv == -CUDART_INF) continue;
       m = fmax(m, log_of(ldg_val(val + p)) + xv);
     }
@@ -64,7 +64,7 @@ __device__ __forceinline__ double group_row(const VT* __restrict__ val, const ui
     double s = 0.0;
     if (m != -CUDART_INF)
       for (int p = b + gl; p < e; p += G) {
-        const double xv = __ldcg(x + __ldg(idx + p));
+        const double xv = ld_x<XS>(x, __ldg(idx + p));
         if (xv == -CUDART_INF) continue;
         s += exp_term<VT>(log_of(ldg_val(val + p)) + xv - m);
       }
@@ -76,7 +76,11 @@ __device__ __forceinline__ double group_row(const VT* __restrict__ val, const ui
 
 // G: lanes per row in fast mode (8 for short rows: 4 rows in flight per warp,
 // the next rows' bounds loaded one step ahead; 32 for long rows).
-template <class VT, int G = 32>
+// XS: the gathered vector staged in shared memory at the start of every half
+// (n * 8 bytes per CTA; mid-size sketches, n <= kStageMaxN): each entry's x
+// then costs a shared load instead of a second, dependent L2 round trip.
+constexpr int64_t kStageMaxN = 12288;  // 96 KB per CTA, two CTAs per SM
+template <class VT, int G = 32, bool XS = false>
 struct SparseOp {
   static constexpr int kThreads = loopcore::kBlock;
   static constexpr int kMinBlocks = 2;
@@ -96,6 +100,13 @@ struct SparseOp {
     const uint32_t* idx = ROLE == 0 ? col_idx : row_idx;
     const VT* vv = ROLE == 0 ? val : val_t;
     const int lane = threadIdx.x & 31;
+    if (XS && !DET) {
+      extern __shared__ __align__(16) double x_stage[];
+      __syncthreads();  // the previous half's readers are done
+      for (int64_t i = threadIdx.x; i < n; i += blockDim.x) x_stage[i] = __ldcg(x + i);
+      __syncthreads();
+      x = x_stage;
+    }
     if (DET) {
       const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
       const int64_t nth = (int64_t)gridDim.x * blockDim.x;
@@ -118,7 +129,7 @@ struct SparseOp {
           if (lane == 0) out[i] = __ldcg(old + i);
           continue;
         }
-        const double tmp = row_apply<LOG, false, VT>(vv, idx, __ldg(ptr + i), __ldg(ptr + i + 1), x, lane);
+        const double tmp = row_apply<LOG, false, VT, XS>(vv, idx, __ldg(ptr + i), __ldg(ptr + i + 1), x, lane);
         if (lane == 0)
           err += finalize_atom<LOG>(i, tmp, __ldcg(old + i), __ldg(wgt + i), exponent, policy, t, ne, dyn, out, flag,
                                     masks);
@@ -148,7 +159,7 @@ struct SparseOp {
         }
         const VT* vr = vv + b;
         const uint32_t* ir = idx + b;
-        const double tmp = group_row<G, LOG, VT>(vr, ir, 0, (int)(e - b), x, gl);
+        const double tmp = group_row<G, LOG, VT, XS>(vr, ir, 0, (int)(e - b), x, gl);
         if (in && gl == 0) {
           if (!live) out[i] = __ldcg(old + i);
           else
@@ -173,7 +184,7 @@ __global__ void coverage_kernel(const long long* row_ptr, const long long* col_p
   }
 }
 
-template <bool LOG, class VT, int G>
+template <bool LOG, class VT, int G, bool XS = false>
 void run_g(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, double exponent, int policy, LoopState& st,
            LoopOut& out);
 
@@ -187,11 +198,18 @@ void run_t(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, double expon
   const int64_t warps = (int64_t)ctx->num_sms * 2 * (loopcore::kBlock / 32);
   const bool short_rows = ctx->row_lanes == 8 ||
                           (ctx->row_lanes == 0 && sk->nnz <= 256 * sk->n && sk->n > 4 * warps);
-  if (!ctx->deterministic && short_rows) run_g<LOG, VT, 8>(ctx, sk, cfg, exponent, policy, st, out);
-  else run_g<LOG, VT, 32>(ctx, sk, cfg, exponent, policy, st, out);
+  const bool stage = !ctx->deterministic && ctx->stage_x && sk->n <= kStageMaxN;
+  if (!ctx->deterministic && short_rows) {
+    if (stage) run_g<LOG, VT, 8, true>(ctx, sk, cfg, exponent, policy, st, out);
+    else run_g<LOG, VT, 8>(ctx, sk, cfg, exponent, policy, st, out);
+  } else if (stage) {
+    run_g<LOG, VT, 32, true>(ctx, sk, cfg, exponent, policy, st, out);
+  } else {
+    run_g<LOG, VT, 32>(ctx, sk, cfg, exponent, policy, st, out);
+  }
 }
 
-template <bool LOG, class VT, int G>
+template <bool LOG, class VT, int G, bool XS>
 void run_g(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, double exponent, int policy, LoopState& st,
            LoopOut& out) {
   const int64_t n = sk->n;
@@ -200,7 +218,7 @@ void run_g(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, double expon
   W.col_ne.ensure(n);
   SPK_CUDA(cudaMemcpyAsync(W.row_ne.p, sk->cov_row.p, n, cudaMemcpyDeviceToDevice, ctx->stream));
   SPK_CUDA(cudaMemcpyAsync(W.col_ne.p, sk->cov_col.p, n, cudaMemcpyDeviceToDevice, ctx->stream));
-  SparseOp<VT, G> op;
+  SparseOp<VT, G, XS> op;
   op.n = n;
   op.row_ptr = sk->row_ptr.as<long long>();
   op.col_idx = sk->col_idx.as<uint32_t>();
@@ -218,7 +236,7 @@ void run_g(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, double expon
   // a few SMs two CTAs' rows and make every half wait for them)
   const int64_t useful = (!ctx->deterministic && G < 32) ? (int64_t)1 << 30 : (n + per_block - 1) / per_block;
   loopcore::run_core<LOG>(ctx, op, n, W, sk->cov_empty_rows, sk->cov_empty_cols, cfg, exponent, policy, st, useful,
-                          out);
+                          out, /*exact_grid=*/0, XS ? sizeof(double) * (size_t)n : 0);
 }
 
 }  // namespace

@@ -43,7 +43,15 @@ __device__ __forceinline__ LogK ldg_val(const LogK* p) { return LogK{__ldg(&p->v
 
 // Row value of one half: sum_p val[p] * x[idx[p]] over [b, e) (linear), or
 // the log-sum-exp of log(val[p]) + x[idx[p]] skipping x = -inf (log).
-template <bool LOG, bool DET, class VT>
+// XS: x is a copy staged in shared memory (plain loads); else the global
+// vector, read through L2 (it is rewritten inside the same launch).
+template <bool XS>
+__device__ __forceinline__ double ld_x(const double* x, uint32_t c) {
+  if constexpr (XS) return x[c];
+  else return __ldcg(x + c);
+}
+
+template <bool LOG, bool DET, class VT, bool XS = false>
 __device__ __forceinline__ double row_apply(const VT* __restrict__ val, const uint32_t* __restrict__ idx, long long b,
                                             long long e, const double* x, int lane) {
   if constexpr (!LOG) {
@@ -57,10 +65,10 @@ __device__ __forceinline__ double row_apply(const VT* __restrict__ val, const ui
     for (; p + 32 < e; p += 64) {
       const uint32_t c0 = __ldg(idx + p), c1 = __ldg(idx + p + 32);
       const double w0 = (double)__ldg(val + p), w1 = (double)__ldg(val + p + 32);
-      a0 = fma(w0, __ldcg(x + c0), a0);
-      a1 = fma(w1, __ldcg(x + c1), a1);
+      a0 = fma(w0, ld_x<XS>(x, c0), a0);
+      a1 = fma(w1, ld_x<XS>(x, c1), a1);
     }
-    if (p < e) a0 = fma((double)__ldg(val + p), __ldcg(x + __ldg(idx + p)), a0);
+    if (p < e) a0 = fma((double)__ldg(val + p), ld_x<XS>(x, __ldg(idx + p)), a0);
     return warp_sum(a0 + a1);
   } else {
     if (DET) {  // two passes: max, then the shifted sum (solvers.cpp:99-111)
@@ -84,7 +92,7 @@ __device__ __forceinline__ double row_apply(const VT* __restrict__ val, const ui
     // entry; the warp merges are a plain max and a plain sum
     double m = -CUDART_INF;
     for (long long p = b + lane; p < e; p += 32) {
-      const double xv = __ldcg(x + __ldg(idx + p));
+      const double xv = ld_x<XS>(x, __ldg(idx + p));
       if (xv == -CUDART_INF) continue;
       m = fmax(m, log_of(ldg_val(val + p)) + xv);
     }
@@ -92,7 +100,7 @@ __device__ __forceinline__ double row_apply(const VT* __restrict__ val, const ui
     if (m == -CUDART_INF) return -CUDART_INF;
     double s = 0.0;
     for (long long p = b + lane; p < e; p += 32) {
-      const double xv = __ldcg(x + __ldg(idx + p));
+      const double xv = ld_x<XS>(x, __ldg(idx + p));
       if (xv == -CUDART_INF) continue;
       s += exp_term<VT>(log_of(ldg_val(val + p)) + xv - m);  // a zero K~ (log -inf) adds exp(-inf) = 0
     }

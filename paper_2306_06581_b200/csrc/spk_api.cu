@@ -10,6 +10,7 @@
 #include <mutex>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <memory>
@@ -247,6 +248,7 @@ int spk_ctx_create(int device, spk_ctx** out) {
     SPK_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
     uint64_t keep = ~0ull;
     SPK_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    if (const char* e = std::getenv("SPK_STAGE_X")) ctx->stage_x = std::atoi(e) != 0;  // profiling
   });
   if (rc != SPK_OK) {
     std::fprintf(stderr, "spk_ctx_create: %s\n", ctx->err_msg.c_str());
