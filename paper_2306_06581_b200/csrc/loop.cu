@@ -34,7 +34,7 @@ template <int G, bool LOG, class VT, bool XS = false>
 __device__ __forceinline__ double group_row(const VT* __restrict__ val, const uint32_t* __restrict__ idx, int b, int e,
                                             const double* x, int gl) {
   if constexpr (!LOG) {
-    // four independent index -> x chains in flight per lane
+    // four independent index -> x chains in flight per lane (eight: no gain, 36.9k against 37.5k at C2)
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
     int p = b + gl;
     for (; p + 3 * G < e; p += 4 * G) {
@@ -196,9 +196,10 @@ void run_t(spk_ctx* ctx, spk_sketch* sk, const spk_solver_cfg& cfg, double expon
   // each warp several rows in sequence (measured: C5-sparse 13.5k -> 16.4k
   // iterations/s; C2, 10k rows = ~2 per warp, keeps a warp per row)
   const int64_t warps = (int64_t)ctx->num_sms * 2 * (loopcore::kBlock / 32);
-  const bool short_rows = ctx->row_lanes == 8 ||
-                          (ctx->row_lanes == 0 && sk->nnz <= 256 * sk->n && sk->n > 4 * warps);
   const bool stage = !ctx->deterministic && ctx->stage_x && sk->n <= kStageMaxN;
+  // (with x staged in shared memory the 8-lane rows win at C2 too: 37.3k against 32.5k)
+  const bool short_rows = ctx->row_lanes == 8 ||
+                          (ctx->row_lanes == 0 && sk->nnz <= 256 * sk->n && (stage || sk->n > 4 * warps));
   if (!ctx->deterministic && short_rows) {
     if (stage) run_g<LOG, VT, 8, true>(ctx, sk, cfg, exponent, policy, st, out);
     else run_g<LOG, VT, 8>(ctx, sk, cfg, exponent, policy, st, out);
