@@ -10,29 +10,37 @@
 // Layout (built once per sketch, for the CSR and for the CSC mirror):
 //   output atoms (this half's rows) are cut into Q row slabs of ~equal entry
 //   count; each slab is served by S CTAs (S = 2: a CTA pair, each reading
-//   one half of x, so every SM stages n/2 instead of n scalings per half);
-//   input atoms are cut into B blocks of W <= 4096 atoms (one 32 KB x tile).
-//   Inside a CTA the slab's rows are cut into 15 warp ranges of ~equal entry
-//   count. Entries are ordered (CTA, warp, block, chunk): each warp's half is
-//   ONE contiguous stream of 32-entry chunks, every chunk holding 32 DISTINCT
-//   rows (so lanes add into shared accumulators without atomics) spread over
-//   the shared-memory banks; inside a row the columns still ascend across
-//   chunks, so each part of a row is summed in the reference's j order
-//   (spmv, proj/src/sparsify.cpp:203-213; spmv_t :215-226 on the CSC).
-//   Entries are packed (row_local << 16 | col_local) + value, and four
-//   consecutive chunks are interleaved per lane, so one 16-byte load gives a
-//   lane its entries of 4 chunks: the stream goes HBM -> registers directly.
+//   one half of x -- equal halves -- so every SM stages n/2 instead of n
+//   scalings per half); a CTA's columns are cut into blocks of W <= 4096
+//   atoms (one 32 KB x tile). Inside a CTA the slab's rows are cut into 15
+//   warp ranges of ~equal entry count. Entries are ordered (CTA, warp, block,
+//   chunk): each warp's half is ONE contiguous stream of 32-entry chunks,
+//   every chunk holding 32 DISTINCT rows (so lanes add into shared
+//   accumulators without atomics). Which entries of a (warp, block) segment
+//   share a chunk is chosen by color_warp_kernel so that a half-warp's 16
+//   accumulators and its 16 gathered x lie in 16 different bank pairs wherever
+//   the segment allows. A row's entries are therefore summed chunk by chunk,
+//   not in column order (sparsify.cpp:203-226 order is the CSR loop's and the
+//   deterministic mode's; this fast mode agrees with it to ~5e-15).
+//   Entries are packed (row_local << 16 | new-block flag << 12 | col_local)
+//   + value; the first chunk of every block carries the flag, so the loop
+//   reads no per-block offsets; four consecutive chunks are interleaved per
+//   lane, so one 16-byte load gives a lane its entries of 4 chunks: the
+//   stream goes HBM -> registers directly. Padding (value 0) adds into 16
+//   sink rows behind the slab's accumulators.
 // Half-step (inside the persistent loop, loop_core.cuh), 16 warps per CTA:
 //   * producer warp: cp.async.bulk (TMA) of the CTA's x tiles through a
 //     STG-deep ring (full/empty mbarriers);
-//   * 15 consumer warps stream their entries with coalesced 16-byte loads,
-//     kDepth groups (512 entries) in flight per warp, evict-first in L2 (the
-//     stream never fits; x must stay), gather x from the shared tile and add
-//     v * x into their rows' fp64 shared accumulators;
-//   * S = 2: the pair swaps the partial sums of each other's rows through L2
-//     (one flag per pair, no grid barrier) and each CTA finalizes half of the
-//     slab as p0 + p1.
+//   * 15 consumer warps stream their entries with coalesced 16-byte loads in
+//     two register sets of kDepth groups (one is folded while the other is in
+//     flight), evict-first in L2 (the stream never fits; x must stay), gather
+//     x from the shared tile and add v * x into their rows' fp64 shared
+//     accumulators;
+//   * S = 2: the pair is a 2-CTA cluster and each CTA finalizes half of the
+//     slab as p0 + p1, reading the partner's sums over DSMEM (or swapping them
+//     through L2 when the pairs cannot be co-scheduled as clusters).
 // L2->SM traffic per half: the entry stream + Q * n * 8 bytes of x tiles.
+// DESIGN.md section 4.1 has the measurements behind each of these choices.
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
