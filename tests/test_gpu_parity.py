@@ -571,6 +571,39 @@ def test_tiled_sampler_matches_two_pass(ctx, oracle):
             assert np.array_equal(outs[0][2], outs[1][2])
 
 
+def test_tiled_sampler_dense_budgets(ctx, oracle):
+    """Budgets close to n^2: most p* reach 1 (every draw kept), so every 32-column
+    step of a fully supported tile queues all its lanes for the exact decision
+    (the candidate queue fills and drains several times per step). Tiled
+    single-pass sampler against the exact two-pass kernels and the oracle."""
+    from paper_2306_06581_b200 import _lib as L
+
+    n = 416
+    x = oracle.rng_doubles(31, 0, 3 * n).reshape(n, 3)
+    y = oracle.rng_doubles(32, 0, 3 * n).reshape(n, 3)
+    w = 0.05 + oracle.rng_doubles(33, 1, 2 * n)
+    a, b = w[:n] / w[:n].sum(), w[n:] / w[n:].sum()
+    kern = spk.Coords(x, y, "sqeuclid", 0.0, scale=1.0, eps=0.5)
+    Cm, _ = oracle.pairwise_cost(x, y, "sqeuclid", 0.0)
+    K, r = oracle.kernel_from_cost(Cm, 0.5)
+    assert r == 1.0
+    for frac in (0.3, 0.6, 0.95):
+        s = frac * n * n
+        p = oracle.plan("ot", a, b, K, r, math.inf, 0.5, 0.0)
+        so = oracle.poisson_sparsify(K, p, s, 21)
+        oracle.free_plan(p)
+        outs = []
+        for two_pass in (0, 1):
+            ctx.set_option(L.OPT_TWO_PASS_SAMPLER, two_pass)
+            outs.append(ctx.sketch(kern, a, b, "ot", math.inf, 0.5, s, 21).csr())
+        ctx.set_option(L.OPT_TWO_PASS_SAMPLER, 0)
+        for rp, ci, vv in outs:
+            assert np.array_equal(rp, so[0]) and np.array_equal(ci, so[1]), frac
+            np.testing.assert_allclose(vv, so[2], rtol=value_rtol("sqeuclid"), atol=SUBNORMAL_ATOL)
+        assert np.array_equal(outs[0][2], outs[1][2])
+        assert len(so[1]) > 0.25 * n * n * frac
+
+
 def test_config3_frame_pair(ctx, oracle):
     """Config 3 (one WFR frame pair at full size, n = 12544): UOT grid plan on
     a 22%-support kernel, fp32 sketch values, log-domain loop. Index sets bit
