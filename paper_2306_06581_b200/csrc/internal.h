@@ -162,7 +162,7 @@ struct spk_ctx {
   int use_blocked = 2;         // fast sparse loop layout: 0 CSR/CSC, 1 slab x block, 2 auto (n >= kBlockedAutoMinN and chunk padding <= 80%)
   int blocked_max_w = 16384;   // cap on the shared tile width (tests force many blocks)
   int blocked_split = 0;       // column parts per row slab: 0 auto, 1, 2
-  int stage_x = 1;             // grid loop: stage the gathered vector in shared memory when n <= 12288 (SPK_STAGE_X=0 disables)
+  int stage_x = 1;             // grid loop: stage the gathered vector in shared memory when n <= 24576 (SPK_STAGE_X=0 disables)
   int blocked_spread = 1;      // slab x block layout: 1 = chunks by edge colouring (row and column bank classes), 2 = greedy column dealing, 0 = plain
   int blocked_cluster = 1;     // CTA pairs as 2-CTA clusters (DSMEM partial sums) when they all fit
   int batch_cluster = 2;       // batched log loop: CTAs (SMs) per sketch, 1 / 2 / 4
