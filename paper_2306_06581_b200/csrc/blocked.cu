@@ -529,8 +529,12 @@ struct BlockedOp {
 
 // Per row: entries whose column lies before `split` (columns ascend in a row).
 __global__ void split_count_kernel(const long long* ptr, const uint32_t* idx, int64_t n_out, uint32_t split,
-                                   int* cnt0) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_out; i += (int64_t)gridDim.x * blockDim.x) {
+                                   long long* cnt0) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= n_out; i += (int64_t)gridDim.x * blockDim.x) {
+    if (i == n_out) {  // one element past the rows: the exclusive scan's total lands here
+      cnt0[i] = 0;
+      continue;
+    }
     long long lo = ptr[i], hi = ptr[i + 1];
     const long long b = lo;
     while (lo < hi) {
@@ -538,7 +542,59 @@ __global__ void split_count_kernel(const long long* ptr, const uint32_t* idx, in
       if (idx[mid] < split) lo = mid + 1;
       else hi = mid;
     }
-    cnt0[i] = (int)(lo - b);
+    cnt0[i] = lo - b;
+  }
+}
+
+// Row slabs of ~equal entry count: slab k starts at the first row whose
+// prefix reaches m k / Q (ptr is the prefix: one binary search per slab).
+__global__ void slab_cut_kernel(const long long* ptr, int64_t n_out, int64_t m, int Q, int* slab_row0) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k > Q) return;
+  if (k == 0 || k == Q) {
+    slab_row0[k] = k == 0 ? 0 : (int)n_out;
+    return;
+  }
+  const long long target = (long long)((double)m * k / Q);
+  int64_t lo = 0, hi = n_out + 1;  // first index with ptr[index] >= target
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (ptr[mid] < target) lo = mid + 1;
+    else hi = mid;
+  }
+  slab_row0[k] = (int)min(lo, n_out);
+}
+
+// The 15 warp ranges of every (slab, column part): ~equal entries of that part.
+// pre0[r] = entries of rows [0, r) left of the split (S = 2); one thread per (slab, part).
+__global__ void warp_cut_kernel(const long long* ptr, const long long* pre0, const int* slab_row0, int Q, int S,
+                                int* warp_end) {
+  const int id = blockIdx.x * blockDim.x + threadIdx.x;
+  if (id >= Q * S) return;
+  const int q = id / S, part = id % S;
+  const int a = slab_row0[q], z = slab_row0[q + 1];
+  auto pref = [&](int r) -> long long {  // entries of this part in rows [a, r)
+    const long long tot = ptr[r] - ptr[a];
+    if (S == 1) return tot;
+    const long long p0 = pre0[r] - pre0[a];
+    return part == 0 ? p0 : tot - p0;
+  };
+  const long long e1 = pref(z);
+  int prev = a;
+  for (int wv = 0; wv < kNW; ++wv) {
+    int r_end = z;
+    if (wv + 1 < kNW) {
+      const long long target = (long long)((double)e1 * (wv + 1) / kNW);
+      int lo = a, hi = z;  // first r in [a, z) with pref(r) >= target, else z
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (pref(mid) < target) lo = mid + 1;
+        else hi = mid;
+      }
+      r_end = max(prev, lo);
+    }
+    warp_end[id * kNW + wv] = r_end;
+    prev = r_end;
   }
 }
 
@@ -546,19 +602,34 @@ __global__ void split_count_kernel(const long long* ptr, const uint32_t* idx, in
 // it (stably) lists each segment's rows grouped by shared-memory bank class,
 // every row's entries consecutive in column order; chunk c then takes list
 // positions c, c+C, ... and so spreads its rows over all banks.
-__global__ void key_kernel(const long long* ptr, const uint32_t* idx, int64_t n_out, const int* slab_of,
-                           const unsigned char* warp_of, const int* slab_row0_of_row, int W, int S, int Bh,
-                           uint32_t split, uint32_t* seg, unsigned long long* key) {
+__global__ void key_kernel(const long long* ptr, const uint32_t* idx, int64_t n_out, const int* slab_row0, int Q,
+                           const int* warp_end, int W, int S, int Bh, uint32_t split, uint32_t* seg,
+                           unsigned long long* key) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t i = warp; i < n_out; i += nw) {
-    const uint32_t rl = (uint32_t)(i - slab_row0_of_row[i]);
+    // the row's slab (the last one starting at or before it) and its warp in each column part
+    int lo = 0, hi = Q;
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (slab_row0[mid] <= i) lo = mid;
+      else hi = mid;
+    }
+    const uint32_t slab = (uint32_t)lo;
+    const uint32_t rl = (uint32_t)(i - slab_row0[slab]);
+    uint32_t wv_of[2] = {0u, 0u};
+    for (int part = 0; part < S; ++part) {
+      const int* we = warp_end + ((int)slab * S + part) * kNW;
+      int wv = 0;
+      while (wv + 1 < kNW && we[wv] <= i) ++wv;
+      wv_of[part] = (uint32_t)wv;
+    }
     for (long long q = ptr[i] + lane; q < ptr[i + 1]; q += 32) {
       const uint32_t part = idx[q] >= split ? 1u : 0u;  // split = n_in when S = 1
       const uint32_t blk = (idx[q] - (part ? split : 0u)) / (uint32_t)W;  // block inside the part
-      const uint32_t cta = (uint32_t)slab_of[i] * (uint32_t)S + part;
-      const uint32_t sg = (cta * kNW + warp_of[part * n_out + i]) * (uint32_t)Bh + blk;
+      const uint32_t cta = slab * (uint32_t)S + part;
+      const uint32_t sg = (cta * kNW + wv_of[part]) * (uint32_t)Bh + blk;
       seg[q] = sg;
       key[q] = ((unsigned long long)sg << 20) | ((unsigned long long)(rl & 15u) << 16) | rl;
     }
@@ -1029,16 +1100,13 @@ bool build_blocked(spk_ctx* ctx, int P, int S, int W, int64_t n_out, int64_t n_i
     tph.reset(new Timer(ctx->stream));
   };
   const int Q = P / S;
-  std::vector<long long> ptr(n_out + 1);
-  download(ctx, ptr.data(), ptr_d, sizeof(long long) * (n_out + 1));
+  cudaStream_t s = ctx->stream;
+  // row slabs of ~equal entry count (device: one binary search of the row prefix per slab)
+  out.slab_row0.alloc(sizeof(int) * (Q + 1));
+  slab_cut_kernel<<<(Q + 1 + 127) / 128, 128, 0, s>>>(ptr_d.as<long long>(), n_out, m, Q, out.slab_row0.as<int>());
+  ++ctx->launches;
   std::vector<int> slab_row0(Q + 1);
-  slab_row0[0] = 0;
-  for (int k = 1; k < Q; ++k) {
-    const long long target = (long long)((double)m * k / Q);
-    int r = (int)(std::lower_bound(ptr.begin(), ptr.end(), target) - ptr.begin());
-    slab_row0[k] = std::max<int>(std::min<int64_t>(r, n_out), slab_row0[k - 1]);
-  }
-  slab_row0[Q] = (int)n_out;
+  download(ctx, slab_row0.data(), out.slab_row0, sizeof(int) * (Q + 1));
   int max_rows = 0;
   for (int k = 0; k < Q; ++k) max_rows = std::max(max_rows, slab_row0[k + 1] - slab_row0[k]);
   if (max_rows + kSinkRows >= 65535) return false;
@@ -1050,62 +1118,37 @@ bool build_blocked(spk_ctx* ctx, int P, int S, int W, int64_t n_out, int64_t n_i
   const int nb0 = (int)((split + W - 1) / W), nb1 = (int)((n_in - split + W - 1) / W);
   const int B = nb0 + nb1;
   const int Bh = std::max(nb0, nb1);
-  cudaStream_t s = ctx->stream;
-  // entries of each row inside each column part
-  std::vector<int> cnt0(n_out);
+  // warp ranges of every (slab, part): equal shares of the part's entries
+  // (prefix of the per-row counts left of the split, then 14 binary searches)
+  DBuf d_pre0, d_warp_end(sizeof(int) * (size_t)Q * S * kNW);
   if (S == 2) {
-    DBuf d_cnt0(sizeof(int) * std::max<int64_t>(n_out, 1));
-    split_count_kernel<<<grid_cap(ctx, n_out), 256, 0, s>>>(ptr_d.as<long long>(), idx_d.as<uint32_t>(), n_out,
-                                                             (uint32_t)split,
-                                                             d_cnt0.as<int>());
-    ++ctx->launches;
-    download(ctx, cnt0.data(), d_cnt0, sizeof(int) * n_out);
+    DBuf d_cnt0(sizeof(long long) * (n_out + 1));
+    d_pre0.alloc(sizeof(long long) * (n_out + 1));
+    split_count_kernel<<<grid_cap(ctx, n_out + 1), 256, 0, s>>>(ptr_d.as<long long>(), idx_d.as<uint32_t>(), n_out,
+                                                                 (uint32_t)split, d_cnt0.as<long long>());
+    size_t tb0 = 0;
+    SPK_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb0, d_cnt0.as<long long>(), d_pre0.as<long long>(),
+                                           (int)(n_out + 1), s));
+    ctx->scratch.ensure(tb0);
+    SPK_CUDA(cub::DeviceScan::ExclusiveSum(ctx->scratch.p, tb0, d_cnt0.as<long long>(), d_pre0.as<long long>(),
+                                           (int)(n_out + 1), s));
+    ctx->launches += 2;
+    SPK_CUDA(cudaStreamSynchronize(s));  // d_cnt0 is freed on leaving this scope
   }
-  std::vector<int> slab_of(n_out), slab_row0_of_row(n_out);
-  std::vector<unsigned char> warp_of((size_t)S * n_out);
-  std::vector<long long> pref(n_out + 1);
-  for (int k = 0; k < Q; ++k) {
-    const int a = slab_row0[k], z = slab_row0[k + 1];
-    for (int r = a; r < z; ++r) {
-      slab_of[r] = k;
-      slab_row0_of_row[r] = a;
-    }
-    for (int part = 0; part < S; ++part) {
-      // entries of this part per row, prefix-summed over the slab
-      pref[a] = 0;
-      for (int r = a; r < z; ++r) {
-        const long long tot = ptr[r + 1] - ptr[r];
-        const long long e = S == 1 ? tot : (part == 0 ? cnt0[r] : tot - cnt0[r]);
-        pref[r + 1] = pref[r] + e;
-      }
-      const long long e1 = pref[z];
-      int prev = a;
-      for (int wv = 0; wv < kNW; ++wv) {
-        int r_end = z;
-        if (wv + 1 < kNW) {
-          const long long target = (long long)((double)e1 * (wv + 1) / kNW);
-          r_end = std::max(prev, (int)(std::lower_bound(pref.begin() + a, pref.begin() + z, target) - pref.begin()));
-        }
-        for (int r = prev; r < r_end; ++r) warp_of[(size_t)part * n_out + r] = (unsigned char)wv;
-        prev = r_end;
-      }
-    }
-  }
+  warp_cut_kernel<<<(Q * S + 127) / 128, 128, 0, s>>>(ptr_d.as<long long>(), d_pre0.as<long long>(),
+                                                        out.slab_row0.as<int>(), Q, S, d_warp_end.as<int>());
+  ++ctx->launches;
   const int64_t nkeys = (int64_t)Q * S * kNW * Bh;
   if (nkeys >= (1LL << 32)) return false;
   const int64_t mm = std::max<int64_t>(m, 1);
-  DBuf d_slab_of, d_warp_of, d_s0r;
-  upload(ctx, d_slab_of, slab_of.data(), sizeof(int) * n_out);
-  upload(ctx, d_warp_of, warp_of.data(), warp_of.size());
-  upload(ctx, d_s0r, slab_row0_of_row.data(), sizeof(int) * n_out);
   DBuf keys(sizeof(uint32_t) * mm), keys_s(sizeof(uint32_t) * mm), iota(sizeof(uint32_t) * mm),
       perm(sizeof(uint32_t) * mm), hist(sizeof(unsigned long long) * nkeys),
       key64(sizeof(unsigned long long) * mm), key64_s(sizeof(unsigned long long) * mm);
   SPK_CUDA(cudaMemsetAsync(hist.p, 0, hist.bytes, s));
   phase("host cuts");
   key_kernel<<<grid_cap(ctx, n_out * 32), 256, 0, s>>>(ptr_d.as<long long>(), idx_d.as<uint32_t>(), n_out,
-                                                        d_slab_of.as<int>(), d_warp_of.as<unsigned char>(),
-                                                        d_s0r.as<int>(), W, S, Bh, (uint32_t)split, keys.as<uint32_t>(),
+                                                        out.slab_row0.as<int>(), Q, d_warp_end.as<int>(), W, S, Bh,
+                                                        (uint32_t)split, keys.as<uint32_t>(),
                                                         key64.as<unsigned long long>());
   iota_u32<<<grid_cap(ctx, m), 256, 0, s>>>(iota.as<uint32_t>(), m);
   key_hist_kernel<<<grid_cap(ctx, m), 256, 0, s>>>(keys.as<uint32_t>(), m, hist.as<unsigned long long>());
@@ -1174,7 +1217,6 @@ bool build_blocked(spk_ctx* ctx, int P, int S, int W, int64_t n_out, int64_t n_i
   upload(ctx, d_seg, seg_base.data(), sizeof(long long) * nkeys);
   upload(ctx, d_nch, nch.data(), sizeof(long long) * nkeys);
   upload(ctx, out.off, off.data(), sizeof(long long) * off.size());
-  upload(ctx, out.slab_row0, slab_row0.data(), sizeof(int) * (Q + 1));
   out.packed.alloc(sizeof(uint32_t) * total);
   out.val.alloc((size_t)vbytes * total);
   const uint32_t pad = (uint32_t)max_rows << 16;  // padding entry: the half's sink row, column 0, value 0
