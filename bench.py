@@ -398,17 +398,18 @@ def run_ours(args, ws, rank, local):
         px, py, pa, pb = (t.numpy() for t in pins)
         kernel_h = spk.Coords(px, py, w.cost, w.eta, scale=w.scale, eps=w.eps)
         e2e_times = []
-        for k in range(2):
+        for k in range(4):  # the first call grows the memory pool; the median of the other three is reported
             torch.cuda.synchronize()
             t1 = time.perf_counter()
             r = ctx.spar_sink(kernel_h, pa, pb, cfg, w.s, 7, opts, uot=w.uot)
             torch.cuda.synchronize()
             e2e_times.append(time.perf_counter() - t1)
-        e2e_t = max_over_ranks(e2e_times[-1], ws)
+        e2e_t = max_over_ranks(sorted(e2e_times[1:])[1], ws)
         h2d = w.x.nbytes + w.y.nbytes + w.a.nbytes + w.b.nbytes
         d2h = r.u.nbytes + r.v.nbytes + 8 * 4
         e2e = {"value": ws * r.report["iterations"] / e2e_t, "unit": "iters/s", "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h, "solve_s": e2e_t, "objective": r.report["objective"],
+               "d2h_bytes_per_step": d2h, "solve_s": e2e_t, "solve_s_all": [round(x, 4) for x in e2e_times],
+               "objective": r.report["objective"],
                "phases_s": {"plan": r.report["t_plan_s"], "sample": r.report["t_sample_s"],
                             "loop": r.report["t_loop_s"], "readout": r.report["t_readout_s"]}}
 
