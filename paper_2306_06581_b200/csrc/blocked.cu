@@ -1141,9 +1141,11 @@ bool build_blocked(spk_ctx* ctx, int P, int S, int W, int64_t n_out, int64_t n_i
   const int64_t nkeys = (int64_t)Q * S * kNW * Bh;
   if (nkeys >= (1LL << 32)) return false;
   const int64_t mm = std::max<int64_t>(m, 1);
-  DBuf keys(sizeof(uint32_t) * mm), keys_s(sizeof(uint32_t) * mm), iota(sizeof(uint32_t) * mm),
-      perm(sizeof(uint32_t) * mm), hist(sizeof(unsigned long long) * nkeys),
-      key64(sizeof(unsigned long long) * mm), key64_s(sizeof(unsigned long long) * mm);
+  DBuf &iota = tmp_buf(ctx, 0, sizeof(uint32_t) * mm), &perm = tmp_buf(ctx, 1, sizeof(uint32_t) * mm),
+       &keys = tmp_buf(ctx, 2, sizeof(uint32_t) * mm), &keys_s = tmp_buf(ctx, 3, sizeof(uint32_t) * mm),
+       &key64 = tmp_buf(ctx, 4, sizeof(unsigned long long) * mm),
+       &key64_s = tmp_buf(ctx, 5, sizeof(unsigned long long) * mm);
+  DBuf hist(sizeof(unsigned long long) * nkeys);
   SPK_CUDA(cudaMemsetAsync(hist.p, 0, hist.bytes, s));
   phase("host cuts");
   key_kernel<<<grid_cap(ctx, n_out * 32), 256, 0, s>>>(ptr_d.as<long long>(), idx_d.as<uint32_t>(), n_out,
@@ -1165,8 +1167,9 @@ bool build_blocked(spk_ctx* ctx, int P, int S, int W, int64_t n_out, int64_t n_i
                                            (int)m, 0, 20 + end_bit, s));
   ++ctx->launches;
   // run starts / lengths -> chunk counts -> conflict-free placement
-  DBuf rl(sizeof(uint32_t) * mm), start(sizeof(uint32_t) * mm), runlen(sizeof(uint32_t) * mm),
-      maxrun(sizeof(unsigned int) * nkeys);
+  DBuf &rl = tmp_buf(ctx, 6, sizeof(uint32_t) * mm), &start = tmp_buf(ctx, 7, sizeof(uint32_t) * mm),
+       &runlen = tmp_buf(ctx, 8, sizeof(uint32_t) * mm);
+  DBuf maxrun(sizeof(unsigned int) * nkeys);
   SPK_CUDA(cudaMemsetAsync(maxrun.p, 0, maxrun.bytes, s));
   split_kernel<<<grid_cap(ctx, m), 256, 0, s>>>(key64_s.as<unsigned long long>(), m, keys_s.as<uint32_t>(),
                                                 rl.as<uint32_t>());
@@ -1226,12 +1229,12 @@ bool build_blocked(spk_ctx* ctx, int P, int S, int W, int64_t n_out, int64_t n_i
   ctx->launches += 2;
   SPK_CUDA(cudaMemsetAsync(out.val.p, 0, out.val.bytes, s));
   if (m > 0) {
-    DBuf newpos(sizeof(int) * mm);
-    SPK_CUDA(cudaMemsetAsync(newpos.p, 0xff, newpos.bytes, s));
+    DBuf& newpos = tmp_buf(ctx, 9, sizeof(int) * mm);
+    SPK_CUDA(cudaMemsetAsync(newpos.p, 0xff, sizeof(int) * mm, s));
     phase("runs + host offsets");
     const bool direct = ctx->blocked_spread == 1;
     if (ctx->blocked_spread) {
-      DBuf colc(mm);
+      DBuf& colc = tmp_buf(ctx, 10, mm);
       colclass_kernel<<<grid_cap(ctx, m), 256, 0, s>>>(perm.as<uint32_t>(), idx_d.as<uint32_t>(), W, (uint32_t)split, m,
                                                        colc.as<unsigned char>());
       if (direct) {

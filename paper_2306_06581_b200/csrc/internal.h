@@ -181,7 +181,19 @@ struct spk_ctx {
   std::string err_msg;
   // scratch
   spk::DBuf scratch;
+  // Large per-build temporaries (sort keys, permutations, sampler pools): kept
+  // for the context's lifetime and grown on demand. Allocating and freeing
+  // gigabytes of them per sketch made the stream-ordered pool map fresh memory
+  // every other build (0.2-0.3 s stalls in build_csc / build_blocked).
+  spk::DBuf tmp[16];
 };
+
+namespace spk {
+inline DBuf& tmp_buf(spk_ctx* ctx, int slot, size_t bytes) {
+  ctx->tmp[slot].ensure(bytes);
+  return ctx->tmp[slot];
+}
+}  // namespace spk
 
 namespace spk {
 

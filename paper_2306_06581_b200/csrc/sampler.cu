@@ -1593,7 +1593,8 @@ void sample_sketch(spk_ctx* ctx, DevKernel& dk, const PlanInfo& plan, double s, 
     long long pool = 0;
     SPK_CUDA(cudaMemcpyAsync(&pool, off.as<long long>() + n, sizeof pool, cudaMemcpyDeviceToHost, ctx->stream));
     SPK_CUDA(cudaStreamSynchronize(ctx->stream));
-    DBuf pcol(sizeof(uint32_t) * std::max<long long>(pool, 1)), pval(vbytes * std::max<long long>(pool, 1));
+    DBuf &pcol = tmp_buf(ctx, 11, sizeof(uint32_t) * std::max<long long>(pool, 1)),
+         &pval = tmp_buf(ctx, 12, vbytes * std::max<long long>(pool, 1));
     DBuf rcnt(sizeof(int) * n), ovf(sizeof(unsigned int));
     SPK_CUDA(cudaMemsetAsync(ovf.p, 0, sizeof(unsigned int), ctx->stream));
     TiledArgs A = tiled_args(ctx, dk);
@@ -1706,8 +1707,8 @@ void build_csc(spk_ctx* ctx, spk_sketch* sk) {
   SPK_CUDA(cudaMemsetAsync(cnt.p, 0, cnt.bytes, ctx->stream));
   SPK_CUDA(cudaMemsetAsync(sk->col_ptr.p, 0, sizeof(long long), ctx->stream));
   if (m > 0) {
-    DBuf rows(sizeof(uint32_t) * m), keys_out(sizeof(uint32_t) * m), iota(sizeof(uint32_t) * m),
-        perm(sizeof(uint32_t) * m);
+    DBuf &iota = tmp_buf(ctx, 0, sizeof(uint32_t) * m), &perm = tmp_buf(ctx, 1, sizeof(uint32_t) * m),
+         &rows = tmp_buf(ctx, 2, sizeof(uint32_t) * m), &keys_out = tmp_buf(ctx, 3, sizeof(uint32_t) * m);
     expand_rows_kernel<<<grid_for_rows(ctx, n, 8), 256, 0, ctx->stream>>>(sk->row_ptr.as<long long>(), n,
                                                                            rows.as<uint32_t>());
     iota_kernel<<<grid_for(ctx, m, 256), 256, 0, ctx->stream>>>(iota.as<uint32_t>(), m);
