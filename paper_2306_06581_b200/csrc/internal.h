@@ -186,6 +186,21 @@ struct spk_ctx {
   // gigabytes of them per sketch made the stream-ordered pool map fresh memory
   // every other build (0.2-0.3 s stalls in build_csc / build_blocked).
   spk::DBuf tmp[16];
+  // Batched UOT builds: a^g / b^g of the measures already seen in this batch
+  // (config 3's 496 pairs use 32 frames; the host pow of 2 n weights per pair
+  // was a fifth of the batch's sketch time). Set for the duration of
+  // spk_sketch_build_batch only.
+  struct WeightCache* wcache = nullptr;
+};
+
+struct WeightCache {
+  struct Entry {
+    const double* src;  // the caller's row (alive for the duration of the call)
+    unsigned long long hash;
+    double exponent;
+    std::vector<double> w;
+  };
+  std::vector<Entry> entries;
 };
 
 namespace spk {

@@ -1272,7 +1272,6 @@ bool cache_uot_kernel(spk_ctx* ctx, DevKernel& dk, double g_k) {
 
 bool plan_weights(spk_ctx* ctx, DevKernel& dk, const double* a, const double* b, int plan_kind, double lambda,
                   double eps, PlanInfo& plan) {
-  (void)ctx;
   const int64_t n = dk.n;
   plan.kind = plan_kind;
   plan.theta = 0.0;
@@ -1295,8 +1294,27 @@ bool plan_weights(spk_ctx* ctx, DevKernel& dk, const double* a, const double* b,
   } else if (plan_kind == SPK_PLAN_UOT) {  // sparsify.cpp:102-107
     const double g_ab = lambda / (2.0 * lambda + eps);
     plan.g_k = eps / (2.0 * lambda + eps);
-    for (int64_t i = 0; i < n; ++i) plan.row_w[i] = std::pow(a[i], g_ab);
-    for (int64_t j = 0; j < n; ++j) plan.col_w[j] = std::pow(b[j], g_ab);
+    auto powers = [&](const double* src, std::vector<double>& out) {
+      WeightCache* wc = ctx->wcache;
+      unsigned long long h = 1469598103934665603ull;
+      if (wc) {
+        for (int64_t i = 0; i < n; ++i) {
+          unsigned long long bits;
+          std::memcpy(&bits, src + i, sizeof bits);
+          h = (h ^ bits) * 1099511628211ull;
+        }
+        for (const WeightCache::Entry& e : wc->entries)
+          if (e.hash == h && e.exponent == g_ab && (int64_t)e.w.size() == n &&
+              std::memcmp(e.src, src, sizeof(double) * n) == 0) {
+            out = e.w;
+            return;
+          }
+      }
+      for (int64_t i = 0; i < n; ++i) out[i] = std::pow(src[i], g_ab);
+      if (wc && wc->entries.size() < 256) wc->entries.push_back({src, h, g_ab, out});
+    };
+    powers(a, plan.row_w);
+    powers(b, plan.col_w);
   } else if (plan_kind == SPK_PLAN_BARYCENTER) {  // sparsify.cpp:122-128
     double sb = 0.0;
     for (int64_t j = 0; j < n; ++j) sb += (plan.col_w[j] = std::sqrt(b[j]));

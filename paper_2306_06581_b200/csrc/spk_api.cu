@@ -486,6 +486,12 @@ int spk_sketch_build_batch(spk_ctx* ctx, const spk_kernel_desc* kd, int count, c
     if (plan_kind == SPK_PLAN_UOT && count >= 2 && lambda > 0.0 && epsilon > 0.0 && !ctx->force_two_pass)
       cache_uot_kernel(ctx, dk, epsilon / (2.0 * lambda + epsilon));
     std::vector<std::unique_ptr<spk_sketch>> made;
+    WeightCache wcache;
+    struct CacheScope {
+      spk_ctx* c;
+      ~CacheScope() { c->wcache = nullptr; }
+    } scope{ctx};
+    ctx->wcache = &wcache;
     for (int k = 0; k < count; ++k) {
       auto sk = std::make_unique<spk_sketch>();
       sk->ctx = ctx;
