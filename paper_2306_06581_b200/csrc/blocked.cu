@@ -60,7 +60,7 @@ namespace spk {
 namespace {
 
 #ifndef SPK_NW
-#define SPK_NW 15  // variant builds (profiling): 7 and 11 consumer warps measured slower, DESIGN.md section 6
+#define SPK_NW 15  // variant builds (profiling): 7 and 11 consumer warps measured slower, DESIGN.md section 4.1
 #endif
 constexpr int kNW = SPK_NW;             // consumer warps per CTA (+1 producer = 16 warps: 4 per SMSP, 128 registers)
 constexpr int kThreadsBlocked = 32 * (kNW + 1);
@@ -791,7 +791,8 @@ __global__ void __launch_bounds__(32 * kSlotWarps) slot_warp_kernel(
 // one-row-once-per-chunk rule) are then dealt to the half-chunk with room
 // where they add the fewest wavefronts. Measured at config 4: 3.8 / 4.05
 // wavefronts per accumulator / gather access with the run-length placement
-// plus greedy column dealing (slot_warp_kernel), ~2.8 / 2.8 with this.
+// plus greedy column dealing (slot_warp_kernel), 3.12 / 2.93 with this
+// (the layout analysed by scratch-free tooling: SPK_DUMP_BLOCKED writes the head of the key stream).
 // One warp per segment; all state in shared memory. newpos[q] = chunk * 32 +
 // lane, or -1 (whole segment) when the segment does not fit this scheme.
 // Two instances: segments of up to 512 entries in up to 16 chunks (all of config
