@@ -6,7 +6,7 @@
 #include <cstdio>
 #include <cstdint>
 #include <cuda_runtime.h>
-__device__ __forceinline__ double lds(uint32_t a) { double v; asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a)); return v; }
+__device__ __forceinline__ double lds(uint32_t a) { double v; asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a) : "memory"); return v; }
 __device__ __forceinline__ void sts(uint32_t a, double v) { asm volatile("st.shared.f64 [%0], %1;" :: "r"(a), "d"(v)); }
 __device__ int slot(int p, int l) {
   switch (p) {
@@ -29,19 +29,21 @@ __global__ void k(int p, int iters, long long* out, double* sink) {
   for (int i = threadIdx.x; i < 4096; i += blockDim.x) sm[i] = i;
   __syncthreads();
   const int l = threadIdx.x & 31;
-  const uint32_t a = (uint32_t)__cvta_generic_to_shared(sm) + 8u * (uint32_t)slot(p, l);
-  double acc = 0;
+  // every warp reads its own rows (same bank pattern): identical addresses across warps would be merged
+  const uint32_t a = (uint32_t)__cvta_generic_to_shared(sm) + 8u * (uint32_t)(slot(p, l) + 16 * (threadIdx.x >> 5));
+  double acc = 0, accs[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   __syncthreads();
   const long long t0 = clock64();
   for (int i = 0; i < iters; ++i) {
 #pragma unroll
     for (int u = 0; u < 16; ++u) {
-      if (STORE) sts(a + 2048u * (u & 7), acc); else acc += lds(a + 2048u * (u & 7));
+      if (STORE) sts(a + 1024u * u, acc); else accs[u & 7] += lds(a + 1024u * u);  // 8 chains: not DADD-latency bound
     }
   }
   __syncthreads();
   const long long t1 = clock64();
   if (threadIdx.x == 0) out[0] = t1 - t0;
+  for (int u = 0; u < 8; ++u) acc += accs[u];
   if (acc == 1.2345) sink[0] = acc;
 }
 int main() {
