@@ -243,10 +243,14 @@ __global__ void plan_rows_cached_kernel(const double* Kg, int64_t n, DPlan P, lo
   }
 }
 
+// EMIT with slot_cap != nullptr: single pass into per-row slots (row_ptr = slot
+// offsets; kept counts to row_cnt_i, a row outgrowing its slot sets *overflow
+// and the caller redoes the sketch with the count / emit pair).
 template <bool EMIT, class VT>
 __global__ void sample_rows_cached_kernel(const double* K, const double* Kg, int64_t n, DPlan P, double s,
                                           uint64_t seed, long long* row_cnt, const long long* row_ptr,
-                                          uint32_t* col_out, VT* val_out) {
+                                          uint32_t* col_out, VT* val_out, const int* slot_cap = nullptr,
+                                          int* row_cnt_i = nullptr, unsigned int* overflow = nullptr) {
   const int lane = threadIdx.x & 31;
   const unsigned lt_mask = (1u << lane) - 1u;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -283,14 +287,21 @@ __global__ void sample_rows_cached_kernel(const double* K, const double* Kg, int
       }
       const unsigned km = __ballot_sync(0xffffffffu, keep);
       if (EMIT && keep) {
-        const long long pos = out0 + cnt + __popc(km & lt_mask);
-        const double k = K[i * n + j];
-        col_out[pos] = (uint32_t)j;
-        val_out[pos] = (VT)(ps >= 1.0 ? k : k / ps);
+        const long long rel = cnt + __popc(km & lt_mask);
+        if (!slot_cap || rel < slot_cap[i]) {
+          const long long pos = out0 + rel;
+          const double k = K[i * n + j];
+          col_out[pos] = (uint32_t)j;
+          val_out[pos] = (VT)(ps >= 1.0 ? k : k / ps);
+        }
       }
       cnt += __popc(km);
     }
     if (!EMIT && lane == 0) row_cnt[i] = cnt;
+    if (EMIT && slot_cap && lane == 0) {
+      row_cnt_i[i] = (int)cnt;
+      if (cnt > slot_cap[i]) atomicExch(overflow, 1u);
+    }
   }
 }
 
@@ -1554,9 +1565,67 @@ void sample_sketch(spk_ctx* ctx, DevKernel& dk, const PlanInfo& plan, double s, 
   const bool cached = !dk.dense && plan.kind == SPK_PLAN_UOT && !plan.factorized && dk.cKg.p &&
                       dk.cache_g == plan.g_k && row0 == 0 && n == ncols;
   if (cached) {
-    // ---- K and K^g_k of this kernel are resident (batched UOT sketches): count, scan, emit ----
-    DBuf cnt(sizeof(long long) * n);
+    // ---- K and K^g_k of this kernel are resident (batched UOT sketches) ----
     const int grid = grid_for_rows(ctx, n, 8);
+    if (plan.have_rows && !ctx->force_two_pass) {
+      // single pass into row slots sized from the plan's row masses (as the tiled sampler)
+      DBuf cap(sizeof(int) * n), capll(sizeof(long long) * n), off(sizeof(long long) * (n + 1));
+      slot_cap_kernel<<<grid_for(ctx, n, 256), 256, 0, ctx->stream>>>(
+          n, 0, dk.n, plan.d_row_nnz.as<long long>(), plan.d_row_sum.as<double>(), rw.as<double>(), 0.0, 0, plan.inv,
+          s, P.theta_mode, P.omt, P.unif, cap.as<int>());
+      int_to_ll_kernel<<<grid_for(ctx, n, 256), 256, 0, ctx->stream>>>(cap.as<int>(), n, capll.as<long long>());
+      ctx->launches += 2;
+      SPK_CUDA(cudaMemsetAsync(off.p, 0, sizeof(long long), ctx->stream));
+      size_t tb = 0;
+      SPK_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb, capll.as<long long>(), off.as<long long>() + 1, (int)n,
+                                             ctx->stream));
+      ctx->scratch.ensure(tb);
+      SPK_CUDA(cub::DeviceScan::InclusiveSum(ctx->scratch.p, tb, capll.as<long long>(), off.as<long long>() + 1,
+                                             (int)n, ctx->stream));
+      long long pool = 0;
+      SPK_CUDA(cudaMemcpyAsync(&pool, off.as<long long>() + n, sizeof pool, cudaMemcpyDeviceToHost, ctx->stream));
+      SPK_CUDA(cudaStreamSynchronize(ctx->stream));
+      DBuf &pcol = tmp_buf(ctx, 11, sizeof(uint32_t) * std::max<long long>(pool, 1)),
+           &pval = tmp_buf(ctx, 12, vbytes * std::max<long long>(pool, 1));
+      DBuf rcnt(sizeof(int) * n), ovf(sizeof(unsigned int));
+      SPK_CUDA(cudaMemsetAsync(ovf.p, 0, sizeof(unsigned int), ctx->stream));
+      if (value_type == SPK_VALUES_F32)
+        sample_rows_cached_kernel<true, float><<<grid, 256, 0, ctx->stream>>>(
+            dk.cK.as<double>(), dk.cKg.as<double>(), n, P, s, seed, nullptr, off.as<long long>(),
+            pcol.as<uint32_t>(), pval.as<float>(), cap.as<int>(), rcnt.as<int>(), ovf.as<unsigned int>());
+      else
+        sample_rows_cached_kernel<true, double><<<grid, 256, 0, ctx->stream>>>(
+            dk.cK.as<double>(), dk.cKg.as<double>(), n, P, s, seed, nullptr, off.as<long long>(),
+            pcol.as<uint32_t>(), pval.as<double>(), cap.as<int>(), rcnt.as<int>(), ovf.as<unsigned int>());
+      ++ctx->launches;
+      unsigned int overflow = 0;
+      download(ctx, &overflow, ovf, sizeof overflow);
+      if (!overflow) {
+        int_to_ll_kernel<<<grid_for(ctx, n, 256), 256, 0, ctx->stream>>>(rcnt.as<int>(), n, capll.as<long long>());
+        ++ctx->launches;
+        SPK_CUDA(cudaMemsetAsync(sk->row_ptr.p, 0, sizeof(long long), ctx->stream));
+        SPK_CUDA(cub::DeviceScan::InclusiveSum(ctx->scratch.p, tb, capll.as<long long>(),
+                                               sk->row_ptr.as<long long>() + 1, (int)n, ctx->stream));
+        long long nnz = 0;
+        SPK_CUDA(cudaMemcpyAsync(&nnz, sk->row_ptr.as<long long>() + n, sizeof nnz, cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+        SPK_CUDA(cudaStreamSynchronize(ctx->stream));
+        if (nnz > 0xffffffffLL) fail(SPK_E_BUDGET_TOO_LARGE, "sketch exceeds 2^32 entries");
+        sk->nnz = nnz;
+        sk->col_idx.alloc(sizeof(uint32_t) * std::max<long long>(nnz, 1));
+        sk->values.alloc(vbytes * std::max<long long>(nnz, 1));
+        compact_kernel<<<grid_for_rows(ctx, n, 8), 256, 0, ctx->stream>>>(
+            n, off.as<long long>(), sk->row_ptr.as<long long>(), pcol.as<uint32_t>(), pval.as<unsigned char>(),
+            (int)vbytes, sk->col_idx.as<uint32_t>(), sk->values.as<unsigned char>());
+        ++ctx->launches;
+        SPK_CUDA(cudaGetLastError());
+        build_csc(ctx, sk);
+        sk->kernel_mean = sketch_kernel_mean(ctx, sk);
+        return;
+      }
+      // a row outgrew its slot: the exact count / emit pair below
+    }
+    DBuf cnt(sizeof(long long) * n);
     sample_rows_cached_kernel<false, double><<<grid, 256, 0, ctx->stream>>>(
         dk.cK.as<double>(), dk.cKg.as<double>(), n, P, s, seed, cnt.as<long long>(), nullptr, nullptr, nullptr);
     ++ctx->launches;
