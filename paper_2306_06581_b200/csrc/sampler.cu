@@ -1298,7 +1298,9 @@ void make_dev_kernel(spk_ctx* ctx, const spk_kernel_desc* kd, double default_eps
     dk.scale = 1.0;
     KSrc S = make_src(dk);
     bool tiled = false;
-    if (dk.kind == SPK_COST_SQEUCLID && n >= 2048) {  // cost = d2 itself (cost_entry<0>)
+    // cost = d2 itself (cost_entry<0>) or its correctly rounded square root (cost_entry<1>: monotone, so the
+    // largest cost is the root of the largest d2)
+    if ((dk.kind == SPK_COST_SQEUCLID || dk.kind == SPK_COST_EUCLID) && n >= 2048) {
       const int rb = (int)((n + 255) / 256);
       const int parts = (int)std::max<int64_t>(1, std::min<int64_t>(64, (int64_t)ctx->num_sms * 8 / rb));
       const dim3 grid(rb, parts);
@@ -1328,6 +1330,7 @@ void make_dev_kernel(spk_ctx* ctx, const spk_kernel_desc* kd, double default_eps
     SPK_CUDA(cudaStreamSynchronize(ctx->stream));
     double c0;
     std::memcpy(&c0, &bits, sizeof c0);
+    if (tiled && dk.kind == SPK_COST_EUCLID) c0 = std::sqrt(c0);
     dk.scale = c0;
     dk.max_normalised = true;
   }

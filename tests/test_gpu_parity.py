@@ -604,6 +604,28 @@ def test_tiled_sampler_dense_budgets(ctx, oracle):
         assert len(so[1]) > 0.25 * n * n * frac
 
 
+def test_max_cost_tiled(ctx):
+    """c0 = max finite cost of the C / max normalisation (geometry.cpp:61) from the
+    tiled max-d2 pass (n >= 2048, squared-Euclidean and Euclidean costs): the
+    same bits as the pairwise sequential-order computation, so every normalised
+    cost is unchanged."""
+    rng = np.random.default_rng(3)
+    n = 3000
+    x = rng.normal(size=(n, 3))
+    y = rng.normal(size=(n, 3)) + 0.5
+    s = np.zeros((n, n))
+    for k in range(3):  # d2 summed over the dimensions in order, no FMA (geometry.cpp:16-59)
+        diff = x[:, None, k] - y[None, :, k]
+        s = s + diff * diff
+    qi = np.arange(64, dtype=np.int64)
+    qj = (qi * 7 + 3) % n
+    for kind in ("sqeuclid", "euclid"):
+        full = np.sqrt(s) if kind == "euclid" else s
+        cost, _, c0 = ctx.cost_kernel(spk.Coords(x, y, kind, eps=0.1), qi, qj)
+        assert c0 == full.max()
+        assert np.array_equal(cost, full[qi, qj] / full.max())
+
+
 def test_config3_frame_pair(ctx, oracle):
     """Config 3 (one WFR frame pair at full size, n = 12544): UOT grid plan on
     a 22%-support kernel, fp32 sketch values, log-domain loop. Index sets bit
