@@ -154,6 +154,14 @@ void build_sketch(spk_ctx* ctx, DevKernel& dk, const double* a, const double* b,
   }
   NvtxRange r("spk:sample");
   Timer ts(ctx->stream);
+  // UOT on a coordinate kernel with a well-filled support: the tiled sampler
+  // bounds K^g_k per entry with cos / log / exp2 and still takes the exact
+  // exp / pow path for every candidate; evaluating K and K^g_k once for all
+  // pairs and sampling from them is cheaper (config 2: 3.9 -> 1.8 ms). A
+  // batch (spk_sketch_build_batch) has them already.
+  if (plan_kind == SPK_PLAN_UOT && !dk.dense && !ctx->force_two_pass && !plan.factorized && lambda > 0.0 && eps > 0.0 &&
+      (double)plan.kernel_nnz > 0.1 * (double)dk.n * (double)dk.n)
+    cache_uot_kernel(ctx, dk, eps / (2.0 * lambda + eps));
   sample_sketch(ctx, dk, plan, s, seed, value_type, sk);
   *t_sample = ts.stop();
   set_weights(ctx, sk, a, b);
