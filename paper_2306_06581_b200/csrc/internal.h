@@ -316,6 +316,8 @@ struct DevKernel {
 
 // Fill dk.cK / dk.cKg for UOT plans with exponent g_k when n^2 entries fit the budget; false otherwise.
 bool cache_uot_kernel(spk_ctx* ctx, DevKernel& dk, double g_k);
+// Fraction of nonzero kernel entries among 4096 pseudo-random pairs (coordinate form).
+double probe_support_fraction(spk_ctx* ctx, DevKernel& dk);
 
 void make_dev_kernel(spk_ctx* ctx, const spk_kernel_desc* kd, double default_eps, DevKernel& dk,
                      bool need_cost);

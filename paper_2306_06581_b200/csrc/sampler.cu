@@ -1336,6 +1336,30 @@ void make_dev_kernel(spk_ctx* ctx, const spk_kernel_desc* kd, double default_eps
   }
 }
 
+namespace {
+// Support fraction of a coordinate kernel from 4096 pseudo-random pairs.
+__global__ void support_probe_kernel(KSrc S, unsigned int* hits) {
+  const unsigned int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t h = splitmix64(0x5eedull + t);
+  const int64_t i = (int64_t)((h >> 32) % (uint64_t)S.n), j = (int64_t)((h & 0xffffffffull) % (uint64_t)S.n);
+  const bool nz = kernel_entry(S, i, j) != 0.0;
+  const unsigned m = __ballot_sync(0xffffffffu, nz);
+  if ((threadIdx.x & 31) == 0 && m) atomicAdd(hits, (unsigned int)__popc(m));
+}
+}  // namespace
+
+double probe_support_fraction(spk_ctx* ctx, DevKernel& dk) {
+  if (dk.dense) return dk.nnz_ratio;
+  DBuf hits(sizeof(unsigned int));
+  SPK_CUDA(cudaMemsetAsync(hits.p, 0, sizeof(unsigned int), ctx->stream));
+  KSrc S = make_src(dk);
+  support_probe_kernel<<<16, 256, 0, ctx->stream>>>(S, hits.as<unsigned int>());
+  ++ctx->launches;
+  unsigned int h = 0;
+  download(ctx, &h, hits, sizeof h);
+  return (double)h / 4096.0;
+}
+
 bool cache_uot_kernel(spk_ctx* ctx, DevKernel& dk, double g_k) {
   if (dk.dense || !(g_k > 0.0 && g_k < 1.0)) return false;
   if (dk.cKg.p && dk.cache_g == g_k) return true;
