@@ -334,6 +334,7 @@ struct PlanInfo {
   // plan-pass outputs kept on the device (grid plans): per-row support size
   // and unnormalised row mass, used to size the sampler's row slots
   DBuf d_row_nnz, d_row_sum;  // indexed by GLOBAL row
+  mutable DBuf d_rw, d_cw;    // row_w / col_w on the device (uploaded once: the plan pass and the sampler share them)
   bool have_rows = false;
   bool zero_mass = false;
 };

@@ -1455,9 +1455,11 @@ void plan_pass_rows(spk_ctx* ctx, DevKernel& dk, const PlanInfo& plan, int64_t r
   const int64_t n = dk.n;
   const int64_t rows = row1 - row0;
   if (rows <= 0) return;
-  DBuf rw, cw;
-  upload(ctx, rw, plan.row_w.data(), sizeof(double) * n);
-  upload(ctx, cw, plan.col_w.data(), sizeof(double) * n);
+  if (!plan.d_rw.p) {
+    upload(ctx, plan.d_rw, plan.row_w.data(), sizeof(double) * n);
+    upload(ctx, plan.d_cw, plan.col_w.data(), sizeof(double) * n);
+  }
+  DBuf &rw = plan.d_rw, &cw = plan.d_cw;
   DPlan P{};
   P.row_w = rw.as<double>();
   P.col_w = cw.as<double>();
@@ -1640,9 +1642,11 @@ void sample_sketch(spk_ctx* ctx, DevKernel& dk, const PlanInfo& plan, double s, 
   const int64_t n = row1 - row0;  // rows sampled here (all of them unless sharded)
   const double nn = static_cast<double>(ncols) * static_cast<double>(ncols);
   if (!(s > 0.0) || s >= nn) fail(SPK_E_BUDGET_TOO_LARGE, "budget s must satisfy 0 < s < n^2");
-  DBuf rw, cw;
-  upload(ctx, rw, plan.row_w.data(), sizeof(double) * ncols);
-  upload(ctx, cw, plan.col_w.data(), sizeof(double) * ncols);
+  if (!plan.d_rw.p) {
+    upload(ctx, plan.d_rw, plan.row_w.data(), sizeof(double) * ncols);
+    upload(ctx, plan.d_cw, plan.col_w.data(), sizeof(double) * ncols);
+  }
+  DBuf &rw = plan.d_rw, &cw = plan.d_cw;
   DPlan P = device_plan(plan, rw.as<double>(), cw.as<double>());
   KSrc S = make_src(dk);
 
